@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the B-ADMM barycenter hot path (arXiv 1510.00012, Alg. 4) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload 5] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (driver launch for N > 1)
+
+A "step" is one full round of the centroid update for every cluster:
+ad2_barycenter_init (sort, cost, rho, Pi2 init) -> T/tau x (ad2_badmm_step(tau);
+ad2_update_support()) -> ad2_objective (device->host read of the result).  Inputs are resident
+in HBM when the timed region starts (value); e2e repeats the step from pinned host buffers
+through the same C ABI with the host<->device copies inside the timed region.
+
+metric: B-ADMM plan-entry-iterations/s = sum_k m*m_k * T / step time, all ranks (whole job).
+Members are sharded over ranks (entry-balanced contiguous shards, fixed total N: strong
+scaling); the per-cluster w/x partial sums are NCCL all-reduced inside libad2.
+The state (Pi1, Pi2, Lambda, C: 41 GB at cfg5) is far larger than L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1510_00012_b200 import workloads as wl  # noqa: E402
+from paper_1510_00012_b200.sharding import shard_bounds  # noqa: E402
+
+METRIC = "B-ADMM plan-entry-iterations/sec"
+UNIT = "entry-iter/s"
+BYTES_PER_ENTRY = 16          # algorithmic bytes per entry-iteration: r+w Pi-state and Lambda
+CACHE = os.environ.get("AD2_BENCH_CACHE", "/dev/shm/ad2_bench")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------------------ data
+
+def load_bundle(cfg: int, rank: int, world: int, barrier) -> wl.Bundle:
+    """Rank 0 generates the seeded bundle (or finds it cached in /dev/shm); other ranks load it."""
+    path = os.path.join(CACHE, f"cfg{cfg}_seed0_v1")
+    keys = ["offsets", "supports", "weights", "labels", "x0", "w0"]
+    done = os.path.join(path, "meta.json")
+    if rank == 0 and not os.path.exists(done):
+        t = time.time()
+        b = wl.make_config(cfg)
+        log(f"[bench] generated {b.name} in {time.time() - t:.1f}s")
+        try:
+            os.makedirs(path, exist_ok=True)
+            for k in keys:
+                np.save(os.path.join(path, k + ".npy"), getattr(b, k))
+            json.dump({"name": b.name, "d": b.d, "m": b.m, "K": b.K, "dtype": b.dtype}, open(done + ".tmp", "w"))
+            os.replace(done + ".tmp", done)
+        except OSError as e:
+            log(f"[bench] cache write failed: {e}")
+        if world == 1 or not os.path.exists(done):
+            barrier()
+            return b
+    barrier()
+    meta = json.load(open(done))
+    arrs = {k: np.load(os.path.join(path, k + ".npy")) for k in keys}
+    sched = wl.make_config(cfg, N=64, K=1).sched if cfg != 1 else wl.make_config(1).sched
+    return wl.Bundle(meta["name"], meta["d"], meta["m"], meta["K"], dtype=meta["dtype"], sched=sched, **arrs)
+
+
+# ------------------------------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ ours
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1510_00012_b200 import ad2
+    from paper_1510_00012_b200.sharding import bootstrap_nccl
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    barrier = (lambda: dist.barrier(device_ids=[local_rank])) if world > 1 else (lambda: None)
+    b = load_bundle(args.workload, rank, world, barrier)
+    s = b.sched
+    T, tau = s.T, s.tau
+    bounds = shard_bounds(b.offsets, world)
+    mine = b.subset(np.arange(bounds[rank], bounds[rank + 1])) if world > 1 else b
+    entries_local = mine.entries()
+    entries_total = b.entries()
+    stream = torch.cuda.current_stream(dev)
+    ctx = ad2.Context(local_rank, stream.cuda_stream)
+    if world > 1:
+        bootstrap_nccl(ctx)
+
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    D = dict(offsets=t(mine.offsets), supports=t(mine.supports), weights=t(mine.weights), labels=t(mine.labels),
+             x0=t(b.x0), w0=t(b.w0))
+    obj_box = {}
+
+    def step(arr, mem):
+        ctx.init(arr["offsets"], arr["supports"], arr["weights"], arr["labels"], arr["x0"], arr["w0"], b.K, b.m,
+                 s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype)
+        ad2.run_schedule(ctx, T, tau)
+        obj_box["obj"] = ctx.objective()               # device -> host read of the result (syncs)
+
+    def timed(fn, K, W):
+        for _ in range(W):
+            fn()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = ctx.info()["launches"]
+        e0.record(stream)
+        for _ in range(K):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = e0.elapsed_time(e1) / K
+        launches = ctx.info()["launches"] - l0
+        if world > 1:
+            x = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            ms = float(x.item())
+        return ms, launches
+
+    ctx.set_profiling(True)          # event nodes around every iteration kernel (live, in-graph)
+    with ClockSampler(local_rank) as clk:
+        ms, launches = timed(lambda: step(D, "device"), args.steps, args.warmup)
+    launch_ms, step_graph_ms = ctx.prof_read()
+    info = ctx.info()
+    value = entries_total * T / (ms / 1e3)
+
+    # dominant kernel: the fused iteration kernel (launches 1..n-1 of each step graph)
+    fused = launch_ms[1:-1] if len(launch_ms) > 2 else launch_ms
+    avg_fused_ms = float(np.mean(fused))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = BYTES_PER_ENTRY * entries_local / (avg_fused_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if prof.get("workload") == b.name and prof.get("kernel_variant") == "fused":
+            traffic = prof.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    iter_share = float(np.sum(launch_ms)) / (ms) if ms > 0 else None
+
+    # e2e: the same step through the C ABI from pinned host buffers (H2D inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        H = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+             dict(offsets=mine.offsets, supports=mine.supports, weights=mine.weights, labels=mine.labels,
+                  x0=b.x0, w0=b.w0).items()}
+        xo = torch.empty(b.x0.shape, dtype=H["x0"].dtype).pin_memory()
+        wo = torch.empty(b.w0.shape, dtype=H["w0"].dtype).pin_memory()
+
+        def step_host():
+            step(H, "host")
+            ctx.centroids_into(xo, wo, mem="host")
+
+        ctx.set_profiling(False)
+        ms_e2e, _ = timed(step_host, max(1, min(args.steps, 3)), 1)
+        h2d = sum(v.numel() * v.element_size() for v in H.values())
+        d2h = xo.numel() * xo.element_size() + wo.numel() * wo.element_size() + 2 * 8 * b.K
+        e2e = {"value": entries_total * T / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(b, budget_s=args.cpu_budget)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if b.dtype == "f32" else "f64", "data": "synthetic",
+        "config": {"workload": b.name, "N": b.N, "K": b.K, "m": b.m, "d": b.d, "T": T, "tau": tau,
+                   "entries_per_iter": entries_total, "step": "1 round: init + T/tau x (step(tau), update_support) + objective",
+                   "parallelism": f"dp{world} (members sharded, NCCL all-reduce of per-cluster partials)",
+                   "l2": "inputs larger than L2 (state %.1f GB)" % (info["state_bytes"] / 1e9),
+                   "kernel_variant": "fused" if info["variant"] == 1 else "generic"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_badmm_warp<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
+                     "bytes_per_entry": BYTES_PER_ENTRY, "entries_per_launch": entries_local,
+                     "avg_launch_ms": avg_fused_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "iteration_kernels_share_of_step": iter_share},
+        "iter_only": {"value": entries_total * T / ((np.sum(launch_ms) * T / max(1, len(launch_ms) - 1)) / 1e3),
+                      "note": "iteration kernels only (event-timed), excluding consensus/init/objective"},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ oracle
+
+def oracle_sample(b: wl.Bundle, budget_s: float):
+    """A bounded sample of the workload for the oracle: the first members of cluster 0, sized so
+    T iterations take about budget_s on this host (estimated from a 1-iteration probe)."""
+    import oracle
+    mem = np.nonzero(b.labels == 0)[0]
+    s = b.sched
+    n_try = min(len(mem), 2000)
+    sub = b.subset(mem[:n_try])
+    t = time.time()
+    oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, 1, 1, s.rule, s.rho0, s.eps, 1e-5,
+                          want_state=False)
+    rate = b.m * sub.n / max(1e-6, time.time() - t)
+    want = int(budget_s * rate / (b.m * s.T) / max(1, float(np.mean(b.sizes))))
+    take = int(min(len(mem), max(50, want)))
+    return b.subset(mem[:take]), take
+
+
+def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, sub=None):
+    import oracle
+    s = b.sched
+    if sub is None:
+        sub, _ = oracle_sample(b, budget_s)
+    t = time.time()
+    oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0, s.eps,
+                          1e-5, want_state=False)
+    dt = time.time() - t
+    return {"value": b.m * sub.n * s.T / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"cluster 0 of {b.name}: first {sub.N} members ({b.m * sub.n} plan entries), T={s.T}, "
+                      f"tau={s.tau}, fp64, {dt:.1f}s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle as it stands, on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    b = load_bundle(args.workload, 0, 1, lambda: None)
+    sub, _ = oracle_sample(b, args.cpu_budget / max(1, args.steps + args.warmup) * 2)
+    for _ in range(args.warmup):
+        cpu_baseline(b, sub=sub)
+    t = time.time()
+    vals = [cpu_baseline(b, sub=sub) for _ in range(args.steps)]
+    ms = (time.time() - t) / max(1, args.steps) * 1e3
+    v = float(np.mean([x["value"] for x in vals]))
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": b.name, "N": b.N, "K": b.K, "m": b.m, "d": b.d, "T": b.sched.T, "tau": b.sched.tau},
+           "cpu_baseline": {"kind": "oracle", "cores": vals[-1]["cores"], "sample": vals[-1]["sample"], "value": v},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", type=int, default=5, help="BASELINE.json config (1-based)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,177 @@
+/*
+ * ad2.h — C ABI of libad2: the modified Bregman-ADMM Wasserstein-barycenter update of
+ * AD2-clustering (Ye, Wu, Wang, Li; arXiv 1510.00012, Algorithm 4) on NVIDIA B200 (sm_100a).
+ *
+ * "P:n" = PAPER.md line n (the paper's LaTeX source); equations are named by their LaTeX
+ * label (the PDF numbers them (1)-(24), SURVEY.md §0 has the map).
+ *
+ * Problem.  N members P^(k) = {(w_j^(k), x_j^(k)), j = 1..m_k} in R^d, each with a
+ * cluster label l^(k) in [0, K).  For every cluster c the library keeps a centroid
+ * P_c = {(w_i, x_i), i = 1..m} and the B-ADMM state of each member: Pi^(k,1), Pi^(k,2),
+ * Lambda^(k) in R^{m x m_k}, and runs Alg. 4:
+ *
+ *   init            : C^(k) = (||x_i - x_j^(k)||^2)_ij; rho_c = rho0 * mean_{k in c,i,j} C_ij
+ *                     (Eq.rho, reading X1); Lambda = 0; Pi^(k,2) = w_i w_j^(k)
+ *                      or the cached Pi^(k,2) for warm members
+ *   step (1 iter)   : Pi^(k,1) (Eq.badmmc0b, Eq.badmmc0); pt^(k,1) (Eq.badmmc1b);
+ *                     w by R1 (Eq.badmmw) or R2 (Eq.badmmw2) — a reduction
+ *                     over all members of the cluster, on all ranks; Pi^(k,2) (Eq.badmmc1);
+ *                     Lambda += rho (Pi^(k,1) - Pi^(k,2)) (Eq.badmm2)
+ *   update_support  : x_i = sum_k sum_j pi2_ij x_j^(k) / sum_k sum_j pi2_ij (Eq.updatex, P:342-351,
+ *                     readings X5, X12), then C is rebuilt; rho stays fixed (X2)
+ *   objective       : F_c = (1/N_c) sum_{k in c} <C^(k), Pi^(k,1)> (X14)
+ *
+ * The caller drives the schedule of Alg. 4: for e in 1..T/tau: step(tau); update_support().
+ *
+ * Conventions
+ *  - All calls are made from one host thread per context; a context is NOT thread-safe.
+ *  - Compute is asynchronous on the context's CUDA stream (the stream given to ad2_create).
+ *    Calls that return host data (init, objective, getters with AD2_HOST, sync) synchronise it.
+ *  - Argument errors are detected before any state changes and return AD2_ERR_ARG.
+ *    Device-side faults (a non-finite plan/weight) are latched and returned by the next
+ *    synchronising call as AD2_ERR_NONFINITE.  No C++ exception crosses this ABI.
+ *  - There is no CPU fallback: without a CUDA device ad2_create returns AD2_ERR_CUDA.
+ *  - Floating-point buffers are float (AD2_F32) or double (AD2_F64) per the batch dtype.
+ *    eps is params->eps in both precisions (reading X3).
+ *  - Multi-GPU: one context per GPU/process, each with its own member shard; every
+ *    rank calls every function with the same d, m, K, params, x0, w0 and the same schedule.
+ *    The per-cluster partial sums (w: K*m per iteration, x: K*m*(d+1) per support update, rho
+ *    and objective: K) are summed across ranks by NCCL all-reduce over NVLink.
+ */
+#ifndef AD2_H
+#define AD2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AD2_ABI_VERSION 1
+
+typedef struct ad2_ctx_s *ad2_ctx;
+
+typedef enum { AD2_F32 = 0, AD2_F64 = 1 } ad2_dtype;
+typedef enum { AD2_R1 = 0, AD2_R2 = 1 } ad2_rule;          /* Eq.badmmw / Eq.badmmw2 */
+typedef enum { AD2_DEVICE = 0, AD2_HOST = 1 } ad2_mem;     /* where a caller buffer lives */
+typedef enum { AD2_PI1 = 0, AD2_PI2 = 1, AD2_LAMBDA = 2, AD2_COST = 3 } ad2_plan;
+
+typedef enum {
+    AD2_OK = 0,
+    AD2_ERR_ARG = 1,        /* bad argument (shape, pointer, offsets, label range, weights off the simplex) */
+    AD2_ERR_OOM = 2,        /* device allocation failed */
+    AD2_ERR_CUDA = 3,       /* CUDA runtime error (message in ad2_last_error) */
+    AD2_ERR_NCCL = 4,       /* NCCL error or NCCL unavailable */
+    AD2_ERR_NONFINITE = 5,  /* a plan row mass / weight became non-finite (latched, async) */
+    AD2_ERR_ZERO_RHO = 6,   /* a cluster's mean cost is 0 (rho = 0) */
+    AD2_ERR_EMPTY = 7,      /* a cluster has no members on any rank */
+    AD2_ERR_STATE = 8       /* call out of order (e.g. step before init) */
+} ad2_status;
+
+/* One rank's member shard in the paper's ragged layout.  Borrowed, read-only,
+ * only during ad2_barycenter_init (the library copies what it needs). */
+typedef struct {
+    ad2_dtype dtype;
+    ad2_mem mem;                /* where offsets/supports/weights/labels (and x0/w0) live */
+    int32_t d;                  /* support dimension, >= 1 */
+    int32_t m;                  /* centroid support size, >= 1 */
+    int32_t K;                  /* number of clusters, >= 1 */
+    int64_t n_members;          /* N on this rank, >= 0 */
+    const int64_t *offsets;     /* [N+1], offsets[0] = 0, m_k = offsets[k+1]-offsets[k] >= 1 */
+    const void *supports;       /* [offsets[N]][d] row-major: x_j^(k) = supports[offsets[k]+j] */
+    const void *weights;        /* [offsets[N]]: w^(k) on the simplex, |sum - 1| <= 1e-6 (f64) or
+                                   1e-5 (f32); renormalised by its sum (O1) */
+    const int32_t *labels;      /* [N], each in [0, K) */
+} ad2_batch;
+
+typedef struct {
+    double rho0;                /* > 0; rho_c = rho0 * mean cost of cluster c (X1); paper default 2 */
+    double eps;                 /* >= 0; floor of Eq.badmmc0b / Eq.badmmc1b, paper 1e-16 */
+    int32_t rule;               /* AD2_R1 or AD2_R2 */
+    int32_t cost_mode;          /* 0: cache C in HBM (default); other values reserved */
+} ad2_params;
+
+typedef struct {
+    int32_t abi_version;
+    int32_t dtype, d, m, K;
+    int64_t n_members;          /* on this rank */
+    int64_t n_points;           /* sum_k m_k on this rank */
+    int64_t entries;            /* sum_k m * m_k on this rank (plan entries per iteration) */
+    int64_t n_items;            /* work items (per-cluster member chunks) */
+    int32_t variant;            /* 1 = fused warp-per-member kernels, 0 = generic kernels */
+    int32_t mp, nch;            /* fused-kernel row tile (8/16/32) and column chunks */
+    int32_t nranks, rank;
+    int64_t launches;           /* kernels launched by this context so far (graph nodes counted) */
+    int64_t state_bytes;        /* device bytes owned by the context */
+} ad2_info;
+
+/* Create a context on CUDA device `cuda_device`; `cuda_stream` is a cudaStream_t (NULL = legacy
+ * default stream) that every later call enqueues on.  out receives the handle. */
+ad2_status ad2_create(ad2_ctx *out, int cuda_device, void *cuda_stream);
+
+/* Fill `id_out` (128 bytes, an ncclUniqueId) on one rank, to be broadcast by the caller (e.g.
+ * through torch.distributed) before ad2_attach_nccl.  Returns AD2_ERR_NCCL if libnccl.so.2
+ * cannot be loaded. */
+ad2_status ad2_nccl_unique_id(void *id_out);
+
+/* Join an NCCL communicator of `nranks` ranks (this one is `rank`), created from `unique_id`.
+ * Must precede ad2_barycenter_init.  nranks == 1 is allowed (all-reduce degenerates to a copy). */
+ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void *unique_id);
+
+/* Start a round (a1-a3 of SURVEY.md §8(a)): copy/sort the batch by cluster, build C, compute
+ * rho per cluster (fixed for the round, X2), Lambda = 0, Pi^(2) = product measure or, for
+ * members with warm_mask[k] != 0, the Pi^(2) this context holds for that member from the
+ * previous round (its m_k and the ctx m/dtype must be unchanged; else AD2_ERR_ARG).
+ *   x0 [K][m][d], w0 [K][m]: initial centroids (same memory space as batch->mem), copied.
+ *   warm_mask: host [N] or NULL (all cold).   rho_out: host double[K] or NULL.
+ * Synchronises.  Returns AD2_ERR_EMPTY / AD2_ERR_ZERO_RHO per cluster conditions. */
+ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch *batch, const ad2_params *params,
+                               const void *x0, const void *w0, const uint8_t *warm_mask,
+                               double *rho_out);
+
+/* n_iters >= 0 B-ADMM iterations at fixed x (a4-a8), then the support-update partial sums of
+ * the final Pi^(2) are formed for ad2_update_support.  Asynchronous (one CUDA graph per n). */
+ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters);
+
+/* a9: x update from the Pi^(2) of the last step (Eq.updatex), C rebuilt.  AD2_ERR_STATE if no
+ * step has run since init.  Asynchronous. */
+ad2_status ad2_update_support(ad2_ctx ctx);
+
+/* a10: obj_out (host double[K]) = (1/N_c) sum_k <C^(k), Pi^(k,1)> with the last Pi^(1) and the
+ * current x.  AD2_ERR_STATE if no step has run since init.  Synchronises. */
+ad2_status ad2_objective(ad2_ctx ctx, double *obj_out);
+
+/* Current centroids: x [K][m][d], w [K][m] in the ctx dtype, into `where` memory. */
+ad2_status ad2_get_centroids(ad2_ctx ctx, void *x, void *w, ad2_mem where);
+
+/* One state array for all members of this rank, in the caller's ORIGINAL member order:
+ * member k's m x m_k block at out + m*offsets[k], COLUMN-major (entry (i,j) at j*m + i).
+ * `which` selects Pi^(1), Pi^(2), Lambda or the cost C.  Synchronises for AD2_HOST. */
+ad2_status ad2_get_plans(ad2_ctx ctx, int which, void *out, ad2_mem where);
+
+/* Per-cluster rho (host double[K]) of the current round. */
+ad2_status ad2_get_rho(ad2_ctx ctx, double *rho_out);
+
+ad2_status ad2_get_info(ad2_ctx ctx, ad2_info *info);
+
+/* Kernel timing: when enabled, every B-ADMM iteration-kernel launch of later steps is bracketed
+ * by CUDA events on the launching stream (event-record nodes inside the step graph).
+ * ad2_prof_read fills launch_ms[0..min(capacity, n)-1] with the durations (ms) of the most
+ * recent step's launches in order [first (phase 1 only), fused x (n_iters-1), last (phase 2
+ * only)], *n_launches = n_iters + 1, and *step_ms = first start to last end.  Synchronises. */
+ad2_status ad2_set_profiling(ad2_ctx ctx, int enable);
+ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64_t *n_launches,
+                         double *step_ms);
+
+/* Wait for all work of the context; returns a latched device error if any. */
+ad2_status ad2_sync(ad2_ctx ctx);
+
+const char *ad2_last_error(ad2_ctx ctx);
+const char *ad2_status_string(ad2_status s);
+void ad2_destroy(ad2_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AD2_H */

@@ -1,0 +1,251 @@
+"""Thin ctypes binding of libad2 (include/ad2.h) — argument marshalling only.
+
+Every arithmetic step runs in the CUDA kernels of ``libad2.so``.  There is no CPU fallback: if
+the library is missing or no CUDA device is present, the calls raise ``RuntimeError``.
+
+Arrays may be torch tensors (CUDA tensors for ``mem="device"``, CPU — ideally pinned — tensors
+for ``mem="host"``) or numpy arrays (host).  Names follow the paper:
+``offsets``/``supports``/``weights`` = the ragged members P^(k), ``labels`` = l^(k),
+``x``/``w`` = centroid support points and weights, Pi1/Pi2/Lambda = the B-ADMM state.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libad2.so")
+
+F32, F64 = 0, 1
+R1, R2 = 0, 1
+DEVICE, HOST = 0, 1
+PI1, PI2, LAMBDA, COST = 0, 1, 2, 3
+
+STATUS = {0: "ok", 1: "ARG", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "NONFINITE", 6: "ZERO_RHO", 7: "EMPTY",
+          8: "STATE"}
+
+
+class AD2Error(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"AD2_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Batch(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("mem", C.c_int), ("d", C.c_int32), ("m", C.c_int32), ("K", C.c_int32),
+                ("n_members", C.c_int64), ("offsets", C.c_void_p), ("supports", C.c_void_p),
+                ("weights", C.c_void_p), ("labels", C.c_void_p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("rho0", C.c_double), ("eps", C.c_double), ("rule", C.c_int32), ("cost_mode", C.c_int32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("dtype", C.c_int32), ("d", C.c_int32), ("m", C.c_int32),
+                ("K", C.c_int32), ("n_members", C.c_int64), ("n_points", C.c_int64), ("entries", C.c_int64),
+                ("n_items", C.c_int64), ("variant", C.c_int32), ("mp", C.c_int32), ("nch", C.c_int32),
+                ("nranks", C.c_int32), ("rank", C.c_int32), ("launches", C.c_int64),
+                ("state_bytes", C.c_int64)]
+
+
+EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
+           "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
+           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_sync", "ad2_last_error",
+           "ad2_status_string", "ad2_destroy"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libad2.so (RuntimeError if it has not been built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libad2.so not built at {path}; run `python -m paper_1510_00012_b200.build`")
+    L = C.CDLL(path)
+    p, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    L.ad2_create.argtypes = [C.POINTER(p), C.c_int, p]
+    L.ad2_nccl_unique_id.argtypes = [p]
+    L.ad2_attach_nccl.argtypes = [p, C.c_int, C.c_int, p]
+    L.ad2_barycenter_init.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), p, p, p, p]
+    L.ad2_badmm_step.argtypes = [p, i32]
+    L.ad2_update_support.argtypes = [p]
+    L.ad2_objective.argtypes = [p, p]
+    L.ad2_get_centroids.argtypes = [p, p, p, C.c_int]
+    L.ad2_get_plans.argtypes = [p, C.c_int, p, C.c_int]
+    L.ad2_get_rho.argtypes = [p, p]
+    L.ad2_get_info.argtypes = [p, C.POINTER(Info)]
+    L.ad2_set_profiling.argtypes = [p, C.c_int]
+    L.ad2_prof_read.argtypes = [p, p, i64, C.POINTER(i64), C.POINTER(d)]
+    L.ad2_sync.argtypes = [p]
+    L.ad2_last_error.argtypes = [p]
+    L.ad2_last_error.restype = C.c_char_p
+    L.ad2_status_string.argtypes = [C.c_int]
+    L.ad2_status_string.restype = C.c_char_p
+    L.ad2_destroy.argtypes = [p]
+    L.ad2_destroy.restype = None
+    for f in EXPORTS:
+        if f not in ("ad2_last_error", "ad2_status_string", "ad2_destroy"):
+            getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = C.create_string_buffer(128)
+    st = L.ad2_nccl_unique_id(buf)
+    if st != 0:
+        raise AD2Error(st, "ncclGetUniqueId failed / NCCL not loadable")
+    return buf.raw
+
+
+class Context:
+    """One B-ADMM barycenter context on one GPU (one per rank)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self.L = load_library()
+        h = C.c_void_p()
+        st = self.L.ad2_create(C.byref(h), int(device), C.c_void_p(stream) if stream else None)
+        if st != 0:
+            raise AD2Error(st, "ad2_create failed (no CUDA device?)")
+        self.h = h
+        self.K = self.m = self.d = None
+        self.dtype = None
+        self._keep = []
+
+    def _chk(self, st: int):
+        if st != 0:
+            raise AD2Error(st, self.L.ad2_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ad2_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def attach_nccl(self, nranks: int, rank: int, unique_id: bytes):
+        self._chk(self.L.ad2_attach_nccl(self.h, nranks, rank, C.c_char_p(unique_id)))
+
+    def init(self, offsets, supports, weights, labels, x0, w0, K: int, m: int, rho0=2.0, eps=1e-16,
+             rule=R1, warm_mask=None, mem: str = "device", dtype: Optional[str] = None) -> np.ndarray:
+        """ad2_barycenter_init; returns rho per cluster (host float64 [K])."""
+        if dtype is None:
+            dt = getattr(supports, "dtype", None)
+            dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
+        d = int(supports.shape[1]) if supports.shape[0] > 0 else int(x0.shape[-1])
+        b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K),
+                  int(len(labels)), _ptr(offsets), _ptr(supports), _ptr(weights), _ptr(labels))
+        prm = Params(float(rho0), float(eps), int(rule), 0)
+        wm = None
+        if warm_mask is not None:
+            wm = np.ascontiguousarray(np.asarray(warm_mask), dtype=np.uint8)
+        rho = np.zeros(int(K))
+        self._chk(self.L.ad2_barycenter_init(self.h, C.byref(b), C.byref(prm), _ptr(x0), _ptr(w0),
+                                             _ptr(wm), rho.ctypes.data))
+        self.K, self.m, self.d, self.dtype = int(K), int(m), d, dtype
+        self._offsets = offsets
+        self._offsets_host = None
+        return rho
+
+    @property
+    def offsets_host(self) -> np.ndarray:
+        if self._offsets_host is None:
+            o = self._offsets
+            self._offsets_host = np.asarray(o.cpu() if hasattr(o, "cpu") else o)
+        return self._offsets_host
+
+    def step(self, n_iters: int):
+        self._chk(self.L.ad2_badmm_step(self.h, int(n_iters)))
+
+    def update_support(self):
+        self._chk(self.L.ad2_update_support(self.h))
+
+    def objective(self) -> np.ndarray:
+        out = np.zeros(self.K)
+        self._chk(self.L.ad2_objective(self.h, out.ctypes.data))
+        return out
+
+    def _np_dtype(self):
+        return np.float64 if self.dtype == "f64" else np.float32
+
+    def centroids(self):
+        x = np.empty((self.K, self.m, self.d), self._np_dtype())
+        w = np.empty((self.K, self.m), self._np_dtype())
+        self._chk(self.L.ad2_get_centroids(self.h, x.ctypes.data, w.ctypes.data, HOST))
+        return x, w
+
+    def centroids_into(self, x, w, mem: str = "device"):
+        self._chk(self.L.ad2_get_centroids(self.h, _ptr(x), _ptr(w), HOST if mem == "host" else DEVICE))
+
+    def plans(self, which: int) -> np.ndarray:
+        """Concatenated member blocks in caller order, column-major m x m_k each."""
+        n = int(self.offsets_host[-1])
+        out = np.empty(self.m * n, self._np_dtype())
+        self._chk(self.L.ad2_get_plans(self.h, int(which), out.ctypes.data, HOST))
+        return out
+
+    def member_matrices(self, which: int):
+        """List of m x m_k matrices (row i = centroid point, col j = member point)."""
+        cat = self.plans(which)
+        off = self.offsets_host
+        m = self.m
+        return [cat[m * off[k]: m * off[k + 1]].reshape(off[k + 1] - off[k], m).T for k in range(len(off) - 1)]
+
+    def rho(self) -> np.ndarray:
+        out = np.zeros(self.K)
+        self._chk(self.L.ad2_get_rho(self.h, out.ctypes.data))
+        return out
+
+    def info(self) -> dict:
+        i = Info()
+        self._chk(self.L.ad2_get_info(self.h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in Info._fields_}
+
+    def set_profiling(self, enable: bool):
+        self._chk(self.L.ad2_set_profiling(self.h, 1 if enable else 0))
+
+    def prof_read(self):
+        """(per-launch ms of the last step's iteration kernels, step ms)."""
+        buf = np.zeros(4096)
+        n, step = C.c_int64(), C.c_double()
+        self._chk(self.L.ad2_prof_read(self.h, buf.ctypes.data, len(buf), C.byref(n), C.byref(step)))
+        return buf[:min(n.value, len(buf))].copy(), step.value
+
+    def sync(self):
+        self._chk(self.L.ad2_sync(self.h))
+
+
+def run_schedule(ctx: Context, T: int, tau: int):
+    """Alg. 4's schedule (reading X6): step(tau); update_support() per full tau block."""
+    done = 0
+    while done < T:
+        n = min(tau, T - done)
+        ctx.step(n)
+        done += n
+        if n == tau:
+            ctx.update_support()

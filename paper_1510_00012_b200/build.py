@@ -1,0 +1,60 @@
+"""Build libad2.so (the CUDA path) in-tree for sm_100a.
+
+    python -m paper_1510_00012_b200.build        # nvcc -gencode arch=compute_100a,code=sm_100a
+
+The .so is written next to this file so it travels with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SO = os.path.join(HERE, "libad2.so")
+CSRC = os.path.join(HERE, "csrc")
+SRCS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+DEPS = SRCS + [os.path.join(CSRC, "ad2_kernels.cuh"), os.path.join(ROOT, "include", "ad2.h")]
+OBJ_DIR = os.path.join(ROOT, "build", "obj")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "128"]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc each translation unit for sm_100a (in parallel), then link libad2.so."""
+    if not (force or needs_build()):
+        return SO
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = [os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o") for src in SRCS]
+
+    def cc(pair):
+        src, obj = pair
+        cmd = [NVCC] + CFLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", obj, src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        return r.stderr
+
+    with ThreadPoolExecutor(max_workers=min(len(SRCS), os.cpu_count() or 4)) as ex:
+        logs = list(ex.map(cc, zip(SRCS, objs)))
+    if verbose:
+        print("".join(logs))
+    tmp = SO + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"])
+    os.replace(tmp, SO)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

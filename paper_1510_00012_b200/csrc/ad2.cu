@@ -1,0 +1,847 @@
+// ad2.cu — libad2: C ABI (include/ad2.h) over the sm_100a kernels in ad2_kernels.cuh.
+// Modified B-ADMM barycenter update of AD2-clustering (arXiv 1510.00012, Alg. 4).
+//
+// Host responsibilities only: argument checks, the cluster sort of the member shard (a stable
+// counting sort, so each cluster's members are contiguous and every reduction has a fixed
+// order), work-item tables, device buffers, CUDA-graph capture of a step, NCCL all-reduce of
+// the per-cluster partial sums.  Every arithmetic step of the method runs in the kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ad2.h"
+#include "ad2_kernels.cuh"
+
+using namespace ad2k;
+
+// ------------------------------------------------------------------------------------------
+// NCCL, resolved at run time (the library loads on hosts without NCCL; torch's bundled
+// libnccl.so.2 is reused when already loaded into the process).
+// ------------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+  return g_nccl.ok;
+}
+
+// growable device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+      cap = 0;
+    }
+    size_t b = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) cap = b;
+    return e;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t nodes = 0;
+  std::vector<cudaEvent_t> ev;   // profiling: [start, end] per iteration-kernel launch
+  ~StepGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+}  // namespace
+
+struct ad2_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;     // caller's stream (all work is ordered on it)
+  cudaStream_t cap = nullptr;        // private stream used only for graph capture
+  std::string msg;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // round shape
+  int state = 0;                     // 0 created, 1 initialised, 2 stepped (P/Q/x-partials valid)
+  ad2_dtype dtype = AD2_F32;
+  int d = 0, m = 0, K = 0, rule = 0;
+  double rho0 = 2.0, eps = 1e-16;
+  int64_t N = 0, n = 0, n_items = 0;
+  int variant = 0, mp = 0, nch = 0, dp = 0;
+  size_t es = 4;                     // element size
+
+  // host tables
+  std::vector<int32_t> order;        // sorted position -> caller member index
+  std::vector<int64_t> pos_of;       // caller member index -> sorted position
+  std::vector<int64_t> h_off;        // sorted offsets [N+1]
+  std::vector<int64_t> h_orig_off;   // caller offsets [N+1]
+  std::vector<int64_t> h_item_mb, h_cl_item;
+  std::vector<int32_t> h_item_cl;
+  std::vector<double> h_rho;
+  std::vector<double> h_nmem;        // global members per cluster
+
+  // device buffers
+  DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm;
+  DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
+  DBuf stage_off, stage_Y, stage_W, stage_lab, tmp_out;
+
+  std::map<int, StepGraph*> graphs;
+  bool prof = false;
+  StepGraph* last_graph = nullptr;
+  int64_t launches = 0;
+
+  ~ad2_ctx_s() {
+    clear_graphs();
+    if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
+    if (cap) cudaStreamDestroy(cap);
+  }
+  void clear_graphs() {
+    for (auto& kv : graphs) delete kv.second;
+    graphs.clear();
+    last_graph = nullptr;
+  }
+  ad2_status fail(ad2_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    msg = buf;
+    return s;
+  }
+};
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return ctx->fail(e_ == cudaErrorMemoryAllocation ? AD2_ERR_OOM : AD2_ERR_CUDA,          \
+                       "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define CHK(call)                         \
+  do {                                    \
+    ad2_status s_ = (call);               \
+    if (s_ != AD2_OK) return s_;          \
+  } while (0)
+
+static ad2_status launch_check(ad2_ctx ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx->fail(AD2_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  ctx->launches++;
+  return AD2_OK;
+}
+
+static ad2_status allreduce(ad2_ctx ctx, void* buf, size_t count, ncclDataType_t dt, cudaStream_t s) {
+  if (!ctx->comm) return AD2_OK;
+  ncclResult_t r = g_nccl.AllReduce(buf, buf, count, dt, ncclSum, ctx->comm, s);
+  if (r != ncclSuccess)
+    return ctx->fail(AD2_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+  return AD2_OK;
+}
+
+static ncclDataType_t nccl_t(ad2_ctx ctx) { return ctx->dtype == AD2_F64 ? ncclFloat64 : ncclFloat32; }
+
+// ------------------------------------------------------------------------------------------
+// kernel dispatch
+// ------------------------------------------------------------------------------------------
+template <typename T>
+static IterArgs<T> iter_args(ad2_ctx ctx) {
+  IterArgs<T> a;
+  a.off = ctx->d_off.as<int64_t>();
+  a.item_mb = ctx->d_item_mb.as<int64_t>();
+  a.item_cl = ctx->d_item_cl.as<int32_t>();
+  a.Y = ctx->Y.as<T>();
+  a.om = ctx->om.as<T>();
+  a.P = ctx->P.as<T>();
+  a.Q = ctx->Q.as<T>();
+  a.L = ctx->L.as<T>();
+  a.Cc = ctx->Cc.as<T>();
+  a.w = ctx->w.as<T>();
+  a.rho = ctx->rho.as<T>();
+  a.kx = ctx->kx.as<T>();
+  a.pw = ctx->pw.as<T>();
+  a.px = ctx->px.as<T>();
+  a.err = ctx->d_err.as<int>();
+  a.m = ctx->m;
+  a.d = ctx->d;
+  a.rule = ctx->rule;
+  a.eps = (T)ctx->eps;
+  return a;
+}
+
+// fused-kernel launchers live in inst_<dtype>_mp<MP>.cu (compiled in parallel)
+template <typename T, int MP>
+void launch_warp(int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
+
+template <typename T>
+static void launch_iter_T(ad2_ctx ctx, int mode, cudaStream_t s) {
+  IterArgs<T> a = iter_args<T>(ctx);
+  if (ctx->n_items == 0) return;
+  if (ctx->variant == 1) {
+    if (ctx->mp == 8) launch_warp<T, 8>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+    else if (ctx->mp == 16) launch_warp<T, 16>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+    else launch_warp<T, 32>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+  } else {
+    dim3 g((unsigned)((ctx->n_items + 127) / 128)), b(128);
+    T* scr = ctx->scr.as<T>();
+    if (mode == P1ONLY) k_badmm_generic<T, P1ONLY><<<g, b, 0, s>>>(a, scr, ctx->n_items);
+    else if (mode == FUSED) k_badmm_generic<T, FUSED><<<g, b, 0, s>>>(a, scr, ctx->n_items);
+    else k_badmm_generic<T, P2ONLY><<<g, b, 0, s>>>(a, scr, ctx->n_items);
+  }
+}
+
+static ad2_status launch_iter(ad2_ctx ctx, int mode, cudaStream_t s) {
+  if (ctx->dtype == AD2_F64) launch_iter_T<double>(ctx, mode, s);
+  else launch_iter_T<float>(ctx, mode, s);
+  if (ctx->n_items == 0) return AD2_OK;
+  return launch_check(ctx, "k_badmm");
+}
+
+// consensus w: per-cluster sum of item partials, all-reduce across ranks, finalise R1/R2
+template <typename T>
+static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
+  const bool fin = ctx->comm == nullptr;
+  const size_t sh = sizeof(T) * (size_t)ctx->m;
+  k_wsum<T><<<ctx->K, 128, sh, s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->Sw.as<T>(),
+                                    ctx->w.as<T>(), ctx->rule, fin ? 1 : 0, ctx->d_err.as<int>());
+  CHK(launch_check(ctx, "k_wsum"));
+  if (!fin) {
+    CHK(allreduce(ctx, ctx->Sw.p, (size_t)ctx->K * ctx->m, nccl_t(ctx), s));
+    k_wfinal<T><<<ctx->K, 128, sh, s>>>(ctx->Sw.as<T>(), ctx->w.as<T>(), ctx->m, ctx->rule, ctx->d_err.as<int>());
+    CHK(launch_check(ctx, "k_wfinal"));
+  }
+  return AD2_OK;
+}
+
+static ad2_status consensus(ad2_ctx ctx, cudaStream_t s) {
+  return ctx->dtype == AD2_F64 ? consensus_T<double>(ctx, s) : consensus_T<float>(ctx, s);
+}
+
+template <typename T>
+static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
+  if (ctx->n_items > 0) {
+    k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+        ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
+        ctx->x.as<T>(), ctx->Cc.as<T>(), with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d);
+    CHK(launch_check(ctx, "k_cost"));
+  }
+  return AD2_OK;
+}
+
+static ad2_status build_cost(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
+  return ctx->dtype == AD2_F64 ? build_cost_T<double>(ctx, with_sum, s) : build_cost_T<float>(ctx, with_sum, s);
+}
+
+static ad2_status cluster_dsum(ad2_ctx ctx, cudaStream_t s) {
+  k_dsum_cl<<<(ctx->K + 127) / 128, 128, 0, s>>>(ctx->pd.as<double>(), ctx->d_cl_item.as<int64_t>(),
+                                                  ctx->Sd.as<double>(), ctx->K);
+  CHK(launch_check(ctx, "k_dsum_cl"));
+  return allreduce(ctx, ctx->Sd.p, (size_t)ctx->K, ncclFloat64, s);
+}
+
+static ad2_status read_err(ad2_ctx ctx) {
+  int h = 0;
+  CU(cudaMemcpyAsync(&h, ctx->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (h & ERR_WEIGHTS) return ctx->fail(AD2_ERR_ARG, "member weights off the simplex (|sum-1| > tol)");
+  if (h & ERR_NONFINITE) return ctx->fail(AD2_ERR_NONFINITE, "non-finite plan row mass or weight");
+  return AD2_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// ABI
+// ------------------------------------------------------------------------------------------
+// ABI functions: C linkage comes from their declarations in ad2.h
+
+const char* ad2_status_string(ad2_status s) {
+  switch (s) {
+    case AD2_OK: return "ok";
+    case AD2_ERR_ARG: return "invalid argument";
+    case AD2_ERR_OOM: return "out of device memory";
+    case AD2_ERR_CUDA: return "CUDA error";
+    case AD2_ERR_NCCL: return "NCCL error";
+    case AD2_ERR_NONFINITE: return "non-finite value";
+    case AD2_ERR_ZERO_RHO: return "rho is zero (all costs zero in a cluster)";
+    case AD2_ERR_EMPTY: return "empty cluster";
+    case AD2_ERR_STATE: return "call out of order";
+  }
+  return "unknown";
+}
+
+const char* ad2_last_error(ad2_ctx ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
+
+
+static ad2_status set_dev(ad2_ctx ctx) {
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return ctx->fail(AD2_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return AD2_OK;
+}
+
+ad2_status ad2_create(ad2_ctx* out, int cuda_device, void* cuda_stream) {
+  if (!out) return AD2_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return AD2_ERR_CUDA;
+  }
+  if (cuda_device < 0 || cuda_device >= ndev) return AD2_ERR_ARG;
+  ad2_ctx ctx = new (std::nothrow) ad2_ctx_s();
+  if (!ctx) return AD2_ERR_OOM;
+  ctx->device = cuda_device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  if (cudaSetDevice(cuda_device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking) != cudaSuccess ||
+      ctx->d_err.reserve(4 * sizeof(int)) != cudaSuccess ||
+      cudaMemset(ctx->d_err.p, 0, 4 * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return AD2_ERR_CUDA;
+  }
+  *out = ctx;
+  return AD2_OK;
+}
+
+void ad2_destroy(ad2_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  else cudaDeviceSynchronize();
+  delete ctx;
+}
+
+ad2_status ad2_nccl_unique_id(void* id_out) {
+  if (!id_out) return AD2_ERR_ARG;
+  if (!nccl_load()) return AD2_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return AD2_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id_out, &id, sizeof id);
+  return AD2_OK;
+}
+
+ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void* unique_id) {
+  if (!ctx || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return AD2_ERR_ARG;
+  if (ctx->comm) return ctx->fail(AD2_ERR_STATE, "NCCL communicator already attached");
+  if (!nccl_load()) return ctx->fail(AD2_ERR_NCCL, "libnccl.so.2 not loadable");
+  CHK(set_dev(ctx));
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof id);
+  ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return ctx->fail(AD2_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+  }
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->clear_graphs();
+  return AD2_OK;
+}
+
+template <typename T>
+static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, double wtol) {
+  if (ctx->N == 0) return;
+  k_gather<T><<<(unsigned)((ctx->N + 3) / 4), 128, 0, ctx->stream>>>(
+      ctx->d_order.as<int32_t>(), ctx->d_orig_off.as<int64_t>(), ctx->d_off.as<int64_t>(), (const T*)Ysrc,
+      (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, wtol, ctx->d_err.as<int>());
+}
+
+template <typename T>
+static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
+  if (ctx->n_items == 0) return;
+  k_init_plans<T><<<(unsigned)ctx->n_items, 128, 0, ctx->stream>>>(
+      ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
+      warm ? ctx->d_warm.as<int64_t>() : nullptr, ctx->om.as<T>(), ctx->w.as<T>(), ctx->Q.as<T>(), dst,
+      ctx->L.as<T>(), ctx->m);
+}
+
+ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
+                               const void* w0, const uint8_t* warm_mask, double* rho_out) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!b || !prm || !x0 || !w0) return ctx->fail(AD2_ERR_ARG, "null batch/params/x0/w0");
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
+  if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
+  if (b->d < 1 || b->m < 1 || b->K < 1 || b->n_members < 0 || b->n_members > INT32_MAX)
+    return ctx->fail(AD2_ERR_ARG, "shape d=%d m=%d K=%d N=%lld", b->d, b->m, b->K, (long long)b->n_members);
+  if (b->n_members > 0 && (!b->offsets || !b->supports || !b->weights || !b->labels))
+    return ctx->fail(AD2_ERR_ARG, "null batch array");
+  if (!(prm->rho0 > 0.0) || !std::isfinite(prm->rho0) || !(prm->eps >= 0.0) || !std::isfinite(prm->eps) ||
+      (prm->rule != AD2_R1 && prm->rule != AD2_R2) || prm->cost_mode != 0)
+    return ctx->fail(AD2_ERR_ARG, "params rho0=%g eps=%g rule=%d cost_mode=%d", prm->rho0, prm->eps, prm->rule,
+                     prm->cost_mode);
+  CHK(set_dev(ctx));
+  const int64_t N = b->n_members;
+  const int d = b->d, m = b->m, K = b->K;
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  const bool host = b->mem == AD2_HOST;
+  const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+
+  // ---- host copies of the ragged index arrays; validation before any state changes
+  std::vector<int64_t> off(N + 1, 0);
+  std::vector<int32_t> lab(N);
+  if (N > 0) {
+    CU(cudaMemcpyAsync(off.data(), b->offsets, sizeof(int64_t) * (N + 1), host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(lab.data(), b->labels, sizeof(int32_t) * N, host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  if (off[0] != 0) return ctx->fail(AD2_ERR_ARG, "offsets[0] != 0");
+  int64_t mkmax = 0;
+  for (int64_t k = 0; k < N; ++k) {
+    const int64_t mk = off[k + 1] - off[k];
+    if (mk < 1) return ctx->fail(AD2_ERR_ARG, "member %lld has m_k=%lld < 1", (long long)k, (long long)mk);
+    if (lab[k] < 0 || lab[k] >= K) return ctx->fail(AD2_ERR_ARG, "label %d of member %lld out of [0,%d)", lab[k], (long long)k, K);
+    mkmax = std::max(mkmax, mk);
+  }
+  const int64_t n = off[N];
+  std::vector<int64_t> warm_src;
+  const bool warm = warm_mask != nullptr && N > 0;
+  if (warm) {
+    bool any = false;
+    for (int64_t k = 0; k < N; ++k) any |= warm_mask[k] != 0;
+    if (any && (ctx->state < 1 || ctx->dtype != b->dtype || ctx->m != m))
+      return ctx->fail(AD2_ERR_ARG, "warm start without a compatible previous round");
+    warm_src.assign(N, -1);
+    for (int64_t k = 0; k < N; ++k) {
+      if (!warm_mask[k]) continue;
+      if (k >= ctx->N) return ctx->fail(AD2_ERR_ARG, "warm member %lld not in previous round", (long long)k);
+      const int64_t ps = ctx->pos_of[k];
+      const int64_t omk = ctx->h_off[ps + 1] - ctx->h_off[ps];
+      if (omk != off[k + 1] - off[k]) return ctx->fail(AD2_ERR_ARG, "warm member %lld changed m_k", (long long)k);
+      warm_src[k] = (int64_t)m * ctx->h_off[ps];   // indexed by caller member; remapped below
+    }
+  }
+
+  // ---- stable counting sort by cluster -> contiguous clusters, fixed reduction order
+  std::vector<int64_t> cnt(K + 1, 0), npts_local(K, 0);
+  for (int64_t k = 0; k < N; ++k) {
+    cnt[lab[k] + 1]++;
+    npts_local[lab[k]] += off[k + 1] - off[k];
+  }
+  for (int c = 0; c < K; ++c) cnt[c + 1] += cnt[c];
+  std::vector<int64_t> cstart(cnt.begin(), cnt.end());
+  std::vector<int32_t> order(N);
+  std::vector<int64_t> pos_of(N);
+  {
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t k = 0; k < N; ++k) {
+      const int64_t s = fill[lab[k]]++;
+      order[s] = (int32_t)k;
+      pos_of[k] = s;
+    }
+  }
+  std::vector<int64_t> soff(N + 1, 0);
+  for (int64_t s = 0; s < N; ++s) soff[s + 1] = soff[s] + (off[order[s] + 1] - off[order[s]]);
+  std::vector<int64_t> warm_sorted;
+  if (warm) {
+    warm_sorted.resize(N);
+    for (int64_t s = 0; s < N; ++s) warm_sorted[s] = warm_src[order[s]];
+  }
+
+  // ---- kernel variant
+  int variant = 0, mp = 0, nch = 0, dp = 0;
+  const int dmax = b->dtype == AD2_F64 ? 16 : 64;
+  for (int cand : {8, 16, 32}) {
+    if (m <= cand && mkmax <= (cand == 32 ? 32 : 2 * cand) && d <= dmax) {
+      variant = 1;
+      mp = cand;
+      nch = mkmax <= cand ? 1 : 2;
+      dp = d <= 4 ? 4 : (d <= 16 ? 16 : 64);
+      break;
+    }
+  }
+  const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * ITEM_PASSES : 1;
+  std::vector<int64_t> item_mb, cl_item(K + 1, 0);
+  std::vector<int32_t> item_cl;
+  for (int c = 0; c < K; ++c) {
+    cl_item[c] = (int64_t)item_cl.size();
+    for (int64_t s = cstart[c]; s < cstart[c + 1]; s += per_item) {
+      item_mb.push_back(s);
+      item_cl.push_back(c);
+    }
+  }
+  cl_item[K] = (int64_t)item_cl.size();
+  item_mb.push_back(N);
+  const int64_t n_items = (int64_t)item_cl.size();
+
+  // ---- device buffers
+  const size_t E = (size_t)m * (size_t)n;
+  CU(ctx->Y.reserve(es * (size_t)n * d));
+  CU(ctx->om.reserve(es * (size_t)n));
+  CU(ctx->P.reserve(es * E));
+  CU(ctx->L.reserve(es * E));
+  CU(ctx->Cc.reserve(es * E));
+  if (!warm) CU(ctx->Q.reserve(es * E));
+  CU(ctx->x.reserve(es * (size_t)K * m * d));
+  CU(ctx->w.reserve(es * (size_t)K * m));
+  CU(ctx->rho.reserve(es * K));
+  CU(ctx->kx.reserve(es * K));
+  CU(ctx->rho_d.reserve(8 * (size_t)K));
+  CU(ctx->pw.reserve(es * (size_t)n_items * m));
+  CU(ctx->px.reserve(es * (size_t)n_items * m * (d + 1)));
+  CU(ctx->Sw.reserve(es * (size_t)K * m));
+  CU(ctx->Sx.reserve(es * (size_t)K * m * (d + 1)));
+  CU(ctx->pd.reserve(8 * (size_t)n_items));
+  CU(ctx->Sd.reserve(8 * (size_t)K));
+  CU(ctx->npts.reserve(8 * (size_t)K * 2));
+  if (variant == 0) CU(ctx->scr.reserve(es * (size_t)n_items * 2 * m));
+  CU(ctx->d_order.reserve(sizeof(int32_t) * N));
+  CU(ctx->d_off.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->d_orig_off.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
+  CU(ctx->d_item_cl.reserve(sizeof(int32_t) * n_items));
+  CU(ctx->d_cl_item.reserve(sizeof(int64_t) * (K + 1)));
+  if (warm) CU(ctx->d_warm.reserve(sizeof(int64_t) * N));
+  ctx->clear_graphs();
+
+  // ---- commit the new round shape
+  ctx->dtype = b->dtype;
+  ctx->es = es;
+  ctx->d = d;
+  ctx->m = m;
+  ctx->K = K;
+  ctx->rule = prm->rule;
+  ctx->rho0 = prm->rho0;
+  ctx->eps = prm->eps;
+  ctx->N = N;
+  ctx->n = n;
+  ctx->n_items = n_items;
+  ctx->variant = variant;
+  ctx->mp = mp;
+  ctx->nch = nch;
+  ctx->dp = dp;
+  ctx->order.swap(order);
+  ctx->pos_of.swap(pos_of);
+  ctx->h_off.swap(soff);
+  ctx->h_orig_off.swap(off);
+  ctx->h_item_mb.swap(item_mb);
+  ctx->h_item_cl.swap(item_cl);
+  ctx->h_cl_item.swap(cl_item);
+  ctx->state = 0;
+  cudaStream_t s = ctx->stream;
+
+  CU(cudaMemsetAsync(ctx->d_err.p, 0, 4 * sizeof(int), s));
+  if (N > 0) {
+    CU(cudaMemcpyAsync(ctx->d_order.p, ctx->order.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->d_off.p, ctx->h_off.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->d_orig_off.p, ctx->h_orig_off.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    if (warm) CU(cudaMemcpyAsync(ctx->d_warm.p, warm_sorted.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemcpyAsync(ctx->d_item_mb.p, ctx->h_item_mb.data(), sizeof(int64_t) * (n_items + 1), cudaMemcpyHostToDevice, s));
+  if (n_items > 0)
+    CU(cudaMemcpyAsync(ctx->d_item_cl.p, ctx->h_item_cl.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(ctx->d_cl_item.p, ctx->h_cl_item.data(), sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, s));
+
+  // ---- member data into the sorted layout
+  const void* Ysrc = b->supports;
+  const void* Wsrc = b->weights;
+  if (host && N > 0) {
+    CU(ctx->stage_Y.reserve(es * (size_t)n * d));
+    CU(ctx->stage_W.reserve(es * (size_t)n));
+    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+    Ysrc = ctx->stage_Y.p;
+    Wsrc = ctx->stage_W.p;
+  }
+  const double wtol = b->dtype == AD2_F64 ? 1e-6 : 1e-5;
+  if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
+  else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
+  if (N > 0) CHK(launch_check(ctx, "k_gather"));
+  CU(cudaMemcpyAsync(ctx->x.p, x0, es * (size_t)K * m * d, h2d, s));
+  CU(cudaMemcpyAsync(ctx->w.p, w0, es * (size_t)K * m, h2d, s));
+
+  // ---- Pi^(2),0 and Lambda = 0 (warm: new Pi2 built in P from the old Q, then swapped)
+  if (warm) {
+    if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, true, ctx->P.as<double>());
+    else launch_init_plans<float>(ctx, true, ctx->P.as<float>());
+    if (n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
+    std::swap(ctx->P.p, ctx->Q.p);
+    std::swap(ctx->P.cap, ctx->Q.cap);
+    CU(ctx->P.reserve(es * E));
+  } else {
+    if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
+    else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());
+    if (n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
+  }
+
+  // ---- global member / point counts per cluster (EMPTY check, rho denominator, 1/N_c)
+  std::vector<double> cnts(2 * (size_t)K);
+  for (int c = 0; c < K; ++c) {
+    cnts[c] = (double)(cstart[c + 1] - cstart[c]);
+    cnts[K + c] = (double)npts_local[c];
+  }
+  CU(cudaMemcpyAsync(ctx->npts.p, cnts.data(), sizeof(double) * 2 * K, cudaMemcpyHostToDevice, s));
+  CHK(allreduce(ctx, ctx->npts.p, 2 * (size_t)K, ncclFloat64, s));
+  CU(cudaMemcpyAsync(cnts.data(), ctx->npts.p, sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  ctx->h_nmem.assign(cnts.begin(), cnts.begin() + K);
+  for (int c = 0; c < K; ++c)
+    if (cnts[c] == 0.0) return ctx->fail(AD2_ERR_EMPTY, "cluster %d has no members", c);
+
+  // ---- C and rho (Eq.rho, X1/X2)
+  CHK(build_cost(ctx, true, s));
+  CHK(cluster_dsum(ctx, s));
+  if (b->dtype == AD2_F64)
+    k_rho<double><<<(K + 127) / 128, 128, 0, s>>>(ctx->Sd.as<double>(), ctx->npts.as<double>() + K, K, m, prm->rho0,
+                                                 ctx->rho.as<double>(), ctx->kx.as<double>(), ctx->rho_d.as<double>());
+  else
+    k_rho<float><<<(K + 127) / 128, 128, 0, s>>>(ctx->Sd.as<double>(), ctx->npts.as<double>() + K, K, m, prm->rho0,
+                                                ctx->rho.as<float>(), ctx->kx.as<float>(), ctx->rho_d.as<double>());
+  CHK(launch_check(ctx, "k_rho"));
+  ctx->h_rho.assign(K, 0.0);
+  CU(cudaMemcpyAsync(ctx->h_rho.data(), ctx->rho_d.p, sizeof(double) * K, cudaMemcpyDeviceToHost, s));
+  CHK(read_err(ctx));
+  for (int c = 0; c < K; ++c)
+    if (!(ctx->h_rho[c] > 0.0) || !std::isfinite(ctx->h_rho[c]))
+      return ctx->fail(AD2_ERR_ZERO_RHO, "cluster %d: rho = %g", c, ctx->h_rho[c]);
+  if (rho_out) memcpy(rho_out, ctx->h_rho.data(), sizeof(double) * K);
+  ctx->state = 1;
+  return AD2_OK;
+}
+
+// one step = n iterations of Alg. 4 at fixed x, captured once per n into a CUDA graph
+static ad2_status capture_step(ad2_ctx ctx, int n, StepGraph** out) {
+  StepGraph* g = new StepGraph();
+  cudaStream_t s = ctx->cap;
+  const int64_t l0 = ctx->launches;
+  if (ctx->prof) {
+    g->ev.resize(2 * (size_t)n + 2);
+    for (auto& e : g->ev) CU(cudaEventCreate(&e));
+  }
+  CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  ad2_status st = AD2_OK;
+  for (int t = 0; t <= n && st == AD2_OK; ++t) {
+    const int mode = t == 0 ? P1ONLY : (t == n ? P2ONLY : FUSED);
+    if (ctx->prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
+    st = launch_iter(ctx, mode, s);
+    if (ctx->prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
+    if (st == AD2_OK && t < n) st = consensus(ctx, s);
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (st != AD2_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    delete g;
+    return st;
+  }
+  if (e != cudaSuccess) {
+    delete g;
+    return ctx->fail(AD2_ERR_CUDA, "capture: %s", cudaGetErrorString(e));
+  }
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    delete g;
+    return ctx->fail(AD2_ERR_CUDA, "instantiate: %s", cudaGetErrorString(e));
+  }
+  g->nodes = ctx->launches - l0;
+  ctx->launches = l0;
+  *out = g;
+  return AD2_OK;
+}
+
+ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (n_iters < 0) return ctx->fail(AD2_ERR_ARG, "n_iters < 0");
+  if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "step before init");
+  if (n_iters == 0) return AD2_OK;
+  CHK(set_dev(ctx));
+  auto it = ctx->graphs.find(n_iters);
+  StepGraph* g = nullptr;
+  if (it == ctx->graphs.end()) {
+    CHK(capture_step(ctx, n_iters, &g));
+    ctx->graphs[n_iters] = g;
+  } else {
+    g = it->second;
+  }
+  CU(cudaGraphLaunch(g->exec, ctx->stream));
+  ctx->launches += g->nodes;
+  ctx->last_graph = g;
+  ctx->state = 2;
+  return AD2_OK;
+}
+
+template <typename T>
+static ad2_status update_support_T(ad2_ctx ctx) {
+  cudaStream_t s = ctx->stream;
+  k_xsum<T><<<ctx->K, 128, 0, s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->d, ctx->Sx.as<T>());
+  CHK(launch_check(ctx, "k_xsum"));
+  CHK(allreduce(ctx, ctx->Sx.p, (size_t)ctx->K * ctx->m * (ctx->d + 1), nccl_t(ctx), s));
+  k_xfinal<T><<<ctx->K, 128, 0, s>>>(ctx->Sx.as<T>(), ctx->w.as<T>(), ctx->x.as<T>(), ctx->m, ctx->d);
+  CHK(launch_check(ctx, "k_xfinal"));
+  return build_cost(ctx, false, s);
+}
+
+ad2_status ad2_update_support(ad2_ctx ctx) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "update_support needs a step since init (X6)");
+  CHK(set_dev(ctx));
+  return ctx->dtype == AD2_F64 ? update_support_T<double>(ctx) : update_support_T<float>(ctx);
+}
+
+ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
+  if (!ctx || !obj_out) return ctx ? ctx->fail(AD2_ERR_ARG, "null obj_out") : AD2_ERR_ARG;
+  if (ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "objective needs a step since init");
+  CHK(set_dev(ctx));
+  cudaStream_t s = ctx->stream;
+  if (ctx->n_items > 0) {
+    if (ctx->dtype == AD2_F64)
+      k_objective<double><<<(unsigned)ctx->n_items, 128, 0, s>>>(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(),
+                                                                  ctx->Cc.as<double>(), ctx->P.as<double>(), ctx->pd.as<double>(), ctx->m);
+    else
+      k_objective<float><<<(unsigned)ctx->n_items, 128, 0, s>>>(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(),
+                                                                 ctx->Cc.as<float>(), ctx->P.as<float>(), ctx->pd.as<double>(), ctx->m);
+    CHK(launch_check(ctx, "k_objective"));
+  }
+  CHK(cluster_dsum(ctx, s));
+  std::vector<double> S(ctx->K);
+  CU(cudaMemcpyAsync(S.data(), ctx->Sd.p, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, s));
+  CHK(read_err(ctx));
+  for (int c = 0; c < ctx->K; ++c) obj_out[c] = S[c] / ctx->h_nmem[c];
+  return AD2_OK;
+}
+
+ad2_status ad2_get_centroids(ad2_ctx ctx, void* x, void* w, ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
+  CHK(set_dev(ctx));
+  const cudaMemcpyKind kind = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (x) CU(cudaMemcpyAsync(x, ctx->x.p, ctx->es * (size_t)ctx->K * ctx->m * ctx->d, kind, ctx->stream));
+  if (w) CU(cudaMemcpyAsync(w, ctx->w.p, ctx->es * (size_t)ctx->K * ctx->m, kind, ctx->stream));
+  if (where == AD2_HOST) return read_err(ctx);
+  return AD2_OK;
+}
+
+ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!out || which < 0 || which > 3) return ctx->fail(AD2_ERR_ARG, "get_plans args");
+  if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
+  if (which == AD2_PI1 && ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "Pi1 exists after a step");
+  CHK(set_dev(ctx));
+  const DBuf* src = which == AD2_PI1 ? &ctx->P : which == AD2_PI2 ? &ctx->Q : which == AD2_LAMBDA ? &ctx->L : &ctx->Cc;
+  const size_t bytes = ctx->es * (size_t)ctx->m * ctx->n;
+  void* dst = out;
+  if (where == AD2_HOST) {
+    CU(ctx->tmp_out.reserve(bytes));
+    dst = ctx->tmp_out.p;
+  }
+  if (ctx->N > 0) {
+    const unsigned grid = (unsigned)((ctx->N + 3) / 4);
+    if (ctx->dtype == AD2_F64)
+      k_scatter_plans<double><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
+                                                             ctx->d_orig_off.as<int64_t>(), (const double*)src->p,
+                                                             (double*)dst, ctx->N, ctx->m);
+    else
+      k_scatter_plans<float><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
+                                                            ctx->d_orig_off.as<int64_t>(), (const float*)src->p,
+                                                            (float*)dst, ctx->N, ctx->m);
+    CHK(launch_check(ctx, "k_scatter_plans"));
+  }
+  if (where == AD2_HOST) {
+    CU(cudaMemcpyAsync(out, dst, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    return read_err(ctx);
+  }
+  return AD2_OK;
+}
+
+ad2_status ad2_get_rho(ad2_ctx ctx, double* rho_out) {
+  if (!ctx || !rho_out) return AD2_ERR_ARG;
+  if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
+  memcpy(rho_out, ctx->h_rho.data(), sizeof(double) * ctx->K);
+  return AD2_OK;
+}
+
+ad2_status ad2_get_info(ad2_ctx ctx, ad2_info* info) {
+  if (!ctx || !info) return AD2_ERR_ARG;
+  memset(info, 0, sizeof *info);
+  info->abi_version = AD2_ABI_VERSION;
+  info->dtype = ctx->dtype;
+  info->d = ctx->d;
+  info->m = ctx->m;
+  info->K = ctx->K;
+  info->n_members = ctx->N;
+  info->n_points = ctx->n;
+  info->entries = (int64_t)ctx->m * ctx->n;
+  info->n_items = ctx->n_items;
+  info->variant = ctx->variant;
+  info->mp = ctx->mp;
+  info->nch = ctx->nch;
+  info->nranks = ctx->nranks;
+  info->rank = ctx->rank;
+  info->launches = ctx->launches;
+  const DBuf* all[] = {&ctx->Y, &ctx->om, &ctx->P, &ctx->Q, &ctx->L, &ctx->Cc, &ctx->x, &ctx->w, &ctx->pw,
+                       &ctx->px, &ctx->Sw, &ctx->Sx, &ctx->pd, &ctx->scr, &ctx->stage_Y, &ctx->stage_W, &ctx->tmp_out};
+  for (auto p : all) info->state_bytes += (int64_t)p->cap;
+  return AD2_OK;
+}
+
+ad2_status ad2_set_profiling(ad2_ctx ctx, int enable) {
+  if (!ctx) return AD2_ERR_ARG;
+  if ((enable != 0) != ctx->prof) {
+    ctx->prof = enable != 0;
+    ctx->clear_graphs();
+  }
+  return AD2_OK;
+}
+
+ad2_status ad2_prof_read(ad2_ctx ctx, double* launch_ms, int64_t capacity, int64_t* n_launches,
+                         double* step_ms) {
+  if (!ctx) return AD2_ERR_ARG;
+  StepGraph* g = ctx->last_graph;
+  if (!g || g->ev.empty()) return ctx->fail(AD2_ERR_STATE, "no profiled step");
+  CHK(set_dev(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  const int64_t nl = (int64_t)g->ev.size() / 2;
+  for (int64_t t = 0; t < nl && t < capacity && launch_ms; ++t) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, g->ev[2 * t], g->ev[2 * t + 1]));
+    launch_ms[t] = ms;
+  }
+  float all = 0.f;
+  CU(cudaEventElapsedTime(&all, g->ev.front(), g->ev.back()));
+  if (n_launches) *n_launches = nl;
+  if (step_ms) *step_ms = all;
+  return AD2_OK;
+}
+
+ad2_status ad2_sync(ad2_ctx ctx) {
+  if (!ctx) return AD2_ERR_ARG;
+  CHK(set_dev(ctx));
+  return read_err(ctx);
+}

@@ -1,0 +1,576 @@
+// ad2_kernels.cuh — sm_100a kernels of the modified B-ADMM barycenter path (arXiv 1510.00012,
+// Alg. 4).  "P:n" = PAPER.md line n.  Included only by ad2.cu.
+//
+// Device layout: members are sorted by cluster; member s owns
+// the contiguous column-major m x m_s block [m*off[s], m*off[s+1]) of every plan-shaped array
+// (Pi^(1) in P, Pi^(2) in Q, Lambda in L, cost C in Cc): entry (i, j) at m*off[s] + j*m + i.
+// This is the paper's Pi in R^{m x n} with column j = member support point j.
+//
+// Iteration kernels run per work item = a run of consecutive members of ONE cluster; each item
+// writes its own partial sums (no float atomics), and the cluster reduction kernels add the
+// items of a cluster in item order, so every result is deterministic.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace ad2k {
+
+enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2 };
+enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2 };
+
+constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels
+constexpr int ITEM_PASSES = 8;    // member passes per warp per work item
+
+// exp(v) is evaluated as ex(v * kx): kx = log2(e)/rho with MUFU ex2.approx for fp32,
+// kx = 1/rho with the IEEE double exp for fp64 (fp64 has no MUFU path).
+template <typename T> struct Num;
+template <> struct Num<float> {
+  static __device__ __forceinline__ float ex(float a) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+  }
+  static __device__ __forceinline__ float ld(const float* p) { return __ldcs(p); }
+  static __device__ __forceinline__ void st(float* p, float v) { __stcs(p, v); }
+};
+template <> struct Num<double> {
+  static __device__ __forceinline__ double ex(double a) { return exp(a); }
+  static __device__ __forceinline__ double ld(const double* p) { return __ldcs(p); }
+  static __device__ __forceinline__ void st(double* p, double v) { __stcs(p, v); }
+};
+
+template <typename T>
+struct IterArgs {
+  const int64_t* off;      // [N+1] sorted member point offsets
+  const int64_t* item_mb;  // [n_items+1] first sorted member of each item
+  const int32_t* item_cl;  // [n_items] cluster of each item
+  const T* Y;              // [n][d] supports, sorted
+  const T* om;             // [n] member weights w^(k)_j, renormalised
+  T* P;                    // Pi^(1)
+  T* Q;                    // Pi^(2)
+  T* L;                    // Lambda
+  const T* Cc;             // cost C
+  const T* w;              // [K][m] consensus weights
+  const T* rho;            // [K]
+  const T* kx;             // [K] exponent scale (see Num)
+  T* pw;                   // [n_items][m]   partial sum over members of wt (R1) or sqrt(wt) (R2)
+  T* px;                   // [n_items][m][d+1] partial sums of pi2_ij y_j and pi2_ij
+  int* err;
+  int m, d, rule;
+  T eps;
+};
+
+// ---------------------------------------------------------------------------------------------
+// Fused warp-per-member iteration kernel.  One warp holds G = 32/MP members at once, lane
+// (seg, i) = row i of member seg; a row lives in registers (MK = MP*NCH columns, predicated to
+// j < m_k).  Row sums are lane-local; column sums use a transpose-reduce butterfly inside the
+// MP-lane segment (MP-1 shuffles per MP columns).
+//
+//   MODE P1ONLY (first iteration of a step): Pi2 = Q, Lambda = L ->
+//            Eq.badmmc0b/c0 -> P = Pi1;  Eq.badmmc1b row masses -> pw
+//   MODE FUSED  (iterations 2..n): phase 2 of iteration t-1 (Eq.badmmc1 with the consensus w
+//            of t-1, Eq.badmm2) then phase 1 of iteration t; P, L rewritten in place.
+//            pt^(1) of t-1 is recomputed from (Pi1, Lambda^{t-2}) instead of being stored.
+//   MODE P2ONLY (end of a step): phase 2 only -> Q = Pi2, L = Lambda, and the support-update
+//            partials sum_j pi2_ij y_j, sum_j pi2_ij -> px.
+// ---------------------------------------------------------------------------------------------
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+  using type = float4;
+  static __device__ __forceinline__ float hsum(float4 v) { return ((v.x + v.y) + v.z) + v.w; }
+};
+template <> struct Vec16<double> {
+  using type = double2;
+  static __device__ __forceinline__ double hsum(double2 v) { return v.x + v.y; }
+};
+
+template <typename T, int MP, int NCH, int MODE, int DP>
+__global__ void __launch_bounds__(NWARP * 32)
+k_badmm_warp(const IterArgs<T> a) {
+  using N = Num<T>;
+  using V = typename Vec16<T>::type;
+  constexpr int G = 32 / MP;
+  constexpr int MK = MP * NCH;
+  constexpr int E = 16 / (int)sizeof(T);      // elements per 16-byte shared-memory chunk
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = lane / MP, i = lane - seg * MP;
+  const int item = blockIdx.x;
+  const int c = a.item_cl[item];
+  const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
+  const int m = a.m;
+  const bool rowok = i < m;
+  const T kx = a.kx[c];
+  const T rho = a.rho[c];
+  const T eps = a.eps;
+  const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
+  T accw = T(0);
+  T accm = T(0);
+  T accx[DP];
+#pragma unroll
+  for (int t = 0; t < DP; ++t) accx[t] = T(0);
+  bool bad = false;
+
+  for (int64_t k0 = mb + (int64_t)warp * G; k0 < me; k0 += NWARP * G) {   // warp-uniform
+    const int64_t k = k0 + seg;
+    const bool has = k < me;
+    const int64_t o0 = has ? a.off[k] : 0;
+    const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
+    const int64_t base = (int64_t)m * o0 + i;
+    T p[MK], l[MK], q[MK];
+#pragma unroll
+    for (int j = 0; j < MK; ++j) {
+      const bool ok = rowok && j < mk;
+      const int64_t e = base + (int64_t)j * m;
+      p[j] = ok ? N::ld((MODE == P1ONLY ? a.Q : a.P) + e) : T(0);
+      l[j] = ok ? N::ld(a.L + e) : T(0);
+    }
+    if constexpr (MODE == P1ONLY) {
+#pragma unroll
+      for (int j = 0; j < MK; ++j) q[j] = p[j];            // Pi2^(0)
+    } else {
+      // ---- phase 2 of the previous iteration: pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b),
+      //      Pi2 = pt1 / rowsum * w_i (Eq.badmmc1), Lambda += rho (Pi1 - Pi2) (Eq.badmm2)
+      T r = T(0);
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        q[j] = ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
+        r += q[j];
+      }
+      const T f = (has && rowok) ? wi / r : T(0);
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        q[j] = q[j] * f;
+        if (ok) l[j] = l[j] + rho * (p[j] - q[j]);
+      }
+    }
+    if constexpr (MODE == P2ONLY) {
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        const int64_t e = base + (int64_t)j * m;
+        if (ok) { N::st(a.Q + e, q[j]); N::st(a.L + e, l[j]); }
+      }
+      // support-update partials (Eq.updatex with X5): sum_j pi2_ij y_j and sum_j pi2_ij
+      const T* yk = a.Y + o0 * a.d;
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        if (j < mk) {                                      // q[j] = 0 on invalid rows
+          accm += q[j];
+#pragma unroll
+          for (int t = 0; t < DP; ++t)
+            if (t < a.d) accx[t] += q[j] * __ldg(yk + (int64_t)j * a.d + t);
+        }
+      }
+    } else {
+      // ---- phase 1: pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        const T cst = ok ? N::ld(a.Cc + base + (int64_t)j * m) : T(0);
+        p[j] = ok ? q[j] * N::ex(-(cst + l[j]) * kx) + eps : T(0);
+      }
+      // column sums over the m rows through a per-warp shared tile (row u = column u of a
+      // chunk, 16-byte chunks XOR-swizzled by u so both the scalar writes and the vector
+      // reads are bank-conflict free); lane (seg, u) sums column u of its member.
+      __shared__ __align__(16) T s_tile[NWARP][MP][32];
+      __shared__ __align__(16) T s_f[NWARP][G][MK];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < MP; ++u)
+          s_tile[warp][u][(((lane / E) ^ (u & 7)) * E) + (lane % E)] = p[ch * MP + u];
+        __syncwarp();
+        T s = T(0);
+#pragma unroll
+        for (int cc = 0; cc < MP / E; ++cc) {
+          const V v = *reinterpret_cast<const V*>(&s_tile[warp][i][((seg * (MP / E) + cc) ^ (i & 7)) * E]);
+          s += Vec16<T>::hsum(v);
+        }
+        const int jc = ch * MP + i;
+        // Eq.badmmc0: Pi1_ij = pt2_ij / colsum_j * w_j^(k)
+        s_f[warp][seg][jc] = (jc < mk) ? __ldg(a.om + o0 + jc) / s : T(0);
+      }
+      __syncwarp();
+      T r2 = T(0);
+#pragma unroll
+      for (int jj = 0; jj < MK; jj += E) {
+        const V fv = *reinterpret_cast<const V*>(&s_f[warp][seg][jj]);
+        const T* fe = reinterpret_cast<const T*>(&fv);
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+          const int j = jj + u;
+          const bool ok = rowok && j < mk;
+          p[j] = p[j] * fe[u];
+          // Eq.badmmc1b with Lambda^n (X4): pt1 = Pi1 exp(Lambda/rho) + eps; row mass
+          r2 += ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
+        }
+      }
+      T R = r2;
+#pragma unroll
+      for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
+      if (has && rowok) {
+        const T wt = r2 / R;
+        accw += (a.rule == 1) ? sqrt(wt) : wt;
+        bad |= !isfinite(wt);
+      }
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        const int64_t e = base + (int64_t)j * m;
+        if (ok) {
+          N::st(a.P + e, p[j]);
+          if (MODE == FUSED) N::st(a.L + e, l[j]);
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(a.err, ERR_NONFINITE);
+
+  // fixed-order combination of the warps' / segments' per-row accumulators -> item partial
+  if constexpr (MODE != P2ONLY) {
+    __shared__ T sw[NWARP * G][MP];
+    sw[warp * G + seg][i] = accw;
+    __syncthreads();
+    if (threadIdx.x < m) {
+      T s = T(0);
+#pragma unroll
+      for (int u = 0; u < NWARP * G; ++u) s += sw[u][threadIdx.x];
+      a.pw[(int64_t)item * m + threadIdx.x] = s;
+    }
+  } else {
+    __shared__ T sx[NWARP * G][MP][DP + 1];
+#pragma unroll
+    for (int t = 0; t < DP; ++t) sx[warp * G + seg][i][t] = accx[t];
+    sx[warp * G + seg][i][DP] = accm;
+    __syncthreads();
+    const int d = a.d;
+    for (int v = threadIdx.x; v < m * (d + 1); v += NWARP * 32) {
+      const int ii = v / (d + 1), t = v - ii * (d + 1);
+      const int tt = (t == d) ? DP : t;
+      T s = T(0);
+#pragma unroll
+      for (int u = 0; u < NWARP * G; ++u) s += sx[u][ii][tt];
+      a.px[(int64_t)item * m * (d + 1) + v] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Generic iteration kernel: any m, m_k, d.  One thread per member (work item = 1 member), state
+// in global memory, row masses in a per-member scratch [2m].  Same MODE semantics as above.
+// ---------------------------------------------------------------------------------------------
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128)
+k_badmm_generic(const IterArgs<T> a, T* __restrict__ scr, int64_t n_items) {
+  using N = Num<T>;
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const int64_t k = a.item_mb[it];                 // one member per item
+  const int c = a.item_cl[it];
+  const int m = a.m, d = a.d;
+  const int64_t o0 = a.off[k];
+  const int mk = (int)(a.off[k + 1] - o0);
+  const int64_t base = (int64_t)m * o0;
+  const T kx = a.kx[c], rho = a.rho[c], eps = a.eps;
+  const T* w = a.w + (int64_t)c * m;
+  T* r = scr + it * 2 * m;
+  T* r2 = r + m;
+  bool bad = false;
+  if (MODE != P1ONLY) {
+    for (int i = 0; i < m; ++i) {
+      T s = T(0);
+      for (int j = 0; j < mk; ++j) {
+        const int64_t e = base + (int64_t)j * m + i;
+        s += a.P[e] * N::ex(a.L[e] * kx) + eps;
+      }
+      r[i] = s;
+    }
+    if (MODE == P2ONLY) {
+      T* px = a.px + it * m * (d + 1);
+      for (int v = 0; v < m * (d + 1); ++v) px[v] = T(0);
+    }
+    for (int j = 0; j < mk; ++j)
+      for (int i = 0; i < m; ++i) {
+        const int64_t e = base + (int64_t)j * m + i;
+        const T p = a.P[e];
+        const T b = p * N::ex(a.L[e] * kx) + eps;
+        const T q = b * (w[i] / r[i]);
+        const T ln = a.L[e] + rho * (p - q);
+        a.L[e] = ln;
+        if (MODE == P2ONLY) {
+          a.Q[e] = q;
+          T* px = a.px + it * m * (d + 1) + (int64_t)i * (d + 1);
+          for (int t = 0; t < d; ++t) px[t] += q * a.Y[(o0 + j) * d + t];
+          px[d] += q;
+        } else {
+          a.P[e] = q * N::ex(-(a.Cc[e] + ln) * kx) + eps;      // pt2 stored in P for now
+        }
+      }
+    if (MODE == P2ONLY) return;
+  } else {
+    for (int j = 0; j < mk; ++j)
+      for (int i = 0; i < m; ++i) {
+        const int64_t e = base + (int64_t)j * m + i;
+        a.P[e] = a.Q[e] * N::ex(-(a.Cc[e] + a.L[e]) * kx) + eps;
+      }
+  }
+  for (int i = 0; i < m; ++i) r2[i] = T(0);
+  for (int j = 0; j < mk; ++j) {
+    T s = T(0);
+    for (int i = 0; i < m; ++i) s += a.P[base + (int64_t)j * m + i];
+    const T f = a.om[o0 + j] / s;
+    for (int i = 0; i < m; ++i) {
+      const int64_t e = base + (int64_t)j * m + i;
+      const T p = a.P[e] * f;
+      a.P[e] = p;
+      r2[i] += p * N::ex(a.L[e] * kx) + eps;
+    }
+  }
+  T R = T(0);
+  for (int i = 0; i < m; ++i) R += r2[i];
+  for (int i = 0; i < m; ++i) {
+    const T wt = r2[i] / R;
+    bad |= !isfinite(wt);
+    a.pw[it * m + i] = (a.rule == 1) ? sqrt(wt) : wt;
+  }
+  if (bad) atomicOr(a.err, ERR_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Cluster reductions (one CTA per cluster, items added in item order).
+// ---------------------------------------------------------------------------------------------
+// w consensus: S_i = sum over the cluster's items of pw; with `finalize` (single rank) also
+//   R1 (Eq.badmmw):  w_i = S_i / sum_i S_i          R2 (Eq.badmmw2): w_i = S_i^2 / sum_i S_i^2
+template <typename T>
+__global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_item, int m,
+                       T* __restrict__ S, T* __restrict__ w, int rule, int finalize, int* err) {
+  const int c = blockIdx.x;
+  const int64_t ib = cl_item[c], ie = cl_item[c + 1];
+  extern __shared__ unsigned char smraw[];
+  T* sh = reinterpret_cast<T*>(smraw);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    T s = T(0);
+    for (int64_t it = ib; it < ie; ++it) s += pw[it * m + i];
+    S[(int64_t)c * m + i] = s;
+    sh[i] = (rule == 1) ? s * s : s;
+  }
+  if (!finalize) return;
+  __syncthreads();
+  __shared__ T tot;
+  if (threadIdx.x == 0) {
+    T t = T(0);
+    for (int i = 0; i < m; ++i) t += sh[i];
+    tot = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const T v = sh[i] / tot;
+    if (!isfinite(v)) atomicOr(err, ERR_NONFINITE);
+    w[(int64_t)c * m + i] = v;
+  }
+}
+
+template <typename T>
+__global__ void k_wfinal(const T* __restrict__ S, T* __restrict__ w, int m, int rule, int* err) {
+  const int c = blockIdx.x;
+  extern __shared__ unsigned char smraw[];
+  T* sh = reinterpret_cast<T*>(smraw);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const T s = S[(int64_t)c * m + i];
+    sh[i] = (rule == 1) ? s * s : s;
+  }
+  __syncthreads();
+  __shared__ T tot;
+  if (threadIdx.x == 0) {
+    T t = T(0);
+    for (int i = 0; i < m; ++i) t += sh[i];
+    tot = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const T v = sh[i] / tot;
+    if (!isfinite(v)) atomicOr(err, ERR_NONFINITE);
+    w[(int64_t)c * m + i] = v;
+  }
+}
+
+// x partial sums -> Sx[K][m][d+1]
+template <typename T>
+__global__ void k_xsum(const T* __restrict__ px, const int64_t* __restrict__ cl_item, int m, int d,
+                       T* __restrict__ Sx) {
+  const int c = blockIdx.x;
+  const int64_t ib = cl_item[c], ie = cl_item[c + 1];
+  const int W = m * (d + 1);
+  for (int v = threadIdx.x; v < W; v += blockDim.x) {
+    T s = T(0);
+    for (int64_t it = ib; it < ie; ++it) s += px[it * W + v];
+    Sx[(int64_t)c * W + v] = s;
+  }
+}
+
+// Eq.updatex (X5, X12): x_i = sum pi2_ij y_j / sum pi2_ij unless w_i < 1e-12
+template <typename T>
+__global__ void k_xfinal(const T* __restrict__ Sx, const T* __restrict__ w, T* __restrict__ x, int m,
+                         int d) {
+  const int c = blockIdx.x;
+  for (int v = threadIdx.x; v < m * d; v += blockDim.x) {
+    const int i = v / d, t = v - i * d;
+    if (w[(int64_t)c * m + i] < T(1e-12)) continue;
+    const T* s = Sx + ((int64_t)c * m + i) * (d + 1);
+    x[((int64_t)c * m + i) * d + t] = s[t] / s[d];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Cost build C_ij = sum_t (x_it - y_jt)^2 (difference form), optional per-item double
+// sums of C for rho (Eq.rho, X1).  CTA per item, warp per member, lane per entry.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_cost(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+       const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
+       T* __restrict__ Cc, double* __restrict__ psum, int m, int d) {
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T* xc = x + (int64_t)c * m * d;
+  double acc = 0.0;
+  for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
+    const int64_t o0 = off[k];
+    const int mk = (int)(off[k + 1] - o0);
+    const int64_t base = (int64_t)m * o0;
+    for (int e = lane; e < m * mk; e += 32) {
+      const int j = e / m, i = e - j * m;
+      T s = T(0);
+      for (int t = 0; t < d; ++t) {
+        const T df = xc[i * d + t] - Y[(o0 + j) * d + t];
+        s += df * df;
+      }
+      Cc[base + e] = s;
+      acc += (double)s;
+    }
+  }
+  if (psum) {
+    for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+    __shared__ double sh[4];
+    if (lane == 0) sh[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
+  }
+}
+
+// surrogate objective partials (X14): sum_k <C, Pi1> per item, in double
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_objective(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+            const T* __restrict__ Cc, const T* __restrict__ P, double* __restrict__ psum, int m) {
+  const int item = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
+    const int64_t base = (int64_t)m * off[k];
+    const int64_t ne = (int64_t)m * (off[k + 1] - off[k]);
+    T s = T(0);
+    for (int64_t e = lane; e < ne; e += 32) s += Cc[base + e] * P[base + e];
+    acc += (double)s;
+  }
+  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+  __shared__ double sh[4];
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
+}
+
+// per-cluster sum of per-item doubles (fixed order)
+static __global__ void k_dsum_cl(const double* __restrict__ psum, const int64_t* __restrict__ cl_item,
+                          double* __restrict__ S, int K) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  double s = 0.0;
+  for (int64_t it = cl_item[c]; it < cl_item[c + 1]; ++it) s += psum[it];
+  S[c] = s;
+}
+
+// rho_c = rho0 * sumC_c / (m * npts_c) (Eq.rho with X1); kx per Num
+template <typename T>
+__global__ void k_rho(const double* __restrict__ sumC, const double* __restrict__ npts, int K, int m,
+                      double rho0, T* __restrict__ rho, T* __restrict__ kx, double* __restrict__ rho_d) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  const double r = rho0 * sumC[c] / ((double)m * npts[c]);
+  rho_d[c] = r;
+  rho[c] = (T)r;
+  kx[c] = (sizeof(T) == 4) ? (T)(1.4426950408889634 / r) : (T)(1.0 / r);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Layout kernels: gather the caller's members into the cluster-sorted layout (renormalising the
+// member weights), initial plans, and the state read-back in caller order.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
+         const int64_t* __restrict__ dst_off, const T* __restrict__ Ysrc, const T* __restrict__ Wsrc,
+         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, double wtol, int* err) {
+  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= N) return;
+  const int64_t k = order[s];
+  const int64_t so = src_off[k], dsto = dst_off[s];
+  const int mk = (int)(src_off[k + 1] - so);
+  for (int64_t e = lane; e < (int64_t)mk * d; e += 32) Y[dsto * d + e] = Ysrc[so * d + e];
+  double sum = 0.0;
+  for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
+  for (int h = 16; h >= 1; h >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, h);
+  if (lane == 0 && !(fabs(sum - 1.0) <= wtol)) atomicOr(err, ERR_WEIGHTS);
+  T tot = T(0);   // renormalise in the working precision, sequential order like the oracle
+  if (lane == 0)
+    for (int j = 0; j < mk; ++j) tot += Wsrc[so + j];
+  tot = __shfl_sync(0xffffffffu, tot, 0);
+  for (int j = lane; j < mk; j += 32) om[dsto + j] = Wsrc[so + j] / tot;
+}
+
+// Pi^(2),0 = w_i w_j^(k) or, for warm members, the cached block;
+// Lambda = 0.  Writes the new Pi2 into `dst` (a buffer distinct from the warm source).
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+             const int32_t* __restrict__ item_cl, const int64_t* __restrict__ warm_src,
+             const T* __restrict__ om, const T* __restrict__ w, const T* __restrict__ Qold,
+             T* __restrict__ dst, T* __restrict__ L, int m) {
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
+    const int64_t o0 = off[k];
+    const int64_t ne = (int64_t)m * (off[k + 1] - o0);
+    const int64_t base = (int64_t)m * o0;
+    const int64_t src = warm_src ? warm_src[k] : -1;
+    for (int64_t e = lane; e < ne; e += 32) {
+      const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
+      dst[base + e] = (src >= 0) ? Qold[src + e] : w[(int64_t)c * m + i] * om[o0 + j];
+      L[base + e] = T(0);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
+                const int64_t* __restrict__ orig_off, const T* __restrict__ src, T* __restrict__ dst,
+                int64_t N, int m) {
+  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= N) return;
+  const int64_t k = order[s];
+  const int64_t ne = (int64_t)m * (off[s + 1] - off[s]);
+  const T* a = src + (int64_t)m * off[s];
+  T* b = dst + (int64_t)m * orig_off[k];
+  for (int64_t e = lane; e < ne; e += 32) b[e] = a[e];
+}
+
+}  // namespace ad2k

@@ -111,13 +111,32 @@ def _segment_normalise(v: np.ndarray, offsets: np.ndarray) -> np.ndarray:
     return v / np.repeat(s, np.diff(offsets))
 
 
-def _dirichlet_ragged(rng, alpha: float, offsets: np.ndarray, chunk: int = 1 << 24) -> np.ndarray:
+_CHUNK = 1 << 22      # points per generator chunk (fixed: part of the workload definition)
+
+
+def _chunk_rng(seed_rng_key, c: int):
+    seed, cfg, purpose = seed_rng_key
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed, spawn_key=(cfg, purpose, c))))
+
+
+def _parallel_chunks(n: int, fn):
+    """Run fn(chunk_index, a, b) over fixed-size chunks on a thread pool (numpy's generators
+    release the GIL); results depend only on the chunk index, not on the thread count."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    nch = (n + _CHUNK - 1) // _CHUNK
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(lambda c: fn(c, c * _CHUNK, min(n, (c + 1) * _CHUNK)), range(nch)))
+
+
+def _dirichlet_ragged(key, alpha: float, offsets: np.ndarray) -> np.ndarray:
     n = int(offsets[-1])
     g = np.empty(n, np.float64)
-    for a in range(0, n, chunk):
-        b = min(n, a + chunk)
-        g[a:b] = rng.standard_gamma(alpha, size=b - a)
-    # a member whose gammas all underflow would have no mass; gamma(0.5) never returns 0 in fp64
+
+    def fill(c, a, b):
+        g[a:b] = _chunk_rng(key, c).standard_gamma(alpha, size=b - a)
+    _parallel_chunks(n, fill)
+    # a member whose gammas all underflow would have no mass; gamma(alpha) never returns 0 in fp64
     return _segment_normalise(g, offsets)
 
 
@@ -133,23 +152,38 @@ def _zipf_ragged(rng, s: float, offsets: np.ndarray) -> np.ndarray:
     return _segment_normalise(rank.astype(np.float64) ** (-s), offsets)
 
 
-def _gmm_points(rng_comp, rng_noise, means: np.ndarray, sigma: float, n: int, out_dtype,
-                chunk: int = 1 << 22) -> np.ndarray:
+def _gmm_points(key, means: np.ndarray, sigma: float, n: int, out_dtype) -> np.ndarray:
     """Each point picks a mixture component uniformly, plus N(0, sigma^2 I)."""
     ncomp, d = means.shape
     Y = np.empty((n, d), out_dtype)
-    for a in range(0, n, chunk):
-        b = min(n, a + chunk)
-        comp = rng_comp.integers(0, ncomp, size=b - a)
-        noise = rng_noise.standard_normal((b - a, d))
-        Y[a:b] = means[comp] + sigma * noise
+    mt = means.astype(out_dtype)
+
+    def fill(c, a, b):
+        r = _chunk_rng(key, c)
+        comp = r.integers(0, ncomp, size=b - a)
+        noise = r.standard_normal((b - a, d), dtype=out_dtype)
+        noise *= out_dtype(sigma)
+        noise += mt[comp]
+        Y[a:b] = noise
+    _parallel_chunks(n, fill)
     return Y
 
 
 def member_means(b: Bundle) -> np.ndarray:
     """Weighted mean of each member's support (harness feature for k-means++ init)."""
-    Yw = b.supports.astype(np.float64) * b.weights.astype(np.float64)[:, None]
-    return np.add.reduceat(Yw, b.offsets[:-1], axis=0)
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    out = np.empty((b.N, b.d), np.float64)
+    step = 1 << 18                                   # members per task
+
+    def task(a):
+        e = min(b.N, a + step)
+        lo, hi = int(b.offsets[a]), int(b.offsets[e])
+        Yw = b.supports[lo:hi].astype(np.float64) * b.weights[lo:hi].astype(np.float64)[:, None]
+        out[a:e] = np.add.reduceat(Yw, b.offsets[a:e] - lo, axis=0)
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(task, range(0, b.N, step)))
+    return out
 
 
 def _nearest(points: np.ndarray, centres: np.ndarray, chunk: int = 1 << 16) -> np.ndarray:
@@ -174,10 +208,10 @@ def kmeanspp(points: np.ndarray, K: int, rng, lloyd_iters: int = 10) -> np.ndarr
         d2 = np.minimum(d2, ((points - centres[c]) ** 2).sum(1))
     for _ in range(lloyd_iters):
         lab = _nearest(points, centres)
-        for c in range(K):
-            sel = lab == c
-            if sel.any():
-                centres[c] = points[sel].mean(0)
+        cnt = np.bincount(lab, minlength=K)
+        for t in range(points.shape[1]):
+            s = np.bincount(lab, weights=points[:, t], minlength=K)
+            centres[cnt > 0, t] = s[cnt > 0] / cnt[cnt > 0]
     return centres
 
 
@@ -270,8 +304,8 @@ def make_config(cfg: int, N: Optional[int] = None, K: Optional[int] = None, seed
         sizes = np.full(N, 6, np.int64)
         off = _offsets(sizes)
         means = rs(_P_CENTRES).uniform(-5.0, 5.0, size=(3, d))
-        Y = _gmm_points(rs(_P_COMP), rs(_P_NOISE), means, 1.0, int(off[-1]), np.float64)
-        W = _dirichlet_ragged(rs(_P_WEIGHTS), 1.0, off)
+        Y = _gmm_points((seed, ck, _P_NOISE), means, 1.0, int(off[-1]), np.float64)
+        W = _dirichlet_ragged((seed, ck, _P_WEIGHTS), 1.0, off)
         labels = np.zeros(N, np.int32)
         pick = rs(_P_INIT).choice(int(off[-1]), size=m, replace=False)   # X9: 6 distinct pooled points
         x0 = Y[pick][None].astype(np.float64)
@@ -284,16 +318,16 @@ def make_config(cfg: int, N: Optional[int] = None, K: Optional[int] = None, seed
         sizes = rs(_P_SIZES).integers(8, 17, size=N).astype(np.int64)
         off = _offsets(sizes)
         centres = rs(_P_CENTRES).uniform(0.0, 1.0, size=(32, d))
-        Y = _gmm_points(rs(_P_COMP), rs(_P_NOISE), centres, 0.05, int(off[-1]), np.float64)
-        W = _dirichlet_ragged(rs(_P_WEIGHTS), 1.0, off)
+        Y = _gmm_points((seed, ck, _P_NOISE), centres, 0.05, int(off[-1]), np.float64)
+        W = _dirichlet_ragged((seed, ck, _P_WEIGHTS), 1.0, off)
         sched = Schedule(T=100, tau=10, rounds=10)
     elif cfg in (3, 5):
         d, m, Kc = 16, 32, (64 if cfg == 3 else 256)
         sizes = np.clip(rs(_P_SIZES).poisson(20.0, size=N), 4, 32).astype(np.int64)
         off = _offsets(sizes)
         means = 2.0 * rs(_P_CENTRES).standard_normal((64, d))            # N(0, 4 I)
-        Y = _gmm_points(rs(_P_COMP), rs(_P_NOISE), means, 1.0, int(off[-1]), np.float32)
-        W = _dirichlet_ragged(rs(_P_WEIGHTS), 0.5, off)
+        Y = _gmm_points((seed, ck, _P_NOISE), means, 1.0, int(off[-1]), np.float32)
+        W = _dirichlet_ragged((seed, ck, _P_WEIGHTS), 0.5, off)
         sched = Schedule(T=50, tau=10, rounds=10 if cfg == 3 else 3)
     elif cfg == 4:
         d, m, Kc = 64, 64, 100
@@ -347,11 +381,11 @@ def make_random(N: int, m: int, d: int, K: int = 1, mk_range=(1, 8), seed: int =
     sizes = rs(_P_SIZES).integers(lo, hi + 1, size=N).astype(np.int64)
     off = _offsets(sizes)
     Y = spread * rs(_P_NOISE).standard_normal((int(off[-1]), d))
-    W = _dirichlet_ragged(rs(_P_WEIGHTS), alpha, off)
+    W = _dirichlet_ragged((seed, ck, _P_WEIGHTS), alpha, off)
     labels = (np.arange(N) % K).astype(np.int32)
     rs(_P_SAMPLE).shuffle(labels)
     x0 = spread * rs(_P_INIT).standard_normal((K, m, d))
-    w0 = _dirichlet_ragged(rs(_P_CENTRES), 2.0, _offsets(np.full(K, m))).reshape(K, m)
+    w0 = _dirichlet_ragged((seed, ck, _P_CENTRES), 2.0, _offsets(np.full(K, m))).reshape(K, m)
     b = Bundle(f"random_N{N}_m{m}_d{d}_K{K}", d, m, K, off, Y, W, labels, x0, w0, dtype,
                Schedule(T=T, tau=tau, rule=rule))
     return _cast(b)

@@ -1,0 +1,220 @@
+"""GPU (CUDA path through the C ABI) vs fp64 oracle parity, north_star tolerances:
+  fp64, after one iteration (+ support update): Pi/w/x within 1e-10 relative (hybrid floor 1e-14*max)
+  fp32, after one iteration:                      within 1e-5 relative (hybrid)
+  fp32, after the full schedule:                  objective 1e-3 rel, w 1e-4 abs, x 1e-3 rel
+Both sides read the same seeded bundle (paper_1510_00012_b200.workloads) with the same labels
+and initial centroids, cluster by cluster.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1510_00012_b200 import workloads as wl
+from paper_1510_00012_b200 import ad2
+from tests.harness import run_gpu, assert_hybrid
+
+pytestmark = pytest.mark.gpu
+
+
+def compare_round(b, T, tau, rule=0, *, rtol_plan, rtol_x, atol_w, rtol_obj=None, check_plans=True, ctx=None,
+                  mem="device", nccl=False, clusters=None, floor=1e-4):
+    ctx, rho, obj = run_gpu(b, T, tau, rule, mem=mem, nccl=nccl, ctx=ctx)
+    ores, members = oracle.run_bundle(b, T=T, tau=tau, rule=rule, clusters=clusters, want_state=check_plans)
+    x, w = ctx.centroids()
+    mats = {}
+    if check_plans:
+        mats = {n: ctx.member_matrices(wch) for n, wch in (("Pi1", ad2.PI1), ("Pi2", ad2.PI2), ("Lam", ad2.LAMBDA))}
+    for c, r in ores.items():
+        assert rho[c] == pytest.approx(r.rho, rel=1e-12 if b.dtype == "f64" else 1e-6)
+        assert np.abs(w[c] - r.w).max() <= atol_w, f"w cluster {c}: {np.abs(w[c] - r.w).max()}"
+        assert_hybrid(x[c], r.x, rtol_x, floor=1e-2, what=f"x cluster {c}")
+        if rtol_obj is not None:
+            assert obj[c] == pytest.approx(r.obj, rel=rtol_obj), f"objective cluster {c}"
+        if check_plans:
+            for name in ("Pi1", "Pi2"):
+                got = np.concatenate([mats[name][k].ravel() for k in members[c]])
+                want = np.concatenate([M.ravel() for M in r.mats[name]])
+                assert_hybrid(got, want, rtol_plan, floor=floor, what=f"{name} cluster {c}")
+            # Lambda = rho * (accumulated difference of nearly equal plans): compare on rho's scale
+            got = np.concatenate([mats["Lam"][k].ravel() for k in members[c]])
+            want = np.concatenate([M.ravel() for M in r.mats["Lam"]])
+            assert np.abs(got - want).max() <= rtol_plan * r.rho * max(1.0, np.abs(want).max() / r.rho) * 10
+    return ctx, ores
+
+
+# ------------------------------------------------------------------ fp64, one iteration, 1e-10
+
+def test_cfg1_fp64_one_iteration():
+    b = wl.make_config(1)
+    compare_round(b, T=1, tau=1, rtol_plan=1e-10, rtol_x=1e-10, atol_w=1e-12, floor=1e-4)
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_cfg1_fp64_full_schedule(rule):
+    b = wl.make_config(1)
+    compare_round(b, T=100, tau=20, rule=rule, rtol_plan=1e-8, rtol_x=1e-9, atol_w=1e-10, rtol_obj=1e-9)
+
+
+@pytest.mark.parametrize("m,mk,d", [(5, (1, 9), 3), (16, (1, 16), 2), (13, (20, 30), 4), (40, (1, 12), 3),
+                                    (64, (20, 64), 5)])
+def test_fp64_ragged_shapes_one_and_five_iterations(m, mk, d):
+    """Ragged m_k (incl. m_k = 1), m not a power of two, the two-chunk and generic kernels."""
+    b = wl.make_random(300, m, d, K=3, mk_range=mk, seed=m, dtype="f64", T=1, tau=1)
+    compare_round(b, T=1, tau=1, rtol_plan=1e-10, rtol_x=1e-10, atol_w=1e-12)
+    compare_round(b, T=5, tau=2, rtol_plan=1e-9, rtol_x=1e-9, atol_w=1e-11, rtol_obj=1e-9)
+
+
+# ------------------------------------------------------------------ fp32
+
+@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000)])
+def test_fp32_one_iteration(cfg, N):
+    b = wl.make_config(cfg, N=N)
+    compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
+
+
+@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000)])
+def test_fp32_full_schedule(cfg, N):
+    b = wl.make_config(cfg, N=N)
+    compare_round(b, T=b.sched.T, tau=b.sched.tau, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3,
+                  check_plans=False)
+
+
+def test_fp32_r2_rule():
+    b = wl.make_config(3, N=1500, K=6)
+    compare_round(b, T=1, tau=1, rule=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
+    compare_round(b, T=30, tau=10, rule=1, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3,
+                  check_plans=False)
+
+
+@pytest.mark.parametrize("m,mk,d", [(6, (1, 40), 2), (32, (30, 64), 16), (48, (4, 32), 16)])
+def test_fp32_ragged_shapes(m, mk, d):
+    b = wl.make_random(500, m, d, K=4, mk_range=mk, seed=7 + m, dtype="f32", T=1, tau=1)
+    compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
+
+
+# ------------------------------------------------------------------ paths that must agree exactly
+
+def _state(ctx):
+    x, w = ctx.centroids()
+    return x, w, ctx.plans(ad2.PI1), ctx.plans(ad2.PI2), ctx.plans(ad2.LAMBDA), ctx.objective()
+
+
+def test_host_batch_equals_device_batch():
+    b = wl.make_config(3, N=1200, K=5)
+    a = _state(run_gpu(b, 20, 10, mem="device")[0])
+    h = _state(run_gpu(b, 20, 10, mem="host")[0])
+    for u, v in zip(a, h):
+        np.testing.assert_array_equal(u, v)
+
+
+def test_nccl_single_rank_equals_local():
+    b = wl.make_config(2, N=1500, K=4)
+    a = _state(run_gpu(b, 20, 10)[0])
+    n = _state(run_gpu(b, 20, 10, nccl=True)[0])
+    for u, v in zip(a, n):
+        np.testing.assert_array_equal(u, v)
+
+
+def test_deterministic_rerun_and_profiling_does_not_change_results():
+    b = wl.make_config(5, N=2000, K=8)
+    a = _state(run_gpu(b, 20, 10)[0])
+    c = _state(run_gpu(b, 20, 10, profile=True)[0])
+    for u, v in zip(a, c):
+        np.testing.assert_array_equal(u, v)
+
+
+def test_member_order_does_not_matter_beyond_rounding():
+    """Permuting the caller's members only changes the caller-order read-back (the library sorts
+    by cluster with a stable counting sort, so the reduction order is unchanged)."""
+    b = wl.make_config(3, N=1000, K=4)
+    perm = np.random.default_rng(0).permutation(b.N)
+    bp = b.subset(perm)
+    x1, w1, *_ = _state(run_gpu(b, 10, 5)[0])
+    x2, w2, *_ = _state(run_gpu(bp, 10, 5)[0])
+    # stable sort keeps each cluster's relative member order -> not identical in general
+    np.testing.assert_allclose(w1, w2, atol=1e-6)
+    np.testing.assert_allclose(x1, x2, rtol=1e-5, atol=1e-5)
+
+
+def test_warm_start_second_round():
+    """Round 2 warm-starts Pi^(2) for members whose label is unchanged."""
+    b = wl.make_config(3, N=1200, K=5)
+    ctx, _, _ = run_gpu(b, 10, 5)
+    x1, w1 = ctx.centroids()
+    pi2_gpu = ctx.member_matrices(ad2.PI2)
+    warm = np.ones(b.N, np.uint8)
+    warm[::3] = 0
+    run_gpu(b, 10, 5, ctx=ctx, warm_mask=warm, x0=x1, w0=w1)
+    x2, w2 = ctx.centroids()
+    for c in range(b.K):
+        mem = np.nonzero(b.labels == c)[0]
+        sub = b.subset(mem)
+        r = oracle.badmm_centroid(x1[c], w1[c], sub.offsets, sub.supports, sub.weights, 10, 5, 0, 2.0, 1e-16, 1e-5,
+                                  warm=[pi2_gpu[k] for k in mem], warm_mask=warm[mem])
+        assert np.abs(w2[c] - r.w).max() <= 1e-4
+        assert_hybrid(x2[c], r.x, 1e-3, floor=1e-2, what=f"x c{c}")
+
+
+# ------------------------------------------------------------------ invariants at larger size
+
+def test_invariants_cfg3_full_size():
+    b = wl.make_config(3)
+    ctx, rho, obj = run_gpu(b, 20, 10)
+    x, w = ctx.centroids()
+    assert np.abs(w.sum(1) - 1).max() < 1e-5 and (w >= 0).all()                       # P2
+    P1 = ctx.member_matrices(ad2.PI1)
+    P2 = ctx.member_matrices(ad2.PI2)
+    L = ctx.member_matrices(ad2.LAMBDA)
+    rng = np.random.default_rng(0)
+    for k in rng.choice(b.N, 300, replace=False):
+        c = b.labels[k]
+        om = b.member(k)[1].astype(np.float64)
+        np.testing.assert_allclose(P1[k].sum(0), om / om.sum(), rtol=2e-5, atol=1e-9)  # P1 columns
+        np.testing.assert_allclose(P2[k].sum(1), w[c], rtol=2e-5, atol=1e-9)          # P1 rows
+        assert abs(L[k].astype(np.float64).sum()) <= 1e-4 * rho[c]                     # P3
+    assert np.isfinite(obj).all() and (obj > 0).all()
+
+
+def test_full_size_sampled_clusters_cfg3():
+    """Bench launch configuration (full cfg3 shape); the oracle recomputes two sampled clusters."""
+    b = wl.make_config(3)
+    T, tau = b.sched.T, b.sched.tau
+    ctx, rho, obj = run_gpu(b, T, tau)
+    x, w = ctx.centroids()
+    ores, _ = oracle.run_bundle(b, T=T, tau=tau, clusters=[0, 37], want_state=False)
+    for c, r in ores.items():
+        assert np.abs(w[c] - r.w).max() <= 1e-4
+        assert_hybrid(x[c], r.x, 1e-3, floor=1e-2, what=f"x c{c}")
+        assert obj[c] == pytest.approx(r.obj, rel=1e-3)
+
+
+# ------------------------------------------------------------------ errors
+
+def test_errors():
+    import torch
+    b = wl.make_random(10, 4, 2, K=3, mk_range=(2, 3), seed=1, dtype="f32")
+    ctx = ad2.Context(0)
+    with pytest.raises(ad2.AD2Error, match="STATE"):
+        ctx.step(1)
+    lab = b.labels.copy()
+    lab[:] = 0                                                       # clusters 1, 2 empty
+    with pytest.raises(ad2.AD2Error, match="EMPTY"):
+        ctx.init(b.offsets, b.supports, b.weights, lab, b.x0, b.w0, 3, 4, mem="host")
+    bad = b.weights.copy()
+    bad[0] += 0.1
+    with pytest.raises(ad2.AD2Error, match="ARG"):
+        ctx.init(b.offsets, b.supports, bad, b.labels, b.x0, b.w0, 3, 4, mem="host")
+    lab = b.labels.copy()
+    lab[0] = 7
+    with pytest.raises(ad2.AD2Error, match="ARG"):
+        ctx.init(b.offsets, b.supports, b.weights, lab, b.x0, b.w0, 3, 4, mem="host")
+    Y0 = np.zeros_like(b.supports)
+    x0 = np.zeros_like(b.x0)
+    with pytest.raises(ad2.AD2Error, match="ZERO_RHO"):
+        ctx.init(b.offsets, Y0, b.weights, b.labels, x0, b.w0, 3, 4, mem="host")
+    ctx.init(b.offsets, b.supports, b.weights, b.labels, b.x0, b.w0, 3, 4, mem="host")
+    with pytest.raises(ad2.AD2Error, match="STATE"):
+        ctx.update_support()
+    ctx.step(3)
+    ctx.update_support()
+    assert np.isfinite(ctx.objective()).all()
