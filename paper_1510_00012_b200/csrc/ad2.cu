@@ -104,6 +104,7 @@ struct ad2_ctx_s {
   double rho0 = 2.0, eps = 1e-16;
   int64_t N = 0, n = 0, n_items = 0;
   int variant = 0, mp = 0, nch = 0, dp = 0;
+  int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   size_t es = 4;                     // element size
 
   // host tables
@@ -194,6 +195,9 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.L = ctx->L.as<T>();
   a.Cc = ctx->Cc.as<T>();
   a.w = ctx->w.as<T>();
+  a.x = ctx->x.as<T>();
+  a.ld = ctx->ld;
+  a.dy = ctx->dy;
   a.rho = ctx->rho.as<T>();
   a.kx = ctx->kx.as<T>();
   a.pw = ctx->pw.as<T>();
@@ -208,16 +212,17 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
 
 // fused-kernel launchers live in inst_<dtype>_mp<MP>.cu (compiled in parallel)
 template <typename T, int MP>
-void launch_warp(int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
+void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
 
 template <typename T>
 static void launch_iter_T(ad2_ctx ctx, int mode, cudaStream_t s) {
   IterArgs<T> a = iter_args<T>(ctx);
   if (ctx->n_items == 0) return;
-  if (ctx->variant == 1) {
-    if (ctx->mp == 8) launch_warp<T, 8>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
-    else if (ctx->mp == 16) launch_warp<T, 16>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
-    else launch_warp<T, 32>(mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+  if (ctx->variant >= 1) {
+    const int v = ctx->variant;
+    if (ctx->mp == 8) launch_warp<T, 8>(v, mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+    else if (ctx->mp == 16) launch_warp<T, 16>(v, mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
+    else launch_warp<T, 32>(v, mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
   } else {
     dim3 g((unsigned)((ctx->n_items + 127) / 128)), b(128);
     T* scr = ctx->scr.as<T>();
@@ -254,19 +259,42 @@ static ad2_status consensus(ad2_ctx ctx, cudaStream_t s) {
   return ctx->dtype == AD2_F64 ? consensus_T<double>(ctx, s) : consensus_T<float>(ctx, s);
 }
 
+// Cost: variants 0/1 keep C in HBM (k_cost, optional per-item sums); variant 2 recomputes C
+// inside the iteration kernel, so only the rho numerator is formed here (k_cost_rows).
 template <typename T>
 static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
-  if (ctx->n_items > 0) {
-    k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
-        ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
-        ctx->x.as<T>(), ctx->Cc.as<T>(), with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d);
-    CHK(launch_check(ctx, "k_cost"));
+  if (ctx->n_items == 0) return AD2_OK;
+  if (ctx->variant == 2) {
+    if (!with_sum) return AD2_OK;
+    if (ctx->dp <= 4)
+      k_cost_rows<T, 4><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+          ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
+          ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld, ctx->dy);
+    else
+      k_cost_rows<T, 16><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+          ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
+          ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld, ctx->dy);
+    return launch_check(ctx, "k_cost_rows");
   }
-  return AD2_OK;
+  k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+      ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
+      ctx->x.as<T>(), ctx->Cc.as<T>(), with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->ld, ctx->dy);
+  return launch_check(ctx, "k_cost");
 }
 
 static ad2_status build_cost(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
   return ctx->dtype == AD2_F64 ? build_cost_T<double>(ctx, with_sum, s) : build_cost_T<float>(ctx, with_sum, s);
+}
+
+// C into ctx->Cc for read-back (variant 2 keeps no cache)
+template <typename T>
+static ad2_status materialise_cost_T(ad2_ctx ctx, cudaStream_t s) {
+  if (ctx->n_items == 0) return AD2_OK;
+  CU(ctx->Cc.reserve(ctx->es * (size_t)ctx->ld * ctx->n));
+  k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+      ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
+      ctx->x.as<T>(), ctx->Cc.as<T>(), nullptr, ctx->m, ctx->d, ctx->ld, ctx->dy);
+  return launch_check(ctx, "k_cost");
 }
 
 static ad2_status cluster_dsum(ad2_ctx ctx, cudaStream_t s) {
@@ -380,7 +408,7 @@ static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, doubl
   if (ctx->N == 0) return;
   k_gather<T><<<(unsigned)((ctx->N + 3) / 4), 128, 0, ctx->stream>>>(
       ctx->d_order.as<int32_t>(), ctx->d_orig_off.as<int64_t>(), ctx->d_off.as<int64_t>(), (const T*)Ysrc,
-      (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, wtol, ctx->d_err.as<int>());
+      (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, ctx->dy, wtol, ctx->d_err.as<int>());
 }
 
 template <typename T>
@@ -389,7 +417,7 @@ static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
   k_init_plans<T><<<(unsigned)ctx->n_items, 128, 0, ctx->stream>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
       warm ? ctx->d_warm.as<int64_t>() : nullptr, ctx->om.as<T>(), ctx->w.as<T>(), ctx->Q.as<T>(), dst,
-      ctx->L.as<T>(), ctx->m);
+      ctx->L.as<T>(), ctx->m, ctx->ld);
 }
 
 ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
@@ -444,7 +472,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
       const int64_t ps = ctx->pos_of[k];
       const int64_t omk = ctx->h_off[ps + 1] - ctx->h_off[ps];
       if (omk != off[k + 1] - off[k]) return ctx->fail(AD2_ERR_ARG, "warm member %lld changed m_k", (long long)k);
-      warm_src[k] = (int64_t)m * ctx->h_off[ps];   // indexed by caller member; remapped below
+      warm_src[k] = (int64_t)ctx->ld * ctx->h_off[ps];   // indexed by caller member; remapped below
     }
   }
 
@@ -475,17 +503,31 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   }
 
   // ---- kernel variant
+  //   2: TMA-staged fused warp kernel, cost recomputed in-kernel (m <= 32, m_k <= MK, d <= 16)
+  //   1: fused warp kernel with direct loads and a cost cache (m <= 32, m_k <= MK, d <= 64, fp32)
+  //   0: generic one-thread-per-member kernels (anything else)
   int variant = 0, mp = 0, nch = 0, dp = 0;
-  const int dmax = b->dtype == AD2_F64 ? 16 : 64;
+  const int E = (int)(16 / es);
   for (int cand : {8, 16, 32}) {
-    if (m <= cand && mkmax <= (cand == 32 ? 32 : 2 * cand) && d <= dmax) {
-      variant = 1;
+    if (m <= cand && mkmax <= (cand == 32 ? 32 : 2 * cand)) {
+      const int dyp = (d + E - 1) / E * E;
+      if (d <= 16) {
+        variant = 2;
+        dp = dyp <= 4 ? 4 : 16;
+      } else if (b->dtype == AD2_F32 && d <= 64) {
+        variant = 1;
+        dp = 64;
+      } else {
+        break;
+      }
       mp = cand;
       nch = mkmax <= cand ? 1 : 2;
-      dp = d <= 4 ? 4 : (d <= 16 ? 16 : 64);
       break;
     }
   }
+  const int ld = variant == 2 ? (m + E - 1) / E * E : m;
+  const int dy = variant == 2 ? (d + E - 1) / E * E : d;
+  if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");
   const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * ITEM_PASSES : 1;
   std::vector<int64_t> item_mb, cl_item(K + 1, 0);
   std::vector<int32_t> item_cl;
@@ -501,13 +543,13 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   const int64_t n_items = (int64_t)item_cl.size();
 
   // ---- device buffers
-  const size_t E = (size_t)m * (size_t)n;
-  CU(ctx->Y.reserve(es * (size_t)n * d));
+  const size_t EL = (size_t)ld * (size_t)n;
+  CU(ctx->Y.reserve(es * (size_t)n * dy));
   CU(ctx->om.reserve(es * (size_t)n));
-  CU(ctx->P.reserve(es * E));
-  CU(ctx->L.reserve(es * E));
-  CU(ctx->Cc.reserve(es * E));
-  if (!warm) CU(ctx->Q.reserve(es * E));
+  CU(ctx->P.reserve(es * EL));
+  CU(ctx->L.reserve(es * EL));
+  if (variant != 2) CU(ctx->Cc.reserve(es * EL));
+  if (!warm) CU(ctx->Q.reserve(es * EL));
   CU(ctx->x.reserve(es * (size_t)K * m * d));
   CU(ctx->w.reserve(es * (size_t)K * m));
   CU(ctx->rho.reserve(es * K));
@@ -546,6 +588,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   ctx->mp = mp;
   ctx->nch = nch;
   ctx->dp = dp;
+  ctx->ld = ld;
+  ctx->dy = dy;
   ctx->order.swap(order);
   ctx->pos_of.swap(pos_of);
   ctx->h_off.swap(soff);
@@ -593,7 +637,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
     if (n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
     std::swap(ctx->P.p, ctx->Q.p);
     std::swap(ctx->P.cap, ctx->Q.cap);
-    CU(ctx->P.reserve(es * E));
+    CU(ctx->P.reserve(es * EL));
   } else {
     if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
     else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());
@@ -721,12 +765,32 @@ ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
   CHK(set_dev(ctx));
   cudaStream_t s = ctx->stream;
   if (ctx->n_items > 0) {
-    if (ctx->dtype == AD2_F64)
-      k_objective<double><<<(unsigned)ctx->n_items, 128, 0, s>>>(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(),
-                                                                  ctx->Cc.as<double>(), ctx->P.as<double>(), ctx->pd.as<double>(), ctx->m);
-    else
-      k_objective<float><<<(unsigned)ctx->n_items, 128, 0, s>>>(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(),
-                                                                 ctx->Cc.as<float>(), ctx->P.as<float>(), ctx->pd.as<double>(), ctx->m);
+    const unsigned g = (unsigned)ctx->n_items;
+    const int64_t* off = ctx->d_off.as<int64_t>();
+    const int64_t* imb = ctx->d_item_mb.as<int64_t>();
+    const int32_t* icl = ctx->d_item_cl.as<int32_t>();
+    double* pd = ctx->pd.as<double>();
+    if (ctx->variant == 2) {
+      if (ctx->dtype == AD2_F64) {
+        if (ctx->dp <= 4)
+          k_cost_rows<double, 4><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(),
+                                                   ctx->P.as<double>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
+        else
+          k_cost_rows<double, 16><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(),
+                                                    ctx->P.as<double>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
+      } else {
+        if (ctx->dp <= 4)
+          k_cost_rows<float, 4><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(),
+                                                  ctx->P.as<float>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
+        else
+          k_cost_rows<float, 16><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(),
+                                                   ctx->P.as<float>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
+      }
+    } else if (ctx->dtype == AD2_F64) {
+      k_objective<double><<<g, 128, 0, s>>>(off, imb, ctx->Cc.as<double>(), ctx->P.as<double>(), pd, ctx->ld);
+    } else {
+      k_objective<float><<<g, 128, 0, s>>>(off, imb, ctx->Cc.as<float>(), ctx->P.as<float>(), pd, ctx->ld);
+    }
     CHK(launch_check(ctx, "k_objective"));
   }
   CHK(cluster_dsum(ctx, s));
@@ -754,6 +818,9 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
   if (which == AD2_PI1 && ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "Pi1 exists after a step");
   CHK(set_dev(ctx));
+  if (which == AD2_COST && ctx->variant == 2) {
+    CHK(ctx->dtype == AD2_F64 ? materialise_cost_T<double>(ctx, ctx->stream) : materialise_cost_T<float>(ctx, ctx->stream));
+  }
   const DBuf* src = which == AD2_PI1 ? &ctx->P : which == AD2_PI2 ? &ctx->Q : which == AD2_LAMBDA ? &ctx->L : &ctx->Cc;
   const size_t bytes = ctx->es * (size_t)ctx->m * ctx->n;
   void* dst = out;
@@ -766,11 +833,11 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
     if (ctx->dtype == AD2_F64)
       k_scatter_plans<double><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                              ctx->d_orig_off.as<int64_t>(), (const double*)src->p,
-                                                             (double*)dst, ctx->N, ctx->m);
+                                                             (double*)dst, ctx->N, ctx->m, ctx->ld);
     else
       k_scatter_plans<float><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                             ctx->d_orig_off.as<int64_t>(), (const float*)src->p,
-                                                            (float*)dst, ctx->N, ctx->m);
+                                                            (float*)dst, ctx->N, ctx->m, ctx->ld);
     CHK(launch_check(ctx, "k_scatter_plans"));
   }
   if (where == AD2_HOST) {

@@ -52,12 +52,15 @@ struct IterArgs {
   T* L;                    // Lambda
   const T* Cc;             // cost C
   const T* w;              // [K][m] consensus weights
+  const T* x;              // [K][m][d] centroid support points
   const T* rho;            // [K]
   const T* kx;             // [K] exponent scale (see Num)
   T* pw;                   // [n_items][m]   partial sum over members of wt (R1) or sqrt(wt) (R2)
   T* px;                   // [n_items][m][d+1] partial sums of pi2_ij y_j and pi2_ij
   int* err;
   int m, d, rule;
+  int ld;                  // leading dimension of a member block (rows; >= m)
+  int dy;                  // row stride of Y (>= d, zero-padded)
   T eps;
 };
 
@@ -433,7 +436,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_cost(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
        const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
-       T* __restrict__ Cc, double* __restrict__ psum, int m, int d) {
+       T* __restrict__ Cc, double* __restrict__ psum, int m, int d, int ld, int dy) {
   const int item = blockIdx.x;
   const int c = item_cl[item];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -442,14 +445,15 @@ k_cost(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
   for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
     const int64_t o0 = off[k];
     const int mk = (int)(off[k + 1] - o0);
-    const int64_t base = (int64_t)m * o0;
-    for (int e = lane; e < m * mk; e += 32) {
-      const int j = e / m, i = e - j * m;
+    const int64_t base = (int64_t)ld * o0;
+    for (int e = lane; e < ld * mk; e += 32) {
+      const int j = e / ld, i = e - j * ld;
       T s = T(0);
-      for (int t = 0; t < d; ++t) {
-        const T df = xc[i * d + t] - Y[(o0 + j) * d + t];
-        s += df * df;
-      }
+      if (i < m)
+        for (int t = 0; t < d; ++t) {
+          const T df = xc[i * d + t] - Y[(o0 + j) * dy + t];
+          s += df * df;
+        }
       Cc[base + e] = s;
       acc += (double)s;
     }
@@ -463,17 +467,60 @@ k_cost(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
   }
 }
 
+
+// Row-wise cost sums without a C cache (variant 2): lane = centroid row i holds x_i in
+// registers, y_j is a broadcast load.  With P == nullptr: per-item sum of C (Eq.rho numerator);
+// otherwise per-item sum of C .* P (surrogate objective).  double accumulation.
+template <typename T, int DP>
+__global__ void __launch_bounds__(128)
+k_cost_rows(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+            const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
+            const T* __restrict__ P, double* __restrict__ psum, int m, int d, int ld, int dy) {
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    const int i = r0 + lane;
+    const bool rowok = i < m;
+    T xr[DP];
+#pragma unroll
+    for (int t = 0; t < DP; ++t) xr[t] = (rowok && t < d) ? x[((int64_t)c * m + i) * d + t] : T(0);
+    for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
+      const int64_t o0 = off[k];
+      const int mk = (int)(off[k + 1] - o0);
+      T s = T(0);
+      for (int j = 0; j < mk; ++j) {
+        T cst = T(0);
+#pragma unroll
+        for (int t = 0; t < DP; ++t)
+          if (t < d) {
+            const T df = xr[t] - __ldg(Y + (o0 + j) * dy + t);
+            cst += df * df;
+          }
+        if (rowok) s += P ? cst * P[(int64_t)ld * (o0 + j) + i] : cst;
+      }
+      acc += (double)s;
+    }
+  }
+  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+  __shared__ double sh[4];
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
+}
+
 // surrogate objective partials (X14): sum_k <C, Pi1> per item, in double
 template <typename T>
 __global__ void __launch_bounds__(128)
 k_objective(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
-            const T* __restrict__ Cc, const T* __restrict__ P, double* __restrict__ psum, int m) {
+            const T* __restrict__ Cc, const T* __restrict__ P, double* __restrict__ psum, int ld) {
   const int item = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc = 0.0;
   for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
-    const int64_t base = (int64_t)m * off[k];
-    const int64_t ne = (int64_t)m * (off[k + 1] - off[k]);
+    const int64_t base = (int64_t)ld * off[k];
+    const int64_t ne = (int64_t)ld * (off[k + 1] - off[k]);
     T s = T(0);
     for (int64_t e = lane; e < ne; e += 32) s += Cc[base + e] * P[base + e];
     acc += (double)s;
@@ -515,14 +562,17 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
          const int64_t* __restrict__ dst_off, const T* __restrict__ Ysrc, const T* __restrict__ Wsrc,
-         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, double wtol, int* err) {
+         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, double wtol, int* err) {
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
   const int64_t k = order[s];
   const int64_t so = src_off[k], dsto = dst_off[s];
   const int mk = (int)(src_off[k + 1] - so);
-  for (int64_t e = lane; e < (int64_t)mk * d; e += 32) Y[dsto * d + e] = Ysrc[so * d + e];
+  for (int64_t e = lane; e < (int64_t)mk * dy; e += 32) {
+    const int64_t j = e / dy, t = e - j * dy;
+    Y[dsto * dy + e] = (t < d) ? Ysrc[(so + j) * d + t] : T(0);
+  }
   double sum = 0.0;
   for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
   for (int h = 16; h >= 1; h >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, h);
@@ -541,18 +591,18 @@ __global__ void __launch_bounds__(128)
 k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
              const int32_t* __restrict__ item_cl, const int64_t* __restrict__ warm_src,
              const T* __restrict__ om, const T* __restrict__ w, const T* __restrict__ Qold,
-             T* __restrict__ dst, T* __restrict__ L, int m) {
+             T* __restrict__ dst, T* __restrict__ L, int m, int ld) {
   const int item = blockIdx.x;
   const int c = item_cl[item];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
     const int64_t o0 = off[k];
-    const int64_t ne = (int64_t)m * (off[k + 1] - o0);
-    const int64_t base = (int64_t)m * o0;
+    const int64_t ne = (int64_t)ld * (off[k + 1] - o0);
+    const int64_t base = (int64_t)ld * o0;
     const int64_t src = warm_src ? warm_src[k] : -1;
     for (int64_t e = lane; e < ne; e += 32) {
-      const int j = (int)(e / m), i = (int)(e - (int64_t)j * m);
-      dst[base + e] = (src >= 0) ? Qold[src + e] : w[(int64_t)c * m + i] * om[o0 + j];
+      const int j = (int)(e / ld), i = (int)(e - (int64_t)j * ld);
+      dst[base + e] = (src >= 0) ? Qold[src + e] : (i < m ? w[(int64_t)c * m + i] * om[o0 + j] : T(0));
       L[base + e] = T(0);
     }
   }
@@ -562,15 +612,18 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
                 const int64_t* __restrict__ orig_off, const T* __restrict__ src, T* __restrict__ dst,
-                int64_t N, int m) {
+                int64_t N, int m, int ld) {
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
   const int64_t k = order[s];
   const int64_t ne = (int64_t)m * (off[s + 1] - off[s]);
-  const T* a = src + (int64_t)m * off[s];
+  const T* a = src + (int64_t)ld * off[s];
   T* b = dst + (int64_t)m * orig_off[k];
-  for (int64_t e = lane; e < ne; e += 32) b[e] = a[e];
+  for (int64_t e = lane; e < ne; e += 32) {
+    const int64_t j = e / m, i = e - j * m;
+    b[e] = a[j * ld + i];
+  }
 }
 
 }  // namespace ad2k

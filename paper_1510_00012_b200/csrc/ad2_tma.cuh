@@ -1,0 +1,317 @@
+// ad2_tma.cuh — the fused B-ADMM iteration kernel with per-warp TMA (cp.async.bulk) staging.
+// Modified B-ADMM of AD2-clustering (arXiv 1510.00012, Alg. 4; "P:n" = PAPER.md line).
+//
+// Each warp owns a 2-stage shared-memory pipeline.  A pass = G = 32/MP consecutive members of
+// one cluster; their Pi / Lambda blocks (contiguous, column-major, leading dimension ld) and
+// their support points Y (row stride dy) are brought in by three 1-D bulk copies completing on
+// an mbarrier, the next pass's copies are in flight while this pass computes, and the results
+// leave by bulk stores from the same shared-memory slots.  The cost C = ||x_i - y_j||^2 is
+// recomputed from the staged supports (difference form, d <= DP FMAs per entry) instead of
+// being read from HBM, so an iteration moves 16 B per plan entry plus ~dy*4/m B of supports.
+#pragma once
+#include "ad2_kernels.cuh"
+
+namespace ad2k {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni W%=;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <typename T, int MP, int NCH, int DP>
+struct TmaLayout {
+  static constexpr int G = 32 / MP;
+  static constexpr int MK = MP * NCH;
+  static constexpr int CAP = 32 * MK;          // plan entries staged per pass (G*MP rows x MK cols)
+  static constexpr int YCAP = G * MK * DP;     // support coordinates staged per pass
+  static constexpr int STAGE = 2 * CAP + YCAP; // elements: [P|L|Y]
+  static constexpr int TILE = MP * 32;
+  static constexpr int FB = G * MK;
+  static constexpr size_t WARP_BYTES =
+      ((sizeof(T) * (size_t)(2 * STAGE + TILE + FB) + 16 + 127) / 128) * 128;
+  static constexpr size_t CTA_BYTES = NWARP * WARP_BYTES;
+};
+
+template <typename T, int MP, int NCH, int MODE, int DP>
+__global__ void __launch_bounds__(NWARP * 32)
+k_badmm_tma(const IterArgs<T> a) {
+  using N = Num<T>;
+  using V = typename Vec16<T>::type;
+  using Lay = TmaLayout<T, MP, NCH, DP>;
+  constexpr int G = Lay::G, MK = Lay::MK, CAP = Lay::CAP;
+  constexpr int E = 16 / (int)sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* wb = reinterpret_cast<T*>(smem_raw + (size_t)warp * Lay::WARP_BYTES);
+  T* const sPL = wb;                                   // two stages of [P | L | Y]
+  T* const tile = wb + 2 * Lay::STAGE;                 // column-sum transpose tile [MP][32]
+  T* const fbuf = tile + Lay::TILE;                    // per-column factors [G][MK]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(
+      reinterpret_cast<unsigned char*>(fbuf + Lay::FB) + ((16 - ((uintptr_t)(fbuf + Lay::FB) & 15)) & 15));
+
+  const int seg = lane / MP, i = lane - seg * MP;
+  const int item = blockIdx.x;
+  const int c = a.item_cl[item];
+  const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
+  const int m = a.m, ld = a.ld, dy = a.dy;
+  const bool rowok = i < m;
+  const T kx = a.kx[c];
+  const T rho = a.rho[c];
+  const T eps = a.eps;
+  const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
+  T xr[DP];                                            // centroid support point x_i (zero-padded)
+#pragma unroll
+  for (int t = 0; t < DP; ++t) xr[t] = (rowok && t < a.d) ? a.x[((int64_t)c * m + i) * a.d + t] : T(0);
+  T accw = T(0), accm = T(0);
+  T accx[(MODE == P2ONLY) ? DP : 1];
+#pragma unroll
+  for (int t = 0; t < ((MODE == P2ONLY) ? DP : 1); ++t) accx[t] = T(0);
+  bool bad = false;
+
+  const T* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
+  T* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
+  const int64_t step = (int64_t)NWARP * G;
+
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int t) {                            // lane 0 only
+    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;
+    if (k0 >= me) return;
+    const int64_t k1 = (k0 + G < me) ? k0 + G : me;
+    const int64_t p0 = a.off[k0], p1 = a.off[k1];
+    const uint32_t bp = (uint32_t)((int64_t)ld * (p1 - p0) * (int64_t)sizeof(T));
+    const uint32_t by = (uint32_t)((int64_t)dy * (p1 - p0) * (int64_t)sizeof(T));
+    T* st = sPL + (t & 1) * Lay::STAGE;
+    mbar_expect_tx(&bar[t & 1], 2 * bp + by);
+    tma_load(st, src_plan + (int64_t)ld * p0, bp, &bar[t & 1]);
+    tma_load(st + CAP, a.L + (int64_t)ld * p0, bp, &bar[t & 1]);
+    tma_load(st + 2 * CAP, a.Y + (int64_t)dy * p0, by, &bar[t & 1]);
+  };
+  if (lane == 0) issue(0);
+
+  for (int t = 0;; ++t) {
+    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;   // warp-uniform
+    if (k0 >= me) break;
+    if (lane == 0) {
+      bulk_wait_read_all();          // stores of pass t-1 have left the other stage
+      issue(t + 1);
+    }
+    mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+    T* const st = sPL + (t & 1) * Lay::STAGE;
+    const int64_t k1 = (k0 + G < me) ? k0 + G : me;
+    const int64_t pbase = a.off[k0];
+    const int64_t k = k0 + seg;
+    const bool has = k < k1;
+    const int64_t o0 = has ? a.off[k] : pbase;
+    const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
+    const int rel = (int)(o0 - pbase);
+    T* const Ps = st + (int64_t)ld * rel;
+    T* const Ls = st + CAP + (int64_t)ld * rel;
+    const T* const Ys = st + 2 * CAP + (int64_t)dy * rel;
+
+    T p[MK], l[MK], q[MK];
+#pragma unroll
+    for (int j = 0; j < MK; ++j) {
+      const bool ok = rowok && j < mk;
+      p[j] = ok ? Ps[j * ld + i] : T(0);
+      l[j] = ok ? Ls[j * ld + i] : T(0);
+    }
+    if constexpr (MODE == P1ONLY) {
+#pragma unroll
+      for (int j = 0; j < MK; ++j) q[j] = p[j];                       // Pi2^(0)
+    } else {
+      // phase 2 of the previous iteration: Eq.badmmc1b (Lambda^{n}), Eq.badmmc1, Eq.badmm2
+      T r = T(0);
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        q[j] = ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
+        r += q[j];
+      }
+      const T f = (has && rowok) ? wi / r : T(0);
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        q[j] = q[j] * f;
+        if (ok) l[j] = l[j] + rho * (p[j] - q[j]);
+      }
+    }
+    if constexpr (MODE == P2ONLY) {
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        if (rowok && j < mk) {
+          Ps[j * ld + i] = q[j];
+          Ls[j * ld + i] = l[j];
+        }
+      }
+      // support-update partials (Eq.updatex, X5): sum_j pi2_ij y_j and sum_j pi2_ij
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        if (j < mk) {
+          accm += q[j];
+#pragma unroll
+          for (int tt = 0; tt < DP / E; ++tt) {
+            if (tt * E < dy) {
+              const V v = *reinterpret_cast<const V*>(Ys + j * dy + tt * E);
+              const T* ve = reinterpret_cast<const T*>(&v);
+#pragma unroll
+              for (int u = 0; u < E; ++u) accx[tt * E + u] += q[j] * ve[u];
+            }
+          }
+        }
+      }
+    } else {
+      // phase 1: C_ij = ||x_i - y_j||^2, pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        const bool ok = rowok && j < mk;
+        T cst = T(0);
+        if (j < mk) {
+#pragma unroll
+          for (int tt = 0; tt < DP / E; ++tt) {
+            if (tt * E < dy) {
+              const V v = *reinterpret_cast<const V*>(Ys + j * dy + tt * E);
+              const T* ve = reinterpret_cast<const T*>(&v);
+#pragma unroll
+              for (int u = 0; u < E; ++u) {
+                const T df = xr[tt * E + u] - ve[u];
+                cst += df * df;
+              }
+            }
+          }
+        }
+        p[j] = ok ? q[j] * N::ex(-(cst + l[j]) * kx) + eps : T(0);
+      }
+      // column sums (Eq.badmmc0 denominators) through the swizzled transpose tile
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < MP; ++u) tile[u * 32 + ((((lane / E) ^ (u & 7))) * E) + (lane % E)] = p[ch * MP + u];
+        __syncwarp();
+        T s = T(0);
+#pragma unroll
+        for (int cc = 0; cc < MP / E; ++cc) {
+          const V v = *reinterpret_cast<const V*>(&tile[i * 32 + ((seg * (MP / E) + cc) ^ (i & 7)) * E]);
+          s += Vec16<T>::hsum(v);
+        }
+        const int jc = ch * MP + i;
+        fbuf[seg * MK + jc] = (jc < mk) ? __ldg(a.om + o0 + jc) / s : T(0);   // Eq.badmmc0
+      }
+      __syncwarp();
+      T r2 = T(0);
+#pragma unroll
+      for (int jj = 0; jj < MK; jj += E) {
+        const V fv = *reinterpret_cast<const V*>(&fbuf[seg * MK + jj]);
+        const T* fe = reinterpret_cast<const T*>(&fv);
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+          const int j = jj + u;
+          const bool ok = rowok && j < mk;
+          p[j] = p[j] * fe[u];
+          r2 += ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);   // Eq.badmmc1b row mass
+        }
+      }
+      T R = r2;
+#pragma unroll
+      for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
+      if (has && rowok) {
+        const T wt = r2 / R;
+        accw += (a.rule == 1) ? sqrt(wt) : wt;
+        bad |= !isfinite(wt);
+      }
+#pragma unroll
+      for (int j = 0; j < MK; ++j) {
+        if (rowok && j < mk) {
+          Ps[j * ld + i] = p[j];
+          if (MODE == FUSED) Ls[j * ld + i] = l[j];
+        }
+      }
+    }
+    // results leave by bulk stores from the same slots
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t p1 = a.off[k1];
+      const uint32_t bp = (uint32_t)((int64_t)ld * (p1 - pbase) * (int64_t)sizeof(T));
+      tma_store(dst_plan + (int64_t)ld * pbase, st, bp);
+      if (MODE != P1ONLY) tma_store(a.L + (int64_t)ld * pbase, st + CAP, bp);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  if (bad) atomicOr(a.err, ERR_NONFINITE);
+
+  // fixed-order combination of the per-row accumulators -> this item's partial sums
+  if constexpr (MODE != P2ONLY) {
+    __shared__ T sw[NWARP * G][MP];
+    sw[warp * G + seg][i] = accw;
+    __syncthreads();
+    if (threadIdx.x < m) {
+      T s = T(0);
+#pragma unroll
+      for (int u = 0; u < NWARP * G; ++u) s += sw[u][threadIdx.x];
+      a.pw[(int64_t)item * m + threadIdx.x] = s;
+    }
+  } else {
+    __shared__ T sx[NWARP * G][MP][DP + 1];
+#pragma unroll
+    for (int t = 0; t < DP; ++t) sx[warp * G + seg][i][t] = accx[t];
+    sx[warp * G + seg][i][DP] = accm;
+    __syncthreads();
+    const int d = a.d;
+    for (int v = threadIdx.x; v < m * (d + 1); v += NWARP * 32) {
+      const int ii = v / (d + 1), t = v - ii * (d + 1);
+      const int tt = (t == d) ? DP : t;
+      T s = T(0);
+#pragma unroll
+      for (int u = 0; u < NWARP * G; ++u) s += sx[u][ii][tt];
+      a.px[(int64_t)item * m * (d + 1) + v] = s;
+    }
+  }
+}
+
+}  // namespace ad2k

@@ -1,11 +1,29 @@
-// inst_f64_mp8.cu — explicit instantiations of the fused B-ADMM kernel for T=double, MP=8
-// (split so nvcc compiles the template set in parallel).  See ad2_kernels.cuh.
-#include "ad2_kernels.cuh"
+// inst_f64_mp8.cu — explicit instantiations of the fused B-ADMM iteration kernels for
+// T=double, MP=8 (split per (dtype, MP) so nvcc compiles the template set in parallel).
+//   variant 2: k_badmm_tma  (TMA-staged, cost recomputed; ad2_tma.cuh)
+//   variant 1: k_badmm_warp (direct loads, cached cost; ad2_kernels.cuh)
+#include "ad2_tma.cuh"
 
 namespace ad2k {
 
 template <int NCH, int DP>
-static void go(int mode, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
+static void go_tma(int mode, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
+  using Lay = TmaLayout<double, 8, NCH, DP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_badmm_tma<double, 8, NCH, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_tma<double, 8, NCH, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_tma<double, 8, NCH, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    attr = true;
+  }
+  dim3 g((unsigned)n_items), b(NWARP * 32);
+  if (mode == P1ONLY) k_badmm_tma<double, 8, NCH, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == FUSED) k_badmm_tma<double, 8, NCH, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else k_badmm_tma<double, 8, NCH, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+}
+
+template <int NCH, int DP>
+static void go_warp(int mode, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
   dim3 g((unsigned)n_items), b(NWARP * 32);
   if (mode == P1ONLY) k_badmm_warp<double, 8, NCH, P1ONLY, 1><<<g, b, 0, s>>>(a);
   else if (mode == FUSED) k_badmm_warp<double, 8, NCH, FUSED, 1><<<g, b, 0, s>>>(a);
@@ -13,10 +31,14 @@ static void go(int mode, const IterArgs<double>& a, int64_t n_items, cudaStream_
 }
 
 template <int NCH>
-static void go_dp(int mode, int dp, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
-  if (dp <= 4) go<NCH, 4>(mode, a, n_items, s);
-  else go<NCH, 16>(mode, a, n_items, s);
-
+static void go_nch(int variant, int mode, int dp, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
+  if (variant == 2) {
+    if (dp <= 4) go_tma<NCH, 4>(mode, a, n_items, s);
+    else go_tma<NCH, 16>(mode, a, n_items, s);
+  } else {
+    if (dp <= 4) go_warp<NCH, 4>(mode, a, n_items, s);
+    else go_warp<NCH, 16>(mode, a, n_items, s);
+  }
 }
 
 }  // namespace ad2k
@@ -24,10 +46,11 @@ static void go_dp(int mode, int dp, const IterArgs<double>& a, int64_t n_items, 
 using namespace ad2k;
 
 template <typename T, int MP>
-void launch_warp(int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
+void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
 
 template <>
-void launch_warp<double, 8>(int mode, int nch, int dp, const IterArgs<double>& a, int64_t n_items, cudaStream_t s) {
-  if (nch == 2) go_dp<2>(mode, dp, a, n_items, s);
-  else go_dp<1>(mode, dp, a, n_items, s);
+void launch_warp<double, 8>(int variant, int mode, int nch, int dp, const IterArgs<double>& a, int64_t n_items,
+                           cudaStream_t s) {
+  if (nch == 2) go_nch<2>(variant, mode, dp, a, n_items, s);
+  else go_nch<1>(variant, mode, dp, a, n_items, s);
 }

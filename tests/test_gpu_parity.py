@@ -27,7 +27,7 @@ def compare_round(b, T, tau, rule=0, *, rtol_plan, rtol_x, atol_w, rtol_obj=None
     for c, r in ores.items():
         assert rho[c] == pytest.approx(r.rho, rel=1e-12 if b.dtype == "f64" else 1e-6)
         assert np.abs(w[c] - r.w).max() <= atol_w, f"w cluster {c}: {np.abs(w[c] - r.w).max()}"
-        assert_hybrid(x[c], r.x, rtol_x, floor=1e-2, what=f"x cluster {c}")
+        assert_hybrid(x[c], r.x, rtol_x, floor=1.0, what=f"x cluster {c}")
         if rtol_obj is not None:
             assert obj[c] == pytest.approx(r.obj, rel=rtol_obj), f"objective cluster {c}"
         if check_plans:
@@ -137,22 +137,27 @@ def test_member_order_does_not_matter_beyond_rounding():
 
 
 def test_warm_start_second_round():
-    """Round 2 warm-starts Pi^(2) for members whose label is unchanged."""
+    """Round 2 warm-starts Pi^(2) for members whose label is unchanged.  Each side
+    carries its own round-1 state into round 2 (no oracle input comes from the GPU)."""
     b = wl.make_config(3, N=1200, K=5)
-    ctx, _, _ = run_gpu(b, 10, 5)
-    x1, w1 = ctx.centroids()
-    pi2_gpu = ctx.member_matrices(ad2.PI2)
     warm = np.ones(b.N, np.uint8)
     warm[::3] = 0
+    ctx, _, _ = run_gpu(b, 10, 5)
+    x1, w1 = ctx.centroids()
     run_gpu(b, 10, 5, ctx=ctx, warm_mask=warm, x0=x1, w0=w1)
     x2, w2 = ctx.centroids()
     for c in range(b.K):
         mem = np.nonzero(b.labels == c)[0]
         sub = b.subset(mem)
-        r = oracle.badmm_centroid(x1[c], w1[c], sub.offsets, sub.supports, sub.weights, 10, 5, 0, 2.0, 1e-16, 1e-5,
-                                  warm=[pi2_gpu[k] for k in mem], warm_mask=warm[mem])
-        assert np.abs(w2[c] - r.w).max() <= 1e-4
-        assert_hybrid(x2[c], r.x, 1e-3, floor=1e-2, what=f"x c{c}")
+        r1 = oracle.badmm_centroid(b.x0[c], b.w0[c], sub.offsets, sub.supports, sub.weights, 10, 5, 0, 2.0, 1e-16,
+                                   1e-5)
+        r2 = oracle.badmm_centroid(r1.x, r1.w, sub.offsets, sub.supports, sub.weights, 10, 5, 0, 2.0, 1e-16, 1e-5,
+                                   warm=r1.mats["Pi2"], warm_mask=warm[mem])
+        assert np.abs(w2[c] - r2.w).max() <= 1e-4
+        assert_hybrid(x2[c], r2.x, 1e-3, floor=1.0, what=f"x c{c}")
+        # a cold round 2 from the same centroids differs: the warm start is really used
+        r2c = oracle.badmm_centroid(r1.x, r1.w, sub.offsets, sub.supports, sub.weights, 10, 5, 0, 2.0, 1e-16, 1e-5)
+        assert np.abs(r2c.w - r2.w).max() > 1e-4
 
 
 # ------------------------------------------------------------------ invariants at larger size
@@ -184,7 +189,7 @@ def test_full_size_sampled_clusters_cfg3():
     ores, _ = oracle.run_bundle(b, T=T, tau=tau, clusters=[0, 37], want_state=False)
     for c, r in ores.items():
         assert np.abs(w[c] - r.w).max() <= 1e-4
-        assert_hybrid(x[c], r.x, 1e-3, floor=1e-2, what=f"x c{c}")
+        assert_hybrid(x[c], r.x, 1e-3, floor=1.0, what=f"x c{c}")
         assert obj[c] == pytest.approx(r.obj, rel=1e-3)
 
 
