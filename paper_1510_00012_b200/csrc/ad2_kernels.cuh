@@ -562,7 +562,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
          const int64_t* __restrict__ dst_off, const T* __restrict__ Ysrc, const T* __restrict__ Wsrc,
-         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, double wtol, int* err) {
+         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, int yy_col, double wtol, int* err) {
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
@@ -571,7 +571,16 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
   const int mk = (int)(src_off[k + 1] - so);
   for (int64_t e = lane; e < (int64_t)mk * dy; e += 32) {
     const int64_t j = e / dy, t = e - j * dy;
-    Y[dsto * dy + e] = (t < d) ? Ysrc[(so + j) * d + t] : T(0);
+    T v = T(0);
+    if (t < d) {
+      v = Ysrc[(so + j) * d + t];
+    } else if (t == yy_col) {                    // |y_j|^2 for the dot-product form of the cost
+      for (int u = 0; u < d; ++u) {
+        const T c = Ysrc[(so + j) * d + u];
+        v += c * c;
+      }
+    }
+    Y[dsto * dy + e] = v;
   }
   double sum = 0.0;
   for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];

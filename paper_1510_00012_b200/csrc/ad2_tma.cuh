@@ -79,6 +79,7 @@ k_badmm_tma(const IterArgs<T> a) {
   using Lay = TmaLayout<T, MP, NCH, DP>;
   constexpr int G = Lay::G, MK = Lay::MK, CAP = Lay::CAP;
   constexpr int E = 16 / (int)sizeof(T);
+  constexpr int NB = MK / 4;                          // column blocks (warp-uniform skip past m_k)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* wb = reinterpret_cast<T*>(smem_raw + (size_t)warp * Lay::WARP_BYTES);
@@ -88,19 +89,27 @@ k_badmm_tma(const IterArgs<T> a) {
   uint64_t* const bar = reinterpret_cast<uint64_t*>(
       reinterpret_cast<unsigned char*>(fbuf + Lay::FB) + ((16 - ((uintptr_t)(fbuf + Lay::FB) & 15)) & 15));
 
+  // lane (seg, i): row i of the seg-th member of a pass.  Blocks have ld == MP rows; rows
+  // i >= m are zero padding and stay zero (eps_r = 0 there), so no per-entry row predicates.
   const int seg = lane / MP, i = lane - seg * MP;
   const int item = blockIdx.x;
   const int c = a.item_cl[item];
   const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
-  const int m = a.m, ld = a.ld, dy = a.dy;
+  const int m = a.m, d = a.d, dy = a.dy;
   const bool rowok = i < m;
   const T kx = a.kx[c];
   const T rho = a.rho[c];
-  const T eps = a.eps;
+  const T eps_r = rowok ? a.eps : T(0);
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
-  T xr[DP];                                            // centroid support point x_i (zero-padded)
+  // cost operands: C_ij = (|x_i|^2 + |y_j|^2) + sum_t (-2 x_it) y_jt, |y_j|^2 staged at Y[j][d]
+  T xn[DP];
+  T xx = T(0);
 #pragma unroll
-  for (int t = 0; t < DP; ++t) xr[t] = (rowok && t < a.d) ? a.x[((int64_t)c * m + i) * a.d + t] : T(0);
+  for (int t = 0; t < DP; ++t) {
+    const T v = (rowok && t < d) ? a.x[((int64_t)c * m + i) * d + t] : T(0);
+    xx += v * v;
+    xn[t] = T(-2) * v;
+  }
   T accw = T(0), accm = T(0);
   T accx[(MODE == P2ONLY) ? DP : 1];
 #pragma unroll
@@ -122,12 +131,12 @@ k_badmm_tma(const IterArgs<T> a) {
     if (k0 >= me) return;
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
     const int64_t p0 = a.off[k0], p1 = a.off[k1];
-    const uint32_t bp = (uint32_t)((int64_t)ld * (p1 - p0) * (int64_t)sizeof(T));
+    const uint32_t bp = (uint32_t)((int64_t)MP * (p1 - p0) * (int64_t)sizeof(T));
     const uint32_t by = (uint32_t)((int64_t)dy * (p1 - p0) * (int64_t)sizeof(T));
     T* st = sPL + (t & 1) * Lay::STAGE;
     mbar_expect_tx(&bar[t & 1], 2 * bp + by);
-    tma_load(st, src_plan + (int64_t)ld * p0, bp, &bar[t & 1]);
-    tma_load(st + CAP, a.L + (int64_t)ld * p0, bp, &bar[t & 1]);
+    tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
+    tma_load(st + CAP, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
     tma_load(st + 2 * CAP, a.Y + (int64_t)dy * p0, by, &bar[t & 1]);
   };
   if (lane == 0) issue(0);
@@ -136,101 +145,118 @@ k_badmm_tma(const IterArgs<T> a) {
     const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;   // warp-uniform
     if (k0 >= me) break;
     if (lane == 0) {
-      bulk_wait_read_all();          // stores of pass t-1 have left the other stage
+      bulk_wait_read_all();          // stores of pass t-1 have left the stage about to be refilled
       issue(t + 1);
     }
-    mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
-    T* const st = sPL + (t & 1) * Lay::STAGE;
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
     const int64_t pbase = a.off[k0];
     const int64_t k = k0 + seg;
     const bool has = k < k1;
     const int64_t o0 = has ? a.off[k] : pbase;
     const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
+    const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
+    T omv[NCH];                                        // w^(k)_j for the column this lane sums
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) omv[ch] = (ch * MP + i < mk) ? __ldg(a.om + o0 + ch * MP + i) : T(0);
+    mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+    T* const st = sPL + (t & 1) * Lay::STAGE;
     const int rel = (int)(o0 - pbase);
-    T* const Ps = st + (int64_t)ld * rel;
-    T* const Ls = st + CAP + (int64_t)ld * rel;
-    const T* const Ys = st + 2 * CAP + (int64_t)dy * rel;
+    T* const Ps = st + MP * rel;
+    T* const Ls = st + CAP + MP * rel;
+    const T* const Ys = st + 2 * CAP + dy * rel;
 
     T p[MK], l[MK], q[MK];
 #pragma unroll
-    for (int j = 0; j < MK; ++j) {
-      const bool ok = rowok && j < mk;
-      p[j] = ok ? Ps[j * ld + i] : T(0);
-      l[j] = ok ? Ls[j * ld + i] : T(0);
+    for (int jb = 0; jb < NB; ++jb) {
+      if (4 * jb >= mkw) break;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * jb + u;
+        p[j] = Ps[j * MP + i];
+        l[j] = Ls[j * MP + i];
+      }
     }
     if constexpr (MODE == P1ONLY) {
 #pragma unroll
       for (int j = 0; j < MK; ++j) q[j] = p[j];                       // Pi2^(0)
     } else {
-      // phase 2 of the previous iteration: Eq.badmmc1b (Lambda^{n}), Eq.badmmc1, Eq.badmm2
+      // phase 2 of the previous iteration: Eq.badmmc1b (Lambda^n), Eq.badmmc1, Eq.badmm2
       T r = T(0);
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        q[j] = ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
-        r += q[j];
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
+          const T b = p[j] * N::ex(l[j] * kx) + eps_r;
+          q[j] = (j < mk) ? b : T(0);
+          r += q[j];
+        }
       }
       const T f = (has && rowok) ? wi / r : T(0);
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        q[j] = q[j] * f;
-        if (ok) l[j] = l[j] + rho * (p[j] - q[j]);
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
+          q[j] = q[j] * f;
+          l[j] = l[j] + rho * (p[j] - q[j]);
+        }
       }
     }
     if constexpr (MODE == P2ONLY) {
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        if (rowok && j < mk) {
-          Ps[j * ld + i] = q[j];
-          Ls[j * ld + i] = l[j];
-        }
-      }
-      // support-update partials (Eq.updatex, X5): sum_j pi2_ij y_j and sum_j pi2_ij
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        if (j < mk) {
-          accm += q[j];
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
+          if (j < mk) {
+            Ps[j * MP + i] = q[j];
+            Ls[j * MP + i] = l[j];
+            // support-update partials (Eq.updatex, X5): sum_j pi2_ij y_j and sum_j pi2_ij
+            accm += q[j];
 #pragma unroll
-          for (int tt = 0; tt < DP / E; ++tt) {
-            if (tt * E < dy) {
+            for (int tt = 0; tt < DP / E; ++tt) {
               const V v = *reinterpret_cast<const V*>(Ys + j * dy + tt * E);
               const T* ve = reinterpret_cast<const T*>(&v);
 #pragma unroll
-              for (int u = 0; u < E; ++u) accx[tt * E + u] += q[j] * ve[u];
+              for (int u2 = 0; u2 < E; ++u2) accx[tt * E + u2] += q[j] * ve[u2];
             }
           }
         }
       }
     } else {
-      // phase 1: C_ij = ||x_i - y_j||^2, pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
+      // phase 1: C_ij, pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        T cst = T(0);
-        if (j < mk) {
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
+          const T* yj = Ys + j * dy;
+          T cst = xx + yj[d];
 #pragma unroll
           for (int tt = 0; tt < DP / E; ++tt) {
-            if (tt * E < dy) {
-              const V v = *reinterpret_cast<const V*>(Ys + j * dy + tt * E);
-              const T* ve = reinterpret_cast<const T*>(&v);
+            const V v = *reinterpret_cast<const V*>(yj + tt * E);
+            const T* ve = reinterpret_cast<const T*>(&v);
 #pragma unroll
-              for (int u = 0; u < E; ++u) {
-                const T df = xr[tt * E + u] - ve[u];
-                cst += df * df;
-              }
-            }
+            for (int u2 = 0; u2 < E; ++u2) cst = fma(xn[tt * E + u2], ve[u2], cst);
           }
+          const T av = q[j] * N::ex(-(cst + l[j]) * kx) + eps_r;
+          p[j] = (j < mk) ? av : T(0);
         }
-        p[j] = ok ? q[j] * N::ex(-(cst + l[j]) * kx) + eps : T(0);
       }
       // column sums (Eq.badmmc0 denominators) through the swizzled transpose tile
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         __syncwarp();
 #pragma unroll
-        for (int u = 0; u < MP; ++u) tile[u * 32 + ((((lane / E) ^ (u & 7))) * E) + (lane % E)] = p[ch * MP + u];
+        for (int u = 0; u < MP; ++u) {
+          if (ch * MP + (u & ~3) >= mkw) break;
+          tile[u * 32 + ((((lane / E) ^ (u & 7))) * E) + (lane % E)] = p[ch * MP + u];
+        }
         __syncwarp();
         T s = T(0);
 #pragma unroll
@@ -239,20 +265,26 @@ k_badmm_tma(const IterArgs<T> a) {
           s += Vec16<T>::hsum(v);
         }
         const int jc = ch * MP + i;
-        fbuf[seg * MK + jc] = (jc < mk) ? __ldg(a.om + o0 + jc) / s : T(0);   // Eq.badmmc0
+        fbuf[seg * MK + jc] = (jc < mk) ? omv[ch] / s : T(0);          // Eq.badmmc0
       }
       __syncwarp();
       T r2 = T(0);
 #pragma unroll
-      for (int jj = 0; jj < MK; jj += E) {
-        const V fv = *reinterpret_cast<const V*>(&fbuf[seg * MK + jj]);
-        const T* fe = reinterpret_cast<const T*>(&fv);
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+        T fe[4];
 #pragma unroll
-        for (int u = 0; u < E; ++u) {
-          const int j = jj + u;
-          const bool ok = rowok && j < mk;
+        for (int u = 0; u < 4; u += E) {
+          const V fv = *reinterpret_cast<const V*>(&fbuf[seg * MK + 4 * jb + u]);
+#pragma unroll
+          for (int u2 = 0; u2 < E; ++u2) fe[u + u2] = reinterpret_cast<const T*>(&fv)[u2];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
           p[j] = p[j] * fe[u];
-          r2 += ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);   // Eq.badmmc1b row mass
+          const T b = p[j] * N::ex(l[j] * kx) + eps_r;                  // Eq.badmmc1b row mass
+          r2 += (j < mk) ? b : T(0);
         }
       }
       T R = r2;
@@ -264,10 +296,15 @@ k_badmm_tma(const IterArgs<T> a) {
         bad |= !isfinite(wt);
       }
 #pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        if (rowok && j < mk) {
-          Ps[j * ld + i] = p[j];
-          if (MODE == FUSED) Ls[j * ld + i] = l[j];
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * jb + u;
+          if (j < mk) {
+            Ps[j * MP + i] = p[j];
+            if (MODE == FUSED) Ls[j * MP + i] = l[j];
+          }
         }
       }
     }
@@ -276,9 +313,9 @@ k_badmm_tma(const IterArgs<T> a) {
     __syncwarp();
     if (lane == 0) {
       const int64_t p1 = a.off[k1];
-      const uint32_t bp = (uint32_t)((int64_t)ld * (p1 - pbase) * (int64_t)sizeof(T));
-      tma_store(dst_plan + (int64_t)ld * pbase, st, bp);
-      if (MODE != P1ONLY) tma_store(a.L + (int64_t)ld * pbase, st + CAP, bp);
+      const uint32_t bp = (uint32_t)((int64_t)MP * (p1 - pbase) * (int64_t)sizeof(T));
+      tma_store(dst_plan + (int64_t)MP * pbase, st, bp);
+      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * pbase, st + CAP, bp);
       bulk_commit();
     }
   }
@@ -302,7 +339,6 @@ k_badmm_tma(const IterArgs<T> a) {
     for (int t = 0; t < DP; ++t) sx[warp * G + seg][i][t] = accx[t];
     sx[warp * G + seg][i][DP] = accm;
     __syncthreads();
-    const int d = a.d;
     for (int v = threadIdx.x; v < m * (d + 1); v += NWARP * 32) {
       const int ii = v / (d + 1), t = v - ii * (d + 1);
       const int tt = (t == d) ? DP : t;
