@@ -212,6 +212,14 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
 
 // fused-kernel launchers live in inst_<dtype>_mp<MP>.cu (compiled in parallel)
 template <typename T, int MP>
+size_t tma_cta_bytes(int nch, int dp);
+
+static size_t tma_bytes(ad2_dtype dt, int mp, int nch, int dp) {
+  if (dt == AD2_F64)
+    return mp == 8 ? tma_cta_bytes<double, 8>(nch, dp) : mp == 16 ? tma_cta_bytes<double, 16>(nch, dp) : tma_cta_bytes<double, 32>(nch, dp);
+  return mp == 8 ? tma_cta_bytes<float, 8>(nch, dp) : mp == 16 ? tma_cta_bytes<float, 16>(nch, dp) : tma_cta_bytes<float, 32>(nch, dp);
+}
+template <typename T, int MP>
 void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
 
 template <typename T>
@@ -244,7 +252,7 @@ template <typename T>
 static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
   const bool fin = ctx->comm == nullptr;
   const size_t sh = sizeof(T) * (size_t)ctx->m;
-  k_wsum<T><<<ctx->K, 128, sh, s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->Sw.as<T>(),
+  k_wsum<T><<<ctx->K, 256, sh + 256 * sizeof(T), s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->Sw.as<T>(),
                                     ctx->w.as<T>(), ctx->rule, fin ? 1 : 0, ctx->d_err.as<int>());
   CHK(launch_check(ctx, "k_wsum"));
   if (!fin) {
@@ -523,6 +531,18 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
       mp = cand;
       nch = mkmax <= cand ? 1 : 2;
       break;
+    }
+  }
+  if (variant == 2) {                       // the staged pipeline must fit the SM's shared memory
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) {
+      if (b->dtype == AD2_F32 && d <= 64) {
+        variant = 1;
+        dp = d <= 4 ? 4 : (d <= 16 ? 16 : 64);
+      } else {
+        variant = 0;
+      }
     }
   }
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP

@@ -351,18 +351,32 @@ k_badmm_generic(const IterArgs<T> a, T* __restrict__ scr, int64_t n_items) {
 template <typename T>
 __global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_item, int m,
                        T* __restrict__ S, T* __restrict__ w, int rule, int finalize, int* err) {
+  // rows in passes of R = min(m, blockDim); S = blockDim/R slices take items s, s+S, ... in order,
+  // then slice partials are added in slice order: deterministic for a fixed launch shape.
   const int c = blockIdx.x;
   const int64_t ib = cl_item[c], ie = cl_item[c + 1];
   extern __shared__ unsigned char smraw[];
-  T* sh = reinterpret_cast<T*>(smraw);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+  T* red = reinterpret_cast<T*>(smraw);               // [blockDim]
+  T* sh = red + blockDim.x;                            // [m]
+  const int R = m < (int)blockDim.x ? m : (int)blockDim.x;
+  const int NS = (int)blockDim.x / R;
+  const int r = threadIdx.x % R, sl = threadIdx.x / R;
+  for (int i0 = 0; i0 < m; i0 += R) {
+    const int i = i0 + r;
     T s = T(0);
-    for (int64_t it = ib; it < ie; ++it) s += pw[it * m + i];
-    S[(int64_t)c * m + i] = s;
-    sh[i] = (rule == 1) ? s * s : s;
+    if (sl < NS && i < m)
+      for (int64_t it = ib + sl; it < ie; it += NS) s += pw[it * m + i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (sl == 0 && i < m) {
+      T t = T(0);
+      for (int u = 0; u < NS; ++u) t += red[u * R + r];
+      S[(int64_t)c * m + i] = t;
+      sh[i] = (rule == 1) ? t * t : t;
+    }
+    __syncthreads();
   }
   if (!finalize) return;
-  __syncthreads();
   __shared__ T tot;
   if (threadIdx.x == 0) {
     T t = T(0);

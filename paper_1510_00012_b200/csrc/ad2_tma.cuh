@@ -62,13 +62,16 @@ struct TmaLayout {
   static constexpr int G = 32 / MP;
   static constexpr int MK = MP * NCH;
   static constexpr int CAP = 32 * MK;          // plan entries staged per pass (G*MP rows x MK cols)
-  static constexpr int YCAP = G * MK * DP;     // support coordinates staged per pass
+  static constexpr int DYMAX = DP + 16 / (int)sizeof(T);   // Y row: DP coordinates + |y|^2 (+pad)
+  static constexpr int YCAP = G * MK * DYMAX;  // support coordinates staged per pass
   static constexpr int STAGE = 2 * CAP + YCAP; // elements: [P|L|Y]
   static constexpr int TILE = MP * 32;
   static constexpr int FB = G * MK;
   static constexpr size_t WARP_BYTES =
       ((sizeof(T) * (size_t)(2 * STAGE + TILE + FB) + 16 + 127) / 128) * 128;
   static constexpr size_t CTA_BYTES = NWARP * WARP_BYTES;
+  // static shared memory of the kernel (item-partial combination), for the capacity check
+  static constexpr size_t STATIC_BYTES = sizeof(T) * (size_t)NWARP * G * MP * (DP + 1);
 };
 
 template <typename T, int MP, int NCH, int MODE, int DP>

@@ -47,6 +47,20 @@ static void go_nch(int variant, int mode, int dp, const IterArgs<float>& a, int6
 using namespace ad2k;
 
 template <typename T, int MP>
+size_t tma_cta_bytes(int nch, int dp);
+
+template <>
+size_t tma_cta_bytes<float, 16>(int nch, int dp) {
+  auto f = [](size_t a, size_t b) { return a + b; };
+  if (nch == 2 && 16 < 32) {
+    if (dp <= 4) return f(TmaLayout<float, 16, (16 < 32 ? 2 : 1), 4>::CTA_BYTES, TmaLayout<float, 16, (16 < 32 ? 2 : 1), 4>::STATIC_BYTES);
+    return f(TmaLayout<float, 16, (16 < 32 ? 2 : 1), 16>::CTA_BYTES, TmaLayout<float, 16, (16 < 32 ? 2 : 1), 16>::STATIC_BYTES);
+  }
+  if (dp <= 4) return f(TmaLayout<float, 16, 1, 4>::CTA_BYTES, TmaLayout<float, 16, 1, 4>::STATIC_BYTES);
+  return f(TmaLayout<float, 16, 1, 16>::CTA_BYTES, TmaLayout<float, 16, 1, 16>::STATIC_BYTES);
+}
+
+template <typename T, int MP>
 void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
 
 template <>
