@@ -416,7 +416,7 @@ static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, doubl
   if (ctx->N == 0) return;
   k_gather<T><<<(unsigned)((ctx->N + 3) / 4), 128, 0, ctx->stream>>>(
       ctx->d_order.as<int32_t>(), ctx->d_orig_off.as<int64_t>(), ctx->d_off.as<int64_t>(), (const T*)Ysrc,
-      (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, ctx->dy, ctx->variant == 2 ? ctx->d : -1, wtol,
+      (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, ctx->dy, ctx->variant == 2 ? (ctx->dp == 4 ? 3 : 16) : -1, wtol,
       ctx->d_err.as<int>());
 }
 
@@ -547,7 +547,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   }
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
   const int ld = variant == 2 ? mp : m;
-  const int dy = variant == 2 ? std::max(dp, (d + 1 + E - 1) / E * E) : d;
+  const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : d;     // = TmaLayout::DY
   if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");
   const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * ITEM_PASSES : 1;
   std::vector<int64_t> item_mb, cl_item(K + 1, 0);

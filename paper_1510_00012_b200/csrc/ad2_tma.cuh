@@ -62,8 +62,10 @@ struct TmaLayout {
   static constexpr int G = 32 / MP;
   static constexpr int MK = MP * NCH;
   static constexpr int CAP = 32 * MK;          // plan entries staged per pass (G*MP rows x MK cols)
-  static constexpr int DYMAX = DP + 16 / (int)sizeof(T);   // Y row: DP coordinates + |y|^2 (+pad)
-  static constexpr int YCAP = G * MK * DYMAX;  // support coordinates staged per pass
+  // Y row = [y_0..y_{d-1}, 0.., |y|^2 at YYI, 0..] with DY elements (16-byte multiple)
+  static constexpr int DY = (DP == 4) ? 4 : DP + 16 / (int)sizeof(T);
+  static constexpr int YYI = (DP == 4) ? 3 : DP;
+  static constexpr int YCAP = G * MK * DY;     // support coordinates staged per pass
   static constexpr int STAGE = 2 * CAP + YCAP; // elements: [P|L|Y]
   static constexpr int TILE = MP * 32;
   static constexpr int FB = G * MK;
@@ -74,15 +76,36 @@ struct TmaLayout {
   static constexpr size_t STATIC_BYTES = sizeof(T) * (size_t)NWARP * G * MP * (DP + 1);
 };
 
+// pair arithmetic: packed f32x2 (FADD2/FMUL2/FFMA2, sm_100) for fp32, componentwise for fp64
+template <typename T> struct Pr;
+template <> struct Pr<float> {
+  using t = float2;
+  static __device__ __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+  static __device__ __forceinline__ float2 add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+  static __device__ __forceinline__ float2 mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+  static __device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+};
+template <> struct Pr<double> {
+  using t = double2;
+  static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+  static __device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+  static __device__ __forceinline__ double2 mul(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+  static __device__ __forceinline__ double2 fma(double2 a, double2 b, double2 c) {
+    return make_double2(::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y));
+  }
+};
+
 template <typename T, int MP, int NCH, int MODE, int DP>
 __global__ void __launch_bounds__(NWARP * 32)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
+  using PR = Pr<T>;
+  using T2 = typename PR::t;
   using Lay = TmaLayout<T, MP, NCH, DP>;
-  constexpr int G = Lay::G, MK = Lay::MK, CAP = Lay::CAP;
+  constexpr int G = Lay::G, MK = Lay::MK, CAP = Lay::CAP, DY = Lay::DY, YYI = Lay::YYI;
   constexpr int E = 16 / (int)sizeof(T);
-  constexpr int NB = MK / 4;                          // column blocks (warp-uniform skip past m_k)
+  constexpr int NB = MK / 4;                          // column blocks of 4 (2 pairs), skipped past m_k
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* wb = reinterpret_cast<T*>(smem_raw + (size_t)warp * Lay::WARP_BYTES);
@@ -92,26 +115,32 @@ k_badmm_tma(const IterArgs<T> a) {
   uint64_t* const bar = reinterpret_cast<uint64_t*>(
       reinterpret_cast<unsigned char*>(fbuf + Lay::FB) + ((16 - ((uintptr_t)(fbuf + Lay::FB) & 15)) & 15));
 
-  // lane (seg, i): row i of the seg-th member of a pass.  Blocks have ld == MP rows; rows
-  // i >= m are zero padding and stay zero (eps_r = 0 there), so no per-entry row predicates.
+  // Lane (seg, i) = row i of the seg-th member of a pass.  Blocks have MP rows; rows i >= m are
+  // zero padding that stays zero (eps_r = 0 there).  Columns j >= m_k of a block are masked at
+  // load (p = Lambda = 0) and contribute exactly 0 to every sum: row masses are formed as
+  // sum_j p_j e_j + m_k eps (= sum over the m_k real columns of (p_j e_j + eps)).
   const int seg = lane / MP, i = lane - seg * MP;
   const int item = blockIdx.x;
   const int c = a.item_cl[item];
   const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
-  const int m = a.m, d = a.d, dy = a.dy;
+  const int m = a.m, d = a.d;
   const bool rowok = i < m;
   const T kx = a.kx[c];
   const T rho = a.rho[c];
   const T eps_r = rowok ? a.eps : T(0);
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
-  // cost operands: C_ij = (|x_i|^2 + |y_j|^2) + sum_t (-2 x_it) y_jt, |y_j|^2 staged at Y[j][d]
-  T xn[DP];
+  const T2 kx2 = PR::make(kx, kx), nkx2 = PR::make(-kx, -kx), rho2 = PR::make(rho, rho);
+  const T2 nrho2 = PR::make(-rho, -rho), eps2 = PR::make(eps_r, eps_r);
+  // cost C_ij = (|x_i|^2 + |y_j|^2) + sum_t (-2 x_it) y_jt, coordinates taken in pairs
+  T2 xn2[DP / 2];
   T xx = T(0);
 #pragma unroll
-  for (int t = 0; t < DP; ++t) {
-    const T v = (rowok && t < d) ? a.x[((int64_t)c * m + i) * d + t] : T(0);
-    xx += v * v;
-    xn[t] = T(-2) * v;
+  for (int t = 0; t < DP / 2; ++t) {
+    const T v0 = (rowok && 2 * t < d) ? a.x[((int64_t)c * m + i) * d + 2 * t] : T(0);
+    const T v1 = (rowok && 2 * t + 1 < d) ? a.x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
+    xx += v0 * v0;
+    xx += v1 * v1;
+    xn2[t] = PR::make(T(-2) * v0, T(-2) * v1);
   }
   T accw = T(0), accm = T(0);
   T accx[(MODE == P2ONLY) ? DP : 1];
@@ -123,6 +152,13 @@ k_badmm_tma(const IterArgs<T> a) {
   T* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
   const int64_t step = (int64_t)NWARP * G;
 
+  // stale shared memory past a pass's supports must be finite: zero both Y stages once
+  for (int e = lane * E; e < Lay::YCAP; e += 32 * E) {
+    *reinterpret_cast<V*>(sPL + 2 * CAP + e) = V{};
+    *reinterpret_cast<V*>(sPL + Lay::STAGE + 2 * CAP + e) = V{};
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -135,12 +171,12 @@ k_badmm_tma(const IterArgs<T> a) {
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
     const int64_t p0 = a.off[k0], p1 = a.off[k1];
     const uint32_t bp = (uint32_t)((int64_t)MP * (p1 - p0) * (int64_t)sizeof(T));
-    const uint32_t by = (uint32_t)((int64_t)dy * (p1 - p0) * (int64_t)sizeof(T));
+    const uint32_t by = (uint32_t)((int64_t)DY * (p1 - p0) * (int64_t)sizeof(T));
     T* st = sPL + (t & 1) * Lay::STAGE;
     mbar_expect_tx(&bar[t & 1], 2 * bp + by);
     tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
     tma_load(st + CAP, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + 2 * CAP, a.Y + (int64_t)dy * p0, by, &bar[t & 1]);
+    tma_load(st + 2 * CAP, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
   };
   if (lane == 0) issue(0);
 
@@ -158,6 +194,7 @@ k_badmm_tma(const IterArgs<T> a) {
     const int64_t o0 = has ? a.off[k] : pbase;
     const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
     const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
+    const T mkeps = (T)mk * eps_r;
     T omv[NCH];                                        // w^(k)_j for the column this lane sums
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) omv[ch] = (ch * MP + i < mk) ? __ldg(a.om + o0 + ch * MP + i) : T(0);
@@ -166,99 +203,122 @@ k_badmm_tma(const IterArgs<T> a) {
     const int rel = (int)(o0 - pbase);
     T* const Ps = st + MP * rel;
     T* const Ls = st + CAP + MP * rel;
-    const T* const Ys = st + 2 * CAP + dy * rel;
+    const T* const Ys = st + 2 * CAP + DY * rel;
 
-    T p[MK], l[MK], q[MK];
+    T2 p2[MK / 2], l2[MK / 2], q2[MK / 2];
+    // ---- load (columns >= m_k masked to 0) and, unless P1ONLY, the first half of phase 2:
+    //      pe = Pi1 exp(Lambda/rho) (Eq.badmmc1b without eps), r = sum_j pe_j + m_k eps
+    T2 racc = PR::make(T(0), T(0));
 #pragma unroll
     for (int jb = 0; jb < NB; ++jb) {
       if (4 * jb >= mkw) break;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = 4 * jb + u;
-        p[j] = Ps[j * MP + i];
-        l[j] = Ls[j * MP + i];
-      }
-    }
-    if constexpr (MODE == P1ONLY) {
-#pragma unroll
-      for (int j = 0; j < MK; ++j) q[j] = p[j];                       // Pi2^(0)
-    } else {
-      // phase 2 of the previous iteration: Eq.badmmc1b (Lambda^n), Eq.badmmc1, Eq.badmm2
-      T r = T(0);
-#pragma unroll
-      for (int jb = 0; jb < NB; ++jb) {
-        if (4 * jb >= mkw) break;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          const T b = p[j] * N::ex(l[j] * kx) + eps_r;
-          q[j] = (j < mk) ? b : T(0);
-          r += q[j];
-        }
-      }
-      const T f = (has && rowok) ? wi / r : T(0);
-#pragma unroll
-      for (int jb = 0; jb < NB; ++jb) {
-        if (4 * jb >= mkw) break;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          q[j] = q[j] * f;
-          l[j] = l[j] + rho * (p[j] - q[j]);
+      for (int h = 0; h < 2; ++h) {
+        const int jp = 2 * jb + h, j = 2 * jp;
+        const bool v0 = j < mk, v1 = j + 1 < mk;
+        const T pa = Ps[j * MP + i], pb = Ps[(j + 1) * MP + i];
+        const T la = Ls[j * MP + i], lb = Ls[(j + 1) * MP + i];
+        p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
+        l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
+        if constexpr (MODE == P1ONLY) {
+          q2[jp] = p2[jp];                                             // Pi2^(0)
+        } else {
+          const T2 ar = PR::mul(l2[jp], kx2);
+          const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
+          q2[jp] = PR::mul(p2[jp], e);
+          racc = PR::add(racc, q2[jp]);
         }
       }
     }
+    T f = T(0);
+    if constexpr (MODE != P1ONLY) {
+      const T r = racc.x + racc.y + mkeps;
+      f = (has && rowok) ? wi / r : T(0);                           // Eq.badmmc1: w_i / rowsum
+    }
+    const T2 f2 = PR::make(f, f), ef2 = PR::make(eps_r * f, eps_r * f);
+
     if constexpr (MODE == P2ONLY) {
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          if (j < mk) {
-            Ps[j * MP + i] = q[j];
-            Ls[j * MP + i] = l[j];
-            // support-update partials (Eq.updatex, X5): sum_j pi2_ij y_j and sum_j pi2_ij
-            accm += q[j];
+        for (int h = 0; h < 2; ++h) {
+          const int jp = 2 * jb + h, j = 2 * jp;
+          const T2 q = PR::fma(q2[jp], f2, ef2);                        // Pi2 = (pe + eps) w_i / r
+          const T2 l = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));  // Eq.badmm2
 #pragma unroll
-            for (int tt = 0; tt < DP / E; ++tt) {
-              const V v = *reinterpret_cast<const V*>(Ys + j * dy + tt * E);
-              const T* ve = reinterpret_cast<const T*>(&v);
+          for (int u = 0; u < 2; ++u) {
+            const int jj = j + u;
+            const T qv = u ? q.y : q.x, lv = u ? l.y : l.x;
+            if (G == 1 || jj < mk) {
+              Ps[jj * MP + i] = qv;
+              Ls[jj * MP + i] = lv;
+            }
+            if (jj < mk) {                   // support-update partials (Eq.updatex, X5)
+              accm += qv;
 #pragma unroll
-              for (int u2 = 0; u2 < E; ++u2) accx[tt * E + u2] += q[j] * ve[u2];
+              for (int tt = 0; tt < DP / E; ++tt) {
+                const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
+                const T* ve = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                for (int u2 = 0; u2 < E; ++u2) accx[tt * E + u2] += qv * ve[u2];
+              }
             }
           }
         }
       }
     } else {
-      // phase 1: C_ij, pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
+      // ---- rest of phase 2 (FUSED) and phase 1:
+      //      C_ij; pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b) -> tile
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          const T* yj = Ys + j * dy;
-          T cst = xx + yj[d];
-#pragma unroll
-          for (int tt = 0; tt < DP / E; ++tt) {
-            const V v = *reinterpret_cast<const V*>(yj + tt * E);
-            const T* ve = reinterpret_cast<const T*>(&v);
-#pragma unroll
-            for (int u2 = 0; u2 < E; ++u2) cst = fma(xn[tt * E + u2], ve[u2], cst);
+        for (int h = 0; h < 2; ++h) {
+          const int jp = 2 * jb + h, j = 2 * jp;
+          T2 q = q2[jp];
+          if constexpr (MODE == FUSED) {
+            q = PR::fma(q2[jp], f2, ef2);                                 // Pi2 (Eq.badmmc1)
+            l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
           }
-          const T av = q[j] * N::ex(-(cst + l[j]) * kx) + eps_r;
-          p[j] = (j < mk) ? av : T(0);
+          T cst[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const T* yj = Ys + (j + u) * DY;
+            T2 c2 = PR::make(xx + yj[YYI], T(0));
+#pragma unroll
+            for (int tt = 0; tt < DP / E; ++tt) {
+              const V v = *reinterpret_cast<const V*>(yj + tt * E);
+              const T2* vp = reinterpret_cast<const T2*>(&v);
+#pragma unroll
+              for (int u2 = 0; u2 < E / 2; ++u2) c2 = PR::fma(xn2[tt * (E / 2) + u2], vp[u2], c2);
+            }
+            cst[u] = c2.x + c2.y;
+          }
+          const T2 ar = PR::mul(PR::add(PR::make(cst[0], cst[1]), l2[jp]), nkx2);
+          const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
+          p2[jp] = PR::fma(q, e, eps2);                                    // pt2 (column j >= m_k: finite)
+          if (j < MP) {                                                    // chunk 0 -> transpose tile
+            tile[j * 32 + ((((lane / E) ^ (j & 7))) * E) + (lane % E)] = p2[jp].x;
+            tile[(j + 1) * 32 + ((((lane / E) ^ ((j + 1) & 7))) * E) + (lane % E)] = p2[jp].y;
+          }
         }
       }
-      // column sums (Eq.badmmc0 denominators) through the swizzled transpose tile
+      // column sums over the m rows (Eq.badmmc0 denominators); NCH == 2 reuses the tile per chunk
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        __syncwarp();
+        if (ch == 1) {
+          __syncwarp();
 #pragma unroll
-        for (int u = 0; u < MP; ++u) {
-          if (ch * MP + (u & ~3) >= mkw) break;
-          tile[u * 32 + ((((lane / E) ^ (u & 7))) * E) + (lane % E)] = p[ch * MP + u];
+          for (int jb = MP / 4; jb < NB; ++jb) {
+            if (4 * jb >= mkw) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * jb + u, jt = j - MP;
+              const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
+              tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;
+            }
+          }
         }
         __syncwarp();
         T s = T(0);
@@ -268,47 +328,42 @@ k_badmm_tma(const IterArgs<T> a) {
           s += Vec16<T>::hsum(v);
         }
         const int jc = ch * MP + i;
-        fbuf[seg * MK + jc] = (jc < mk) ? omv[ch] / s : T(0);          // Eq.badmmc0
+        fbuf[seg * MK + jc] = (jc < mk) ? omv[ch] / s : T(0);           // Eq.badmmc0: w_j^(k) / colsum
       }
       __syncwarp();
-      T r2 = T(0);
+      // ---- Pi1 = pt2 * factor_j; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row masses
+      T2 racc2 = PR::make(T(0), T(0));
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
-        T fe[4];
+        const V fv = *reinterpret_cast<const V*>(&fbuf[seg * MK + 4 * jb]);
+        const T2* fp = reinterpret_cast<const T2*>(&fv);
 #pragma unroll
-        for (int u = 0; u < 4; u += E) {
-          const V fv = *reinterpret_cast<const V*>(&fbuf[seg * MK + 4 * jb + u]);
+        for (int h = 0; h < 2; ++h) {
+          const int jp = 2 * jb + h, j = 2 * jp;
+          const T2 fj = (E == 4) ? fp[h] : *reinterpret_cast<const T2*>(&fbuf[seg * MK + j]);
+          p2[jp] = PR::mul(p2[jp], fj);
+          const T2 ar = PR::mul(l2[jp], kx2);
+          const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
+          racc2 = PR::fma(p2[jp], e, racc2);
 #pragma unroll
-          for (int u2 = 0; u2 < E; ++u2) fe[u + u2] = reinterpret_cast<const T*>(&fv)[u2];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          p[j] = p[j] * fe[u];
-          const T b = p[j] * N::ex(l[j] * kx) + eps_r;                  // Eq.badmmc1b row mass
-          r2 += (j < mk) ? b : T(0);
+          for (int u = 0; u < 2; ++u) {
+            const int jj = j + u;
+            if (G == 1 || jj < mk) {
+              Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
+              if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+            }
+          }
         }
       }
+      const T r2 = racc2.x + racc2.y + mkeps;
       T R = r2;
 #pragma unroll
       for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
       if (has && rowok) {
-        const T wt = r2 / R;
+        const T wt = r2 / R;                                             // normalised row mass
         accw += (a.rule == 1) ? sqrt(wt) : wt;
         bad |= !isfinite(wt);
-      }
-#pragma unroll
-      for (int jb = 0; jb < NB; ++jb) {
-        if (4 * jb >= mkw) break;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * jb + u;
-          if (j < mk) {
-            Ps[j * MP + i] = p[j];
-            if (MODE == FUSED) Ls[j * MP + i] = l[j];
-          }
-        }
       }
     }
     // results leave by bulk stores from the same slots
