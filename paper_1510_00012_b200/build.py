@@ -15,7 +15,8 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libad2.so")
 CSRC = os.path.join(HERE, "csrc")
 SRCS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
-DEPS = SRCS + [os.path.join(CSRC, "ad2_kernels.cuh"), os.path.join(ROOT, "include", "ad2.h")]
+DEPS = SRCS + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + \
+    [os.path.join(ROOT, "include", "ad2.h"), os.path.abspath(__file__)]
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

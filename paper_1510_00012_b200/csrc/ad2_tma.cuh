@@ -61,16 +61,19 @@ template <typename T, int MP, int NCH, int DP>
 struct TmaLayout {
   static constexpr int G = 32 / MP;
   static constexpr int MK = MP * NCH;
-  static constexpr int CAP = 32 * MK;          // plan entries staged per pass (G*MP rows x MK cols)
+  static constexpr int E = 16 / (int)sizeof(T);
   // Y row = [y_0..y_{d-1}, 0.., |y|^2 at YYI, 0..] with DY elements (16-byte multiple)
-  static constexpr int DY = (DP == 4) ? 4 : DP + 16 / (int)sizeof(T);
+  static constexpr int DY = (DP == 4) ? 4 : DP + E;
   static constexpr int YYI = (DP == 4) ? 3 : DP;
-  static constexpr int YCAP = G * MK * DY;     // support coordinates staged per pass
-  static constexpr int STAGE = 2 * CAP + YCAP; // elements: [P|L|Y]
-  static constexpr int TILE = MP * 32;
+  // one pass = [P block | L block | Y block] of G consecutive members, placed in a per-warp ring
+  static constexpr int MAXPASS = (2 * MP + DY) * G * MK;            // elements
+  static constexpr int RING = ((3 * MAXPASS / 2) + 63) / 64 * 64;   // two passes in flight (typ.)
+  // in-bounds over-reads past a pass region: G == 1 reads at most 3 masked columns past m_k
+  static constexpr int SLACK = ((G == 1 ? 4 * DY : MK * DY + MP * MK) + 63) / 64 * 64;
+  static constexpr int TILE = (G == 1) ? 0 : MP * 32;               // G == 1: tile = the pass's P slot
   static constexpr int FB = G * MK;
   static constexpr size_t WARP_BYTES =
-      ((sizeof(T) * (size_t)(2 * STAGE + TILE + FB) + 16 + 127) / 128) * 128;
+      ((sizeof(T) * (size_t)(RING + SLACK + TILE + FB) + 16 + 127) / 128) * 128;
   static constexpr size_t CTA_BYTES = NWARP * WARP_BYTES;
   // static shared memory of the kernel (item-partial combination), for the capacity check
   static constexpr size_t STATIC_BYTES = sizeof(T) * (size_t)NWARP * G * MP * (DP + 1);
@@ -96,22 +99,22 @@ template <> struct Pr<double> {
 };
 
 template <typename T, int MP, int NCH, int MODE, int DP>
-__global__ void __launch_bounds__(NWARP * 32)
+__global__ void __launch_bounds__(NWARP * 32, 3)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
   using PR = Pr<T>;
   using T2 = typename PR::t;
   using Lay = TmaLayout<T, MP, NCH, DP>;
-  constexpr int G = Lay::G, MK = Lay::MK, CAP = Lay::CAP, DY = Lay::DY, YYI = Lay::YYI;
-  constexpr int E = 16 / (int)sizeof(T);
+  constexpr int G = Lay::G, MK = Lay::MK, DY = Lay::DY, YYI = Lay::YYI, RING = Lay::RING;
+  constexpr int E = Lay::E;
   constexpr int NB = MK / 4;                          // column blocks of 4 (2 pairs), skipped past m_k
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* wb = reinterpret_cast<T*>(smem_raw + (size_t)warp * Lay::WARP_BYTES);
-  T* const sPL = wb;                                   // two stages of [P | L | Y]
-  T* const tile = wb + 2 * Lay::STAGE;                 // column-sum transpose tile [MP][32]
-  T* const fbuf = tile + Lay::TILE;                    // per-column factors [G][MK]
+  T* const ring = wb;                                  // per-warp ring of pass regions [P|L|Y]
+  T* const tile_sep = wb + RING + Lay::SLACK;          // G > 1: column-sum transpose tile [MP][32]
+  T* const fbuf = tile_sep + Lay::TILE;                // per-column factors [G][MK]
   uint64_t* const bar = reinterpret_cast<uint64_t*>(
       reinterpret_cast<unsigned char*>(fbuf + Lay::FB) + ((16 - ((uintptr_t)(fbuf + Lay::FB) & 15)) & 15));
 
@@ -152,11 +155,8 @@ k_badmm_tma(const IterArgs<T> a) {
   T* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
   const int64_t step = (int64_t)NWARP * G;
 
-  // stale shared memory past a pass's supports must be finite: zero both Y stages once
-  for (int e = lane * E; e < Lay::YCAP; e += 32 * E) {
-    *reinterpret_cast<V*>(sPL + 2 * CAP + e) = V{};
-    *reinterpret_cast<V*>(sPL + Lay::STAGE + 2 * CAP + e) = V{};
-  }
+  // ring (and its over-read slack) zeroed once: every value it ever holds is then finite
+  for (int e = lane * E; e < RING + Lay::SLACK; e += 32 * E) *reinterpret_cast<V*>(ring + e) = V{};
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
@@ -165,33 +165,48 @@ k_badmm_tma(const IterArgs<T> a) {
     fence_mbar_init();
   }
   __syncwarp();
-  auto issue = [&](int t) {                            // lane 0 only
+  // pass geometry (warp-uniform): points [p0, p1) of members [k0, k1)
+  auto pass_pts = [&](int t, int64_t& p0, int64_t& p1) -> int {
     const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;
-    if (k0 >= me) return;
+    if (k0 >= me) return 0;
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
-    const int64_t p0 = a.off[k0], p1 = a.off[k1];
-    const uint32_t bp = (uint32_t)((int64_t)MP * (p1 - p0) * (int64_t)sizeof(T));
-    const uint32_t by = (uint32_t)((int64_t)DY * (p1 - p0) * (int64_t)sizeof(T));
-    T* st = sPL + (t & 1) * Lay::STAGE;
+    p0 = a.off[k0];
+    p1 = a.off[k1];
+    return (int)(p1 - p0);
+  };
+  auto issue = [&](int t, int base, int64_t p0, int np) {              // lane 0 only
+    const uint32_t bp = (uint32_t)(MP * np * (int)sizeof(T));
+    const uint32_t by = (uint32_t)(DY * np * (int)sizeof(T));
+    T* st = ring + base;
     mbar_expect_tx(&bar[t & 1], 2 * bp + by);
     tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + CAP, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + 2 * CAP, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
+    tma_load(st + MP * np, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
+    tma_load(st + 2 * MP * np, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
   };
-  if (lane == 0) issue(0);
+  int64_t cp0 = 0, cp1 = 0;
+  int cnp = pass_pts(0, cp0, cp1);
+  int cbase = 0;                                       // ring offset of the current pass
+  if (lane == 0 && cnp > 0) issue(0, 0, cp0, cnp);
 
-  for (int t = 0;; ++t) {
-    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;   // warp-uniform
-    if (k0 >= me) break;
-    if (lane == 0) {
-      bulk_wait_read_all();          // stores of pass t-1 have left the stage about to be refilled
-      issue(t + 1);
+  for (int t = 0; cnp > 0; ++t) {
+    // place pass t+1 behind pass t (or at the ring start) while t computes
+    int64_t np0 = 0, np1 = 0;
+    const int nnp = pass_pts(t + 1, np0, np1);
+    const int csize = (2 * MP + DY) * cnp, nsize = (2 * MP + DY) * nnp;
+    int nbase = -1;
+    if (nnp > 0) {
+      if (cbase + csize + nsize <= RING) nbase = cbase + csize;
+      else if (nsize <= cbase) nbase = 0;
     }
+    if (lane == 0 && nbase >= 0) {
+      bulk_wait_read_all();          // pass t-1 has left its region
+      issue(t + 1, nbase, np0, nnp);
+    }
+    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
-    const int64_t pbase = a.off[k0];
     const int64_t k = k0 + seg;
     const bool has = k < k1;
-    const int64_t o0 = has ? a.off[k] : pbase;
+    const int64_t o0 = has ? a.off[k] : cp0;
     const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
     const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
     const T mkeps = (T)mk * eps_r;
@@ -199,16 +214,17 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) omv[ch] = (ch * MP + i < mk) ? __ldg(a.om + o0 + ch * MP + i) : T(0);
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
-    T* const st = sPL + (t & 1) * Lay::STAGE;
-    const int rel = (int)(o0 - pbase);
+    T* const st = ring + cbase;
+    const int rel = (int)(o0 - cp0);
     T* const Ps = st + MP * rel;
-    T* const Ls = st + CAP + MP * rel;
-    const T* const Ys = st + 2 * CAP + DY * rel;
+    T* const Ls = st + MP * cnp + MP * rel;
+    const T* const Ys = st + 2 * MP * cnp + DY * rel;
+    T* const tile = (G == 1) ? st : tile_sep;          // G == 1: reuse this pass's P slot
 
     T2 p2[MK / 2], l2[MK / 2], q2[MK / 2];
     // ---- load (columns >= m_k masked to 0) and, unless P1ONLY, the first half of phase 2:
     //      pe = Pi1 exp(Lambda/rho) (Eq.badmmc1b without eps), r = sum_j pe_j + m_k eps
-    T2 racc = PR::make(T(0), T(0));
+    T2 racc[2] = {PR::make(T(0), T(0)), PR::make(T(0), T(0))};
 #pragma unroll
     for (int jb = 0; jb < NB; ++jb) {
       if (4 * jb >= mkw) break;
@@ -226,13 +242,13 @@ k_badmm_tma(const IterArgs<T> a) {
           const T2 ar = PR::mul(l2[jp], kx2);
           const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
           q2[jp] = PR::mul(p2[jp], e);
-          racc = PR::add(racc, q2[jp]);
+          racc[h] = PR::add(racc[h], q2[jp]);
         }
       }
     }
     T f = T(0);
     if constexpr (MODE != P1ONLY) {
-      const T r = racc.x + racc.y + mkeps;
+      const T r = (racc[0].x + racc[1].x) + (racc[0].y + racc[1].y) + mkeps;
       f = (has && rowok) ? wi / r : T(0);                           // Eq.badmmc1: w_i / rowsum
     }
     const T2 f2 = PR::make(f, f), ef2 = PR::make(eps_r * f, eps_r * f);
@@ -250,7 +266,7 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             const T qv = u ? q.y : q.x, lv = u ? l.y : l.x;
-            if (G == 1 || jj < mk) {
+            if (jj < mk) {                 // blocks are packed: no tail writes
               Ps[jj * MP + i] = qv;
               Ls[jj * MP + i] = lv;
             }
@@ -268,11 +284,25 @@ k_badmm_tma(const IterArgs<T> a) {
         }
       }
     } else {
-      // ---- rest of phase 2 (FUSED) and phase 1:
+      // ---- rest of phase 2 (FUSED) and phase 1, four columns at a time:
       //      C_ij; pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b) -> tile
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
+        T2 c2[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c2[u] = PR::make(xx + Ys[(4 * jb + u) * DY + YYI], T(0));
+#pragma unroll
+        for (int tt = 0; tt < DP / E; ++tt) {
+          V v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const V*>(Ys + (4 * jb + u) * DY + tt * E);
+#pragma unroll
+          for (int u2 = 0; u2 < E / 2; ++u2)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              c2[u] = PR::fma(xn2[tt * (E / 2) + u2], reinterpret_cast<const T2*>(&v[u])[u2], c2[u]);
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int jp = 2 * jb + h, j = 2 * jp;
@@ -281,58 +311,42 @@ k_badmm_tma(const IterArgs<T> a) {
             q = PR::fma(q2[jp], f2, ef2);                                 // Pi2 (Eq.badmmc1)
             l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
           }
-          T cst[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const T* yj = Ys + (j + u) * DY;
-            T2 c2 = PR::make(xx + yj[YYI], T(0));
-#pragma unroll
-            for (int tt = 0; tt < DP / E; ++tt) {
-              const V v = *reinterpret_cast<const V*>(yj + tt * E);
-              const T2* vp = reinterpret_cast<const T2*>(&v);
-#pragma unroll
-              for (int u2 = 0; u2 < E / 2; ++u2) c2 = PR::fma(xn2[tt * (E / 2) + u2], vp[u2], c2);
-            }
-            cst[u] = c2.x + c2.y;
-          }
-          const T2 ar = PR::mul(PR::add(PR::make(cst[0], cst[1]), l2[jp]), nkx2);
+          const T2 cst = PR::make(c2[2 * h].x + c2[2 * h].y, c2[2 * h + 1].x + c2[2 * h + 1].y);
+          const T2 ar = PR::mul(PR::add(cst, l2[jp]), nkx2);
           const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
           p2[jp] = PR::fma(q, e, eps2);                                    // pt2 (column j >= m_k: finite)
-          if (j < MP) {                                                    // chunk 0 -> transpose tile
-            tile[j * 32 + ((((lane / E) ^ (j & 7))) * E) + (lane % E)] = p2[jp].x;
-            tile[(j + 1) * 32 + ((((lane / E) ^ ((j + 1) & 7))) * E) + (lane % E)] = p2[jp].y;
-          }
         }
       }
-      // column sums over the m rows (Eq.badmmc0 denominators); NCH == 2 reuses the tile per chunk
+      // column sums over the m rows (Eq.badmmc0 denominators) through the swizzled tile
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        if (ch == 1) {
-          __syncwarp();
+        __syncwarp();                                                    // P slot / tile free
 #pragma unroll
-          for (int jb = MP / 4; jb < NB; ++jb) {
-            if (4 * jb >= mkw) break;
+        for (int jb = ch * (MP / 4); jb < (ch + 1) * (MP / 4); ++jb) {
+          if (4 * jb >= mkw) break;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = 4 * jb + u, jt = j - MP;
-              const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
-              tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;
-            }
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * jb + u, jt = j - ch * MP;
+            const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
+            tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;
           }
         }
         __syncwarp();
-        T s = T(0);
-#pragma unroll
-        for (int cc = 0; cc < MP / E; ++cc) {
-          const V v = *reinterpret_cast<const V*>(&tile[i * 32 + ((seg * (MP / E) + cc) ^ (i & 7)) * E]);
-          s += Vec16<T>::hsum(v);
-        }
         const int jc = ch * MP + i;
+        T s = T(1);
+        if (jc < mk) {
+          s = T(0);
+#pragma unroll
+          for (int cc = 0; cc < MP / E; ++cc) {
+            const V v = *reinterpret_cast<const V*>(&tile[i * 32 + ((seg * (MP / E) + cc) ^ (i & 7)) * E]);
+            s += Vec16<T>::hsum(v);
+          }
+        }
         fbuf[seg * MK + jc] = (jc < mk) ? omv[ch] / s : T(0);           // Eq.badmmc0: w_j^(k) / colsum
       }
       __syncwarp();
       // ---- Pi1 = pt2 * factor_j; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row masses
-      T2 racc2 = PR::make(T(0), T(0));
+      T2 racc2[2] = {PR::make(T(0), T(0)), PR::make(T(0), T(0))};
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
@@ -345,18 +359,18 @@ k_badmm_tma(const IterArgs<T> a) {
           p2[jp] = PR::mul(p2[jp], fj);
           const T2 ar = PR::mul(l2[jp], kx2);
           const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
-          racc2 = PR::fma(p2[jp], e, racc2);
+          racc2[h] = PR::fma(p2[jp], e, racc2[h]);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
-            if (G == 1 || jj < mk) {
+            if (jj < mk) {                 // blocks are packed: no tail writes
               Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
               if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
             }
           }
         }
       }
-      const T r2 = racc2.x + racc2.y + mkeps;
+      const T r2 = (racc2[0].x + racc2[1].x) + (racc2[0].y + racc2[1].y) + mkeps;
       T R = r2;
 #pragma unroll
       for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
@@ -370,12 +384,20 @@ k_badmm_tma(const IterArgs<T> a) {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      const int64_t p1 = a.off[k1];
-      const uint32_t bp = (uint32_t)((int64_t)MP * (p1 - pbase) * (int64_t)sizeof(T));
-      tma_store(dst_plan + (int64_t)MP * pbase, st, bp);
-      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * pbase, st + CAP, bp);
+      const uint32_t bp = (uint32_t)(MP * cnp * (int)sizeof(T));
+      tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
+      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cnp, bp);
       bulk_commit();
+      if (nnp > 0 && nbase < 0) {    // pass t+1 did not fit beside pass t: issue it now at the ring start
+        bulk_wait_read_all();
+        issue(t + 1, 0, np0, nnp);
+      }
     }
+    if (nnp > 0 && nbase < 0) nbase = 0;
+    cbase = nbase;
+    cnp = nnp;
+    cp0 = np0;
+    cp1 = np1;
   }
   if (lane == 0) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);

@@ -86,10 +86,17 @@ def test_fp32_r2_rule():
                   check_plans=False)
 
 
-@pytest.mark.parametrize("m,mk,d", [(6, (1, 40), 2), (32, (30, 64), 16), (48, (4, 32), 16)])
+@pytest.mark.parametrize("m,mk,d", [(6, (1, 40), 2), (32, (30, 64), 16), (48, (4, 32), 16), (8, (1, 16), 3),
+                                    (12, (10, 32), 5), (20, (1, 32), 7), (32, (1, 4), 16), (3, (1, 3), 1)])
 def test_fp32_ragged_shapes(m, mk, d):
+    """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
+    two-chunk column sums, tiny m_k, and the generic kernel (m > 32 or m_k > 32)."""
     b = wl.make_random(500, m, d, K=4, mk_range=mk, seed=7 + m, dtype="f32", T=1, tau=1)
-    compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
+    ctx, _ = compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
+    mkmax = int(b.sizes.max())
+    fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
+    assert ctx.info()["variant"] == (2 if fits and d <= 16 else 0)
+    compare_round(b, T=12, tau=4, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False)
 
 
 # ------------------------------------------------------------------ paths that must agree exactly
