@@ -105,6 +105,7 @@ struct ad2_ctx_s {
   int64_t N = 0, n = 0, n_items = 0;
   int variant = 0, mp = 0, nch = 0, dp = 0;
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
+  int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
   size_t es = 4;                     // element size
 
   // host tables
@@ -252,7 +253,7 @@ template <typename T>
 static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
   const bool fin = ctx->comm == nullptr;
   const size_t sh = sizeof(T) * (size_t)ctx->m;
-  k_wsum<T><<<ctx->K, 256, sh + 256 * sizeof(T), s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->Sw.as<T>(),
+  k_wsum<T><<<ctx->K, 256, sh + 256 * sizeof(T), s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->Sw.as<T>(),
                                     ctx->w.as<T>(), ctx->rule, fin ? 1 : 0, ctx->d_err.as<int>());
   CHK(launch_check(ctx, "k_wsum"));
   if (!fin) {
@@ -549,7 +550,17 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   const int ld = variant == 2 ? mp : m;
   const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : d;     // = TmaLayout::DY
   if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");
-  const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * ITEM_PASSES : 1;
+  // work items: variant 2/1 = one CTA's run of member passes (variant 2 sizes it so the grid still
+  // covers every SM a few times), variant 0 = one member
+  int passes = ITEM_PASSES;
+  if (variant == 2) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int64_t per_pass = (int64_t)NWARP * (32 / mp);
+    const int64_t want = N / (per_pass * 6 * (int64_t)sms);          // >= ~6 CTAs per SM slot
+    passes = (int)std::max<int64_t>(4, std::min<int64_t>(32, want));
+  }
+  const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
   std::vector<int64_t> item_mb, cl_item(K + 1, 0);
   std::vector<int32_t> item_cl;
   for (int c = 0; c < K; ++c) {
@@ -576,8 +587,9 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   CU(ctx->rho.reserve(es * K));
   CU(ctx->kx.reserve(es * K));
   CU(ctx->rho_d.reserve(8 * (size_t)K));
-  CU(ctx->pw.reserve(es * (size_t)n_items * m));
-  CU(ctx->px.reserve(es * (size_t)n_items * m * (d + 1)));
+  const int parts = variant == 2 ? NWARP : 1;
+  CU(ctx->pw.reserve(es * (size_t)n_items * parts * m));
+  CU(ctx->px.reserve(es * (size_t)n_items * parts * m * (d + 1)));
   CU(ctx->Sw.reserve(es * (size_t)K * m));
   CU(ctx->Sx.reserve(es * (size_t)K * m * (d + 1)));
   CU(ctx->pd.reserve(8 * (size_t)n_items));
@@ -611,6 +623,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   ctx->dp = dp;
   ctx->ld = ld;
   ctx->dy = dy;
+  ctx->parts = parts;
   ctx->order.swap(order);
   ctx->pos_of.swap(pos_of);
   ctx->h_off.swap(soff);
@@ -765,7 +778,7 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
 template <typename T>
 static ad2_status update_support_T(ad2_ctx ctx) {
   cudaStream_t s = ctx->stream;
-  k_xsum<T><<<ctx->K, 128, 0, s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->m, ctx->d, ctx->Sx.as<T>());
+  k_xsum<T><<<ctx->K, 256, 0, s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->d, ctx->Sx.as<T>());
   CHK(launch_check(ctx, "k_xsum"));
   CHK(allreduce(ctx, ctx->Sx.p, (size_t)ctx->K * ctx->m * (ctx->d + 1), nccl_t(ctx), s));
   k_xfinal<T><<<ctx->K, 128, 0, s>>>(ctx->Sx.as<T>(), ctx->w.as<T>(), ctx->x.as<T>(), ctx->m, ctx->d);

@@ -349,12 +349,12 @@ k_badmm_generic(const IterArgs<T> a, T* __restrict__ scr, int64_t n_items) {
 // w consensus: S_i = sum over the cluster's items of pw; with `finalize` (single rank) also
 //   R1 (Eq.badmmw):  w_i = S_i / sum_i S_i          R2 (Eq.badmmw2): w_i = S_i^2 / sum_i S_i^2
 template <typename T>
-__global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_item, int m,
+__global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_item, int parts, int m,
                        T* __restrict__ S, T* __restrict__ w, int rule, int finalize, int* err) {
   // rows in passes of R = min(m, blockDim); S = blockDim/R slices take items s, s+S, ... in order,
   // then slice partials are added in slice order: deterministic for a fixed launch shape.
   const int c = blockIdx.x;
-  const int64_t ib = cl_item[c], ie = cl_item[c + 1];
+  const int64_t ib = cl_item[c] * parts, ie = cl_item[c + 1] * parts;   // `parts` partial rows per item
   extern __shared__ unsigned char smraw[];
   T* red = reinterpret_cast<T*>(smraw);               // [blockDim]
   T* sh = red + blockDim.x;                            // [m]
@@ -417,10 +417,10 @@ __global__ void k_wfinal(const T* __restrict__ S, T* __restrict__ w, int m, int 
 
 // x partial sums -> Sx[K][m][d+1]
 template <typename T>
-__global__ void k_xsum(const T* __restrict__ px, const int64_t* __restrict__ cl_item, int m, int d,
+__global__ void k_xsum(const T* __restrict__ px, const int64_t* __restrict__ cl_item, int parts, int m, int d,
                        T* __restrict__ Sx) {
   const int c = blockIdx.x;
-  const int64_t ib = cl_item[c], ie = cl_item[c + 1];
+  const int64_t ib = cl_item[c] * parts, ie = cl_item[c + 1] * parts;
   const int W = m * (d + 1);
   for (int v = threadIdx.x; v < W; v += blockDim.x) {
     T s = T(0);

@@ -206,8 +206,12 @@ k_badmm_tma(const IterArgs<T> a) {
     const int64_t k1 = (k0 + G < me) ? k0 + G : me;
     const int64_t k = k0 + seg;
     const bool has = k < k1;
-    const int64_t o0 = has ? a.off[k] : cp0;
-    const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
+    int64_t o0 = cp0;
+    int mk = cnp;                                      // G == 1: the member is the pass
+    if constexpr (G > 1) {
+      o0 = has ? a.off[k] : cp0;
+      mk = has ? (int)(a.off[k + 1] - o0) : 0;
+    }
     const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
     const T mkeps = (T)mk * eps_r;
     T omv[NCH];                                        // w^(k)_j for the column this lane sums
@@ -328,7 +332,7 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * jb + u, jt = j - ch * MP;
             const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
-            tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;
+            if (j < mkw) tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;   // P slot bound
           }
         }
         __syncwarp();
@@ -402,30 +406,26 @@ k_badmm_tma(const IterArgs<T> a) {
   if (lane == 0) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);
 
-  // fixed-order combination of the per-row accumulators -> this item's partial sums
+  // this warp's partial sums of the item (segments added in a fixed butterfly order); the
+  // consensus kernels add the NWARP warp partials of every item in order: no CTA barrier here
+  const int64_t part = (int64_t)item * NWARP + warp;
   if constexpr (MODE != P2ONLY) {
-    __shared__ T sw[NWARP * G][MP];
-    sw[warp * G + seg][i] = accw;
-    __syncthreads();
-    if (threadIdx.x < m) {
-      T s = T(0);
+    T sacc = accw;
 #pragma unroll
-      for (int u = 0; u < NWARP * G; ++u) s += sw[u][threadIdx.x];
-      a.pw[(int64_t)item * m + threadIdx.x] = s;
-    }
+    for (int h = MP; h < 32; h <<= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, h);
+    if (seg == 0 && rowok) a.pw[part * m + i] = sacc;
   } else {
-    __shared__ T sx[NWARP * G][MP][DP + 1];
+    T sm_ = accm;
 #pragma unroll
-    for (int t = 0; t < DP; ++t) sx[warp * G + seg][i][t] = accx[t];
-    sx[warp * G + seg][i][DP] = accm;
-    __syncthreads();
-    for (int v = threadIdx.x; v < m * (d + 1); v += NWARP * 32) {
-      const int ii = v / (d + 1), t = v - ii * (d + 1);
-      const int tt = (t == d) ? DP : t;
-      T s = T(0);
+    for (int h = MP; h < 32; h <<= 1) sm_ += __shfl_xor_sync(0xffffffffu, sm_, h);
+    T* px = a.px + (part * m + i) * (d + 1);
+    if (seg == 0 && rowok) px[d] = sm_;
 #pragma unroll
-      for (int u = 0; u < NWARP * G; ++u) s += sx[u][ii][tt];
-      a.px[(int64_t)item * m * (d + 1) + v] = s;
+    for (int tt = 0; tt < DP; ++tt) {
+      T sx = accx[tt];
+#pragma unroll
+      for (int h = MP; h < 32; h <<= 1) sx += __shfl_xor_sync(0xffffffffu, sx, h);
+      if (seg == 0 && rowok && tt < d) px[tt] = sx;
     }
   }
 }
