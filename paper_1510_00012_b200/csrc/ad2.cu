@@ -5,6 +5,7 @@
 // counting sort, so each cluster's members are contiguous and every reduction has a fixed
 // order), work-item tables, device buffers, CUDA-graph capture of a step, NCCL all-reduce of
 // the per-cluster partial sums.  Every arithmetic step of the method runs in the kernels.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -108,20 +109,17 @@ struct ad2_ctx_s {
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
   size_t es = 4;                     // element size
 
-  // host tables
-  std::vector<int32_t> order;        // sorted position -> caller member index
-  std::vector<int64_t> pos_of;       // caller member index -> sorted position
-  std::vector<int64_t> h_off;        // sorted offsets [N+1]
-  std::vector<int64_t> h_orig_off;   // caller offsets [N+1]
-  std::vector<int64_t> h_item_mb, h_cl_item;
-  std::vector<int32_t> h_item_cl;
+  // host copies (small)
   std::vector<double> h_rho;
   std::vector<double> h_nmem;        // global members per cluster
 
   // device buffers
-  DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm;
+  DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm, d_pos_of;
+  DBuf d_off_old, d_pos_of_old;      // previous round's layout (warm starts)
+  DBuf lay_keys, lay_keys2, lay_iota, lay_sz, lay_cnt, lay_pts, lay_cstart, lay_scal, lay_cub, lay_warm;
+  DBuf stage_lab;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
-  DBuf stage_off, stage_Y, stage_W, stage_lab, tmp_out;
+  DBuf stage_off, stage_Y, stage_W, tmp_out;
 
   std::map<int, StepGraph*> graphs;
   bool prof = false;
@@ -212,6 +210,9 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
 }
 
 // fused-kernel launchers live in inst_<dtype>_mp<MP>.cu (compiled in parallel)
+template <typename T>
+void launch_cost_rows(int dp, const int64_t* off, const int64_t* imb, const int32_t* icl, const T* Y, const T* x,
+                      const T* P, double* psum, int m, int d, int ld, int64_t n_items, cudaStream_t s);
 template <typename T, int MP>
 size_t tma_cta_bytes(int nch, int dp);
 
@@ -275,15 +276,10 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
   if (ctx->n_items == 0) return AD2_OK;
   if (ctx->variant == 2) {
     if (!with_sum) return AD2_OK;
-    if (ctx->dp <= 4)
-      k_cost_rows<T, 4><<<(unsigned)ctx->n_items, 128, 0, s>>>(
-          ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
-          ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld, ctx->dy);
-    else
-      k_cost_rows<T, 16><<<(unsigned)ctx->n_items, 128, 0, s>>>(
-          ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
-          ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld, ctx->dy);
-    return launch_check(ctx, "k_cost_rows");
+    launch_cost_rows<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
+                        ctx->Y.as<T>(), ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld,
+                        ctx->n_items, s);
+    return launch_check(ctx, "k_cost_rows2");
   }
   k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
@@ -451,65 +447,49 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   const bool host = b->mem == AD2_HOST;
   const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
 
-  // ---- host copies of the ragged index arrays; validation before any state changes
-  std::vector<int64_t> off(N + 1, 0);
-  std::vector<int32_t> lab(N);
+  cudaStream_t s = ctx->stream;
+  // ---- index arrays on the device (host batches are staged), validated before any state change
+  const int64_t* off_in = static_cast<const int64_t*>(b->offsets);
+  const int32_t* lab_in = b->labels;
+  if (host && N > 0) {
+    CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
+    CU(ctx->stage_lab.reserve(sizeof(int32_t) * N));
+    CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_lab.p, b->labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    off_in = ctx->stage_off.as<int64_t>();
+    lab_in = ctx->stage_lab.as<int32_t>();
+  }
+  CU(ctx->lay_cnt.reserve(8 * (size_t)K));
+  CU(ctx->lay_pts.reserve(8 * (size_t)K));
+  CU(ctx->lay_scal.reserve(64));
+  CU(ctx->lay_cstart.reserve(8 * ((size_t)K + 1)));
+  CU(cudaMemsetAsync(ctx->lay_cnt.p, 0, 8 * (size_t)K, s));
+  CU(cudaMemsetAsync(ctx->lay_pts.p, 0, 8 * (size_t)K, s));
+  CU(cudaMemsetAsync(ctx->lay_scal.p, 0, 64, s));
+  unsigned long long* scal = ctx->lay_scal.as<unsigned long long>();
+  int64_t n = 0, mkmax = 0;
   if (N > 0) {
-    CU(cudaMemcpyAsync(off.data(), b->offsets, sizeof(int64_t) * (N + 1), host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(lab.data(), b->labels, sizeof(int32_t) * N, host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    CU(ctx->lay_keys.reserve(sizeof(int32_t) * N));
+    CU(ctx->lay_keys2.reserve(sizeof(int32_t) * N));
+    CU(ctx->lay_iota.reserve(sizeof(int32_t) * N));
+    k_layout_hist<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
+        off_in, lab_in, N, K, ctx->lay_keys.as<int32_t>(), ctx->lay_iota.as<int32_t>(),
+        ctx->lay_cnt.as<unsigned long long>(), ctx->lay_pts.as<unsigned long long>(), scal);
+    CHK(launch_check(ctx, "k_layout_hist"));
+    unsigned long long hs[2] = {0, 0};
+    CU(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&n, off_in + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (hs[0] & 1) return ctx->fail(AD2_ERR_ARG, "offsets[0] != 0");
+    if (hs[0] & 2) return ctx->fail(AD2_ERR_ARG, "a member has m_k < 1 or a label outside [0,%d)", K);
+    mkmax = (int64_t)hs[1];
   }
-  if (off[0] != 0) return ctx->fail(AD2_ERR_ARG, "offsets[0] != 0");
-  int64_t mkmax = 0;
-  for (int64_t k = 0; k < N; ++k) {
-    const int64_t mk = off[k + 1] - off[k];
-    if (mk < 1) return ctx->fail(AD2_ERR_ARG, "member %lld has m_k=%lld < 1", (long long)k, (long long)mk);
-    if (lab[k] < 0 || lab[k] >= K) return ctx->fail(AD2_ERR_ARG, "label %d of member %lld out of [0,%d)", lab[k], (long long)k, K);
-    mkmax = std::max(mkmax, mk);
-  }
-  const int64_t n = off[N];
-  std::vector<int64_t> warm_src;
   const bool warm = warm_mask != nullptr && N > 0;
   if (warm) {
     bool any = false;
     for (int64_t k = 0; k < N; ++k) any |= warm_mask[k] != 0;
     if (any && (ctx->state < 1 || ctx->dtype != b->dtype || ctx->m != m))
       return ctx->fail(AD2_ERR_ARG, "warm start without a compatible previous round");
-    warm_src.assign(N, -1);
-    for (int64_t k = 0; k < N; ++k) {
-      if (!warm_mask[k]) continue;
-      if (k >= ctx->N) return ctx->fail(AD2_ERR_ARG, "warm member %lld not in previous round", (long long)k);
-      const int64_t ps = ctx->pos_of[k];
-      const int64_t omk = ctx->h_off[ps + 1] - ctx->h_off[ps];
-      if (omk != off[k + 1] - off[k]) return ctx->fail(AD2_ERR_ARG, "warm member %lld changed m_k", (long long)k);
-      warm_src[k] = (int64_t)ctx->ld * ctx->h_off[ps];   // indexed by caller member; remapped below
-    }
-  }
-
-  // ---- stable counting sort by cluster -> contiguous clusters, fixed reduction order
-  std::vector<int64_t> cnt(K + 1, 0), npts_local(K, 0);
-  for (int64_t k = 0; k < N; ++k) {
-    cnt[lab[k] + 1]++;
-    npts_local[lab[k]] += off[k + 1] - off[k];
-  }
-  for (int c = 0; c < K; ++c) cnt[c + 1] += cnt[c];
-  std::vector<int64_t> cstart(cnt.begin(), cnt.end());
-  std::vector<int32_t> order(N);
-  std::vector<int64_t> pos_of(N);
-  {
-    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t k = 0; k < N; ++k) {
-      const int64_t s = fill[lab[k]]++;
-      order[s] = (int32_t)k;
-      pos_of[k] = s;
-    }
-  }
-  std::vector<int64_t> soff(N + 1, 0);
-  for (int64_t s = 0; s < N; ++s) soff[s + 1] = soff[s] + (off[order[s] + 1] - off[order[s]]);
-  std::vector<int64_t> warm_sorted;
-  if (warm) {
-    warm_sorted.resize(N);
-    for (int64_t s = 0; s < N; ++s) warm_sorted[s] = warm_src[order[s]];
   }
 
   // ---- kernel variant
@@ -561,18 +541,75 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
     passes = (int)std::max<int64_t>(4, std::min<int64_t>(32, want));
   }
   const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
-  std::vector<int64_t> item_mb, cl_item(K + 1, 0);
-  std::vector<int32_t> item_cl;
-  for (int c = 0; c < K; ++c) {
-    cl_item[c] = (int64_t)item_cl.size();
-    for (int64_t s = cstart[c]; s < cstart[c + 1]; s += per_item) {
-      item_mb.push_back(s);
-      item_cl.push_back(c);
-    }
+
+  // ---- from here on the previous round's state is replaced (an error leaves the context
+  //      needing a fresh init): stable radix sort by cluster, sorted offsets, work items
+  ctx->state = 0;
+  ctx->clear_graphs();
+  const int64_t old_N = ctx->N;
+  const int old_ld = ctx->ld;
+  if (warm) {
+    std::swap(ctx->d_off.p, ctx->d_off_old.p);
+    std::swap(ctx->d_off.cap, ctx->d_off_old.cap);
+    std::swap(ctx->d_pos_of.p, ctx->d_pos_of_old.p);
+    std::swap(ctx->d_pos_of.cap, ctx->d_pos_of_old.cap);
   }
-  cl_item[K] = (int64_t)item_cl.size();
-  item_mb.push_back(N);
-  const int64_t n_items = (int64_t)item_cl.size();
+  CU(ctx->d_order.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
+  CU(ctx->d_off.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->d_orig_off.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->d_pos_of.reserve(sizeof(int64_t) * (N > 0 ? N : 1)));
+  CU(ctx->lay_sz.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->d_cl_item.reserve(sizeof(int64_t) * (K + 1)));
+  if (N > 0) {
+    int end_bit = 1;
+    while ((1ll << end_bit) < (long long)K) ++end_bit;
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->lay_keys.as<int32_t>(), ctx->lay_keys2.as<int32_t>(),
+                                    ctx->lay_iota.as<int32_t>(), ctx->d_order.as<int32_t>(), (int)N, 0, end_bit, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, ctx->lay_sz.as<int64_t>(), ctx->d_off.as<int64_t>(), (int)(N + 1), s);
+    CU(ctx->lay_cub.reserve(std::max(tb, tb2)));
+    tb = ctx->lay_cub.cap;
+    CU(cub::DeviceRadixSort::SortPairs(ctx->lay_cub.p, tb, ctx->lay_keys.as<int32_t>(), ctx->lay_keys2.as<int32_t>(),
+                                       ctx->lay_iota.as<int32_t>(), ctx->d_order.as<int32_t>(), (int)N, 0, end_bit, s));
+    k_layout_sorted<<<(unsigned)((N + 1 + 255) / 256), 256, 0, s>>>(ctx->d_order.as<int32_t>(), off_in, N,
+                                                                     ctx->lay_sz.as<int64_t>(), ctx->d_pos_of.as<int64_t>());
+    CHK(launch_check(ctx, "k_layout_sorted"));
+    tb2 = ctx->lay_cub.cap;
+    CU(cub::DeviceScan::ExclusiveSum(ctx->lay_cub.p, tb2, ctx->lay_sz.as<int64_t>(), ctx->d_off.as<int64_t>(),
+                                     (int)(N + 1), s));
+    CU(cudaMemcpyAsync(ctx->d_orig_off.p, off_in, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToDevice, s));
+  } else {
+    CU(cudaMemsetAsync(ctx->d_off.p, 0, sizeof(int64_t), s));
+    CU(cudaMemsetAsync(ctx->d_orig_off.p, 0, sizeof(int64_t), s));
+  }
+  k_layout_items_count<<<1, 1, 0, s>>>(ctx->lay_cnt.as<unsigned long long>(), K, per_item,
+                                       ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), scal);
+  CHK(launch_check(ctx, "k_layout_items_count"));
+  std::vector<unsigned long long> hcnt(K), hpts(K);
+  unsigned long long hsc[3] = {0, 0, 0};
+  CU(cudaMemcpyAsync(hcnt.data(), ctx->lay_cnt.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hpts.data(), ctx->lay_pts.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hsc, scal, sizeof hsc, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const int64_t n_items = (int64_t)hsc[2];
+  CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
+  CU(ctx->d_item_cl.reserve(sizeof(int32_t) * (n_items > 0 ? n_items : 1)));
+  k_layout_items_fill<<<K, 128, 0, s>>>(ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), K, per_item, N,
+                                        ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>());
+  CHK(launch_check(ctx, "k_layout_items_fill"));
+  if (warm) {
+    CU(ctx->lay_warm.reserve((size_t)N));
+    CU(ctx->d_warm.reserve(sizeof(int64_t) * N));
+    CU(cudaMemcpyAsync(ctx->lay_warm.p, warm_mask, (size_t)N, cudaMemcpyHostToDevice, s));
+    k_layout_warm<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
+        ctx->d_order.as<int32_t>(), ctx->lay_warm.as<uint8_t>(), ctx->d_pos_of_old.as<int64_t>(),
+        ctx->d_off_old.as<int64_t>(), old_N, old_ld, ctx->d_off.as<int64_t>(), N, ctx->d_warm.as<int64_t>(), scal);
+    CHK(launch_check(ctx, "k_layout_warm"));
+    unsigned long long h0 = 0;
+    CU(cudaMemcpyAsync(&h0, scal, sizeof h0, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (h0 & 4) return ctx->fail(AD2_ERR_ARG, "a warm member is new or changed m_k");
+  }
 
   // ---- device buffers
   const size_t EL = (size_t)ld * (size_t)n;
@@ -596,14 +633,6 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   CU(ctx->Sd.reserve(8 * (size_t)K));
   CU(ctx->npts.reserve(8 * (size_t)K * 2));
   if (variant == 0) CU(ctx->scr.reserve(es * (size_t)n_items * 2 * m));
-  CU(ctx->d_order.reserve(sizeof(int32_t) * N));
-  CU(ctx->d_off.reserve(sizeof(int64_t) * (N + 1)));
-  CU(ctx->d_orig_off.reserve(sizeof(int64_t) * (N + 1)));
-  CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
-  CU(ctx->d_item_cl.reserve(sizeof(int32_t) * n_items));
-  CU(ctx->d_cl_item.reserve(sizeof(int64_t) * (K + 1)));
-  if (warm) CU(ctx->d_warm.reserve(sizeof(int64_t) * N));
-  ctx->clear_graphs();
 
   // ---- commit the new round shape
   ctx->dtype = b->dtype;
@@ -624,27 +653,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   ctx->ld = ld;
   ctx->dy = dy;
   ctx->parts = parts;
-  ctx->order.swap(order);
-  ctx->pos_of.swap(pos_of);
-  ctx->h_off.swap(soff);
-  ctx->h_orig_off.swap(off);
-  ctx->h_item_mb.swap(item_mb);
-  ctx->h_item_cl.swap(item_cl);
-  ctx->h_cl_item.swap(cl_item);
-  ctx->state = 0;
-  cudaStream_t s = ctx->stream;
 
   CU(cudaMemsetAsync(ctx->d_err.p, 0, 4 * sizeof(int), s));
-  if (N > 0) {
-    CU(cudaMemcpyAsync(ctx->d_order.p, ctx->order.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->d_off.p, ctx->h_off.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->d_orig_off.p, ctx->h_orig_off.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
-    if (warm) CU(cudaMemcpyAsync(ctx->d_warm.p, warm_sorted.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, s));
-  }
-  CU(cudaMemcpyAsync(ctx->d_item_mb.p, ctx->h_item_mb.data(), sizeof(int64_t) * (n_items + 1), cudaMemcpyHostToDevice, s));
-  if (n_items > 0)
-    CU(cudaMemcpyAsync(ctx->d_item_cl.p, ctx->h_item_cl.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(ctx->d_cl_item.p, ctx->h_cl_item.data(), sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, s));
 
   // ---- member data into the sorted layout
   const void* Ysrc = b->supports;
@@ -681,8 +691,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   // ---- global member / point counts per cluster (EMPTY check, rho denominator, 1/N_c)
   std::vector<double> cnts(2 * (size_t)K);
   for (int c = 0; c < K; ++c) {
-    cnts[c] = (double)(cstart[c + 1] - cstart[c]);
-    cnts[K + c] = (double)npts_local[c];
+    cnts[c] = (double)hcnt[c];
+    cnts[K + c] = (double)hpts[c];
   }
   CU(cudaMemcpyAsync(ctx->npts.p, cnts.data(), sizeof(double) * 2 * K, cudaMemcpyHostToDevice, s));
   CHK(allreduce(ctx, ctx->npts.p, 2 * (size_t)K, ncclFloat64, s));
@@ -805,21 +815,12 @@ ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
     const int32_t* icl = ctx->d_item_cl.as<int32_t>();
     double* pd = ctx->pd.as<double>();
     if (ctx->variant == 2) {
-      if (ctx->dtype == AD2_F64) {
-        if (ctx->dp <= 4)
-          k_cost_rows<double, 4><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(),
-                                                   ctx->P.as<double>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
-        else
-          k_cost_rows<double, 16><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(),
-                                                    ctx->P.as<double>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
-      } else {
-        if (ctx->dp <= 4)
-          k_cost_rows<float, 4><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(),
-                                                  ctx->P.as<float>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
-        else
-          k_cost_rows<float, 16><<<g, 128, 0, s>>>(off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(),
-                                                   ctx->P.as<float>(), pd, ctx->m, ctx->d, ctx->ld, ctx->dy);
-      }
+      if (ctx->dtype == AD2_F64)
+        launch_cost_rows<double>(ctx->dp, off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(), ctx->P.as<double>(),
+                                 pd, ctx->m, ctx->d, ctx->ld, ctx->n_items, s);
+      else
+        launch_cost_rows<float>(ctx->dp, off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(), ctx->P.as<float>(),
+                                pd, ctx->m, ctx->d, ctx->ld, ctx->n_items, s);
     } else if (ctx->dtype == AD2_F64) {
       k_objective<double><<<g, 128, 0, s>>>(off, imb, ctx->Cc.as<double>(), ctx->P.as<double>(), pd, ctx->ld);
     } else {

@@ -650,3 +650,102 @@ k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ o
 }
 
 }  // namespace ad2k
+
+namespace ad2k {
+// ---------------------------------------------------------------------------------------------
+// Device-side layout of a round (ad2_barycenter_init): validation + per-cluster histograms, a
+// stable radix sort of the labels (CUB) gives the cluster-sorted member order, scans give the
+// sorted offsets and the work-item table.  Only a handful of scalars come back to the host.
+// scal[0]: error bits (1: offsets[0] != 0, 2: m_k < 1 or label out of range, 4: warm mismatch)
+// scal[1]: max m_k    scal[2]: number of work items
+// ---------------------------------------------------------------------------------------------
+static __global__ void k_layout_hist(const int64_t* __restrict__ off, const int32_t* __restrict__ lab, int64_t N,
+                                     int K, int32_t* __restrict__ keys, int32_t* __restrict__ iota,
+                                     unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ pts,
+                                     unsigned long long* __restrict__ scal) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0 && off[0] != 0) atomicOr(&scal[0], 1ull);
+  unsigned mk32 = 0;
+  if (k < N) {
+    const int64_t mk = off[k + 1] - off[k];
+    int l = lab[k];
+    const bool bad = mk < 1 || mk > 0x7fffffff || l < 0 || l >= K;
+    if (bad) {
+      atomicOr(&scal[0], 2ull);
+      l = 0;
+    } else {
+      atomicAdd(&cnt[l], 1ull);
+      atomicAdd(&pts[l], (unsigned long long)mk);
+      mk32 = (unsigned)mk;
+    }
+    keys[k] = l;
+    iota[k] = (int32_t)k;
+  }
+  const unsigned wmax = __reduce_max_sync(0xffffffffu, mk32);
+  if ((threadIdx.x & 31) == 0 && wmax > 0) atomicMax(&scal[1], (unsigned long long)wmax);
+}
+
+static __global__ void k_layout_sorted(const int32_t* __restrict__ order, const int64_t* __restrict__ off_in,
+                                       int64_t N, int64_t* __restrict__ sz, int64_t* __restrict__ pos_of) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < N) {
+    const int64_t k = order[s];
+    sz[s] = off_in[k + 1] - off_in[k];
+    pos_of[k] = s;
+  } else if (s == N) {
+    sz[N] = 0;
+  }
+}
+
+static __global__ void k_layout_items_count(const unsigned long long* __restrict__ cnt, int K, int64_t per_item,
+                                            int64_t* __restrict__ cstart, int64_t* __restrict__ cl_item,
+                                            unsigned long long* __restrict__ scal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t acc = 0, it = 0;
+  for (int c = 0; c < K; ++c) {
+    cstart[c] = acc;
+    cl_item[c] = it;
+    acc += (int64_t)cnt[c];
+    it += ((int64_t)cnt[c] + per_item - 1) / per_item;
+  }
+  cstart[K] = acc;
+  cl_item[K] = it;
+  scal[2] = (unsigned long long)it;
+}
+
+static __global__ void k_layout_items_fill(const int64_t* __restrict__ cstart, const int64_t* __restrict__ cl_item,
+                                           int K, int64_t per_item, int64_t N, int64_t* __restrict__ item_mb,
+                                           int32_t* __restrict__ item_cl) {
+  const int c = blockIdx.x;
+  for (int64_t it = cl_item[c] + threadIdx.x; it < cl_item[c + 1]; it += blockDim.x) {
+    item_mb[it] = cstart[c] + (it - cl_item[c]) * per_item;
+    item_cl[it] = c;
+  }
+  if (c == K - 1 && threadIdx.x == 0) item_mb[cl_item[K]] = N;
+}
+
+static __global__ void k_layout_warm(const int32_t* __restrict__ order, const uint8_t* __restrict__ warm,
+                                     const int64_t* __restrict__ pos_old, const int64_t* __restrict__ off_old,
+                                     int64_t N_old, int ld_old, const int64_t* __restrict__ off_new, int64_t N,
+                                     int64_t* __restrict__ warm_src, unsigned long long* __restrict__ scal) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  const int64_t k = order[s];
+  if (!warm[k]) {
+    warm_src[s] = -1;
+    return;
+  }
+  if (k >= N_old) {
+    atomicOr(&scal[0], 4ull);
+    warm_src[s] = -1;
+    return;
+  }
+  const int64_t ps = pos_old[k];
+  if (off_old[ps + 1] - off_old[ps] != off_new[s + 1] - off_new[s]) {
+    atomicOr(&scal[0], 4ull);
+    warm_src[s] = -1;
+    return;
+  }
+  warm_src[s] = (int64_t)ld_old * off_old[ps];
+}
+}  // namespace ad2k

@@ -430,4 +430,73 @@ k_badmm_tma(const IterArgs<T> a) {
   }
 }
 
+
+// Row-wise cost sums for variant 2 (no C cache), same staged layout as the iteration kernel:
+// lane = centroid row i holds x_i, y_j rows (stride DY) are broadcast 16-byte loads, and the cost
+// is the difference form sum_t (x_it - y_jt)^2 (no cancellation: these are the reported rho and
+// objective).  P == nullptr: per-item sum of C (Eq.rho numerator); otherwise the
+// per-item sum of C .* Pi1 (surrogate objective).  Accumulated in double.
+template <typename T, int DP>
+__global__ void __launch_bounds__(128)
+k_cost_rows2(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+             const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
+             const T* __restrict__ P, double* __restrict__ psum, int m, int d, int ld) {
+  using V = typename Vec16<T>::type;
+  using PR = Pr<T>;
+  using T2 = typename PR::t;
+  constexpr int E = 16 / (int)sizeof(T);
+  constexpr int DY = (DP == 4) ? 4 : DP + E;
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = lane;
+  const bool rowok = i < m;
+  T2 xr2[DP / 2];
+  T2 msk2[DP / 2];                                    // 1 for real coordinates (t < d), else 0
+#pragma unroll
+  for (int t = 0; t < DP / 2; ++t) {
+    const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
+    const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
+    xr2[t] = PR::make(v0, v1);
+    msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+  }
+  double acc = 0.0;
+  for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
+    const int64_t o0 = off[k];
+    const int mk = (int)(off[k + 1] - o0);
+    T s = T(0);
+    for (int j0 = 0; j0 < mk; j0 += 4) {
+      T2 c2[4];
+      T pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (j0 + u < mk) ? j0 + u : mk - 1;
+        const T* yj = Y + (o0 + j) * DY;
+        c2[u] = PR::make(T(0), T(0));
+#pragma unroll
+        for (int tt = 0; tt < DP / E; ++tt) {
+          const V v = __ldg(reinterpret_cast<const V*>(yj + tt * E));
+#pragma unroll
+          for (int u2 = 0; u2 < E / 2; ++u2) {
+            const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
+            // (x - y) on real coordinates only: padded slots hold |y|^2 and zeros
+            const T2 df = PR::mul(PR::add(xr2[tt * (E / 2) + u2], PR::mul(yv, PR::make(T(-1), T(-1)))),
+                                  msk2[tt * (E / 2) + u2]);
+            c2[u] = PR::fma(df, df, c2[u]);
+          }
+        }
+        pv[u] = (P && rowok) ? P[(int64_t)ld * (o0 + j) + i] : T(1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * pv[u];
+    }
+    acc += (double)s;
+  }
+  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+  __shared__ double sh[4];
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
+}
 }  // namespace ad2k
