@@ -117,7 +117,7 @@ struct ad2_ctx_s {
   DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm, d_pos_of;
   DBuf d_off_old, d_pos_of_old;      // previous round's layout (warm starts)
   DBuf lay_keys, lay_keys2, lay_iota, lay_sz, lay_cnt, lay_pts, lay_cstart, lay_scal, lay_cub, lay_warm;
-  DBuf stage_lab;
+  DBuf stage_lab, mem_cl, pm;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
 
@@ -211,6 +211,9 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
 
 // fused-kernel launchers live in inst_<dtype>_mp<MP>.cu (compiled in parallel)
 template <typename T>
+void launch_cost_member(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const T* Y, const T* x,
+                        const T* P, double* pm, int m, int d, int ld, cudaStream_t s);
+template <typename T>
 void launch_cost_rows(int dp, const int64_t* off, const int64_t* imb, const int32_t* icl, const T* Y, const T* x,
                       const T* P, double* psum, int m, int d, int ld, int64_t n_items, cudaStream_t s);
 template <typename T, int MP>
@@ -276,10 +279,9 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
   if (ctx->n_items == 0) return AD2_OK;
   if (ctx->variant == 2) {
     if (!with_sum) return AD2_OK;
-    launch_cost_rows<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
-                        ctx->Y.as<T>(), ctx->x.as<T>(), nullptr, ctx->pd.as<double>(), ctx->m, ctx->d, ctx->ld,
-                        ctx->n_items, s);
-    return launch_check(ctx, "k_cost_rows2");
+    launch_cost_member<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<T>(),
+                          ctx->x.as<T>(), nullptr, ctx->pm.as<double>(), ctx->m, ctx->d, ctx->ld, s);
+    return launch_check(ctx, "k_cost_member");
   }
   k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
@@ -303,6 +305,11 @@ static ad2_status materialise_cost_T(ad2_ctx ctx, cudaStream_t s) {
 }
 
 static ad2_status cluster_dsum(ad2_ctx ctx, cudaStream_t s) {
+  if (ctx->variant == 2) {      // per-member partials (k_cost_member) over each cluster's member range
+    k_dsum_members<<<ctx->K, 256, 0, s>>>(ctx->pm.as<double>(), ctx->lay_cstart.as<int64_t>(), ctx->Sd.as<double>());
+    CHK(launch_check(ctx, "k_dsum_members"));
+    return allreduce(ctx, ctx->Sd.p, (size_t)ctx->K, ncclFloat64, s);
+  }
   k_dsum_cl<<<(ctx->K + 127) / 128, 128, 0, s>>>(ctx->pd.as<double>(), ctx->d_cl_item.as<int64_t>(),
                                                   ctx->Sd.as<double>(), ctx->K);
   CHK(launch_check(ctx, "k_dsum_cl"));
@@ -597,6 +604,14 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   k_layout_items_fill<<<K, 128, 0, s>>>(ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), K, per_item, N,
                                         ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>());
   CHK(launch_check(ctx, "k_layout_items_fill"));
+  CU(ctx->mem_cl.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
+  CU(ctx->pm.reserve(sizeof(double) * (N > 0 ? N : 1)));
+  if (n_items > 0) {
+    k_member_cluster<<<(unsigned)((n_items + 127) / 128), 128, 0, s>>>(ctx->d_item_mb.as<int64_t>(),
+                                                                         ctx->d_item_cl.as<int32_t>(), n_items,
+                                                                         ctx->mem_cl.as<int32_t>());
+    CHK(launch_check(ctx, "k_member_cluster"));
+  }
   if (warm) {
     CU(ctx->lay_warm.reserve((size_t)N));
     CU(ctx->d_warm.reserve(sizeof(int64_t) * N));
@@ -816,11 +831,13 @@ ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
     double* pd = ctx->pd.as<double>();
     if (ctx->variant == 2) {
       if (ctx->dtype == AD2_F64)
-        launch_cost_rows<double>(ctx->dp, off, imb, icl, ctx->Y.as<double>(), ctx->x.as<double>(), ctx->P.as<double>(),
-                                 pd, ctx->m, ctx->d, ctx->ld, ctx->n_items, s);
+        launch_cost_member<double>(ctx->dp, off, ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<double>(),
+                                   ctx->x.as<double>(), ctx->P.as<double>(), ctx->pm.as<double>(), ctx->m, ctx->d,
+                                   ctx->ld, s);
       else
-        launch_cost_rows<float>(ctx->dp, off, imb, icl, ctx->Y.as<float>(), ctx->x.as<float>(), ctx->P.as<float>(),
-                                pd, ctx->m, ctx->d, ctx->ld, ctx->n_items, s);
+        launch_cost_member<float>(ctx->dp, off, ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<float>(),
+                                  ctx->x.as<float>(), ctx->P.as<float>(), ctx->pm.as<double>(), ctx->m, ctx->d,
+                                  ctx->ld, s);
     } else if (ctx->dtype == AD2_F64) {
       k_objective<double><<<g, 128, 0, s>>>(off, imb, ctx->Cc.as<double>(), ctx->P.as<double>(), pd, ctx->ld);
     } else {

@@ -577,24 +577,23 @@ __global__ void __launch_bounds__(128)
 k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
          const int64_t* __restrict__ dst_off, const T* __restrict__ Ysrc, const T* __restrict__ Wsrc,
          T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, int yy_col, double wtol, int* err) {
+  // warp per member, lane per support point: the point's row [y, 0.., |y|^2 at yy_col, 0..]
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
   const int64_t k = order[s];
   const int64_t so = src_off[k], dsto = dst_off[s];
   const int mk = (int)(src_off[k + 1] - so);
-  for (int64_t e = lane; e < (int64_t)mk * dy; e += 32) {
-    const int64_t j = e / dy, t = e - j * dy;
-    T v = T(0);
-    if (t < d) {
-      v = Ysrc[(so + j) * d + t];
-    } else if (t == yy_col) {                    // |y_j|^2 for the dot-product form of the cost
-      for (int u = 0; u < d; ++u) {
-        const T c = Ysrc[(so + j) * d + u];
-        v += c * c;
-      }
+  for (int j = lane; j < mk; j += 32) {
+    const T* src = Ysrc + (so + j) * d;
+    T* dst = Y + (dsto + j) * dy;
+    T yy = T(0);
+    for (int t = 0; t < d; ++t) {
+      const T v = src[t];
+      yy += v * v;
+      dst[t] = v;
     }
-    Y[dsto * dy + e] = v;
+    for (int t = d; t < dy; ++t) dst[t] = (t == yy_col) ? yy : T(0);
   }
   double sum = 0.0;
   for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
@@ -747,5 +746,32 @@ static __global__ void k_layout_warm(const int32_t* __restrict__ order, const ui
     return;
   }
   warm_src[s] = (int64_t)ld_old * off_old[ps];
+}
+}  // namespace ad2k
+
+namespace ad2k {
+// member cluster of each sorted member (from the work-item table)
+static __global__ void k_member_cluster(const int64_t* __restrict__ item_mb, const int32_t* __restrict__ item_cl,
+                                        int64_t n_items, int32_t* __restrict__ mem_cl) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  for (int64_t s = item_mb[it]; s < item_mb[it + 1]; ++s) mem_cl[s] = item_cl[it];
+}
+
+// per-cluster sum of per-member doubles over the cluster's sorted members [cstart[c], cstart[c+1]):
+// fixed strided order per thread, then a fixed-shape tree -> deterministic
+static __global__ void k_dsum_members(const double* __restrict__ pm, const int64_t* __restrict__ cstart,
+                                      double* __restrict__ S) {
+  const int c = blockIdx.x;
+  __shared__ double red[256];
+  double a = 0.0;
+  for (int64_t s = cstart[c] + threadIdx.x; s < cstart[c + 1]; s += 256) a += pm[s];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int h = 128; h >= 1; h >>= 1) {
+    if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) S[c] = red[0];
 }
 }  // namespace ad2k

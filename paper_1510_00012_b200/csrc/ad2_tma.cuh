@@ -67,7 +67,9 @@ struct TmaLayout {
   static constexpr int YYI = (DP == 4) ? 3 : DP;
   // one pass = [P block | L block | Y block] of G consecutive members, placed in a per-warp ring
   static constexpr int MAXPASS = (2 * MP + DY) * G * MK;            // elements
-  static constexpr int RING = ((3 * MAXPASS / 2) + 63) / 64 * 64;   // two passes in flight (typ.)
+  // regions alternate between the ring's start and its end, so the next pass can be placed while
+  // the current one computes unless both are unusually large (~2% of passes at m_k ~ Poisson(20))
+  static constexpr int RING = ((5 * MAXPASS / 3) + 63) / 64 * 64;
   // in-bounds over-reads past a pass region: G == 1 reads at most 3 masked columns past m_k
   static constexpr int SLACK = ((G == 1 ? 4 * DY : MK * DY + MP * MK) + 63) / 64 * 64;
   static constexpr int TILE = (G == 1) ? 0 : MP * 32;               // G == 1: tile = the pass's P slot
@@ -195,8 +197,11 @@ k_badmm_tma(const IterArgs<T> a) {
     const int csize = (2 * MP + DY) * cnp, nsize = (2 * MP + DY) * nnp;
     int nbase = -1;
     if (nnp > 0) {
-      if (cbase + csize + nsize <= RING) nbase = cbase + csize;
-      else if (nsize <= cbase) nbase = 0;
+      if (cbase == 0) {                                // current at the start: next end-aligned
+        if (RING - nsize >= csize) nbase = RING - nsize;
+      } else if (nsize <= cbase) {                     // current end-aligned: next at the start
+        nbase = 0;
+      }
     }
     if (lane == 0 && nbase >= 0) {
       bulk_wait_read_all();          // pass t-1 has left its region
@@ -499,4 +504,67 @@ k_cost_rows2(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
   __syncthreads();
   if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
 }
+
+// Per-member variant of the row-wise cost sums (one warp per sorted member -> pm[s]), used for
+// rho at init and the objective query: enough warps in flight to hide the load latency.
+template <typename T, int DP>
+__global__ void __launch_bounds__(128)
+k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restrict__ mem_cl,
+              const T* __restrict__ Y, const T* __restrict__ x, const T* __restrict__ P,
+              double* __restrict__ pm, int m, int d, int ld) {
+  using V = typename Vec16<T>::type;
+  using PR = Pr<T>;
+  using T2 = typename PR::t;
+  constexpr int E = 16 / (int)sizeof(T);
+  constexpr int DY = (DP == 4) ? 4 : DP + E;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+  if (sidx >= N) return;
+  const int c = mem_cl[sidx];
+  T2 xr2[DP / 2], msk2[DP / 2];
+  double acc = 0.0;
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    const int i = r0 + lane;
+    const bool rowok = i < m;
+#pragma unroll
+    for (int t = 0; t < DP / 2; ++t) {
+      const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
+      const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
+      xr2[t] = PR::make(v0, v1);
+      msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+    }
+    const int64_t o0 = off[sidx];
+    const int mk = (int)(off[sidx + 1] - o0);
+    T s = T(0);
+    for (int j0 = 0; j0 < mk; j0 += 4) {
+      T2 c2[4];
+      T pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (j0 + u < mk) ? j0 + u : mk - 1;
+        const T* yj = Y + (o0 + j) * DY;
+        c2[u] = PR::make(T(0), T(0));
+#pragma unroll
+        for (int tt = 0; tt < DP / E; ++tt) {
+          const V v = __ldg(reinterpret_cast<const V*>(yj + tt * E));
+#pragma unroll
+          for (int u2 = 0; u2 < E / 2; ++u2) {
+            const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
+            const T2 df = PR::mul(PR::add(xr2[tt * (E / 2) + u2], PR::mul(yv, PR::make(T(-1), T(-1)))),
+                                  msk2[tt * (E / 2) + u2]);
+            c2[u] = PR::fma(df, df, c2[u]);
+          }
+        }
+        pv[u] = (P && rowok) ? P[(int64_t)ld * (o0 + j) + i] : T(1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * pv[u];
+    }
+    acc += (double)s;
+  }
+  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+  if (lane == 0) pm[sidx] = acc;
+}
+
 }  // namespace ad2k

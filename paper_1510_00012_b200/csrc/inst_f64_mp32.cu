@@ -82,3 +82,16 @@ void launch_cost_rows<double>(int dp, const int64_t* off, const int64_t* imb, co
   if (dp <= 4) k_cost_rows2<double, 4><<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, P, psum, m, d, ld);
   else k_cost_rows2<double, 16><<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, P, psum, m, d, ld);
 }
+
+template <typename T>
+void launch_cost_member(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const T* Y, const T* x,
+                        const T* P, double* pm, int m, int d, int ld, cudaStream_t s);
+
+template <>
+void launch_cost_member<double>(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const double* Y,
+                             const double* x, const double* P, double* pm, int m, int d, int ld, cudaStream_t s) {
+  if (N == 0) return;
+  const unsigned g = (unsigned)((N + 3) / 4);
+  if (dp <= 4) k_cost_member<double, 4><<<g, 128, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
+  else k_cost_member<double, 16><<<g, 128, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
+}
