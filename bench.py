@@ -244,10 +244,11 @@ def run_ours(args, rank, world, local_rank):
                    "entries_per_iter": entries_total, "step": "1 round: init + T/tau x (step(tau), update_support) + objective",
                    "parallelism": f"dp{world} (members sharded, NCCL all-reduce of per-cluster partials)",
                    "l2": "inputs larger than L2 (state %.1f GB)" % (info["state_bytes"] / 1e9),
-                   "kernel_variant": "fused" if info["variant"] == 1 else "generic"},
+                   "kernel_variant": {2: "tma", 1: "warp", 0: "generic"}[info["variant"]]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_badmm_warp<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
+                     "kernel": {2: "k_badmm_tma", 1: "k_badmm_warp", 0: "k_badmm_generic"}[info["variant"]]
+                     + "<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
                      "bytes_per_entry": BYTES_PER_ENTRY, "entries_per_launch": entries_local,
                      "avg_launch_ms": avg_fused_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "iteration_kernels_share_of_step": iter_share},

@@ -99,7 +99,7 @@ typedef struct {
     int64_t n_points;           /* sum_k m_k on this rank */
     int64_t entries;            /* sum_k m * m_k on this rank (plan entries per iteration) */
     int64_t n_items;            /* work items (per-cluster member chunks) */
-    int32_t variant;            /* 1 = fused warp-per-member kernels, 0 = generic kernels */
+    int32_t variant;            /* 2 = TMA-staged fused kernels, 1 = fused warp-per-member (cached C), 0 = generic */
     int32_t mp, nch;            /* fused-kernel row tile (8/16/32) and column chunks */
     int32_t nranks, rank;
     int64_t launches;           /* kernels launched by this context so far (graph nodes counted) */
