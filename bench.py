@@ -209,7 +209,8 @@ def run_ours(args, rank, world, local_rank):
             traffic = prof.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    iter_share = float(np.sum(launch_ms)) / (ms) if ms > 0 else None
+    # the profiled graph is one step(tau); a round runs T/tau of them
+    iter_share = float(np.sum(launch_ms)) * (T // tau) / ms if ms > 0 else None
 
     # e2e: the same step through the C ABI from pinned host buffers (H2D inside the timed region)
     e2e = None
@@ -244,10 +245,10 @@ def run_ours(args, rank, world, local_rank):
                    "entries_per_iter": entries_total, "step": "1 round: init + T/tau x (step(tau), update_support) + objective",
                    "parallelism": f"dp{world} (members sharded, NCCL all-reduce of per-cluster partials)",
                    "l2": "inputs larger than L2 (state %.1f GB)" % (info["state_bytes"] / 1e9),
-                   "kernel_variant": {2: "tma", 1: "warp", 0: "generic"}[info["variant"]]},
+                   "kernel_variant": {3: "wide", 2: "tma", 1: "warp", 0: "generic"}[info["variant"]]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": {2: "k_badmm_tma", 1: "k_badmm_warp", 0: "k_badmm_generic"}[info["variant"]]
+                     "kernel": {3: "k_badmm_wide", 2: "k_badmm_tma", 1: "k_badmm_warp", 0: "k_badmm_generic"}[info["variant"]]
                      + "<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
                      "bytes_per_entry": BYTES_PER_ENTRY, "entries_per_launch": entries_local,
                      "avg_launch_ms": avg_fused_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
@@ -270,14 +271,18 @@ def oracle_sample(b: wl.Bundle, budget_s: float):
     import oracle
     mem = np.nonzero(b.labels == 0)[0]
     s = b.sched
-    n_try = min(len(mem), 2000)
-    sub = b.subset(mem[:n_try])
-    t = time.time()
-    oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, 1, 1, s.rule, s.rho0, s.eps, 1e-5,
-                          want_state=False)
-    rate = b.m * sub.n / max(1e-6, time.time() - t)
-    want = int(budget_s * rate / (b.m * s.T) / max(1, float(np.mean(b.sizes))))
-    take = int(min(len(mem), max(50, want)))
+    # probe with the full schedule on a growing prefix until it takes >= 1 s, then scale to budget_s
+    n_try = min(len(mem), 500)
+    while True:
+        sub = b.subset(mem[:n_try])
+        t = time.time()
+        oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
+                              s.eps, 1e-5, want_state=False)
+        dt = time.time() - t
+        if dt >= 1.0 or n_try >= len(mem):
+            break
+        n_try = min(len(mem), n_try * 4)
+    take = int(min(len(mem), max(50, n_try * budget_s / max(dt, 1e-3))))
     return b.subset(mem[:take]), take
 
 

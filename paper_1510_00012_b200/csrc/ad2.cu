@@ -104,7 +104,7 @@ struct ad2_ctx_s {
   int d = 0, m = 0, K = 0, rule = 0;
   double rho0 = 2.0, eps = 1e-16;
   int64_t N = 0, n = 0, n_items = 0;
-  int variant = 0, mp = 0, nch = 0, dp = 0;
+  int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
   size_t es = 4;                     // element size
@@ -226,12 +226,21 @@ static size_t tma_bytes(ad2_dtype dt, int mp, int nch, int dp) {
 }
 template <typename T, int MP>
 void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
+// variant 3 (inst_f32_wide.cu)
+int wide_cfg();
+int wide_npair(int cfg);
+size_t wide_cta_bytes(int cfg);
+void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s);
+void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                      float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
 
 template <typename T>
 static void launch_iter_T(ad2_ctx ctx, int mode, cudaStream_t s) {
   IterArgs<T> a = iter_args<T>(ctx);
   if (ctx->n_items == 0) return;
-  if (ctx->variant >= 1) {
+  if (ctx->variant == 3) {
+    if constexpr (sizeof(T) == 4) launch_wide(ctx->wcfg, mode, ctx->d, a, ctx->n_items, s);
+  } else if (ctx->variant >= 1) {
     const int v = ctx->variant;
     if (ctx->mp == 8) launch_warp<T, 8>(v, mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
     else if (ctx->mp == 16) launch_warp<T, 16>(v, mode, ctx->nch, ctx->dp, a, ctx->n_items, s);
@@ -282,6 +291,14 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
     launch_cost_member<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<T>(),
                           ctx->x.as<T>(), nullptr, ctx->pm.as<double>(), ctx->m, ctx->d, ctx->ld, s);
     return launch_check(ctx, "k_cost_member");
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (ctx->variant == 3) {
+      launch_cost_tile(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
+                       ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
+                       with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->n_items, s);
+      return launch_check(ctx, "k_cost_tile");
+    }
   }
   k_cost<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->Y.as<T>(),
@@ -533,21 +550,37 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
       }
     }
   }
+  //   3: warp-pair fused kernel (ad2_wide.cuh) with a cost cache for m <= 64, m_k <= 64, d <= 64, fp32
+  //      (taken when none of the above fits)
+  int wcfg = 0;
+  if (variant == 0 && b->dtype == AD2_F32 && m <= 64 && mkmax <= 64 && d <= 64) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    wcfg = wide_cfg();
+    if (wide_cta_bytes(wcfg) <= (size_t)optin) {
+      variant = 3;
+      mp = 64;
+      nch = 1;
+      dp = d <= 16 ? 16 : 64;
+    }
+  }
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
-  const int ld = variant == 2 ? mp : m;
-  const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : d;     // = TmaLayout::DY
+  // variant 3: blocks padded to 64 rows; Y rows padded with zeros to a multiple of 4
+  const int ld = (variant == 2 || variant == 3) ? mp : m;
+  const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : (variant == 3 ? (d + 3) / 4 * 4 : d);
   if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");
   // work items: variant 2/1 = one CTA's run of member passes (variant 2 sizes it so the grid still
   // covers every SM a few times), variant 0 = one member
   int passes = ITEM_PASSES;
-  if (variant == 2) {
+  if (variant == 2 || variant == 3) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int64_t per_pass = (int64_t)NWARP * (32 / mp);
+    const int64_t per_pass = variant == 3 ? (int64_t)wide_npair(wcfg) : (int64_t)NWARP * (32 / mp);
     const int64_t want = N / (per_pass * 6 * (int64_t)sms);          // >= ~6 CTAs per SM slot
     passes = (int)std::max<int64_t>(4, std::min<int64_t>(32, want));
   }
-  const int64_t per_item = variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
+  const int64_t per_item = variant == 3 ? (int64_t)wide_npair(wcfg) * passes
+                           : variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
 
   // ---- from here on the previous round's state is replaced (an error leaves the context
   //      needing a fresh init): stable radix sort by cluster, sorted offsets, work items
@@ -639,7 +672,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   CU(ctx->rho.reserve(es * K));
   CU(ctx->kx.reserve(es * K));
   CU(ctx->rho_d.reserve(8 * (size_t)K));
-  const int parts = variant == 2 ? NWARP : 1;
+  const int parts = variant == 2 ? NWARP : (variant == 3 ? wide_npair(wcfg) : 1);
   CU(ctx->pw.reserve(es * (size_t)n_items * parts * m));
   CU(ctx->px.reserve(es * (size_t)n_items * parts * m * (d + 1)));
   CU(ctx->Sw.reserve(es * (size_t)K * m));
@@ -668,6 +701,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   ctx->ld = ld;
   ctx->dy = dy;
   ctx->parts = parts;
+  ctx->wcfg = wcfg;
 
   CU(cudaMemsetAsync(ctx->d_err.p, 0, 4 * sizeof(int), s));
 

@@ -1,0 +1,380 @@
+// ad2_wide.cuh — fused B-ADMM iteration kernel for 32 < m <= 64 (variant 3, fp32): a warp PAIR
+// per member.  Modified B-ADMM of AD2-clustering (arXiv 1510.00012, Alg. 4).
+//
+// Member blocks have WMP = 64 rows (ld = 64, rows >= m zero) and m_k <= WMK = 64 columns.  Lane
+// i of warp h of a pair owns centroid row 32h + i for EVERY column of the member, so row sums are
+// lane-local.  The state does not live in registers (a 64-column row would need ~200): the pass
+// region [P | L | C] of one member is staged by three cp.async.bulk loads into a per-pair ring and
+// the iteration is three column sweeps over shared memory (each entry's intermediate is written
+// back in place), plus a column-sum step in which lane j of the pair reads column j's 64 rows
+// (16 rotated 16-byte loads, bank-conflict free).  C is the cached cost (d up to 64 makes
+// recomputing it per iteration as expensive as reading it), so an iteration
+// moves 20 B per entry: P, L in and out, C in.
+//
+//   MODE P1ONLY: Pi2 (= Q) -> sweep B (Eq.badmmc0b) -> column sums -> sweep C (Eq.badmmc0, the
+//                Eq.badmmc1b row masses) -> P = Pi1, w-partials
+//   MODE FUSED : sweep A (Eq.badmmc1b with Lambda^n, row mass, Lambda + rho Pi1) -> sweep B
+//                (Eq.badmmc1 with the consensus w, Eq.badmm2, then Eq.badmmc0b) -> column sums ->
+//                sweep C -> P = Pi1, L = Lambda, w-partials
+//   MODE P2ONLY: sweep A -> sweep B2 (Eq.badmmc1, Eq.badmm2, support-update partials of
+//                Eq.updatex) -> Q = Pi2, L = Lambda, x-partials
+#pragma once
+#include "ad2_tma.cuh"
+
+namespace ad2k {
+
+constexpr int WMP = 64;     // rows of a member block (ld)
+constexpr int WMK = 64;     // largest m_k
+
+template <int NPAIR, int RING_KB>
+struct WideLayout {
+  static constexpr int RING = RING_KB * 1024 / 4;               // floats per pair
+  // [ring | fbuf[WMK] | Rw[4] | 2 mbarriers]
+  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + WMK + 4) + 16) + 127) / 128 * 128;
+  static constexpr size_t CTA_BYTES = NPAIR * PAIR_BYTES;
+  static_assert(RING >= 3 * WMP * WMK, "ring must hold the largest pass");
+  static_assert(CTA_BYTES <= 227 * 1024, "shared memory");
+};
+
+__device__ __forceinline__ void pair_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int NPAIR, int RING_KB, int MODE, int DP>
+__global__ void __launch_bounds__(NPAIR * 64, 1)
+k_badmm_wide(const IterArgs<float> a) {
+  using Lay = WideLayout<NPAIR, RING_KB>;
+  using N = Num<float>;
+  constexpr int RING = Lay::RING;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, h = warp & 1;
+  float* const ring = reinterpret_cast<float*>(smem_raw + (size_t)pair * Lay::PAIR_BYTES);
+  float* const fbuf = ring + RING;                                 // Eq.badmmc0 column factors
+  float* const Rw = fbuf + WMK;                                    // per-warp row-mass totals
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(Rw + 4);
+  const bool leader = (h == 0 && lane == 0);
+  const int bar_id = 1 + pair;
+  const int ig = 32 * h + lane;                                    // this lane's centroid row
+  const int item = blockIdx.x;
+  const int c = a.item_cl[item];
+  const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
+  const int m = a.m, d = a.d;
+  const bool rowok = ig < m;
+  const float kx = a.kx[c], rho = a.rho[c];
+  const float eps_r = rowok ? a.eps : 0.f;
+  const float wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + ig] : 0.f;
+  const float2 kx2 = make_float2(kx, kx), nkx2 = make_float2(-kx, -kx);
+  const float2 rho2 = make_float2(rho, rho), nrho2 = make_float2(-rho, -rho);
+  const float2 eps2 = make_float2(eps_r, eps_r);
+  float accw = 0.f, accm = 0.f;
+  float accx[(MODE == P2ONLY) ? DP : 1];
+#pragma unroll
+  for (int t = 0; t < ((MODE == P2ONLY) ? DP : 1); ++t) accx[t] = 0.f;
+  bool bad = false;
+  const float* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
+  float* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
+
+  if (leader) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  pair_sync(bar_id);
+
+  auto member = [&](int t, int64_t& p0) -> int {                  // pair-uniform
+    const int64_t k = mb + pair + (int64_t)t * NPAIR;
+    if (k >= me) return 0;
+    p0 = a.off[k];
+    return (int)(a.off[k + 1] - p0);
+  };
+  // pass region [P | L | C] (P2ONLY: [P | L | Y], the supports for the x partials); dy % 4 == 0
+  const int dy = a.dy;
+  const int third = (MODE == P2ONLY) ? dy : WMP;                   // floats per point of the 3rd array
+  auto issue = [&](int t, int base, int64_t p0, int np) {          // leader only
+    const uint32_t bp = (uint32_t)(WMP * np * 4), b3 = (uint32_t)(third * np * 4);
+    float* st = ring + base;
+    mbar_expect_tx(&bar[t & 1], 2 * bp + b3);
+    tma_load(st, src_plan + (int64_t)WMP * p0, bp, &bar[t & 1]);
+    tma_load(st + WMP * np, a.L + (int64_t)WMP * p0, bp, &bar[t & 1]);
+    if (MODE == P2ONLY) tma_load(st + 2 * WMP * np, a.Y + (int64_t)dy * p0, b3, &bar[t & 1]);
+    else tma_load(st + 2 * WMP * np, a.Cc + (int64_t)WMP * p0, b3, &bar[t & 1]);
+  };
+
+  int64_t cp0 = 0;
+  int cnp = member(0, cp0);
+  int cbase = 0;
+  if (leader && cnp > 0) issue(0, 0, cp0, cnp);
+
+  for (int t = 0; cnp > 0; ++t) {
+    // place pass t+1 beside pass t (alternating ring start / ring end) while t computes
+    int64_t np0 = 0;
+    const int nnp = member(t + 1, np0);
+    const int csize = (2 * WMP + third) * cnp, nsize = (2 * WMP + third) * nnp;
+    int nbase = -1;
+    if (nnp > 0) {
+      if (cbase == 0) {
+        if (RING - nsize >= csize) nbase = RING - nsize;
+      } else if (nsize <= cbase) {
+        nbase = 0;
+      }
+    }
+    if (leader && nbase >= 0) {
+      bulk_wait_read_all();            // pass t-1 has left its region
+      issue(t + 1, nbase, np0, nnp);
+    }
+    const int mk = cnp;
+    const int jc = ig;                 // the column this lane sums (jc < mk)
+    const float om_j = (MODE != P2ONLY && jc < mk) ? __ldg(a.om + cp0 + jc) : 0.f;
+    mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+    float* const Ps = ring + cbase;
+    float* const Ls = Ps + WMP * mk;
+    const float* const Cs = Ls + WMP * mk;                         // C (P2ONLY: Y rows, stride dy)
+
+    // ---- sweep A (phase 2 of iteration t-1): pe = Pi1 exp(Lambda/rho) (Eq.badmmc1b without eps),
+    //      row mass r = sum_j pe_j + m_k eps; Ps <- pe, Ls <- Lambda + rho Pi1
+    float f = 0.f;
+    if constexpr (MODE != P1ONLY) {
+      float2 racc = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int j = 0; j < mk; j += 2) {
+        const bool v1 = j + 1 < mk;
+        const int e0 = j * WMP + ig, e1 = e0 + WMP;
+        const float2 p = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
+        const float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
+        const float2 ar = __fmul2_rn(l, kx2);
+        const float2 q = __fmul2_rn(p, make_float2(N::ex(ar.x), N::ex(ar.y)));
+        const float2 lp = __ffma2_rn(rho2, p, l);
+        racc = __fadd2_rn(racc, q);
+        Ps[e0] = q.x;
+        Ls[e0] = lp.x;
+        if (v1) {
+          Ps[e1] = q.y;
+          Ls[e1] = lp.y;
+        }
+      }
+      const float r = (racc.x + racc.y) + (float)mk * eps_r;
+      f = rowok ? wi / r : 0.f;                                      // Eq.badmmc1: w_i / row mass
+    }
+    const float2 f2 = make_float2(f, f), ef2 = make_float2(eps_r * f, eps_r * f);
+
+    if constexpr (MODE == P2ONLY) {
+      // ---- sweep B2: Pi2 = (pe + eps) w_i / r (Eq.badmmc1), Lambda -= rho Pi2 (Eq.badmm2),
+      //      support-update partials sum_j pi2_ij y_j, sum_j pi2_ij (Eq.updatex, X5)
+      for (int j = 0; j < mk; ++j) {
+        const int e0 = j * WMP + ig;
+        const float q = fmaf(Ps[e0], f, eps_r * f);
+        const float l = fmaf(-rho, q, Ls[e0]);
+        Ps[e0] = q;
+        Ls[e0] = l;
+        accm += q;
+        const float* yj = Cs + j * dy;
+#pragma unroll
+        for (int tt = 0; tt < DP / 4; ++tt) {
+          if (4 * tt < d) {
+            const float4 v = *(reinterpret_cast<const float4*>(yj) + tt);
+            accx[4 * tt + 0] = fmaf(q, v.x, accx[4 * tt + 0]);
+            accx[4 * tt + 1] = fmaf(q, v.y, accx[4 * tt + 1]);
+            accx[4 * tt + 2] = fmaf(q, v.z, accx[4 * tt + 2]);
+            accx[4 * tt + 3] = fmaf(q, v.w, accx[4 * tt + 3]);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      pair_sync(bar_id);
+    } else {
+      // ---- sweep B: (FUSED) Pi2 = (pe + eps) f, Lambda^{n+1} = (Lambda + rho Pi1) - rho Pi2;
+      //      pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b) -> Ps
+#pragma unroll 4
+      for (int j = 0; j < mk; j += 2) {
+        const bool v1 = j + 1 < mk;
+        const int e0 = j * WMP + ig, e1 = e0 + WMP;
+        float2 q = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
+        float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
+        const float2 cst = make_float2(Cs[e0], v1 ? Cs[e1] : 0.f);
+        if constexpr (MODE == FUSED) {
+          q = __ffma2_rn(q, f2, ef2);
+          l = __ffma2_rn(nrho2, q, l);
+        }
+        const float2 ar = __fmul2_rn(__fadd2_rn(cst, l), nkx2);
+        const float2 pt = __ffma2_rn(q, make_float2(N::ex(ar.x), N::ex(ar.y)), eps2);
+        Ps[e0] = pt.x;
+        if (MODE == FUSED) Ls[e0] = l.x;
+        if (v1) {
+          Ps[e1] = pt.y;
+          if (MODE == FUSED) Ls[e1] = l.y;
+        }
+      }
+      pair_sync(bar_id);
+      // ---- column sums over the 64 rows (Eq.badmmc0 denominators): lane jc reads its column in
+      //      16 chunks of 4 rows, starting at chunk jc mod 16 (4 lanes per bank quad: no conflicts)
+      if (jc < mk) {
+        const float* col = Ps + jc * WMP;
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int chn = (u + jc) & 15;
+          const float4 v = *reinterpret_cast<const float4*>(col + 4 * chn);
+          s0 = __fadd2_rn(s0, make_float2(v.x, v.y));
+          s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
+        }
+        const float s = (s0.x + s0.y) + (s1.x + s1.y);
+        fbuf[jc] = om_j / s;                                           // Eq.badmmc0: w_j^(k) / colsum
+      }
+      pair_sync(bar_id);
+      // ---- sweep C: Pi1 = pt2 * factor_j -> Ps; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row mass
+      float2 racc = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int j = 0; j < mk; j += 2) {
+        const bool v1 = j + 1 < mk;
+        const int e0 = j * WMP + ig, e1 = e0 + WMP;
+        const float2 pt = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
+        const float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
+        const float2 fj = make_float2(fbuf[j], v1 ? fbuf[j + 1] : 0.f);
+        const float2 p1 = __fmul2_rn(pt, fj);
+        const float2 ar = __fmul2_rn(l, kx2);
+        racc = __ffma2_rn(p1, make_float2(N::ex(ar.x), N::ex(ar.y)), racc);
+        Ps[e0] = p1.x;
+        if (v1) Ps[e1] = p1.y;
+      }
+      const float r2 = (racc.x + racc.y) + (float)mk * eps_r;
+      float R = r2;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
+      if (lane == 0) Rw[h] = R;
+      fence_proxy_async_smem();
+      pair_sync(bar_id);
+      R = Rw[0] + Rw[1];
+      if (rowok) {
+        const float wt = r2 / R;                                       // normalised row mass
+        accw += (a.rule == 1) ? sqrtf(wt) : wt;
+        bad |= !isfinite(wt);
+      }
+    }
+    // ---- results leave by bulk stores from the same slots
+    if (leader) {
+      const uint32_t bp = (uint32_t)(WMP * mk * 4);
+      tma_store(dst_plan + (int64_t)WMP * cp0, Ps, bp);
+      if (MODE != P1ONLY) tma_store(a.L + (int64_t)WMP * cp0, Ls, bp);
+      bulk_commit();
+      if (nnp > 0 && nbase < 0) {      // pass t+1 did not fit beside pass t: issue it at the ring start
+        bulk_wait_read_all();
+        issue(t + 1, 0, np0, nnp);
+      }
+    }
+    if (nnp > 0 && nbase < 0) nbase = 0;
+    cbase = nbase;
+    cnp = nnp;
+    cp0 = np0;
+  }
+  if (leader) bulk_wait_all();
+  if (bad) atomicOr(a.err, ERR_NONFINITE);
+
+  // this pair's partial sums of the item (rows are lane-owned); consensus adds the NPAIR pair
+  // partials of every item in order
+  const int64_t part = (int64_t)item * NPAIR + pair;
+  if constexpr (MODE != P2ONLY) {
+    if (rowok) a.pw[part * m + ig] = accw;
+  } else {
+    if (rowok) {
+      float* px = a.px + (part * m + ig) * (d + 1);
+      px[d] = accm;
+#pragma unroll
+      for (int t = 0; t < DP; ++t)
+        if (t < d) px[t] = accx[t];
+    }
+  }
+}
+
+// Cost build for the cached-C variants: C_ij = |x_i|^2 + |y_j|^2 - 2 x_i.y_j in fp32,
+// clamped at 0, for a 64 x 64 (rows x points) tile per step: X_c^T and a chunk of 64 points are
+// staged in shared memory, each thread accumulates a 4 x 4 register tile of dot products.
+// Entries of rows >= m are written as 0.  With psum != nullptr the per-item double sum of C
+// (Eq.rho numerator) is formed in a fixed order.  One CTA (256 threads) per work item.
+template <int DMAX>
+__global__ void __launch_bounds__(256)
+k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+            const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
+            float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
+  __shared__ __align__(16) float xs[DMAX][68];       // x_c^T (coordinate-major, padded rows)
+  __shared__ __align__(16) float ys[DMAX][68];       // chunk of 64 points, coordinate-major
+  __shared__ float xx[64], yy[64];
+  __shared__ double red[8];
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int tid = threadIdx.x;
+  const int ti = tid & 15, tj = tid >> 4;              // rows 4ti..4ti+3, points 4tj..4tj+3
+  for (int v = tid; v < DMAX * 64; v += 256) {
+    const int t = v >> 6, i = v & 63;
+    xs[t][i] = (i < m && t < d) ? x[((int64_t)c * m + i) * d + t] : 0.f;
+  }
+  __syncthreads();
+  if (tid < 64) {
+    float s = 0.f;
+    for (int t = 0; t < d; ++t) s = fmaf(xs[t][tid], xs[t][tid], s);
+    xx[tid] = s;
+  }
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  for (int64_t q0 = p_beg; q0 < p_end; q0 += 64) {
+    const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
+    __syncthreads();                                   // previous chunk consumed
+    for (int v = tid; v < DMAX * 64; v += 256) {
+      const int j = v / DMAX, t = v - j * DMAX;
+      ys[t][j] = (j < np && t < d) ? Y[(q0 + j) * dy + t] : 0.f;
+    }
+    __syncthreads();
+    if (tid < 64) {
+      float s = 0.f;
+      for (int t = 0; t < d; ++t) s = fmaf(ys[t][tid], ys[t][tid], s);
+      yy[tid] = s;
+    }
+    float a4[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) a4[u][v] = 0.f;
+#pragma unroll 8
+    for (int t = 0; t < DMAX; ++t) {
+      if (t >= d) break;
+      const float4 xv = *reinterpret_cast<const float4*>(&xs[t][4 * ti]);
+      const float4 yv = *reinterpret_cast<const float4*>(&ys[t][4 * tj]);
+      const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a4[u][v] = fmaf(xa[u], ya[v], a4[u][v]);
+    }
+    __syncthreads();                                   // yy ready
+    float s = 0.f;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = 4 * tj + v;
+      if (j < np) {
+        float4 o;
+        float* oe = reinterpret_cast<float*>(&o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = 4 * ti + u;
+          const float cv = (i < m) ? fmaxf(fmaf(-2.f, a4[u][v], xx[i] + yy[j]), 0.f) : 0.f;
+          oe[u] = cv;
+          s += cv;
+        }
+        *reinterpret_cast<float4*>(Cc + (q0 + j) * 64 + 4 * ti) = o;
+      }
+    }
+    acc += (double)s;
+  }
+  if (psum) {
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      psum[item] = t;
+    }
+  }
+}
+
+}  // namespace ad2k

@@ -29,7 +29,11 @@ def compare_round(b, T, tau, rule=0, *, rtol_plan, rtol_x, atol_w, rtol_obj=None
         assert np.abs(w[c] - r.w).max() <= atol_w, f"w cluster {c}: {np.abs(w[c] - r.w).max()}"
         assert_hybrid(x[c], r.x, rtol_x, floor=1.0, what=f"x cluster {c}")
         if rtol_obj is not None:
-            assert obj[c] == pytest.approx(r.obj, rel=rtol_obj), f"objective cluster {c}"
+            # relative, with a floor of rtol_obj/100 x the cluster's mean entry cost (rho / rho0, X1):
+            # the working-precision cost has an absolute error on the data's scale, which decides
+            # clusters whose objective is ~0 (a single member is its own barycenter, P6)
+            floor = rtol_obj * 1e-2 * r.rho / b.sched.rho0
+            assert abs(obj[c] - r.obj) <= rtol_obj * abs(r.obj) + floor, f"objective cluster {c}: {obj[c]} {r.obj}"
         if check_plans:
             for name in ("Pi1", "Pi2"):
                 got = np.concatenate([mats[name][k].ravel() for k in members[c]])
@@ -66,13 +70,13 @@ def test_fp64_ragged_shapes_one_and_five_iterations(m, mk, d):
 
 # ------------------------------------------------------------------ fp32
 
-@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000)])
+@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000), (4, 1500)])
 def test_fp32_one_iteration(cfg, N):
     b = wl.make_config(cfg, N=N)
     compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
 
 
-@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000)])
+@pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000), (4, 1500)])
 def test_fp32_full_schedule(cfg, N):
     b = wl.make_config(cfg, N=N)
     compare_round(b, T=b.sched.T, tau=b.sched.tau, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3,
@@ -86,16 +90,28 @@ def test_fp32_r2_rule():
                   check_plans=False)
 
 
+def expected_variant(m, mkmax, d, dtype="f32"):
+    fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
+    if fits and d <= 16:
+        return 2
+    if fits and dtype == "f32" and d <= 64:
+        return 1
+    if dtype == "f32" and m <= 64 and mkmax <= 64:
+        return 3
+    return 0
+
+
 @pytest.mark.parametrize("m,mk,d", [(6, (1, 40), 2), (32, (30, 64), 16), (48, (4, 32), 16), (8, (1, 16), 3),
-                                    (12, (10, 32), 5), (20, (1, 32), 7), (32, (1, 4), 16), (3, (1, 3), 1)])
+                                    (12, (10, 32), 5), (20, (1, 32), 7), (32, (1, 4), 16), (3, (1, 3), 1),
+                                    (64, (20, 64), 64), (64, (1, 64), 5), (33, (1, 63), 9), (64, (1, 3), 64),
+                                    (40, (60, 64), 64), (64, (1, 80), 3)])
 def test_fp32_ragged_shapes(m, mk, d):
     """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
-    two-chunk column sums, tiny m_k, and the generic kernel (m > 32 or m_k > 32)."""
+    two-chunk column sums, tiny m_k, the warp-pair kernel (32 < m <= 64 or 32 < m_k <= 64, cached
+    cost from the tiled cost build), and the generic kernel (m_k > 64)."""
     b = wl.make_random(500, m, d, K=4, mk_range=mk, seed=7 + m, dtype="f32", T=1, tau=1)
     ctx, _ = compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
-    mkmax = int(b.sizes.max())
-    fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
-    assert ctx.info()["variant"] == (2 if fits and d <= 16 else 0)
+    assert ctx.info()["variant"] == expected_variant(m, int(b.sizes.max()), d)
     compare_round(b, T=12, tau=4, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False)
 
 
