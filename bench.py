@@ -160,7 +160,7 @@ def run_ours(args, rank, world, local_rank):
 
     def step(arr, mem):
         ctx.init(arr["offsets"], arr["supports"], arr["weights"], arr["labels"], arr["x0"], arr["w0"], b.K, b.m,
-                 s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype)
+                 s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype, cost_mode=args.cost_mode)
         ad2.run_schedule(ctx, T, tau)
         obj_box["obj"] = ctx.objective()               # device -> host read of the result (syncs)
 
@@ -245,6 +245,7 @@ def run_ours(args, rank, world, local_rank):
                    "entries_per_iter": entries_total, "step": "1 round: init + T/tau x (step(tau), update_support) + objective",
                    "parallelism": f"dp{world} (members sharded, NCCL all-reduce of per-cluster partials)",
                    "l2": "inputs larger than L2 (state %.1f GB)" % (info["state_bytes"] / 1e9),
+                   "cost_build": ["fp32", "tcgen05-bf16"][args.cost_mode],
                    "kernel_variant": {3: "wide", 2: "tma", 1: "warp", 0: "generic"}[info["variant"]]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -331,6 +332,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cost-mode", type=int, default=0, help="0: fp32 cost build, 1: bf16 tcgen05 (cached-cost kernels)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

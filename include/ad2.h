@@ -56,6 +56,13 @@ typedef enum { AD2_F32 = 0, AD2_F64 = 1 } ad2_dtype;
 typedef enum { AD2_R1 = 0, AD2_R2 = 1 } ad2_rule;          /* Eq.badmmw / Eq.badmmw2 */
 typedef enum { AD2_DEVICE = 0, AD2_HOST = 1 } ad2_mem;     /* where a caller buffer lives */
 typedef enum { AD2_PI1 = 0, AD2_PI2 = 1, AD2_LAMBDA = 2, AD2_COST = 3 } ad2_plan;
+/* Cost build for the cached-cost kernels (m > 32, m_k > 32 or d > 16):
+ *  AD2_COST_FP32   : fp32 FMAs, C = |x|^2 + |y|^2 - 2 x.y clamped at 0 (the parity default);
+ *  AD2_COST_TC_BF16: tcgen05 tensor cores, x and y rounded to bf16, fp32 accumulation in TMEM;
+ *                    |dC| <= 2^-7 |x_i||y_j| (+ fp32 rounding).  SURVEY.md §8(d) config 4.
+ *                    AD2_ERR_ARG when the round does not use the cached-cost warp-pair kernel.
+ * (m <= 32 with d <= 16 recomputes C in fp32 inside the iteration kernel; cost_mode must be 0.) */
+typedef enum { AD2_COST_FP32 = 0, AD2_COST_TC_BF16 = 1 } ad2_cost_mode;
 
 typedef enum {
     AD2_OK = 0,
@@ -89,7 +96,7 @@ typedef struct {
     double rho0;                /* > 0; rho_c = rho0 * mean cost of cluster c (X1); paper default 2 */
     double eps;                 /* >= 0; floor of Eq.badmmc0b / Eq.badmmc1b, paper 1e-16 */
     int32_t rule;               /* AD2_R1 or AD2_R2 */
-    int32_t cost_mode;          /* 0: cache C in HBM (default); other values reserved */
+    int32_t cost_mode;          /* ad2_cost_mode: how C is built when it is cached (see below) */
 } ad2_params;
 
 typedef struct {

@@ -152,7 +152,8 @@ class Context:
         self._chk(self.L.ad2_attach_nccl(self.h, nranks, rank, C.c_char_p(unique_id)))
 
     def init(self, offsets, supports, weights, labels, x0, w0, K: int, m: int, rho0=2.0, eps=1e-16,
-             rule=R1, warm_mask=None, mem: str = "device", dtype: Optional[str] = None) -> np.ndarray:
+             rule=R1, warm_mask=None, mem: str = "device", dtype: Optional[str] = None,
+             cost_mode: int = 0) -> np.ndarray:
         """ad2_barycenter_init; returns rho per cluster (host float64 [K])."""
         if dtype is None:
             dt = getattr(supports, "dtype", None)
@@ -160,7 +161,7 @@ class Context:
         d = int(supports.shape[1]) if supports.shape[0] > 0 else int(x0.shape[-1])
         b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K),
                   int(len(labels)), _ptr(offsets), _ptr(supports), _ptr(weights), _ptr(labels))
-        prm = Params(float(rho0), float(eps), int(rule), 0)
+        prm = Params(float(rho0), float(eps), int(rule), int(cost_mode))
         wm = None
         if warm_mask is not None:
             wm = np.ascontiguousarray(np.asarray(warm_mask), dtype=np.uint8)

@@ -105,6 +105,7 @@ struct ad2_ctx_s {
   double rho0 = 2.0, eps = 1e-16;
   int64_t N = 0, n = 0, n_items = 0;
   int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;
+  int cost_mode = 0;                 // ad2_cost_mode
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
   size_t es = 4;                     // element size
@@ -213,9 +214,6 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
 template <typename T>
 void launch_cost_member(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const T* Y, const T* x,
                         const T* P, double* pm, int m, int d, int ld, cudaStream_t s);
-template <typename T>
-void launch_cost_rows(int dp, const int64_t* off, const int64_t* imb, const int32_t* icl, const T* Y, const T* x,
-                      const T* P, double* psum, int m, int d, int ld, int64_t n_items, cudaStream_t s);
 template <typename T, int MP>
 size_t tma_cta_bytes(int nch, int dp);
 
@@ -233,6 +231,8 @@ size_t wide_cta_bytes(int cfg);
 void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s);
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
                       float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
+void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                    float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
 
 template <typename T>
 static void launch_iter_T(ad2_ctx ctx, int mode, cudaStream_t s) {
@@ -282,7 +282,7 @@ static ad2_status consensus(ad2_ctx ctx, cudaStream_t s) {
 }
 
 // Cost: variants 0/1 keep C in HBM (k_cost, optional per-item sums); variant 2 recomputes C
-// inside the iteration kernel, so only the rho numerator is formed here (k_cost_rows).
+// inside the iteration kernel, so only the rho numerator is formed here (k_cost_member).
 template <typename T>
 static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
   if (ctx->n_items == 0) return AD2_OK;
@@ -293,6 +293,12 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
     return launch_check(ctx, "k_cost_member");
   }
   if constexpr (sizeof(T) == 4) {
+    if (ctx->variant == 3 && ctx->cost_mode == AD2_COST_TC_BF16) {
+      launch_cost_tc(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
+                     ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
+                     with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->n_items, s);
+      return launch_check(ctx, "k_cost_tc");
+    }
     if (ctx->variant == 3) {
       launch_cost_tile(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
                        ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
@@ -461,7 +467,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   if (b->n_members > 0 && (!b->offsets || !b->supports || !b->weights || !b->labels))
     return ctx->fail(AD2_ERR_ARG, "null batch array");
   if (!(prm->rho0 > 0.0) || !std::isfinite(prm->rho0) || !(prm->eps >= 0.0) || !std::isfinite(prm->eps) ||
-      (prm->rule != AD2_R1 && prm->rule != AD2_R2) || prm->cost_mode != 0)
+      (prm->rule != AD2_R1 && prm->rule != AD2_R2) ||
+      (prm->cost_mode != AD2_COST_FP32 && prm->cost_mode != AD2_COST_TC_BF16))
     return ctx->fail(AD2_ERR_ARG, "params rho0=%g eps=%g rule=%d cost_mode=%d", prm->rho0, prm->eps, prm->rule,
                      prm->cost_mode);
   CHK(set_dev(ctx));
@@ -564,6 +571,9 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
       dp = d <= 16 ? 16 : 64;
     }
   }
+  if (prm->cost_mode == AD2_COST_TC_BF16 && variant != 3)
+    return ctx->fail(AD2_ERR_ARG, "cost_mode 1 (bf16 tensor-core cost) needs the cached-cost warp-pair kernel "
+                     "(fp32, m <= 64, m_k <= 64, d <= 64, and m > 32, m_k > 32 or d > 16)");
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
   // variant 3: blocks padded to 64 rows; Y rows padded with zeros to a multiple of 4
   const int ld = (variant == 2 || variant == 3) ? mp : m;
@@ -702,6 +712,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   ctx->dy = dy;
   ctx->parts = parts;
   ctx->wcfg = wcfg;
+  ctx->cost_mode = prm->cost_mode;
 
   CU(cudaMemsetAsync(ctx->d_err.p, 0, 4 * sizeof(int), s));
 

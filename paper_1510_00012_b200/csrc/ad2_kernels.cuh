@@ -33,11 +33,14 @@ template <> struct Num<float> {
   }
   static __device__ __forceinline__ float ld(const float* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(float* p, float v) { __stcs(p, v); }
+  // fp32 normalisations: MUFU reciprocal based quotient (<= 2 ulp), far inside the fp32 parity bar
+  static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
 };
 template <> struct Num<double> {
   static __device__ __forceinline__ double ex(double a) { return exp(a); }
   static __device__ __forceinline__ double ld(const double* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(double* p, double v) { __stcs(p, v); }
+  static __device__ __forceinline__ double div(double a, double b) { return a / b; }
 };
 
 template <typename T>
@@ -482,48 +485,6 @@ k_cost(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
 }
 
 
-// Row-wise cost sums without a C cache (variant 2): lane = centroid row i holds x_i in
-// registers, y_j is a broadcast load.  With P == nullptr: per-item sum of C (Eq.rho numerator);
-// otherwise per-item sum of C .* P (surrogate objective).  double accumulation.
-template <typename T, int DP>
-__global__ void __launch_bounds__(128)
-k_cost_rows(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
-            const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
-            const T* __restrict__ P, double* __restrict__ psum, int m, int d, int ld, int dy) {
-  const int item = blockIdx.x;
-  const int c = item_cl[item];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc = 0.0;
-  for (int r0 = 0; r0 < m; r0 += 32) {
-    const int i = r0 + lane;
-    const bool rowok = i < m;
-    T xr[DP];
-#pragma unroll
-    for (int t = 0; t < DP; ++t) xr[t] = (rowok && t < d) ? x[((int64_t)c * m + i) * d + t] : T(0);
-    for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
-      const int64_t o0 = off[k];
-      const int mk = (int)(off[k + 1] - o0);
-      T s = T(0);
-      for (int j = 0; j < mk; ++j) {
-        T cst = T(0);
-#pragma unroll
-        for (int t = 0; t < DP; ++t)
-          if (t < d) {
-            const T df = xr[t] - __ldg(Y + (o0 + j) * dy + t);
-            cst += df * df;
-          }
-        if (rowok) s += P ? cst * P[(int64_t)ld * (o0 + j) + i] : cst;
-      }
-      acc += (double)s;
-    }
-  }
-  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
-  __shared__ double sh[4];
-  if (lane == 0) sh[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
-}
-
 // surrogate objective partials (X14): sum_k <C, Pi1> per item, in double
 template <typename T>
 __global__ void __launch_bounds__(128)
@@ -584,17 +545,23 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
   const int64_t k = order[s];
   const int64_t so = src_off[k], dsto = dst_off[s];
   const int mk = (int)(src_off[k + 1] - so);
-  for (int j = lane; j < mk; j += 32) {
-    const T* src = Ysrc + (so + j) * d;
-    T* dst = Y + (dsto + j) * dy;
-    T yy = T(0);
-    for (int t = 0; t < d; ++t) {
-      const T v = src[t];
-      yy += v * v;
-      dst[t] = v;
-    }
-    for (int t = d; t < dy; ++t) dst[t] = (t == yy_col) ? yy : T(0);
+  // coordinates: the member's source block is contiguous, read lane-strided (coalesced)
+  const T* srcb = Ysrc + so * d;
+  T* dstb = Y + dsto * dy;
+  for (int e = lane; e < mk * d; e += 32) {
+    const int j = e / d, t = e - j * d;
+    dstb[(int64_t)j * dy + t] = srcb[e];
   }
+  // zero padding and the |y|^2 column (sequential in t, like the oracle's sum): lane per point
+  if (dy > d)
+    for (int j = lane; j < mk; j += 32) {
+      const T* src = srcb + (int64_t)j * d;
+      T* dst = dstb + (int64_t)j * dy;
+      T yy = T(0);
+      if (yy_col >= 0)
+        for (int t = 0; t < d; ++t) yy += src[t] * src[t];
+      for (int t = d; t < dy; ++t) dst[t] = (t == yy_col) ? yy : T(0);
+    }
   double sum = 0.0;
   for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
   for (int h = 16; h >= 1; h >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, h);

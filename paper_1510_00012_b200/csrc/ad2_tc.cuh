@@ -1,0 +1,186 @@
+// ad2_tc.cuh — tensor-core (tcgen05, bf16 in / fp32 accumulate in TMEM) cost build for the
+// cached-cost kernels (d = 64, where C is a dense contraction).
+//
+//   C_ij = |x_i|^2 + |y_j|^2 - 2 x_i . y_j     (squared Euclidean ground distance)
+//
+// For cluster c the points of a work item are contiguous, and the cost blocks of its members
+// (column-major m x m_k, ld = 64) are one contiguous point-major array: C[(p0 + p) * 64 + i].
+// One CTA (4 warps) per work item; per tile of 128 points:
+//   A = Y tile (M = 128 points x K = 64 coords, bf16, K-major, 128-byte swizzle), converted from
+//       the fp32 supports by all threads (|y_p|^2 kept in fp32),
+//   B = x_c (N = 64 centroid rows x K = 64, bf16, K-major, 128-byte swizzle), staged once,
+//   D = A B^T in TMEM (128 lanes = points x 64 fp32 columns = centroid rows), 4 MMAs of K = 16,
+// then each thread reads its point's 64 accumulators (tcgen05.ld 32x32b) and writes the 64
+// costs (256 contiguous bytes) with |x_i|^2 and |y_p|^2 added in fp32 and the result clamped
+// at 0.  bf16 operands bound the error by |dC| <= 2^-7 |x_i| |y_j| (+ fp32 rounding); the fp32
+// FMA build (k_cost_tile) stays the parity default, this one is params->cost_mode = 1.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "ad2_kernels.cuh"
+
+namespace ad2k {
+
+__device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// shared-memory matrix descriptor (sm_100 UMMA): K-major, 128-byte swizzle, 8-row atoms of
+// 1024 bytes (stride byte offset), version 1
+__device__ __forceinline__ uint64_t tc_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);            // start address
+  d |= (uint64_t)1 << 16;                            // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                  // stride byte offset: next 8-row atom
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N = 64, M = 128
+constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+// byte offset of element (row r, k) in a K-major 128B-swizzled tile with 64 bf16 per row
+__device__ __forceinline__ uint32_t tc_sw128_off(int r, int k) {
+  const int chunk = (k >> 3) ^ (r & 7);              // 16-byte chunk, XOR-swizzled by the row
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + chunk * 16 + (k & 7) * 2);
+}
+
+__global__ void __launch_bounds__(128)
+k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+          const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
+          float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
+  __shared__ __align__(1024) unsigned char sA[128 * 128];     // 16 KB, 16 atoms
+  __shared__ __align__(1024) unsigned char sB[64 * 128];      // 8 KB
+  __shared__ float xx[64], yy[128];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ double red[4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(tc_smem(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // B = x_c in bf16 (rows >= m and coordinates >= d are zero), |x_i|^2 in fp32
+  for (int v = tid; v < 64 * 8; v += 128) {            // (row, 8-coordinate chunk)
+    const int r = v >> 3, k0 = (v & 7) * 8;
+    __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      h[u] = __float2bfloat16_rn((r < m && k < d) ? x[((int64_t)c * m + r) * d + k] : 0.f);
+    }
+    *reinterpret_cast<uint4*>(sB + tc_sw128_off(r, k0)) = *reinterpret_cast<const uint4*>(h);
+  }
+  if (tid < 64) {
+    float s = 0.f;
+    for (int k = 0; k < d; ++k) {
+      const float v = tid < m ? x[((int64_t)c * m + tid) * d + k] : 0.f;
+      s = fmaf(v, v, s);
+    }
+    xx[tid] = s;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  uint32_t phase = 0;
+  for (int64_t q0 = p_beg; q0 < p_end; q0 += 128) {
+    const int np = (int)((p_end - q0) < 128 ? (p_end - q0) : 128);
+    // A = Y tile in bf16: 16 threads per point row, 4 coordinates each (coalesced fp32 reads)
+    for (int v = tid; v < 128 * 16; v += 128) {
+      const int r = v >> 4, k0 = (v & 15) * 4;
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < np && k0 < d) f = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0, pad = 0
+      float s = f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((v & 15) == 0) yy[r] = s;
+      __align__(8) __nv_bfloat16 h[4] = {__float2bfloat16_rn(f.x), __float2bfloat16_rn(f.y),
+                                         __float2bfloat16_rn(f.z), __float2bfloat16_rn(f.w)};
+      *reinterpret_cast<uint2*>(sA + tc_sw128_off(r, k0)) = *reinterpret_cast<const uint2*>(h);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = tc_desc_sw128(tc_smem(sA)), db = tc_desc_sw128(tc_smem(sB));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {                    // K = 16 per MMA: +32 bytes in the swizzle atom
+        const uint64_t a_k = da + (uint64_t)(2 * k), b_k = db + (uint64_t)(2 * k);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(a_k), "l"(b_k), "r"(TC_IDESC), "r"(k));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       tc_smem(&mbar))
+                   : "memory");
+    }
+    // wait for the accumulator
+    asm volatile(
+        "{\n\t.reg .pred p;\nTW%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra.uni TW%=;\n}" ::"r"(tc_smem(&mbar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: thread (warp, lane) = point 32 warp + lane; TMEM lanes 32 warp .. 32 warp + 31
+    const int p = 32 * warp + lane;
+    const float yp = yy[p];
+    float s = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * h);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (p < np) {
+        float4* dst = reinterpret_cast<float4*>(Cc + (q0 + p) * 64 + 32 * h);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 32 * h + 4 * u + e;
+            const float dot = __uint_as_float(r[4 * u + e]);
+            o[e] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yp), 0.f) : 0.f;
+            s += o[e];
+          }
+          dst[u] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
+    acc += (double)s;
+    // TMEM and the A tile are reused by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  }
+  if (psum) {
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) psum[item] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+}  // namespace ad2k

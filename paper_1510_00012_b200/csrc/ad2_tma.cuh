@@ -176,14 +176,20 @@ k_badmm_tma(const IterArgs<T> a) {
     p1 = a.off[k1];
     return (int)(p1 - p0);
   };
+  // G == 1: the slots of a pass region hold ceil4(m_k) columns ([P | L | Y] at 0, MP*np4,
+  // 2*MP*np4); the 0-3 padding columns of P and L are zeroed by the lanes, so the column blocks
+  // of 4 need no masks and the stores no predicates.  G > 1: packed slots, masked blocks.
+  constexpr bool PAD = (G == 1);
+  auto slot = [](int np) { return PAD ? ((np + 3) & ~3) : np; };
   auto issue = [&](int t, int base, int64_t p0, int np) {              // lane 0 only
     const uint32_t bp = (uint32_t)(MP * np * (int)sizeof(T));
     const uint32_t by = (uint32_t)(DY * np * (int)sizeof(T));
+    const int ns = slot(np);
     T* st = ring + base;
     mbar_expect_tx(&bar[t & 1], 2 * bp + by);
     tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + MP * np, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + 2 * MP * np, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
+    tma_load(st + MP * ns, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
+    tma_load(st + 2 * MP * ns, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
   };
   int64_t cp0 = 0, cp1 = 0;
   int cnp = pass_pts(0, cp0, cp1);
@@ -194,7 +200,7 @@ k_badmm_tma(const IterArgs<T> a) {
     // place pass t+1 behind pass t (or at the ring start) while t computes
     int64_t np0 = 0, np1 = 0;
     const int nnp = pass_pts(t + 1, np0, np1);
-    const int csize = (2 * MP + DY) * cnp, nsize = (2 * MP + DY) * nnp;
+    const int csize = (2 * MP + DY) * slot(cnp), nsize = (2 * MP + DY) * slot(nnp);
     int nbase = -1;
     if (nnp > 0) {
       if (cbase == 0) {                                // current at the start: next end-aligned
@@ -225,9 +231,16 @@ k_badmm_tma(const IterArgs<T> a) {
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     T* const st = ring + cbase;
     const int rel = (int)(o0 - cp0);
+    const int cns = slot(cnp);
     T* const Ps = st + MP * rel;
-    T* const Ls = st + MP * cnp + MP * rel;
-    const T* const Ys = st + 2 * MP * cnp + DY * rel;
+    T* const Ls = st + MP * cns + MP * rel;
+    const T* const Ys = st + 2 * MP * cns + DY * rel;
+    if constexpr (PAD) {
+      for (int j = mk; j < cns; ++j) {                 // padding columns: p = Lambda = 0
+        Ps[j * MP + i] = T(0);
+        Ls[j * MP + i] = T(0);
+      }
+    }
     T* const tile = (G == 1) ? st : tile_sep;          // G == 1: reuse this pass's P slot
 
     T2 p2[MK / 2], l2[MK / 2], q2[MK / 2];
@@ -240,7 +253,7 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int jp = 2 * jb + h, j = 2 * jp;
-        const bool v0 = j < mk, v1 = j + 1 < mk;
+        const bool v0 = PAD || j < mk, v1 = PAD || j + 1 < mk;
         const T pa = Ps[j * MP + i], pb = Ps[(j + 1) * MP + i];
         const T la = Ls[j * MP + i], lb = Ls[(j + 1) * MP + i];
         p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
@@ -258,7 +271,7 @@ k_badmm_tma(const IterArgs<T> a) {
     T f = T(0);
     if constexpr (MODE != P1ONLY) {
       const T r = (racc[0].x + racc[1].x) + (racc[0].y + racc[1].y) + mkeps;
-      f = (has && rowok) ? wi / r : T(0);                           // Eq.badmmc1: w_i / rowsum
+      f = (has && rowok) ? N::div(wi, r) : T(0);                    // Eq.badmmc1: w_i / rowsum
     }
     const T2 f2 = PR::make(f, f), ef2 = PR::make(eps_r * f, eps_r * f);
 
@@ -275,7 +288,7 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             const T qv = u ? q.y : q.x, lv = u ? l.y : l.x;
-            if (jj < mk) {                 // blocks are packed: no tail writes
+            if (PAD || jj < mk) {          // packed blocks (G > 1): no tail writes
               Ps[jj * MP + i] = qv;
               Ls[jj * MP + i] = lv;
             }
@@ -337,21 +350,27 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * jb + u, jt = j - ch * MP;
             const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
-            if (j < mkw) tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;   // P slot bound
+            if (PAD || j < mkw) tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;   // P slot bound
           }
         }
         __syncwarp();
         const int jc = ch * MP + i;
         T s = T(1);
-        if (jc < mk) {
-          s = T(0);
+        if (jc < mk) {                 // packed pairwise tree over the MP row values
+          T2 sp[MP / E];
 #pragma unroll
           for (int cc = 0; cc < MP / E; ++cc) {
             const V v = *reinterpret_cast<const V*>(&tile[i * 32 + ((seg * (MP / E) + cc) ^ (i & 7)) * E]);
-            s += Vec16<T>::hsum(v);
+            const T2* v2 = reinterpret_cast<const T2*>(&v);
+            sp[cc] = (E == 4) ? PR::add(v2[0], v2[(E == 4) ? 1 : 0]) : v2[0];
           }
+#pragma unroll
+          for (int w = MP / E / 2; w >= 1; w >>= 1)
+#pragma unroll
+            for (int cc = 0; cc < w; ++cc) sp[cc] = PR::add(sp[cc], sp[cc + w]);
+          s = sp[0].x + sp[0].y;
         }
-        fbuf[seg * MK + jc] = (jc < mk) ? omv[ch] / s : T(0);           // Eq.badmmc0: w_j^(k) / colsum
+        fbuf[seg * MK + jc] = (jc < mk) ? N::div(omv[ch], s) : T(0);   // Eq.badmmc0: w_j^(k) / colsum
       }
       __syncwarp();
       // ---- Pi1 = pt2 * factor_j; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row masses
@@ -372,7 +391,7 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
-            if (jj < mk) {                 // blocks are packed: no tail writes
+            if (PAD || jj < mk) {          // packed blocks (G > 1): no tail writes
               Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
               if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
             }
@@ -384,7 +403,7 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
       for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
       if (has && rowok) {
-        const T wt = r2 / R;                                             // normalised row mass
+        const T wt = N::div(r2, R);                                      // normalised row mass
         accw += (a.rule == 1) ? sqrt(wt) : wt;
         bad |= !isfinite(wt);
       }
@@ -395,7 +414,7 @@ k_badmm_tma(const IterArgs<T> a) {
     if (lane == 0) {
       const uint32_t bp = (uint32_t)(MP * cnp * (int)sizeof(T));
       tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
-      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cnp, bp);
+      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cns, bp);
       bulk_commit();
       if (nnp > 0 && nbase < 0) {    // pass t+1 did not fit beside pass t: issue it now at the ring start
         bulk_wait_read_all();
@@ -436,77 +455,12 @@ k_badmm_tma(const IterArgs<T> a) {
 }
 
 
-// Row-wise cost sums for variant 2 (no C cache), same staged layout as the iteration kernel:
-// lane = centroid row i holds x_i, y_j rows (stride DY) are broadcast 16-byte loads, and the cost
-// is the difference form sum_t (x_it - y_jt)^2 (no cancellation: these are the reported rho and
-// objective).  P == nullptr: per-item sum of C (Eq.rho numerator); otherwise the
-// per-item sum of C .* Pi1 (surrogate objective).  Accumulated in double.
-template <typename T, int DP>
-__global__ void __launch_bounds__(128)
-k_cost_rows2(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
-             const int32_t* __restrict__ item_cl, const T* __restrict__ Y, const T* __restrict__ x,
-             const T* __restrict__ P, double* __restrict__ psum, int m, int d, int ld) {
-  using V = typename Vec16<T>::type;
-  using PR = Pr<T>;
-  using T2 = typename PR::t;
-  constexpr int E = 16 / (int)sizeof(T);
-  constexpr int DY = (DP == 4) ? 4 : DP + E;
-  const int item = blockIdx.x;
-  const int c = item_cl[item];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = lane;
-  const bool rowok = i < m;
-  T2 xr2[DP / 2];
-  T2 msk2[DP / 2];                                    // 1 for real coordinates (t < d), else 0
-#pragma unroll
-  for (int t = 0; t < DP / 2; ++t) {
-    const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
-    const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
-    xr2[t] = PR::make(v0, v1);
-    msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
-  }
-  double acc = 0.0;
-  for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
-    const int64_t o0 = off[k];
-    const int mk = (int)(off[k + 1] - o0);
-    T s = T(0);
-    for (int j0 = 0; j0 < mk; j0 += 4) {
-      T2 c2[4];
-      T pv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = (j0 + u < mk) ? j0 + u : mk - 1;
-        const T* yj = Y + (o0 + j) * DY;
-        c2[u] = PR::make(T(0), T(0));
-#pragma unroll
-        for (int tt = 0; tt < DP / E; ++tt) {
-          const V v = __ldg(reinterpret_cast<const V*>(yj + tt * E));
-#pragma unroll
-          for (int u2 = 0; u2 < E / 2; ++u2) {
-            const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
-            // (x - y) on real coordinates only: padded slots hold |y|^2 and zeros
-            const T2 df = PR::mul(PR::add(xr2[tt * (E / 2) + u2], PR::mul(yv, PR::make(T(-1), T(-1)))),
-                                  msk2[tt * (E / 2) + u2]);
-            c2[u] = PR::fma(df, df, c2[u]);
-          }
-        }
-        pv[u] = (P && rowok) ? P[(int64_t)ld * (o0 + j) + i] : T(1);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * pv[u];
-    }
-    acc += (double)s;
-  }
-  for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
-  __shared__ double sh[4];
-  if (lane == 0) sh[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) psum[item] = sh[0] + sh[1] + sh[2] + sh[3];
-}
-
-// Per-member variant of the row-wise cost sums (one warp per sorted member -> pm[s]), used for
-// rho at init and the objective query: enough warps in flight to hide the load latency.
+// Row-wise cost sums for variant 2 (no C cache), one warp per sorted member -> pm[s]: lane i
+// holds x_i, the member's Y rows (stride DY) are broadcast 16-byte loads, and the cost is the
+// difference form sum_t (y_jt - x_it)^2 (no cancellation: these are the reported rho and
+// objective).  P == nullptr: sum of C (Eq.rho numerator); otherwise sum of C .* Pi1
+// (surrogate objective).  Accumulated in double per member; the cluster sums are
+// formed in a fixed order by k_dsum_members.
 template <typename T, int DP>
 __global__ void __launch_bounds__(128)
 k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restrict__ mem_cl,
@@ -521,7 +475,7 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
   const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
   if (sidx >= N) return;
   const int c = mem_cl[sidx];
-  T2 xr2[DP / 2], msk2[DP / 2];
+  T2 nx2[DP / 2], msk2[DP / 2];                      // -x_i (difference form); mask only for DP == 4
   double acc = 0.0;
   for (int r0 = 0; r0 < m; r0 += 32) {
     const int i = r0 + lane;
@@ -530,7 +484,7 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
     for (int t = 0; t < DP / 2; ++t) {
       const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
       const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
-      xr2[t] = PR::make(v0, v1);
+      nx2[t] = PR::make(-v0, -v1);
       msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
     }
     const int64_t o0 = off[sidx];
@@ -550,8 +504,10 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
 #pragma unroll
           for (int u2 = 0; u2 < E / 2; ++u2) {
             const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
-            const T2 df = PR::mul(PR::add(xr2[tt * (E / 2) + u2], PR::mul(yv, PR::make(T(-1), T(-1)))),
-                                  msk2[tt * (E / 2) + u2]);
+            // y - x on the real coordinates: for DP >= 16 the slots [d, DP) of a Y row are 0 (and
+            // |y|^2 sits at DP), for DP == 4 the |y|^2 slot is inside the row and is masked
+            T2 df = PR::add(yv, nx2[tt * (E / 2) + u2]);
+            if constexpr (DP == 4) df = PR::mul(df, msk2[tt * (E / 2) + u2]);
             c2[u] = PR::fma(df, df, c2[u]);
           }
         }

@@ -68,9 +68,9 @@ k_badmm_wide(const IterArgs<float> a) {
   const float2 rho2 = make_float2(rho, rho), nrho2 = make_float2(-rho, -rho);
   const float2 eps2 = make_float2(eps_r, eps_r);
   float accw = 0.f, accm = 0.f;
-  float accx[(MODE == P2ONLY) ? DP : 1];
+  float2 accx[(MODE == P2ONLY) ? DP / 2 : 1];                     // coordinate pairs (FFMA2)
 #pragma unroll
-  for (int t = 0; t < ((MODE == P2ONLY) ? DP : 1); ++t) accx[t] = 0.f;
+  for (int t = 0; t < ((MODE == P2ONLY) ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
   bool bad = false;
   const float* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
   float* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
@@ -161,9 +161,11 @@ k_badmm_wide(const IterArgs<float> a) {
     if constexpr (MODE == P2ONLY) {
       // ---- sweep B2: Pi2 = (pe + eps) w_i / r (Eq.badmmc1), Lambda -= rho Pi2 (Eq.badmm2),
       //      support-update partials sum_j pi2_ij y_j, sum_j pi2_ij (Eq.updatex, X5)
+#pragma unroll 2
       for (int j = 0; j < mk; ++j) {
         const int e0 = j * WMP + ig;
         const float q = fmaf(Ps[e0], f, eps_r * f);
+        const float2 q2 = make_float2(q, q);
         const float l = fmaf(-rho, q, Ls[e0]);
         Ps[e0] = q;
         Ls[e0] = l;
@@ -173,10 +175,8 @@ k_badmm_wide(const IterArgs<float> a) {
         for (int tt = 0; tt < DP / 4; ++tt) {
           if (4 * tt < d) {
             const float4 v = *(reinterpret_cast<const float4*>(yj) + tt);
-            accx[4 * tt + 0] = fmaf(q, v.x, accx[4 * tt + 0]);
-            accx[4 * tt + 1] = fmaf(q, v.y, accx[4 * tt + 1]);
-            accx[4 * tt + 2] = fmaf(q, v.z, accx[4 * tt + 2]);
-            accx[4 * tt + 3] = fmaf(q, v.w, accx[4 * tt + 3]);
+            accx[2 * tt + 0] = __ffma2_rn(q2, make_float2(v.x, v.y), accx[2 * tt + 0]);
+            accx[2 * tt + 1] = __ffma2_rn(q2, make_float2(v.z, v.w), accx[2 * tt + 1]);
           }
         }
       }
@@ -281,7 +281,7 @@ k_badmm_wide(const IterArgs<float> a) {
       px[d] = accm;
 #pragma unroll
       for (int t = 0; t < DP; ++t)
-        if (t < d) px[t] = accx[t];
+        if (t < d) px[t] = (t & 1) ? accx[t / 2].y : accx[t / 2].x;
     }
   }
 }
@@ -329,21 +329,24 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
       for (int t = 0; t < d; ++t) s = fmaf(ys[t][tid], ys[t][tid], s);
       yy[tid] = s;
     }
-    float a4[4][4];
+    float2 a2[2][4];                                   // rows (4ti, 4ti+1) and (4ti+2, 4ti+3) x 4 points
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) a4[u][v] = 0.f;
-#pragma unroll 8
-    for (int t = 0; t < DMAX; ++t) {
-      if (t >= d) break;
+      for (int v = 0; v < 4; ++v) a2[u][v] = make_float2(0.f, 0.f);
+    const int dpad = (d + 3) & ~3;                     // coordinates >= d are zero in xs / ys
+#pragma unroll 4
+    for (int t = 0; t < dpad; ++t) {
       const float4 xv = *reinterpret_cast<const float4*>(&xs[t][4 * ti]);
       const float4 yv = *reinterpret_cast<const float4*>(&ys[t][4 * tj]);
-      const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
+      const float2 x01 = make_float2(xv.x, xv.y), x23 = make_float2(xv.z, xv.w);
+      const float ya[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) a4[u][v] = fmaf(xa[u], ya[v], a4[u][v]);
+      for (int v = 0; v < 4; ++v) {
+        const float2 yy2 = make_float2(ya[v], ya[v]);
+        a2[0][v] = __ffma2_rn(x01, yy2, a2[0][v]);
+        a2[1][v] = __ffma2_rn(x23, yy2, a2[1][v]);
+      }
     }
     __syncthreads();                                   // yy ready
     float s = 0.f;
@@ -356,7 +359,8 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = 4 * ti + u;
-          const float cv = (i < m) ? fmaxf(fmaf(-2.f, a4[u][v], xx[i] + yy[j]), 0.f) : 0.f;
+          const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
+          const float cv = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yy[j]), 0.f) : 0.f;
           oe[u] = cv;
           s += cv;
         }

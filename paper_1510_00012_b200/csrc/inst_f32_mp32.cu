@@ -70,20 +70,6 @@ void launch_warp<float, 32>(int variant, int mode, int nch, int dp, const IterAr
   go_nch<1>(variant, mode, dp, a, n_items, s);
 }
 
-// row-wise cost sums (rho numerator / objective) for variant 2
-template <typename T>
-void launch_cost_rows(int dp, const int64_t* off, const int64_t* imb, const int32_t* icl, const T* Y, const T* x,
-                      const T* P, double* psum, int m, int d, int ld, int64_t n_items, cudaStream_t s);
-
-template <>
-void launch_cost_rows<float>(int dp, const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y,
-                           const float* x, const float* P, double* psum, int m, int d, int ld, int64_t n_items,
-                           cudaStream_t s) {
-  if (n_items == 0) return;
-  if (dp <= 4) k_cost_rows2<float, 4><<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, P, psum, m, d, ld);
-  else k_cost_rows2<float, 16><<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, P, psum, m, d, ld);
-}
-
 template <typename T>
 void launch_cost_member(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const T* Y, const T* x,
                         const T* P, double* pm, int m, int d, int ld, cudaStream_t s);

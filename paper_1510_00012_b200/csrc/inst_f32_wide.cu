@@ -2,6 +2,7 @@
 // and of the tiled cost build (ad2_wide.cuh).
 #include <cstdlib>
 
+#include "ad2_tc.cuh"
 #include "ad2_wide.cuh"
 
 namespace ad2k {
@@ -55,4 +56,10 @@ void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl
   if (n_items == 0) return;
   if (d <= 16) k_cost_tile<16><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
   else k_cost_tile<64><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
+}
+
+void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                    float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
+  if (n_items == 0) return;
+  k_cost_tc<<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
 }

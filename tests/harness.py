@@ -21,7 +21,7 @@ def to_dev(b: wl.Bundle, torch):
 
 
 def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False, ctx=None, warm_mask=None,
-            x0=None, w0=None, profile=False):
+            x0=None, w0=None, profile=False, cost_mode=0):
     """Run one round of Alg. 4 on the GPU; returns (ctx, rho, objective)."""
     from paper_1510_00012_b200 import ad2
     torch = torch_cuda()
@@ -45,7 +45,7 @@ def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False,
         a = dict(offsets=b.offsets, supports=b.supports, weights=b.weights, labels=b.labels,
                  x0=np.ascontiguousarray(x0), w0=np.ascontiguousarray(w0))
     rho = ctx.init(a["offsets"], a["supports"], a["weights"], a["labels"], a["x0"], a["w0"], b.K, b.m,
-                   s.rho0, s.eps, rule, warm_mask=warm_mask, mem=mem, dtype=b.dtype)
+                   s.rho0, s.eps, rule, warm_mask=warm_mask, mem=mem, dtype=b.dtype, cost_mode=cost_mode)
     ad2.run_schedule(ctx, T, tau)
     obj = ctx.objective() if T > 0 else None
     torch.cuda.synchronize()

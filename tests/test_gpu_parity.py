@@ -115,6 +115,48 @@ def test_fp32_ragged_shapes(m, mk, d):
     compare_round(b, T=12, tau=4, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False)
 
 
+# ------------------------------------------------------------------ tensor-core cost build (config 4)
+
+def test_tc_bf16_cost_build_cfg4():
+    """cost_mode 1 (tcgen05, bf16 operands, fp32 accumulation) against the oracle's fp64 cost:
+    |dC| <= 2^-7 |x_i||y_j| (bf16 rounding of both operands, Cauchy-Schwarz) + fp32 rounding;
+    the fp32 build (cost_mode 0) is held to fp32 rounding only.  Partial 128-point tiles, m = 64."""
+    b = wl.make_config(4, N=1500)
+    sample = np.random.default_rng(1).choice(b.N, 200, replace=False)
+    worst = {}
+    for mode in (0, 1):
+        ctx, _, _ = run_gpu(b, 0, 1, cost_mode=mode)
+        assert ctx.info()["variant"] == 3
+        Cg = ctx.member_matrices(ad2.COST)
+        err = 0.0
+        for k in sample:
+            c = b.labels[k]
+            Y = b.member(k)[0].astype(np.float64)
+            x = b.x0[c].astype(np.float64)
+            Co = oracle.cost(x, Y)
+            nx, ny = np.linalg.norm(x, axis=1), np.linalg.norm(Y, axis=1)
+            scale = nx[:, None] ** 2 + ny[None, :] ** 2
+            bound = 4e-6 * scale + (2.0 ** -7 * nx[:, None] * ny[None, :] if mode == 1 else 0.0)
+            d = np.abs(Cg[k].astype(np.float64) - Co)
+            assert (d <= bound).all(), (mode, k, float((d - bound).max()))
+            err = max(err, float(d.max()))
+        worst[mode] = err
+    assert worst[1] > worst[0]          # the tensor-core path really ran on bf16 operands
+    # the whole schedule on the tensor-core cost stays close to the fp32 result (report-only bound)
+    T, tau = b.sched.T, b.sched.tau
+    ctx0, _, obj0 = run_gpu(b, T, tau, cost_mode=0)
+    ctx1, _, obj1 = run_gpu(b, T, tau, cost_mode=1)
+    assert np.isfinite(obj1).all()
+    rel = np.abs(obj1 - obj0) / np.maximum(np.abs(obj0), 1e-3 * np.abs(obj0).max())
+    assert np.median(rel) < 0.05, rel
+
+
+def test_tc_cost_mode_rejected_without_cost_cache():
+    b = wl.make_config(3, N=500, K=4)           # m = 32, d = 16: cost recomputed in-kernel
+    with pytest.raises(ad2.AD2Error, match="ARG"):
+        run_gpu(b, 0, 1, cost_mode=1)
+
+
 # ------------------------------------------------------------------ paths that must agree exactly
 
 def _state(ctx):
