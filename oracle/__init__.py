@@ -53,6 +53,7 @@ def lib():
             build()
             L = C.CDLL(_SO)
             d, i, p, i64 = C.c_double, C.c_int, C.c_void_p, C.c_int64
+            L.ad2o_assign.argtypes = [i, i, i, p, p, i, p, p, p, p, p, p]
             L.ad2o_cost.argtypes = [i, i, i, p, p, p]
             L.ad2o_rho.argtypes = [i, i, p, i, p, p, d, p]
             L.ad2o_rho.restype = d
@@ -189,6 +190,23 @@ def exact_objective(x, w, offsets, Y, omega) -> float:
     w = w / w.sum()
     return float(lib().ad2o_exact_objective(x.shape[0], x.shape[1], _ptr(x), _ptr(w), len(off) - 1,
                                             _ptr(off - off[0]), _ptr(Y), _ptr(om)))
+
+
+def assign(x, w, offsets, Y, omega):
+    """Assignment step (Alg. 1; O7, X13): exact W^2 of every member to every centroid
+    (transportation simplex, no pruning), label = argmin with ties to the lowest index.
+    Returns (labels int32 [N], best W^2 [N], second-best W^2 [N])."""
+    x, w, Y, omega = map(_f64, (x, w, Y, omega))
+    K, m, d = x.shape
+    off = np.ascontiguousarray(offsets, np.int64)
+    off = off - off[0]
+    N = len(off) - 1
+    lab = np.zeros(N, np.int32)
+    best = np.zeros(N)
+    second = np.zeros(N)
+    lib().ad2o_assign(K, m, d, _ptr(x), _ptr(w), N, _ptr(off), _ptr(Y), _ptr(omega), lab.ctypes.data,
+                      _ptr(best), _ptr(second))
+    return lab, best, second
 
 
 # ---- Algorithm 4 ----

@@ -179,3 +179,44 @@ double ad2o_exact_objective(int m, int d, const double *x, const double *w, int 
     }
     return s / (double)N;
 }
+
+/* Assignment step of AD2-clustering (Alg. 1, reading X13):
+ * l^(k) = argmin_c W^2(P_c, P^(k)) by exact OT against EVERY centroid (no pruning), ties to the
+ * lowest c.  Centroid weights w_c and member weights are renormalised by their fp64 sums
+ * (O1).  best[k] = the minimum W^2, second[k] = the runner-up (gap = second - best; +inf if K = 1).
+ * Members are independent: OpenMP over k, no cross-member arithmetic. */
+void ad2o_assign(int K, int m, int d, const double *x, const double *w, int N, const int64_t *off,
+                 const double *Y, const double *omega, int32_t *labels, double *best, double *second)
+{
+    double *wn = (double *)malloc(sizeof(double) * (size_t)K * m);
+    for (int c = 0; c < K; ++c) {
+        double s = 0.0;
+        for (int i = 0; i < m; ++i) s += w[c * m + i];
+        for (int i = 0; i < m; ++i) wn[c * m + i] = w[c * m + i] / s;
+    }
+    #pragma omp parallel for schedule(dynamic, 4)
+    for (int k = 0; k < N; ++k) {
+        const int mk = (int)(off[k + 1] - off[k]);
+        double *om = (double *)malloc(sizeof(double) * (size_t)mk);
+        double s = 0.0;
+        for (int j = 0; j < mk; ++j) s += omega[off[k] + j];
+        for (int j = 0; j < mk; ++j) om[j] = omega[off[k] + j] / s;
+        double b1 = INFINITY, b2 = INFINITY;
+        int lab = -1;
+        for (int c = 0; c < K; ++c) {
+            double W = ad2o_w2sq(m, mk, d, x + (size_t)c * m * d, wn + (size_t)c * m, Y + off[k] * d, om, NULL);
+            if (W < b1) {
+                b2 = b1;
+                b1 = W;
+                lab = c;
+            } else if (W < b2) {
+                b2 = W;
+            }
+        }
+        labels[k] = lab;
+        best[k] = b1;
+        second[k] = b2;
+        free(om);
+    }
+    free(wn);
+}

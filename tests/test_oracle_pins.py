@@ -406,3 +406,58 @@ def test_oracle_errors():
         oracle.badmm_centroid([[1.0]], [1.0], [0, 1], [[1.0]], [1.0], 5, 5)
     with pytest.raises(oracle.OracleError, match="arg"):
         oracle.badmm_centroid([[1.0]], [1.0], [0, 2], [[1.0], [2.0]], [0.5, 0.4], 5, 5)
+
+
+# ---------------------------------------------------------------- O7 assignment (Alg. 1)
+
+def _w2_1d(xa, wa, xb, wb):
+    """1-D W2^2 by the quantile coupling (closed form, independent of the transport simplex)."""
+    ia, ib = np.argsort(xa), np.argsort(xb)
+    xa, wa, xb, wb = xa[ia], wa[ia] / wa.sum(), xb[ib], wb[ib] / wb.sum()
+    Fa, Fb = np.cumsum(wa), np.cumsum(wb)
+    ts = np.unique(np.concatenate([[0.0], Fa[:-1], Fb[:-1], [1.0]]))
+    q = 0.0
+    for t0, t1 in zip(ts[:-1], ts[1:]):
+        tm = 0.5 * (t0 + t1)
+        q += (t1 - t0) * (xa[min(np.searchsorted(Fa, tm), len(xa) - 1)] - xb[min(np.searchsorted(Fb, tm), len(xb) - 1)]) ** 2
+    return q
+
+
+def test_O7_assign_1d_closed_form():
+    """Labels / best / second-best W^2 against the 1-D quantile formula for every (member, centroid)."""
+    rng = np.random.default_rng(11)
+    K, m, N = 5, 4, 40
+    x = rng.normal(0, 3, (K, m, 1))
+    w = rng.dirichlet(np.ones(m), K) * 1.7                       # unnormalised: renormalised inside
+    sizes = rng.integers(1, 7, N)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    Y = rng.normal(0, 3, (off[-1], 1))
+    om = rng.dirichlet(np.ones(off[-1]))                          # per member renormalised inside
+    lab, best, second = oracle.assign(x, w, off, Y, om)
+    for k in range(N):
+        a, b = off[k], off[k + 1]
+        W = np.array([_w2_1d(x[c, :, 0], w[c], Y[a:b, 0], om[a:b]) for c in range(K)])
+        order = np.argsort(W, kind="stable")
+        assert lab[k] == order[0]
+        assert best[k] == pytest.approx(W[order[0]], abs=1e-10)
+        assert second[k] == pytest.approx(W[order[1]], abs=1e-10)
+
+
+def test_O7_assign_identity_and_ties():
+    """A member equal to centroid c is assigned to c with W^2 = 0; duplicated centroids tie and the
+    lowest index wins (X13); translating everything leaves the labels unchanged."""
+    rng = np.random.default_rng(12)
+    K, m, d = 4, 3, 2
+    x = rng.normal(0, 5, (K, m, d))
+    x[3] = x[1]                                                   # centroid 3 duplicates centroid 1
+    w = rng.dirichlet(np.ones(m), K)
+    w[3] = w[1]
+    off = np.arange(K + 1) * m
+    Y = x.reshape(-1, d).copy()
+    om = w.reshape(-1).copy()
+    lab, best, second = oracle.assign(x, w, off, Y, om)
+    assert list(lab) == [0, 1, 2, 1]
+    assert np.abs(best).max() < 1e-12
+    assert second[1] < 1e-12 and second[3] < 1e-12 and second[0] > 1e-3
+    lab2, best2, _ = oracle.assign(x + 7.5, w, off, Y + 7.5, om)
+    assert list(lab2) == list(lab) and np.abs(best2).max() < 1e-10
