@@ -149,6 +149,21 @@ ad2_status ad2_update_support(ad2_ctx ctx);
  * current x.  AD2_ERR_STATE if no step has run since init.  Synchronises. */
 ad2_status ad2_objective(ad2_ctx ctx, double *obj_out);
 
+/* Assignment step of AD2-clustering (Alg. 1, reading X13):
+ * for every member k of `batch` (the caller's ragged layout, dtype and mem as in init; the
+ * batch's labels are ignored) l^(k) = argmin_c W_2^2(P_c, P^(k)), the exact optimal-transport
+ * cost (Eq.primal, squared Euclidean ground cost) to each centroid c of
+ * (x [K][m][d], w [K][m]) in batch->dtype and batch->mem; ties go to the lowest c.  Weights of
+ * both sides are renormalised in fp64; the whole step runs in fp64 on the device (mean and
+ * relaxed-marginal lower bounds prune centroids, survivors are solved exactly by successive
+ * shortest paths).  Outputs in `where` memory: labels_out [N] (int32), w2_out [N] (double, the
+ * minimum W_2^2; may be NULL).  n_exact_out (host, may be NULL): exact problems solved.
+ * Synchronous.  Independent of the B-ADMM round state (needs only a created context).
+ * Errors: AD2_ERR_ARG for bad shapes / offsets / a member + centroid pair whose workspace does
+ * not fit in shared memory; AD2_ERR_NONFINITE if a transport solve failed to terminate. */
+ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch *batch, const void *x, const void *w,
+                      int32_t *labels_out, double *w2_out, ad2_mem where, int64_t *n_exact_out);
+
 /* Current centroids: x [K][m][d], w [K][m] in the ctx dtype, into `where` memory. */
 ad2_status ad2_get_centroids(ad2_ctx ctx, void *x, void *w, ad2_mem where);
 

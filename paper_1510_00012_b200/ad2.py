@@ -54,7 +54,7 @@ class Info(C.Structure):
 
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
-           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_sync", "ad2_last_error",
+           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_sync", "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
 _lib = None
@@ -82,6 +82,7 @@ def load_library(path: str = LIB_PATH):
     L.ad2_get_info.argtypes = [p, C.POINTER(Info)]
     L.ad2_set_profiling.argtypes = [p, C.c_int]
     L.ad2_prof_read.argtypes = [p, p, i64, C.POINTER(i64), C.POINTER(d)]
+    L.ad2_assign.argtypes = [p, C.POINTER(Batch), p, p, p, p, C.c_int, C.POINTER(i64)]
     L.ad2_sync.argtypes = [p]
     L.ad2_last_error.argtypes = [p]
     L.ad2_last_error.restype = C.c_char_p
@@ -236,6 +237,23 @@ class Context:
         n, step = C.c_int64(), C.c_double()
         self._chk(self.L.ad2_prof_read(self.h, buf.ctypes.data, len(buf), C.byref(n), C.byref(step)))
         return buf[:min(n.value, len(buf))].copy(), step.value
+
+    def assign(self, offsets, supports, weights, x, w, mem: str = "device", dtype: Optional[str] = None):
+        """ad2_assign: exact-W2 labels of the members against centroids (x [K][m][d], w [K][m]).
+        Returns (labels int32 [N], W2 float64 [N], number of exact transport solves) on the host."""
+        if dtype is None:
+            dt = getattr(supports, "dtype", None)
+            dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
+        K, m, d = int(x.shape[0]), int(x.shape[1]), int(x.shape[2])
+        N = int(offsets.shape[0]) - 1
+        b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, m, K, N, _ptr(offsets),
+                  _ptr(supports), _ptr(weights), None)
+        lab = np.zeros(max(N, 0), np.int32)
+        w2 = np.zeros(max(N, 0))
+        n_exact = C.c_int64()
+        self._chk(self.L.ad2_assign(self.h, C.byref(b), _ptr(x), _ptr(w), lab.ctypes.data, w2.ctypes.data, HOST,
+                                    C.byref(n_exact)))
+        return lab, w2, int(n_exact.value)
 
     def sync(self):
         self._chk(self.L.ad2_sync(self.h))

@@ -121,6 +121,7 @@ struct ad2_ctx_s {
   DBuf stage_lab, mem_cl, pm;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
+  DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal;   // assignment step scratch
 
   std::map<int, StepGraph*> graphs;
   bool prof = false;
@@ -1001,6 +1002,95 @@ ad2_status ad2_prof_read(ad2_ctx ctx, double* launch_ms, int64_t capacity, int64
   CU(cudaEventElapsedTime(&all, g->ev.front(), g->ev.back()));
   if (n_launches) *n_launches = nl;
   if (step_ms) *step_ms = all;
+  return AD2_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// assignment step (ad2_assign.cu)
+// ------------------------------------------------------------------------------------------
+size_t assign_warp_bytes(int m, int mkmax, int K, int d);
+int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
+                  const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
+                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s);
+void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int* err, cudaStream_t s);
+
+ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
+                      double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!b || !x || !w) return ctx->fail(AD2_ERR_ARG, "assign: null batch/x/w");
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
+  if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
+  if (where != AD2_DEVICE && where != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "where");
+  if (b->d < 1 || b->m < 1 || b->K < 1 || b->n_members < 0 || b->n_members > INT32_MAX)
+    return ctx->fail(AD2_ERR_ARG, "shape d=%d m=%d K=%d N=%lld", b->d, b->m, b->K, (long long)b->n_members);
+  const int64_t N = b->n_members;
+  if (N > 0 && (!b->offsets || !b->supports || !b->weights || !labels_out))
+    return ctx->fail(AD2_ERR_ARG, "null batch array / labels_out");
+  CHK(set_dev(ctx));
+  cudaStream_t s = ctx->stream;
+  const int d = b->d, m = b->m, K = b->K;
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  const bool host = b->mem == AD2_HOST;
+  const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // inputs on the device (host batches are staged)
+  const void* off = b->offsets;
+  const void* Y = b->supports;
+  const void* W = b->weights;
+  int64_t n = 0;
+  if (N > 0) {
+    if (host) {
+      n = static_cast<const int64_t*>(b->offsets)[N];
+      CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
+      CU(ctx->stage_Y.reserve(es * (size_t)n * d));
+      CU(ctx->stage_W.reserve(es * (size_t)n));
+      CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+      off = ctx->stage_off.p;
+      Y = ctx->stage_Y.p;
+      W = ctx->stage_W.p;
+    }
+  }
+  CU(ctx->asg_cx.reserve(es * (size_t)K * m * (d + 1)));
+  CU(cudaMemcpyAsync(ctx->asg_cx.p, x, es * (size_t)K * m * d, h2d, s));
+  CU(cudaMemcpyAsync((char*)ctx->asg_cx.p + es * (size_t)K * m * d, w, es * (size_t)K * m, h2d, s));
+  CU(ctx->asg_x.reserve(8 * ((size_t)K * m * d + (size_t)K * m + (size_t)K * d)));
+  CU(ctx->asg_lab.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
+  CU(ctx->asg_best.reserve(sizeof(double) * (N > 0 ? N : 1)));
+  CU(ctx->asg_scal.reserve(64));
+  CU(cudaMemsetAsync(ctx->asg_scal.p, 0, 64, s));
+  unsigned long long* scal = ctx->asg_scal.as<unsigned long long>();   // [0] mkmax [1] n_exact [2] err
+  int* err = reinterpret_cast<int*>(scal + 2);
+  unsigned long long hs[3] = {0, 0, 0};
+  if (N > 0) {
+    assign_mkmax(static_cast<const int64_t*>(off), N, scal, err, s);
+    CHK(launch_check(ctx, "k_assign_mk"));
+    CU(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (hs[2] & 2) return ctx->fail(AD2_ERR_ARG, "assign: offsets[0] != 0 or a member with m_k < 1");
+  }
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (N > 0 && assign_warp_bytes(m, (int)hs[0], K, d) + 1024 > (size_t)optin)
+    return ctx->fail(AD2_ERR_ARG, "assign: workspace of m=%d, m_k=%llu, K=%d exceeds shared memory", m, hs[0], K);
+  double* xc = ctx->asg_x.as<double>();
+  double* wc = xc + (size_t)K * m * d;
+  double* xb = wc + (size_t)K * m;
+  const void* wdev = (const char*)ctx->asg_cx.p + es * (size_t)K * m * d;
+  if (assign_launch(b->dtype == AD2_F64, static_cast<const int64_t*>(off), N, Y, W, ctx->asg_cx.p, wdev, K, m, d,
+                    (int)hs[0], xc, wc, xb, ctx->asg_lab.as<int32_t>(), ctx->asg_best.as<double>(), scal + 1, err,
+                    optin, s) != 0)
+    return ctx->fail(AD2_ERR_ARG, "assign: workspace does not fit");
+  CHK(launch_check(ctx, "k_assign"));
+  const cudaMemcpyKind d2o = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (N > 0) {
+    CU(cudaMemcpyAsync(labels_out, ctx->asg_lab.p, sizeof(int32_t) * N, d2o, s));
+    if (w2_out) CU(cudaMemcpyAsync(w2_out, ctx->asg_best.p, sizeof(double) * N, d2o, s));
+  }
+  CU(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (n_exact_out) *n_exact_out = (int64_t)hs[1];
+  if (hs[2] & 1) return ctx->fail(AD2_ERR_NONFINITE, "assign: a transport solve did not terminate");
   return AD2_OK;
 }
 

@@ -1,0 +1,367 @@
+// ad2_assign.cu — the assignment step of AD2-clustering on the GPU:
+//
+//   l^(k) = argmin_c W_2^2(P_c, P^(k))           (Alg. 1; ties to the lowest c, X13)
+//
+// W_2^2 is the exact optimal-transport cost (Eq.primal) with the squared Euclidean
+// ground cost, between centroid c (m points, weights w_c) and member k (m_k points, weights
+// w^(k)), both renormalised in fp64.  One warp per member, everything in fp64:
+//   1. lower bound for every centroid from the means: W^2 >= |mean(P_c) - mean(P^(k))|^2
+//      (the squared-Euclidean cost splits into the distance of the means plus a non-negative
+//      term);
+//   2. centroids are visited in increasing bound order until the bound exceeds the best exact
+//      cost found (Elkan-style pruning, without the inter-centroid table); for each
+//      visited centroid the cost matrix is built and the relaxed-marginal bounds
+//      sum_j w_j min_i C_ij and sum_i w_i min_j C_ij (each drops one constraint of Eq.primal)
+//      prune again;
+//   3. survivors are solved exactly by successive shortest paths on the bipartite transport
+//      network (Dijkstra with node potentials on reduced costs, augment along the path by the
+//      bottleneck of supply, demand and reverse-arc flow) — a primal-dual method that ends at
+//      an optimal basic plan, so the cost equals the oracle's transportation simplex up to fp64
+//      rounding.
+// No float atomics: per-member results are written by the member's warp.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/ad2.h"
+
+namespace ad2a {
+
+struct AsgLay {
+  int m, mk, V, K, d;
+  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, bytes;
+  __host__ __device__ void make(int m_, int mk_, int K_, int d_) {
+    m = m_, mk = mk_, K = K_, d = d_;
+    V = m + mk;
+    size_t o = 0;
+    auto take = [&](size_t b) {
+      size_t r = o;
+      o += (b + 15) & ~(size_t)15;
+      return r;
+    };
+    oC = take(8 * (size_t)m * mk);
+    oF = take(8 * (size_t)m * mk);
+    opi = take(8 * (size_t)V);
+    odist = take(8 * (size_t)V);
+    oprev = take(4 * (size_t)V);
+    odone = take(4 * (size_t)V);
+    oarem = take(8 * (size_t)m);
+    obrem = take(8 * (size_t)mk);
+    oom = take(8 * (size_t)mk);
+    oLB = take(8 * (size_t)K);
+    osolv = take(4 * (size_t)((K + 31) / 32));
+    oyb = take(8 * (size_t)d);
+    bytes = o;
+  }
+};
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// exact W^2 by successive shortest paths; C row-major m x mk in smem; returns the cost of the
+// final plan.  err bit 1: no augmenting path / iteration cap (should not happen on a balanced
+// problem).
+__device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, int mk, int lane, int* err) {
+  const int m = L.m, V = m + mk;
+  const double* C = reinterpret_cast<const double*>(ws + L.oC);
+  double* F = reinterpret_cast<double*>(ws + L.oF);
+  double* pi = reinterpret_cast<double*>(ws + L.opi);
+  double* dist = reinterpret_cast<double*>(ws + L.odist);
+  int* prev = reinterpret_cast<int*>(ws + L.oprev);
+  int* done = reinterpret_cast<int*>(ws + L.odone);
+  double* arem = reinterpret_cast<double*>(ws + L.oarem);
+  double* brem = reinterpret_cast<double*>(ws + L.obrem);
+  const double* om = reinterpret_cast<const double*>(ws + L.oom);
+  const double tiny = 1e-14;
+  for (int e = lane; e < m * mk; e += 32) F[e] = 0.0;
+  for (int v = lane; v < V; v += 32) pi[v] = 0.0;
+  for (int i = lane; i < m; i += 32) arem[i] = wn[i];
+  for (int j = lane; j < mk; j += 32) brem[j] = om[j];
+  __syncwarp();
+  const int cap = 8 * V + 256;
+  for (int it = 0;; ++it) {
+    bool hs = false, hd = false;
+    for (int i = lane; i < m; i += 32) hs |= arem[i] > tiny;
+    for (int j = lane; j < mk; j += 32) hd |= brem[j] > tiny;
+    if (!__any_sync(0xffffffffu, hs) || !__any_sync(0xffffffffu, hd)) break;
+    if (it >= cap) {
+      if (lane == 0) atomicOr(err, 1);
+      break;
+    }
+    for (int v = lane; v < V; v += 32) {
+      done[v] = 0;
+      prev[v] = -1;
+      dist[v] = (v < m && arem[v] > tiny) ? 0.0 : CUDART_INF;
+    }
+    __syncwarp();
+    int t = -1;
+    double dt = CUDART_INF;
+    for (int step = 0; step < V; ++step) {
+      double bd = CUDART_INF;
+      int bv = V;
+      for (int v = lane; v < V; v += 32)
+        if (!done[v] && dist[v] < bd) {
+          bd = dist[v];
+          bv = v;
+        }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        if (od < bd || (od == bd && ov < bv)) {
+          bd = od;
+          bv = ov;
+        }
+      }
+      if (bv >= V || !(bd < CUDART_INF)) break;
+      if (lane == 0) done[bv] = 1;
+      if (bv >= m && brem[bv - m] > tiny) {         // the nearest sink with demand left
+        t = bv;
+        dt = bd;
+        __syncwarp();
+        break;
+      }
+      __syncwarp();
+      if (bv >= m) {                                // sink j: reverse arcs j -> i carrying flow
+        const int j = bv - m;
+        for (int i = lane; i < m; i += 32)
+          if (!done[i] && F[i * mk + j] > 0.0) {
+            const double nd = bd - C[i * mk + j] + pi[bv] - pi[i];
+            if (nd < dist[i]) {
+              dist[i] = nd;
+              prev[i] = bv;
+            }
+          }
+      } else {                                      // source i: forward arcs i -> j
+        const int i = bv;
+        for (int j = lane; j < mk; j += 32) {
+          const int v = m + j;
+          if (!done[v]) {
+            const double nd = bd + C[i * mk + j] + pi[i] - pi[v];
+            if (nd < dist[v]) {
+              dist[v] = nd;
+              prev[v] = i;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (t < 0) {
+      if (lane == 0) atomicOr(err, 1);
+      break;
+    }
+    for (int v = lane; v < V; v += 32) pi[v] += done[v] ? dist[v] : dt;   // reduced costs stay >= 0
+    __syncwarp();
+    if (lane == 0) {
+      double del = brem[t - m];
+      int v = t;
+      while (prev[v] >= 0) {
+        const int u = prev[v];
+        if (u >= m) del = fmin(del, F[v * mk + (u - m)]);
+        v = u;
+      }
+      const int s = v;
+      del = fmin(del, arem[s]);
+      v = t;
+      while (prev[v] >= 0) {
+        const int u = prev[v];
+        if (u < m) F[u * mk + (v - m)] += del;
+        else F[v * mk + (u - m)] -= del;
+        v = u;
+      }
+      arem[s] -= del;
+      brem[t - m] -= del;
+    }
+    __syncwarp();
+  }
+  double acc = 0.0;
+  for (int e = lane; e < m * mk; e += 32) acc += F[e] * C[e];
+  return wsum(acc);
+}
+
+// centroids to fp64: weights renormalised by their (sequential) fp64 sum, weighted means
+template <typename T>
+__global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, int K, int m, int d,
+                              double* __restrict__ xc, double* __restrict__ wc, double* __restrict__ xb) {
+  const int c = blockIdx.x;
+  __shared__ double tot;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += (double)w[(int64_t)c * m + i];
+    tot = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) wc[(int64_t)c * m + i] = (double)w[(int64_t)c * m + i] / tot;
+  for (int e = threadIdx.x; e < m * d; e += blockDim.x) xc[(int64_t)c * m * d + e] = (double)x[(int64_t)c * m * d + e];
+  __syncthreads();
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += wc[(int64_t)c * m + i] * xc[((int64_t)c * m + i) * d + t];
+    xb[(int64_t)c * d + t] = s;
+  }
+}
+
+// validation + largest m_k (err bit 2: offsets[0] != 0 or m_k < 1)
+__global__ void k_assign_mk(const int64_t* __restrict__ off, int64_t N, unsigned long long* mkmax, int* err) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0 && off[0] != 0) atomicOr(err, 2);
+  if (k >= N) return;
+  const int64_t mk = off[k + 1] - off[k];
+  if (mk < 1 || mk > 0x7fffffff) atomicOr(err, 2);
+  else atomicMax(mkmax, (unsigned long long)mk);
+}
+
+template <typename T>
+__global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __restrict__ Y,
+                         const T* __restrict__ Wt, const double* __restrict__ xc, const double* __restrict__ wc,
+                         const double* __restrict__ xb, AsgLay L, int32_t* __restrict__ labels,
+                         double* __restrict__ best_out, unsigned long long* __restrict__ n_exact, int* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (k >= N) return;
+  unsigned char* ws = smem + (size_t)warp * L.bytes;
+  const int m = L.m, K = L.K, d = L.d;
+  double* C = reinterpret_cast<double*>(ws + L.oC);
+  double* om = reinterpret_cast<double*>(ws + L.oom);
+  double* LB = reinterpret_cast<double*>(ws + L.oLB);
+  unsigned* solved = reinterpret_cast<unsigned*>(ws + L.osolv);
+  double* yb = reinterpret_cast<double*>(ws + L.oyb);
+  const int64_t o0 = off[k];
+  const int mk = (int)(off[k + 1] - o0);
+  const T* Yk = Y + o0 * d;
+
+  // member weights renormalised in fp64 (O1), member mean
+  double s = 0.0;
+  for (int j = lane; j < mk; j += 32) s += (double)Wt[o0 + j];
+  s = wsum(s);
+  for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
+  __syncwarp();
+  for (int t = lane; t < d; t += 32) {
+    double a = 0.0;
+    for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
+    yb[t] = a;
+  }
+  for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
+  __syncwarp();
+  for (int c = lane; c < K; c += 32) {              // |mean_c - mean_k|^2 <= W^2
+    double a = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const double df = xb[(int64_t)c * d + t] - yb[t];
+      a += df * df;
+    }
+    LB[c] = a;
+  }
+  __syncwarp();
+  const double shrink = 1.0 - 1e-12;               // fp64 rounding margin on the bounds
+  double best = CUDART_INF;
+  int bc = -1;
+  unsigned nsolve = 0;
+  for (int visit = 0; visit < K; ++visit) {
+    __syncwarp();                                   // C / solved of the previous visit consumed
+    double lb = CUDART_INF;
+    int cs = K;
+    for (int c = lane; c < K; c += 32)
+      if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
+        lb = LB[c];
+        cs = c;
+      }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
+      if (ol < lb || (ol == lb && oc < cs)) {
+        lb = ol;
+        cs = oc;
+      }
+    }
+    if (cs >= K) break;
+    const double lbs = lb * shrink;
+    if (lbs > best || (lbs == best && cs > bc)) break;            // no remaining centroid can win
+    if (lane == 0) solved[cs >> 5] |= 1u << (cs & 31);
+    // cost matrix C_ij = |x_ci - y_j|^2, difference form in fp64
+    const double* xk = xc + (int64_t)cs * m * d;
+    for (int e = lane; e < m * mk; e += 32) {
+      const int i = e / mk, j = e - i * mk;
+      double a = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
+        a += df * df;
+      }
+      C[e] = a;
+    }
+    __syncwarp();
+    // relaxed-marginal lower bounds
+    const double* wn = wc + (int64_t)cs * m;
+    double l1 = 0.0, l2 = 0.0;
+    for (int j = lane; j < mk; j += 32) {
+      double mn = CUDART_INF;
+      for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j]);
+      l1 += om[j] * mn;
+    }
+    for (int i = lane; i < m; i += 32) {
+      double mn = CUDART_INF;
+      for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j]);
+      l2 += wn[i] * mn;
+    }
+    const double lbr = fmax(wsum(l1), wsum(l2)) * shrink;
+    if (lbr > best || (lbr == best && cs > bc)) continue;
+    const double W = ssp_w2(L, ws, wn, mk, lane, err);
+    ++nsolve;
+    if (W < best || (W == best && cs < bc)) {
+      best = W;
+      bc = cs;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    labels[k] = bc;
+    if (best_out) best_out[k] = best;
+    atomicAdd(n_exact, (unsigned long long)nsolve);
+  }
+}
+
+}  // namespace ad2a
+
+using namespace ad2a;
+
+size_t assign_warp_bytes(int m, int mkmax, int K, int d) {
+  AsgLay L;
+  L.make(m, mkmax, K, d);
+  return L.bytes;
+}
+
+// x, w: device centroids in the batch dtype; all pointers device
+int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
+                  const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
+                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s) {
+  if (f64) k_assign_prep<double><<<K, 128, 0, s>>>((const double*)x, (const double*)w, K, m, d, xc, wc, xb);
+  else k_assign_prep<float><<<K, 128, 0, s>>>((const float*)x, (const float*)w, K, m, d, xc, wc, xb);
+  if (N == 0) return 0;
+  AsgLay L;
+  L.make(m, mkmax, K, d);
+  int wpc = (int)((size_t)(optin - 1024) / L.bytes);
+  if (wpc < 1) return -1;
+  if (wpc > 8) wpc = 8;
+  const size_t sm = (size_t)wpc * L.bytes;
+  const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
+  if (f64) {
+    cudaFuncSetAttribute(k_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_assign<double><<<grid, 32 * wpc, sm, s>>>(off, N, (const double*)Y, (const double*)Wt, xc, wc, xb, L, labels,
+                                                best, n_exact, err);
+  } else {
+    cudaFuncSetAttribute(k_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_assign<float><<<grid, 32 * wpc, sm, s>>>(off, N, (const float*)Y, (const float*)Wt, xc, wc, xb, L, labels,
+                                               best, n_exact, err);
+  }
+  return 0;
+}
+
+void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int* err, cudaStream_t s) {
+  if (N == 0) return;
+  k_assign_mk<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(off, N, mkmax, err);
+}

@@ -1,0 +1,86 @@
+"""GPU assignment step (ad2_assign) vs the oracle's exact-OT assignment
+(oracle.assign: transportation simplex against every centroid, lowest index on ties).
+
+north_star: labels bit-exact wherever the oracle's distance gap (second-best - best W^2) exceeds
+1e-6, compared on IDENTICAL centroids (both sides get the same x, w).  The minimum W^2 itself is
+an exact LP optimum on both sides (fp64), so it must agree to fp64 rounding: 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1510_00012_b200 import workloads as wl
+from tests.harness import run_gpu, to_dev, torch_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def check_assign(b, x, w, mem="device"):
+    from paper_1510_00012_b200 import ad2
+    torch = torch_cuda()
+    ctx = ad2.Context(0)
+    if mem == "device":
+        a = to_dev(b, torch)
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        wd = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+        lab, w2, n_exact = ctx.assign(a["offsets"], a["supports"], a["weights"], xd, wd, dtype=b.dtype)
+    else:
+        lab, w2, n_exact = ctx.assign(b.offsets, b.supports, b.weights, np.ascontiguousarray(x),
+                                      np.ascontiguousarray(w), mem="host", dtype=b.dtype)
+    olab, obest, osecond = oracle.assign(x, w, b.offsets, b.supports, b.weights)
+    gap = osecond - obest
+    sure = gap > 1e-6
+    assert (lab[sure] == olab[sure]).all(), np.nonzero(lab[sure] != olab[sure])
+    # the GPU's W^2 is the exact minimum too
+    np.testing.assert_allclose(w2, obest, rtol=1e-9, atol=1e-12 * max(1.0, float(np.abs(obest).max())))
+    assert n_exact >= b.N if b.K > 1 else n_exact >= 0
+    ctx.close()
+    return lab, n_exact, sure
+
+
+@pytest.mark.parametrize("cfg,N,K", [(2, 600, 10), (3, 300, 6), (5, 300, 8)])
+def test_assign_initial_centroids(cfg, N, K):
+    b = wl.make_config(cfg, N=N, K=K)
+    lab, n_exact, sure = check_assign(b, b.x0, b.w0)
+    assert sure.mean() > 0.9
+    assert n_exact <= b.N * b.K                       # pruning never adds work
+
+
+def test_assign_cfg4_host_batch():
+    b = wl.make_config(4, N=120, K=5)
+    check_assign(b, b.x0, b.w0, mem="host")
+
+
+def test_assign_after_a_round_on_gpu_centroids():
+    """The AD2 loop: B-ADMM round on the GPU, then labels against those (identical) centroids."""
+    b = wl.make_config(2, N=800, K=6)
+    ctx, _, _ = run_gpu(b, 20, 10)
+    x, w = ctx.centroids()
+    lab, n_exact, sure = check_assign(b, x, w)
+    assert n_exact < b.N * b.K                        # the bounds prune on real clusters
+
+
+@pytest.mark.parametrize("m,mk,d,K,dtype", [(5, (1, 9), 3, 7, "f64"), (3, (1, 1), 2, 4, "f32"),
+                                             (6, (1, 12), 2, 1, "f64"), (33, (30, 40), 4, 3, "f32")])
+def test_assign_ragged_and_edge_shapes(m, mk, d, K, dtype):
+    b = wl.make_random(200, m, d, K=K, mk_range=mk, seed=3 + m, dtype=dtype)
+    lab, _, _ = check_assign(b, b.x0, b.w0)
+    if K == 1:
+        assert (lab == 0).all()
+
+
+def test_assign_identity_and_duplicate_centroids():
+    """Members equal to centroid c get c with W^2 = 0; a duplicated centroid ties to the lower index."""
+    rng = np.random.default_rng(5)
+    K, m, d = 5, 4, 3
+    x = rng.normal(0, 4, (K, m, d))
+    w = rng.dirichlet(np.ones(m), K)
+    x[4], w[4] = x[2], w[2]
+    off = np.arange(K + 1, dtype=np.int64) * m
+    b = wl.Bundle("identity", d, m, K, off, x.reshape(-1, d).copy(), w.reshape(-1).copy(),
+                  np.zeros(K, np.int32), x, w, "f64", wl.Schedule(T=1, tau=1))
+    from paper_1510_00012_b200 import ad2
+    ctx = ad2.Context(0)
+    lab, w2, _ = ctx.assign(b.offsets, b.supports, b.weights, x, w, mem="host", dtype="f64")
+    assert list(lab) == [0, 1, 2, 3, 2]
+    assert np.abs(w2).max() < 1e-12
