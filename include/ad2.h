@@ -186,6 +186,28 @@ ad2_status ad2_set_profiling(ad2_ctx ctx, int enable);
 ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64_t *n_launches,
                          double *step_ms);
 
+/* The AD2 outer loop (Alg. 1, P:259-266 with Alg. 4 as the centroid update; SURVEY.md §8(f)
+ * NEXT #2), on the device: the shard is staged once and stays on this GPU; each
+ * round r = ad2_barycenter_init (round 0 cold; later rounds warm-start Pi^(2) for members whose
+ * label did not change; Lambda reset, X7) -> T iterations with a support update every
+ * tau (X6) -> [ad2_objective into obj_out[r*K..]] -> ad2_assign against the new centroids.
+ * Stops after max_rounds or when the fraction of members (all ranks) whose label changed is
+ * <= stop_frac.  batch->labels are the initial labels; x0/w0 the initial centroids (batch->mem).
+ * Outputs: labels_out [N] (batch->mem; the last assignment), rounds_out (host), changed_out
+ * [max_rounds] (host, may be NULL), obj_out [max_rounds*K] (host, may be NULL).  On return the
+ * context holds the last round (ad2_get_centroids gives the centroids the labels refer to).
+ * AD2_ERR_EMPTY (labels_out still written) if an assignment leaves a cluster without members. */
+typedef struct {
+    int32_t T;                  /* B-ADMM iterations per round */
+    int32_t tau;                /* support update every tau iterations */
+    int32_t max_rounds;         /* outer iterations, >= 1 */
+    double stop_frac;           /* stop when changed labels / N <= stop_frac (0: only when stable) */
+} ad2_loop;
+
+ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch *batch, const ad2_params *params, const ad2_loop *loop,
+                       const void *x0, const void *w0, int32_t *labels_out, int32_t *rounds_out,
+                       double *changed_out, double *obj_out);
+
 /* Wait for all work of the context; returns a latched device error if any. */
 ad2_status ad2_sync(ad2_ctx ctx);
 

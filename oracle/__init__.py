@@ -277,3 +277,47 @@ def run_bundle(bundle, T=None, tau=None, rule=None, clusters=None, nthreads=0, w
                                 T, tau, rule, s.rho0, s.eps, wtol, nthreads=nthreads,
                                 want_state=want_state)
     return out, members
+
+
+def cluster(bundle, T, tau, max_rounds, stop_frac=0.0, rule=None):
+    """The AD2 outer loop (Alg. 1) with Alg. 4 as the centroid update, as SURVEY.md
+    §8(c) O8 fixes it: each round = Alg. 4 per cluster from the current centroids (warm Pi^(2)
+    for members whose label did not change; Lambda reset, X7) -> exact assignment
+    (``assign``, lowest index on ties); stop after max_rounds or when the changed fraction
+    <= stop_frac.  Returns (labels, rounds, changed fractions, per-round surrogate objectives
+    [rounds][K], final x, final w)."""
+    s = bundle.sched
+    rule = s.rule if rule is None else rule
+    wtol = 1e-6 if bundle.dtype == "f64" else 1e-5
+    K = bundle.K
+    lab = np.asarray(bundle.labels, np.int32).copy()
+    x, w = _f64(bundle.x0).copy(), _f64(bundle.w0).copy()
+    prev_pi2, warm_ok = {}, np.zeros(bundle.N, bool)
+    changed, objs = [], []
+    rounds = 0
+    for r in range(max_rounds):
+        nx, nw, pi2 = x.copy(), w.copy(), {}
+        obj = np.zeros(K)
+        for c in range(K):
+            mem = np.nonzero(lab == c)[0]
+            if len(mem) == 0:
+                raise OracleError(f"cluster {c} empty in round {r}")
+            sub = bundle.subset(mem)
+            wm = warm_ok[mem] if r > 0 else None
+            warm = [prev_pi2[k] if warm_ok[k] else np.zeros((bundle.m, int(bundle.offsets[k + 1] - bundle.offsets[k])))
+                    for k in mem] if r > 0 else None
+            res = badmm_centroid(x[c], w[c], sub.offsets, sub.supports, sub.weights, T, tau, rule, s.rho0, s.eps,
+                                 wtol, warm=warm, warm_mask=wm)
+            nx[c], nw[c], obj[c] = res.x, res.w, res.obj
+            for k, P in zip(mem, res.mats["Pi2"]):
+                pi2[k] = P
+        x, w = nx, nw
+        objs.append(obj)
+        new, _, _ = assign(x, w, bundle.offsets, bundle.supports, bundle.weights)
+        warm_ok = new == lab
+        changed.append(float(np.mean(new != lab)))
+        lab, prev_pi2 = new, pi2
+        rounds = r + 1
+        if changed[-1] <= stop_frac:
+            break
+    return lab, rounds, np.array(changed), np.array(objs), x, w

@@ -44,6 +44,10 @@ class Params(C.Structure):
     _fields_ = [("rho0", C.c_double), ("eps", C.c_double), ("rule", C.c_int32), ("cost_mode", C.c_int32)]
 
 
+class Loop(C.Structure):
+    _fields_ = [("T", C.c_int32), ("tau", C.c_int32), ("max_rounds", C.c_int32), ("stop_frac", C.c_double)]
+
+
 class Info(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("dtype", C.c_int32), ("d", C.c_int32), ("m", C.c_int32),
                 ("K", C.c_int32), ("n_members", C.c_int64), ("n_points", C.c_int64), ("entries", C.c_int64),
@@ -54,7 +58,8 @@ class Info(C.Structure):
 
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
-           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_sync", "ad2_last_error",
+           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_cluster", "ad2_sync",
+           "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
 _lib = None
@@ -83,6 +88,8 @@ def load_library(path: str = LIB_PATH):
     L.ad2_set_profiling.argtypes = [p, C.c_int]
     L.ad2_prof_read.argtypes = [p, p, i64, C.POINTER(i64), C.POINTER(d)]
     L.ad2_assign.argtypes = [p, C.POINTER(Batch), p, p, p, p, C.c_int, C.POINTER(i64)]
+    L.ad2_cluster.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), C.POINTER(Loop), p, p, p, C.POINTER(i32),
+                              p, p]
     L.ad2_sync.argtypes = [p]
     L.ad2_last_error.argtypes = [p]
     L.ad2_last_error.restype = C.c_char_p
@@ -254,6 +261,40 @@ class Context:
         self._chk(self.L.ad2_assign(self.h, C.byref(b), _ptr(x), _ptr(w), lab.ctypes.data, w2.ctypes.data, HOST,
                                     C.byref(n_exact)))
         return lab, w2, int(n_exact.value)
+
+    def cluster(self, offsets, supports, weights, labels, x0, w0, K: int, m: int, T: int, tau: int,
+                max_rounds: int, stop_frac: float = 0.0, rho0=2.0, eps=1e-16, rule=R1, mem: str = "device",
+                dtype: Optional[str] = None, cost_mode: int = 0):
+        """ad2_cluster: the AD2 outer loop on the device.  Returns a dict with the final labels
+        (host int32 [N]), rounds run, changed fraction per round and surrogate objectives [rounds][K]."""
+        if dtype is None:
+            dt = getattr(supports, "dtype", None)
+            dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
+        d = int(x0.shape[-1])
+        N = int(labels.shape[0])
+        b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K), N,
+                  _ptr(offsets), _ptr(supports), _ptr(weights), _ptr(labels))
+        prm = Params(float(rho0), float(eps), int(rule), int(cost_mode))
+        lp = Loop(int(T), int(tau), int(max_rounds), float(stop_frac))
+        changed = np.zeros(max_rounds)
+        obj = np.zeros((max_rounds, int(K)))
+        rounds = C.c_int32()
+        if mem == "host":
+            lab = np.zeros(N, np.int32)
+            out = lab.ctypes.data
+        else:
+            import torch
+            lab_t = torch.empty(N, dtype=torch.int32, device=labels.device)
+            out = lab_t.data_ptr()
+        self._chk(self.L.ad2_cluster(self.h, C.byref(b), C.byref(prm), C.byref(lp), _ptr(x0), _ptr(w0), out,
+                                     C.byref(rounds), changed.ctypes.data, obj.ctypes.data))
+        if mem != "host":
+            lab = lab_t.cpu().numpy()
+        self.K, self.m, self.d, self.dtype = int(K), int(m), d, dtype
+        self._offsets = offsets
+        self._offsets_host = None
+        r = rounds.value
+        return {"labels": lab, "rounds": r, "changed": changed[:r], "objective": obj[:r]}
 
     def sync(self):
         self._chk(self.L.ad2_sync(self.h))

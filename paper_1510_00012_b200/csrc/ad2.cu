@@ -122,6 +122,7 @@ struct ad2_ctx_s {
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
   DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal;   // assignment step scratch
+  DBuf cl_lab, cl_lab2, cl_x, cl_w, cl_warm, cl_cnt, cl_off, cl_Y, cl_W;   // outer loop (ad2_cluster)
 
   std::map<int, StepGraph*> graphs;
   bool prof = false;
@@ -457,8 +458,9 @@ static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
       ctx->L.as<T>(), ctx->m, ctx->ld);
 }
 
-ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
-                               const void* w0, const uint8_t* warm_mask, double* rho_out) {
+// warm_dev: warm_mask is a device array (the outer loop's label-diff mask, always "some warm")
+static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0, const void* w0,
+                            const uint8_t* warm_mask, bool warm_dev, double* rho_out) {
   if (!ctx) return AD2_ERR_ARG;
   if (!b || !prm || !x0 || !w0) return ctx->fail(AD2_ERR_ARG, "null batch/params/x0/w0");
   if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
@@ -518,8 +520,9 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   }
   const bool warm = warm_mask != nullptr && N > 0;
   if (warm) {
-    bool any = false;
-    for (int64_t k = 0; k < N; ++k) any |= warm_mask[k] != 0;
+    bool any = warm_dev;
+    if (!warm_dev)
+      for (int64_t k = 0; k < N; ++k) any |= warm_mask[k] != 0;
     if (any && (ctx->state < 1 || ctx->dtype != b->dtype || ctx->m != m))
       return ctx->fail(AD2_ERR_ARG, "warm start without a compatible previous round");
   }
@@ -659,7 +662,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   if (warm) {
     CU(ctx->lay_warm.reserve((size_t)N));
     CU(ctx->d_warm.reserve(sizeof(int64_t) * N));
-    CU(cudaMemcpyAsync(ctx->lay_warm.p, warm_mask, (size_t)N, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->lay_warm.p, warm_mask, (size_t)N,
+                       warm_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     k_layout_warm<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
         ctx->d_order.as<int32_t>(), ctx->lay_warm.as<uint8_t>(), ctx->d_pos_of_old.as<int64_t>(),
         ctx->d_off_old.as<int64_t>(), old_N, old_ld, ctx->d_off.as<int64_t>(), N, ctx->d_warm.as<int64_t>(), scal);
@@ -782,6 +786,11 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
   if (rho_out) memcpy(rho_out, ctx->h_rho.data(), sizeof(double) * K);
   ctx->state = 1;
   return AD2_OK;
+}
+
+ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
+                               const void* w0, const uint8_t* warm_mask, double* rho_out) {
+  return init_impl(ctx, b, prm, x0, w0, warm_mask, false, rho_out);
 }
 
 // one step = n iterations of Alg. 4 at fixed x, captured once per n into a CUDA graph
@@ -1092,6 +1101,124 @@ ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void
   if (n_exact_out) *n_exact_out = (int64_t)hs[1];
   if (hs[2] & 1) return ctx->fail(AD2_ERR_NONFINITE, "assign: a transport solve did not terminate");
   return AD2_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// the AD2 outer loop (Alg. 1, P:259-266 with Alg. 4 as the centroid update)
+// ------------------------------------------------------------------------------------------
+// warm[k] = label unchanged; cnt[0] = changed members, cnt[1 + c] = members of c
+static __global__ void k_label_diff(const int32_t* __restrict__ old_lab, const int32_t* __restrict__ new_lab,
+                                    int64_t N, int K, uint8_t* __restrict__ warm, unsigned long long* __restrict__ cnt) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const int32_t a = old_lab[k], b = new_lab[k];
+  warm[k] = (a == b) ? 1 : 0;
+  if (a != b) atomicAdd(&cnt[0], 1ull);
+  if (b >= 0 && b < K) atomicAdd(&cnt[1 + b], 1ull);
+}
+
+ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const ad2_loop* loop,
+                       const void* x0, const void* w0, int32_t* labels_out, int32_t* rounds_out, double* changed_out,
+                       double* obj_out) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!b || !prm || !loop || !x0 || !w0) return ctx->fail(AD2_ERR_ARG, "cluster: null argument");
+  if (loop->T < 1 || loop->tau < 1 || loop->max_rounds < 1 || !(loop->stop_frac >= 0.0))
+    return ctx->fail(AD2_ERR_ARG, "cluster: T=%d tau=%d max_rounds=%d stop_frac=%g", loop->T, loop->tau,
+                     loop->max_rounds, loop->stop_frac);
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
+  if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
+  if (b->d < 1 || b->m < 1 || b->K < 1 || b->n_members < 0 || b->n_members > INT32_MAX)
+    return ctx->fail(AD2_ERR_ARG, "shape");
+  const int64_t N = b->n_members;
+  if (N > 0 && (!b->offsets || !b->supports || !b->weights || !b->labels || !labels_out))
+    return ctx->fail(AD2_ERR_ARG, "cluster: null batch array / labels_out");
+  CHK(set_dev(ctx));
+  cudaStream_t s = ctx->stream;
+  const int d = b->d, m = b->m, K = b->K;
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  const bool host = b->mem == AD2_HOST;
+  const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // the shard lives on the device for all rounds; labels are the loop's own copy
+  ad2_batch bd = *b;
+  bd.mem = AD2_DEVICE;
+  int64_t n = 0;
+  if (N > 0) {
+    if (host) {
+      n = static_cast<const int64_t*>(b->offsets)[N];
+      CU(ctx->cl_off.reserve(sizeof(int64_t) * (N + 1)));
+      CU(ctx->cl_Y.reserve(es * (size_t)n * d));
+      CU(ctx->cl_W.reserve(es * (size_t)n));
+      CU(cudaMemcpyAsync(ctx->cl_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->cl_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->cl_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+      bd.offsets = ctx->cl_off.as<int64_t>();
+      bd.supports = ctx->cl_Y.p;
+      bd.weights = ctx->cl_W.p;
+    }
+  }
+  CU(ctx->cl_lab.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
+  CU(ctx->cl_lab2.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
+  CU(ctx->cl_warm.reserve((size_t)(N > 0 ? N : 1)));
+  CU(ctx->cl_cnt.reserve(sizeof(unsigned long long) * ((size_t)K + 1)));
+  CU(ctx->cl_x.reserve(es * (size_t)K * m * d));
+  CU(ctx->cl_w.reserve(es * (size_t)K * m));
+  if (N > 0) CU(cudaMemcpyAsync(ctx->cl_lab.p, b->labels, sizeof(int32_t) * N, h2d, s));
+  CU(cudaMemcpyAsync(ctx->cl_x.p, x0, es * (size_t)K * m * d, h2d, s));
+  CU(cudaMemcpyAsync(ctx->cl_w.p, w0, es * (size_t)K * m, h2d, s));
+  std::vector<unsigned long long> hc((size_t)K + 1);
+  int rounds = 0;
+  ad2_status ret = AD2_OK;
+  for (int r = 0; r < loop->max_rounds; ++r) {
+    bd.labels = ctx->cl_lab.as<int32_t>();
+    // round r: Alg. 4 from the current centroids (warm Pi^(2) for members whose label held)
+    CHK(init_impl(ctx, &bd, prm, ctx->cl_x.p, ctx->cl_w.p, r > 0 ? ctx->cl_warm.as<uint8_t>() : nullptr, true,
+                  nullptr));
+    for (int done = 0; done < loop->T;) {
+      const int nit = std::min(loop->tau, loop->T - done);
+      CHK(ad2_badmm_step(ctx, nit));
+      done += nit;
+      if (nit == loop->tau) CHK(ad2_update_support(ctx));
+    }
+    if (obj_out) CHK(ad2_objective(ctx, obj_out + (size_t)r * K));
+    CHK(ad2_get_centroids(ctx, ctx->cl_x.p, ctx->cl_w.p, AD2_DEVICE));
+    // assignment against the new centroids (identical on every rank)
+    CHK(ad2_assign(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE, nullptr));
+    CU(cudaMemsetAsync(ctx->cl_cnt.p, 0, sizeof(unsigned long long) * ((size_t)K + 1), s));
+    if (N > 0) {
+      k_label_diff<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ctx->cl_lab.as<int32_t>(), ctx->cl_lab2.as<int32_t>(),
+                                                              N, K, ctx->cl_warm.as<uint8_t>(),
+                                                              ctx->cl_cnt.as<unsigned long long>());
+      CHK(launch_check(ctx, "k_label_diff"));
+    }
+    if (ctx->comm) {
+      ncclResult_t rr = g_nccl.AllReduce(ctx->cl_cnt.p, ctx->cl_cnt.p, (size_t)K + 1, ncclUint64, ncclSum, ctx->comm, s);
+      if (rr != ncclSuccess) return ctx->fail(AD2_ERR_NCCL, "ncclAllReduce (label counts)");
+    }
+    CU(cudaMemcpyAsync(hc.data(), ctx->cl_cnt.p, sizeof(unsigned long long) * ((size_t)K + 1),
+                       cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    std::swap(ctx->cl_lab.p, ctx->cl_lab2.p);
+    std::swap(ctx->cl_lab.cap, ctx->cl_lab2.cap);
+    rounds = r + 1;
+    unsigned long long total = 0;
+    for (int c = 0; c < K; ++c) total += hc[1 + c];
+    const double frac = total ? (double)hc[0] / (double)total : 0.0;
+    if (changed_out) changed_out[r] = frac;
+    int empty = -1;
+    for (int c = 0; c < K && empty < 0; ++c)
+      if (hc[1 + c] == 0) empty = c;
+    if (empty >= 0) {               // the next round's centroid update would have no members
+      ret = ctx->fail(AD2_ERR_EMPTY, "cluster %d lost all its members after round %d", empty, r);
+      break;
+    }
+    if (frac <= loop->stop_frac) break;   // label-change stopping rule
+  }
+  if (N > 0)
+    CU(cudaMemcpyAsync(labels_out, ctx->cl_lab.p, sizeof(int32_t) * N,
+                       host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  if (rounds_out) *rounds_out = rounds;
+  return ret;
 }
 
 ad2_status ad2_sync(ad2_ctx ctx) {

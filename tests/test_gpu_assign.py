@@ -84,3 +84,51 @@ def test_assign_identity_and_duplicate_centroids():
     lab, w2, _ = ctx.assign(b.offsets, b.supports, b.weights, x, w, mem="host", dtype="f64")
     assert list(lab) == [0, 1, 2, 3, 2]
     assert np.abs(w2).max() < 1e-12
+
+
+# ------------------------------------------------------------------ the outer loop (NEXT #2)
+
+@pytest.mark.parametrize("mem", ["device", "host"])
+def test_cluster_loop_fp64_matches_oracle_loop(mem):
+    """ad2_cluster (fp64, 1e-10 parity per B-ADMM round) against the oracle's loop
+    (oracle.cluster): identical labels every round (the gaps here are >> 1e-6), same rounds,
+    changed fractions and objectives, and the final centroids."""
+    from paper_1510_00012_b200 import ad2
+    b = wl.make_config(3, N=240, K=4, dtype="f64")
+    T, tau, R = 20, 10, 3
+    olab, orounds, ochanged, oobj, ox, ow = oracle.cluster(b, T, tau, R)
+    torch = torch_cuda()
+    ctx = ad2.Context(0)
+    if mem == "device":
+        a = to_dev(b, torch)
+        res = ctx.cluster(a["offsets"], a["supports"], a["weights"], a["labels"], a["x0"], a["w0"], b.K, b.m, T, tau,
+                          R, dtype="f64")
+    else:
+        res = ctx.cluster(b.offsets, b.supports, b.weights, b.labels, b.x0, b.w0, b.K, b.m, T, tau, R, mem="host",
+                          dtype="f64")
+    assert res["rounds"] == orounds
+    np.testing.assert_array_equal(res["labels"], olab)
+    np.testing.assert_allclose(res["changed"], ochanged, atol=0)
+    np.testing.assert_allclose(res["objective"], oobj, rtol=1e-8)
+    x, w = ctx.centroids()
+    np.testing.assert_allclose(w, ow, atol=1e-10)
+    np.testing.assert_allclose(x, ox, rtol=1e-8, atol=1e-9 * np.abs(ox).max())
+
+
+def test_cluster_loop_fp32_stops_on_stable_labels():
+    from paper_1510_00012_b200 import ad2
+    torch = torch_cuda()
+    b = wl.make_config(2, N=1500, K=5)
+    a = to_dev(b, torch)
+    ctx = ad2.Context(0)
+    res = ctx.cluster(a["offsets"], a["supports"], a["weights"], a["labels"], a["x0"], a["w0"], b.K, b.m, 20, 10, 8,
+                      stop_frac=0.01)
+    ch = res["changed"]
+    assert 1 <= res["rounds"] <= 8 and len(ch) == res["rounds"]
+    assert res["rounds"] == 8 or ch[-1] <= 0.01
+    assert np.isfinite(res["objective"]).all()
+    # the returned labels are the exact assignment against the returned centroids
+    x, w = ctx.centroids()
+    lab, _, _ = ctx.assign(a["offsets"], a["supports"], a["weights"], torch.from_numpy(x).cuda(),
+                           torch.from_numpy(w).cuda())
+    np.testing.assert_array_equal(lab, res["labels"])

@@ -461,3 +461,30 @@ def test_O7_assign_identity_and_ties():
     assert second[1] < 1e-12 and second[3] < 1e-12 and second[0] > 1e-3
     lab2, best2, _ = oracle.assign(x + 7.5, w, off, Y + 7.5, om)
     assert list(lab2) == list(lab) and np.abs(best2).max() < 1e-10
+
+
+def test_O8_outer_loop_recovers_separated_groups():
+    """Two groups of distributions 40 units apart, initial labels with 1/4 of each group swapped:
+    round 1's centroids are barycenters of 3:1 mixtures and lie on their majority's side, so the
+    exact assignment recovers the groups (changed fraction = 1/4), round 2 changes nothing and
+    the loop stops (the label-change rule with stop_frac = 0)."""
+    from paper_1510_00012_b200 import workloads as wl
+    rng = np.random.default_rng(21)
+    N, m, d = 40, 3, 2
+    truth = np.repeat([0, 1], N // 2).astype(np.int32)
+    sizes = rng.integers(2, 6, N)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    centre = np.where(truth[:, None] == 0, -20.0, 20.0)
+    Y = np.repeat(centre, sizes, axis=0) + rng.normal(0, 1, (off[-1], d))
+    W = np.concatenate([rng.dirichlet(np.ones(s)) for s in sizes])
+    lab0 = truth.copy()
+    flip = np.concatenate([rng.choice(N // 2, N // 8, replace=False), N // 2 + rng.choice(N // 2, N // 8, replace=False)])
+    lab0[flip] = 1 - lab0[flip]
+    x0 = np.stack([Y[off[k]:off[k] + m] if sizes[k] >= m else np.resize(Y[off[k]:off[k + 1]], (m, d))
+                   for k in (0, N - 1)])
+    w0 = np.full((2, m), 1.0 / m)
+    b = wl.Bundle("two_groups", d, m, 2, off, Y, W, lab0, x0, w0, "f64", wl.Schedule(T=20, tau=10))
+    lab, rounds, changed, objs, x, w = oracle.cluster(b, 20, 10, 5)
+    np.testing.assert_array_equal(lab, truth)
+    assert rounds == 2 and changed[0] == pytest.approx(0.25) and changed[1] == 0.0
+    assert (x[0] < 0).all() and (x[1] > 0).all()
