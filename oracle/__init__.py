@@ -54,6 +54,7 @@ def lib():
             L = C.CDLL(_SO)
             d, i, p, i64 = C.c_double, C.c_int, C.c_void_p, C.c_int64
             L.ad2o_assign.argtypes = [i, i, i, p, p, i, p, p, p, p, p, p]
+            L.ad2o_badmm_table.argtypes = [i, i, p, p, p, p, p, p, i, p, p, i, i, d, d, d, p, p, p, p, p]
             L.ad2o_cost.argtypes = [i, i, i, p, p, p]
             L.ad2o_rho.argtypes = [i, i, p, i, p, p, d, p]
             L.ad2o_rho.restype = d
@@ -321,3 +322,38 @@ def cluster(bundle, T, tau, max_rounds, stop_frac=0.0, rule=None):
         if changed[-1] <= stop_frac:
             break
     return lab, rounds, np.array(changed), np.array(objs), x, w
+
+
+def badmm_table(xs, w0, offsets, ys, omega, D, T, rule=0, rho0=2.0, eps=1e-16, wtol=1e-6, warm=None,
+                warm_mask=None, want_state=True) -> Result:
+    """Alg. 4 on symbolic supports: C^(k)_ij = D[xs_i, ys_j] from the cost table, the
+    support update skipped (fixed symbols).  xs int [m], ys int [n], D [V][V]."""
+    xs = np.ascontiguousarray(xs, np.int32)
+    ys = np.ascontiguousarray(ys, np.int32)
+    w = _f64(w0).copy()
+    omega, D = _f64(omega), _f64(D)
+    off = np.ascontiguousarray(offsets, np.int64)
+    m, N, V = len(xs), len(off) - 1, D.shape[0]
+    E = m * int(off[-1] - off[0])
+    Pi1, Pi2, Lam = (np.empty(E), np.empty(E), np.empty(E)) if want_state else (None, None, None)
+    r, obj = C.c_double(0.0), C.c_double(0.0)
+    warm_cat = wm = None
+    if warm is not None:
+        warm_cat = np.concatenate([_f64(P).ravel() for P in warm])
+        wm = np.ascontiguousarray(warm_mask if warm_mask is not None else np.ones(N), np.uint8)
+    st = lib().ad2o_badmm_table(m, N, _ptr(off), _ptr(ys), _ptr(omega), _ptr(xs), _ptr(w), _ptr(D), V,
+                                _ptr(warm_cat) if warm_cat is not None else None, _ptr(wm) if wm is not None else None,
+                                int(T), int(rule), float(rho0), float(eps), float(wtol),
+                                _ptr(Pi1) if want_state else None, _ptr(Pi2) if want_state else None,
+                                _ptr(Lam) if want_state else None, C.byref(r), C.byref(obj))
+    if st != 0:
+        raise OracleError(f"ad2o_badmm_table: {ERR.get(st, st)}")
+    res = Result()
+    res.x, res.w, res.rho, res.obj = xs.copy(), w, r.value, obj.value
+    res.mats = {}
+    if want_state:
+        sizes = np.diff(off)
+        bounds = np.concatenate([[0], np.cumsum(m * sizes)])
+        for name, cat in (("Pi1", Pi1), ("Pi2", Pi2), ("Lam", Lam)):
+            res.mats[name] = [cat[bounds[k]:bounds[k + 1]].reshape(m, sizes[k]) for k in range(N)]
+    return res

@@ -211,6 +211,48 @@ static int all_finite(const double *v, size_t n)
     return 1;
 }
 
+/* The iterations of Alg. 4 from the initial Pi2 / Lambda already in place, with C
+ * the members' cost matrices.  x != NULL: "Update x per tau loops" (X6) with Eq.updatex
+ * and the C rebuild; x == NULL: fixed (symbolic) support, the update is skipped. */
+static int alg4_iterations(int m, int N, const int64_t *off, const double *omega, double *C, double *Pi1,
+                           double *Pi2, double *Lam, double *B, double *r, double *wt, double *w, int T,
+                           int tau, int rule, double rho, double eps, double *x, int d, const double *Y)
+{
+    int status = AD2O_OK;
+    for (int t = 1; t <= T && status == AD2O_OK; ++t) {
+        /* for k: Pi^(k,1), pt^(k,1) (Alg. 4 P:691-694) */
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int k = 0; k < N; ++k) {
+            int mk = (int)(off[k + 1] - off[k]);
+            size_t b = (size_t)m * off[k];
+            ad2o_pi1(m, mk, Pi2 + b, Lam + b, C + b, omega + off[k], rho, eps, Pi1 + b);
+            ad2o_pi1_tilde(m, mk, Pi1 + b, Lam + b, rho, eps, B + b);
+            ad2o_rowmass(m, mk, B + b, r + (size_t)k * m, wt + (size_t)k * m);
+        }
+        /* w (Alg. 4 P:695) */
+        ad2o_consensus(N, m, wt, rule, w);
+        /* for k: Pi^(k,2), Lambda^(k) (Alg. 4 P:696-699) */
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int k = 0; k < N; ++k) {
+            int mk = (int)(off[k + 1] - off[k]);
+            size_t b = (size_t)m * off[k];
+            ad2o_pi2(m, mk, B + b, w, Pi2 + b);
+            ad2o_dual(m, mk, Lam + b, Pi1 + b, Pi2 + b, rho);
+        }
+        if (!all_finite(w, (size_t)m)) status = AD2O_ERR_NONFINITE;
+        /* "Update x from Eq.updatex per tau loops" (P:690), X6: after every tau iterations */
+        if (x && t % tau == 0 && status == AD2O_OK) {
+            ad2o_update_support(m, d, x, w, N, off, Y, Pi2);
+#pragma omp parallel for schedule(dynamic, 64)
+            for (int k = 0; k < N; ++k) {
+                int mk = (int)(off[k + 1] - off[k]);
+                ad2o_cost(m, mk, d, x, Y + off[k] * d, C + (size_t)m * off[k]);
+            }
+        }
+    }
+    return status;
+}
+
 /* ---------------------------------------------------------------------------------------
  * Algorithm 4 "Centroid Update with B-ADMM" for ONE cluster of N members.
  *
@@ -301,37 +343,8 @@ int ad2o_badmm_centroid(int m, int d, int N, const int64_t *off_in, const double
             }
     }
 
-    for (int t = 1; t <= T && status == AD2O_OK; ++t) {
-        /* for k: Pi^(k,1), pt^(k,1) (Alg. 4 P:691-694) */
-#pragma omp parallel for schedule(dynamic, 64)
-        for (int k = 0; k < N; ++k) {
-            int mk = (int)(off[k + 1] - off[k]);
-            size_t b = (size_t)m * off[k];
-            ad2o_pi1(m, mk, Pi2 + b, Lam + b, C + b, omega + off[k], rho, eps, Pi1 + b);
-            ad2o_pi1_tilde(m, mk, Pi1 + b, Lam + b, rho, eps, B + b);
-            ad2o_rowmass(m, mk, B + b, r + (size_t)k * m, wt + (size_t)k * m);
-        }
-        /* w (Alg. 4 P:695) */
-        ad2o_consensus(N, m, wt, rule, w);
-        /* for k: Pi^(k,2), Lambda^(k) (Alg. 4 P:696-699) */
-#pragma omp parallel for schedule(dynamic, 64)
-        for (int k = 0; k < N; ++k) {
-            int mk = (int)(off[k + 1] - off[k]);
-            size_t b = (size_t)m * off[k];
-            ad2o_pi2(m, mk, B + b, w, Pi2 + b);
-            ad2o_dual(m, mk, Lam + b, Pi1 + b, Pi2 + b, rho);
-        }
-        if (!all_finite(w, (size_t)m)) status = AD2O_ERR_NONFINITE;
-        /* "Update x from Eq.updatex per tau loops" (P:690), X6: after every tau iterations */
-        if (t % tau == 0 && status == AD2O_OK) {
-            ad2o_update_support(m, d, x, w, N, off, Y, Pi2);
-#pragma omp parallel for schedule(dynamic, 64)
-            for (int k = 0; k < N; ++k) {
-                int mk = (int)(off[k + 1] - off[k]);
-                ad2o_cost(m, mk, d, x, Y + off[k] * d, C + (size_t)m * off[k]);
-            }
-        }
-    }
+    if (status == AD2O_OK)
+        status = alg4_iterations(m, N, off, omega, C, Pi1, Pi2, Lam, B, r, wt, w, T, tau, rule, rho, eps, x, d, Y);
     if (status == AD2O_OK && !all_finite(Pi1, E)) status = AD2O_ERR_NONFINITE;
     if (obj_out) *obj_out = (T > 0) ? ad2o_surrogate(m, d, x, N, off, Y, Pi1) : NAN;
     if (Pi1_out) memcpy(Pi1_out, Pi1, sizeof(double) * E);
@@ -348,4 +361,68 @@ int ad2o_max_threads(void)
 #else
     return 1;
 #endif
+}
+
+/* Symbolic supports: the support points are symbols of a fixed set with a given
+ * symbol-to-symbol cost table D (V x V, row-major, D[a*V + b] = cost of centroid symbol a to
+ * member symbol b).  C^(k)_ij = D[xs_i, ys_j]; Alg. 4 runs with the support update skipped
+ * (the symbols are fixed).  Otherwise identical to ad2o_badmm_centroid (same O1, Eq.rho X1,
+ * initialisation, outputs); the objective is (1/N) sum_k <C^(k), Pi^(k,1)>. */
+int ad2o_badmm_table(int m, int N, const int64_t *off_in, const int32_t *ys_in, const double *omega_in,
+                     const int32_t *xs, double *w, const double *D, int V, const double *Pi2_warm,
+                     const uint8_t *warm_mask, int T, int rule, double rho0, double eps, double wtol,
+                     double *Pi1_out, double *Pi2_out, double *Lam_out, double *rho_out, double *obj_out)
+{
+    if (m < 1 || N < 1 || T < 0 || V < 1 || rho0 <= 0.0) return AD2O_ERR_ARG;
+    int64_t *off = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N + 1));
+    for (int k = 0; k <= N; ++k) off[k] = off_in[k] - off_in[0];
+    const int32_t *ys = ys_in + off_in[0];
+    size_t n = (size_t)off[N], E = (size_t)m * n;
+    for (int i = 0; i < m; ++i)
+        if (xs[i] < 0 || xs[i] >= V) { free(off); return AD2O_ERR_ARG; }
+    for (size_t j = 0; j < n; ++j)
+        if (ys[j] < 0 || ys[j] >= V) { free(off); return AD2O_ERR_ARG; }
+    double *omega = (double *)malloc(sizeof(double) * n);
+    double *C = (double *)malloc(sizeof(double) * E);
+    double *Pi1 = (double *)calloc(E, sizeof(double));
+    double *Pi2 = (double *)malloc(sizeof(double) * E);
+    double *Lam = (double *)calloc(E, sizeof(double));
+    double *B = (double *)malloc(sizeof(double) * E);
+    double *r = (double *)malloc(sizeof(double) * (size_t)N * m);
+    double *wt = (double *)malloc(sizeof(double) * (size_t)N * m);
+    int status = AD2O_OK;
+    for (int k = 0; k < N && status == AD2O_OK; ++k) {
+        double s = 0.0;
+        for (int64_t j = off[k]; j < off[k + 1]; ++j) s += omega_in[off_in[0] + j];
+        if (!(fabs(s - 1.0) <= wtol)) status = AD2O_ERR_ARG;
+        for (int64_t j = off[k]; j < off[k + 1]; ++j) omega[j] = omega_in[off_in[0] + j] / s;
+    }
+    double sumC = 0.0;
+    for (int k = 0; k < N; ++k) {
+        int mk = (int)(off[k + 1] - off[k]);
+        size_t b = (size_t)m * off[k];
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < mk; ++j) {
+                C[b + i * mk + j] = D[(size_t)xs[i] * V + ys[off[k] + j]];
+                sumC += C[b + i * mk + j];
+                Pi2[b + i * mk + j] = (Pi2_warm && warm_mask && warm_mask[k]) ? Pi2_warm[b + i * mk + j]
+                                                                              : w[i] * omega[off[k] + j];
+            }
+    }
+    double rho = rho0 * sumC / ((double)m * (double)n);
+    if (rho_out) *rho_out = rho;
+    if (status == AD2O_OK && !(rho > 0.0 && isfinite(rho))) status = AD2O_ERR_ZERO_RHO;
+    if (status == AD2O_OK)
+        status = alg4_iterations(m, N, off, omega, C, Pi1, Pi2, Lam, B, r, wt, w, T, 1, rule, rho, eps, NULL, 0, NULL);
+    if (status == AD2O_OK && !all_finite(Pi1, E)) status = AD2O_ERR_NONFINITE;
+    if (obj_out) {
+        double s = 0.0;
+        for (size_t e = 0; e < E; ++e) s += C[e] * Pi1[e];
+        *obj_out = (T > 0) ? s / (double)N : NAN;
+    }
+    if (Pi1_out) memcpy(Pi1_out, Pi1, sizeof(double) * E);
+    if (Pi2_out) memcpy(Pi2_out, Pi2, sizeof(double) * E);
+    if (Lam_out) memcpy(Lam_out, Lam, sizeof(double) * E);
+    free(off); free(omega); free(C); free(Pi1); free(Pi2); free(Lam); free(B); free(r); free(wt);
+    return status;
 }

@@ -488,3 +488,46 @@ def test_O8_outer_loop_recovers_separated_groups():
     np.testing.assert_array_equal(lab, truth)
     assert rounds == 2 and changed[0] == pytest.approx(0.25) and changed[1] == 0.0
     assert (x[0] < 0).all() and (x[1] > 0).all()
+
+
+# ---------------------------------------------------------------- symbolic supports
+
+def test_symbolic_table_equals_euclidean_with_fixed_support():
+    """With D[a, b] = |e_a - e_b|^2 for an embedding e of the symbols, the symbolic mode is the
+    Euclidean mode on the embedded points with the support update skipped: run both for T < tau
+    (Euclidean never updates x before tau iterations, X6) and compare plans, w and objective."""
+    rng = np.random.default_rng(31)
+    V, m, N = 40, 5, 12
+    emb = rng.normal(0, 1, (V, 3))
+    D = ((emb[:, None, :] - emb[None, :, :]) ** 2).sum(-1)
+    xs = rng.choice(V, m, replace=False)
+    sizes = rng.integers(1, 8, N)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ys = rng.integers(0, V, off[-1])
+    om = np.concatenate([rng.dirichlet(np.ones(s)) for s in sizes])
+    w0 = rng.dirichlet(np.ones(m))
+    T = 7
+    a = oracle.badmm_table(xs, w0, off, ys, om, D, T)
+    b = oracle.badmm_centroid(emb[xs], w0, off, emb[ys], om, T, T + 1)
+    assert a.rho == pytest.approx(b.rho, rel=1e-13)
+    np.testing.assert_allclose(a.w, b.w, rtol=1e-12, atol=1e-15)
+    assert a.obj == pytest.approx(b.obj, rel=1e-12)
+    for k in range(N):
+        np.testing.assert_allclose(a.mats["Pi1"][k], b.mats["Pi1"][k], rtol=1e-11, atol=1e-16)
+
+
+def test_symbolic_support_is_never_updated_and_marginals_hold():
+    rng = np.random.default_rng(32)
+    V, m, N = 30, 4, 10
+    D = rng.uniform(0.1, 3.0, (V, V))                         # any nonnegative table (not a metric)
+    xs = rng.choice(V, m, replace=False)
+    sizes = rng.integers(1, 6, N)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ys = rng.integers(0, V, off[-1])
+    om = np.concatenate([rng.dirichlet(np.ones(s)) for s in sizes])
+    res = oracle.badmm_table(xs, np.full(m, 1.0 / m), off, ys, om, D, 60)
+    np.testing.assert_array_equal(res.x, xs)
+    assert abs(res.w.sum() - 1) < 1e-12 and (res.w >= 0).all()
+    for k in range(N):
+        np.testing.assert_allclose(res.mats["Pi1"][k].sum(0), om[off[k]:off[k + 1]], rtol=1e-12)  # P1 columns
+        np.testing.assert_allclose(res.mats["Pi2"][k].sum(1), res.w, rtol=1e-10, atol=1e-15)     # P1 rows
