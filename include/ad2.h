@@ -62,7 +62,12 @@ typedef enum { AD2_PI1 = 0, AD2_PI2 = 1, AD2_LAMBDA = 2, AD2_COST = 3 } ad2_plan
  *                    |dC| <= 2^-7 |x_i||y_j| (+ fp32 rounding).  SURVEY.md §8(d) config 4.
  *                    AD2_ERR_ARG when the round does not use the cached-cost warp-pair kernel.
  * (m <= 32 with d <= 16 recomputes C in fp32 inside the iteration kernel; cost_mode must be 0.) */
-typedef enum { AD2_COST_FP32 = 0, AD2_COST_TC_BF16 = 1 } ad2_cost_mode;
+typedef enum { AD2_COST_FP32 = 0, AD2_COST_TC_BF16 = 1, AD2_COST_TABLE = 2 } ad2_cost_mode;
+/* AD2_COST_TABLE: symbolic supports — the support points are symbols of a fixed set
+ * with a symbol-to-symbol cost table D (ad2_set_cost_table): batch->d must be 1, batch->supports
+ * and x0 hold int32 symbol ids ([n] and [K][m]), C^(k)_ij = D[x_i][y_j], the support update is
+ * skipped (ad2_update_support is a no-op), ad2_get_centroids returns the int32 ids in x.  Runs
+ * on the cached-cost kernels (variant 3 for fp32 with m, m_k <= 64, else the generic one). */
 
 typedef enum {
     AD2_OK = 0,
@@ -149,6 +154,11 @@ ad2_status ad2_update_support(ad2_ctx ctx);
  * current x.  AD2_ERR_STATE if no step has run since init.  Synchronises. */
 ad2_status ad2_objective(ad2_ctx ctx, double *obj_out);
 
+/* Cost table for AD2_COST_TABLE rounds: D [V][V] row-major (D[a*V + b] = cost between centroid
+ * symbol a and member symbol b, any non-negative values), in `dtype` (must match the batch dtype
+ * of the rounds that use it) and `where` memory; copied.  Synchronous. */
+ad2_status ad2_set_cost_table(ad2_ctx ctx, const void *D, int32_t V, ad2_dtype dtype, ad2_mem where);
+
 /* Assignment step of AD2-clustering (Alg. 1, reading X13):
  * for every member k of `batch` (the caller's ragged layout, dtype and mem as in init; the
  * batch's labels are ignored) l^(k) = argmin_c W_2^2(P_c, P^(k)), the exact optimal-transport
@@ -163,6 +173,12 @@ ad2_status ad2_objective(ad2_ctx ctx, double *obj_out);
  * not fit in shared memory; AD2_ERR_NONFINITE if a transport solve failed to terminate. */
 ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch *batch, const void *x, const void *w,
                       int32_t *labels_out, double *w2_out, ad2_mem where, int64_t *n_exact_out);
+/* The same for symbolic supports: batch->d = 1 with int32 symbol ids in supports,
+ * xs [K][m] int32 centroid symbols, cost from the context's table (ad2_set_cost_table, batch
+ * dtype); there is no mean bound (centroids visited in index order, relaxed-marginal bounds
+ * prune).  AD2_ERR_ARG for an id outside [0, V). */
+ad2_status ad2_assign_symbolic(ad2_ctx ctx, const ad2_batch *batch, const int32_t *xs, const void *w,
+                               int32_t *labels_out, double *w2_out, ad2_mem where, int64_t *n_exact_out);
 
 /* Current centroids: x [K][m][d], w [K][m] in the ctx dtype, into `where` memory. */
 ad2_status ad2_get_centroids(ad2_ctx ctx, void *x, void *w, ad2_mem where);

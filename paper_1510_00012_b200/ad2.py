@@ -23,6 +23,7 @@ F32, F64 = 0, 1
 R1, R2 = 0, 1
 DEVICE, HOST = 0, 1
 PI1, PI2, LAMBDA, COST = 0, 1, 2, 3
+COST_FP32, COST_TC_BF16, COST_TABLE = 0, 1, 2
 
 STATUS = {0: "ok", 1: "ARG", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "NONFINITE", 6: "ZERO_RHO", 7: "EMPTY",
           8: "STATE"}
@@ -58,7 +59,8 @@ class Info(C.Structure):
 
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
-           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_cluster", "ad2_sync",
+           "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
+           "ad2_set_cost_table", "ad2_cluster", "ad2_sync",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
@@ -88,6 +90,8 @@ def load_library(path: str = LIB_PATH):
     L.ad2_set_profiling.argtypes = [p, C.c_int]
     L.ad2_prof_read.argtypes = [p, p, i64, C.POINTER(i64), C.POINTER(d)]
     L.ad2_assign.argtypes = [p, C.POINTER(Batch), p, p, p, p, C.c_int, C.POINTER(i64)]
+    L.ad2_assign_symbolic.argtypes = [p, C.POINTER(Batch), p, p, p, p, C.c_int, C.POINTER(i64)]
+    L.ad2_set_cost_table.argtypes = [p, p, i32, C.c_int, C.c_int]
     L.ad2_cluster.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), C.POINTER(Loop), p, p, p, C.POINTER(i32),
                               p, p]
     L.ad2_sync.argtypes = [p]
@@ -164,9 +168,13 @@ class Context:
              cost_mode: int = 0) -> np.ndarray:
         """ad2_barycenter_init; returns rho per cluster (host float64 [K])."""
         if dtype is None:
-            dt = getattr(supports, "dtype", None)
+            dt = getattr(weights, "dtype", None)
             dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
-        d = int(supports.shape[1]) if supports.shape[0] > 0 else int(x0.shape[-1])
+        if cost_mode == COST_TABLE or len(supports.shape) == 1:
+            d = 1                                             # symbolic supports: int32 ids
+        else:
+            d = int(supports.shape[1]) if supports.shape[0] > 0 else int(x0.shape[-1])
+        self.table = cost_mode == COST_TABLE
         b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K),
                   int(len(labels)), _ptr(offsets), _ptr(supports), _ptr(weights), _ptr(labels))
         prm = Params(float(rho0), float(eps), int(rule), int(cost_mode))
@@ -203,7 +211,11 @@ class Context:
         return np.float64 if self.dtype == "f64" else np.float32
 
     def centroids(self):
-        x = np.empty((self.K, self.m, self.d), self._np_dtype())
+        """(x [K][m][d], w [K][m]); symbolic rounds return the centroid symbol ids x [K][m] (int32)."""
+        if getattr(self, "table", False):
+            x = np.empty((self.K, self.m), np.int32)
+        else:
+            x = np.empty((self.K, self.m, self.d), self._np_dtype())
         w = np.empty((self.K, self.m), self._np_dtype())
         self._chk(self.L.ad2_get_centroids(self.h, x.ctypes.data, w.ctypes.data, HOST))
         return x, w
@@ -268,9 +280,9 @@ class Context:
         """ad2_cluster: the AD2 outer loop on the device.  Returns a dict with the final labels
         (host int32 [N]), rounds run, changed fraction per round and surrogate objectives [rounds][K]."""
         if dtype is None:
-            dt = getattr(supports, "dtype", None)
+            dt = getattr(weights, "dtype", None)
             dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
-        d = int(x0.shape[-1])
+        d = 1 if cost_mode == COST_TABLE else int(x0.shape[-1])
         N = int(labels.shape[0])
         b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K), N,
                   _ptr(offsets), _ptr(supports), _ptr(weights), _ptr(labels))
@@ -291,10 +303,33 @@ class Context:
         if mem != "host":
             lab = lab_t.cpu().numpy()
         self.K, self.m, self.d, self.dtype = int(K), int(m), d, dtype
+        self.table = cost_mode == COST_TABLE
         self._offsets = offsets
         self._offsets_host = None
         r = rounds.value
         return {"labels": lab, "rounds": r, "changed": changed[:r], "objective": obj[:r]}
+
+    def set_cost_table(self, D, dtype: Optional[str] = None, mem: str = "host"):
+        """ad2_set_cost_table: symbol-to-symbol cost table D [V][V] for symbolic rounds."""
+        if dtype is None:
+            dtype = "f64" if str(getattr(D, "dtype", "")) in ("float64", "torch.float64") else "f32"
+        self._chk(self.L.ad2_set_cost_table(self.h, _ptr(D), int(D.shape[0]), F64 if dtype == "f64" else F32,
+                                            HOST if mem == "host" else DEVICE))
+
+    def assign_symbolic(self, offsets, ids, weights, xs, w, mem: str = "device", dtype: Optional[str] = None):
+        """ad2_assign_symbolic: labels of members (int32 symbol ids) against centroid symbols xs [K][m]."""
+        if dtype is None:
+            dtype = "f64" if str(getattr(weights, "dtype", "")) in ("float64", "torch.float64") else "f32"
+        K, m = int(xs.shape[0]), int(xs.shape[1])
+        N = int(offsets.shape[0]) - 1
+        b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, 1, m, K, N, _ptr(offsets),
+                  _ptr(ids), _ptr(weights), None)
+        lab = np.zeros(max(N, 0), np.int32)
+        w2 = np.zeros(max(N, 0))
+        n_exact = C.c_int64()
+        self._chk(self.L.ad2_assign_symbolic(self.h, C.byref(b), _ptr(xs), _ptr(w), lab.ctypes.data, w2.ctypes.data,
+                                             HOST, C.byref(n_exact)))
+        return lab, w2, int(n_exact.value)
 
     def sync(self):
         self._chk(self.L.ad2_sync(self.h))

@@ -121,8 +121,12 @@ struct ad2_ctx_s {
   DBuf stage_lab, mem_cl, pm;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
-  DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal;   // assignment step scratch
+  DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal, asg_tab;   // assignment step scratch
   DBuf cl_lab, cl_lab2, cl_x, cl_w, cl_warm, cl_cnt, cl_off, cl_Y, cl_W;   // outer loop (ad2_cluster)
+  // symbolic supports: cost table D [V][V] (dtype tab_dtype), sorted member ids, centroid ids
+  DBuf tab, ysym, xsym;
+  int tab_V = 0, tab_dtype = -1;
+  bool table = false;                // the current round uses AD2_COST_TABLE
 
   std::map<int, StepGraph*> graphs;
   bool prof = false;
@@ -206,7 +210,7 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.px = ctx->px.as<T>();
   a.err = ctx->d_err.as<int>();
   a.m = ctx->m;
-  a.d = ctx->d;
+  a.d = ctx->table ? 0 : ctx->d;     // symbolic supports: no coordinates (support update skipped)
   a.rule = ctx->rule;
   a.eps = (T)ctx->eps;
   return a;
@@ -288,6 +292,13 @@ static ad2_status consensus(ad2_ctx ctx, cudaStream_t s) {
 template <typename T>
 static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
   if (ctx->n_items == 0) return AD2_OK;
+  if (ctx->table) {
+    k_cost_table<T><<<(unsigned)ctx->n_items, 128, 0, s>>>(
+        ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(), ctx->ysym.as<int32_t>(),
+        ctx->xsym.as<int32_t>(), ctx->tab.as<T>(), ctx->tab_V, ctx->Cc.as<T>(), with_sum ? ctx->pd.as<double>() : nullptr,
+        ctx->m, ctx->ld, ctx->d_err.as<int>());
+    return launch_check(ctx, "k_cost_table");
+  }
   if (ctx->variant == 2) {
     if (!with_sum) return AD2_OK;
     launch_cost_member<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<T>(),
@@ -347,6 +358,7 @@ static ad2_status read_err(ad2_ctx ctx) {
   CU(cudaStreamSynchronize(ctx->stream));
   if (h & ERR_WEIGHTS) return ctx->fail(AD2_ERR_ARG, "member weights off the simplex (|sum-1| > tol)");
   if (h & ERR_NONFINITE) return ctx->fail(AD2_ERR_NONFINITE, "non-finite plan row mass or weight");
+  if (h & ERR_SYMBOL) return ctx->fail(AD2_ERR_ARG, "a symbol id outside [0, V) of the cost table");
   return AD2_OK;
 }
 
@@ -471,9 +483,13 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     return ctx->fail(AD2_ERR_ARG, "null batch array");
   if (!(prm->rho0 > 0.0) || !std::isfinite(prm->rho0) || !(prm->eps >= 0.0) || !std::isfinite(prm->eps) ||
       (prm->rule != AD2_R1 && prm->rule != AD2_R2) ||
-      (prm->cost_mode != AD2_COST_FP32 && prm->cost_mode != AD2_COST_TC_BF16))
+      (prm->cost_mode != AD2_COST_FP32 && prm->cost_mode != AD2_COST_TC_BF16 && prm->cost_mode != AD2_COST_TABLE))
     return ctx->fail(AD2_ERR_ARG, "params rho0=%g eps=%g rule=%d cost_mode=%d", prm->rho0, prm->eps, prm->rule,
                      prm->cost_mode);
+  const bool table = prm->cost_mode == AD2_COST_TABLE;
+  if (table && (b->d != 1 || ctx->tab_V < 1 || ctx->tab_dtype != (int)b->dtype))
+    return ctx->fail(AD2_ERR_ARG, "cost_mode 2 (symbolic) needs d = 1 (int32 symbol ids) and a cost table of the "
+                     "batch dtype (ad2_set_cost_table)");
   CHK(set_dev(ctx));
   const int64_t N = b->n_members;
   const int d = b->d, m = b->m, K = b->K;
@@ -534,6 +550,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   int variant = 0, mp = 0, nch = 0, dp = 0;
   const int E = (int)(16 / es);
   for (int cand : {8, 16, 32}) {
+    if (table) break;                      // symbolic: cost from the table, cached (variants 3 / 0)
     if (m <= cand && mkmax <= (cand == 32 ? 32 : 2 * cand)) {
       if (d <= 16) {
         variant = 2;
@@ -724,19 +741,40 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   // ---- member data into the sorted layout
   const void* Ysrc = b->supports;
   const void* Wsrc = b->weights;
+  const size_t ysz = table ? sizeof(int32_t) * (size_t)n : es * (size_t)n * d;   // symbolic: int32 ids
   if (host && N > 0) {
-    CU(ctx->stage_Y.reserve(es * (size_t)n * d));
+    CU(ctx->stage_Y.reserve(ysz));
     CU(ctx->stage_W.reserve(es * (size_t)n));
-    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
     Ysrc = ctx->stage_Y.p;
     Wsrc = ctx->stage_W.p;
   }
   const double wtol = b->dtype == AD2_F64 ? 1e-6 : 1e-5;
-  if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
-  else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
-  if (N > 0) CHK(launch_check(ctx, "k_gather"));
-  CU(cudaMemcpyAsync(ctx->x.p, x0, es * (size_t)K * m * d, h2d, s));
+  ctx->table = table;
+  if (table) {                      // weights only through k_gather (d = 0); ids gathered separately
+    const int d_save = ctx->d;
+    ctx->d = 0;
+    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
+    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
+    ctx->d = d_save;
+    if (N > 0) CHK(launch_check(ctx, "k_gather"));
+    CU(ctx->ysym.reserve(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)));
+    CU(ctx->xsym.reserve(sizeof(int32_t) * (size_t)K * m));
+    if (N > 0) {
+      k_gather_sym<<<(unsigned)((N + 3) / 4), 128, 0, s>>>(ctx->d_order.as<int32_t>(), ctx->d_orig_off.as<int64_t>(),
+                                                           ctx->d_off.as<int64_t>(), (const int32_t*)Ysrc,
+                                                           ctx->ysym.as<int32_t>(), N);
+      CHK(launch_check(ctx, "k_gather_sym"));
+    }
+    CU(cudaMemcpyAsync(ctx->xsym.p, x0, sizeof(int32_t) * (size_t)K * m, h2d, s));
+    CU(cudaMemsetAsync(ctx->x.p, 0, es * (size_t)K * m * d, s));
+  } else {
+    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
+    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
+    if (N > 0) CHK(launch_check(ctx, "k_gather"));
+    CU(cudaMemcpyAsync(ctx->x.p, x0, es * (size_t)K * m * d, h2d, s));
+  }
   CU(cudaMemcpyAsync(ctx->w.p, w0, es * (size_t)K * m, h2d, s));
 
   // ---- Pi^(2),0 and Lambda = 0 (warm: new Pi2 built in P from the old Q, then swapped)
@@ -869,6 +907,7 @@ static ad2_status update_support_T(ad2_ctx ctx) {
 ad2_status ad2_update_support(ad2_ctx ctx) {
   if (!ctx) return AD2_ERR_ARG;
   if (ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "update_support needs a step since init (X6)");
+  if (ctx->table) return AD2_OK;      // symbolic supports are fixed: the update is skipped
   CHK(set_dev(ctx));
   return ctx->dtype == AD2_F64 ? update_support_T<double>(ctx) : update_support_T<float>(ctx);
 }
@@ -913,7 +952,8 @@ ad2_status ad2_get_centroids(ad2_ctx ctx, void* x, void* w, ad2_mem where) {
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
   CHK(set_dev(ctx));
   const cudaMemcpyKind kind = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  if (x) CU(cudaMemcpyAsync(x, ctx->x.p, ctx->es * (size_t)ctx->K * ctx->m * ctx->d, kind, ctx->stream));
+  if (x && ctx->table) CU(cudaMemcpyAsync(x, ctx->xsym.p, sizeof(int32_t) * (size_t)ctx->K * ctx->m, kind, ctx->stream));
+  else if (x) CU(cudaMemcpyAsync(x, ctx->x.p, ctx->es * (size_t)ctx->K * ctx->m * ctx->d, kind, ctx->stream));
   if (w) CU(cudaMemcpyAsync(w, ctx->w.p, ctx->es * (size_t)ctx->K * ctx->m, kind, ctx->stream));
   if (where == AD2_HOST) return read_err(ctx);
   return AD2_OK;
@@ -1014,18 +1054,36 @@ ad2_status ad2_prof_read(ad2_ctx ctx, double* launch_ms, int64_t capacity, int64
   return AD2_OK;
 }
 
+ad2_status ad2_set_cost_table(ad2_ctx ctx, const void* D, int32_t V, ad2_dtype dtype, ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!D || V < 1 || (dtype != AD2_F32 && dtype != AD2_F64) || (where != AD2_HOST && where != AD2_DEVICE))
+    return ctx->fail(AD2_ERR_ARG, "set_cost_table: D=%p V=%d", D, V);
+  CHK(set_dev(ctx));
+  const size_t bytes = (dtype == AD2_F64 ? 8 : 4) * (size_t)V * V;
+  CU(ctx->tab.reserve(bytes));
+  CU(cudaMemcpyAsync(ctx->tab.p, D, bytes, where == AD2_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->tab_V = V;
+  ctx->tab_dtype = (int)dtype;
+  return AD2_OK;
+}
+
 // ------------------------------------------------------------------------------------------
 // assignment step (ad2_assign.cu)
 // ------------------------------------------------------------------------------------------
 size_t assign_warp_bytes(int m, int mkmax, int K, int d);
 int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
                   const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
+                  const int32_t* xs, const void* D, int V, double* Dtab,
                   int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s);
 void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int* err, cudaStream_t s);
 
-ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
-                      double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
+                              double* w2_out, ad2_mem where, int64_t* n_exact_out, bool symbolic) {
   if (!ctx) return AD2_ERR_ARG;
+  if (symbolic && (b && (b->d != 1 || ctx->tab_V < 1 || ctx->tab_dtype != (int)b->dtype)))
+    return ctx->fail(AD2_ERR_ARG, "symbolic assign needs d = 1 (int32 ids) and a cost table of the batch dtype");
   if (!b || !x || !w) return ctx->fail(AD2_ERR_ARG, "assign: null batch/x/w");
   if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
   if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
@@ -1050,10 +1108,11 @@ ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void
     if (host) {
       n = static_cast<const int64_t*>(b->offsets)[N];
       CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
-      CU(ctx->stage_Y.reserve(es * (size_t)n * d));
+      const size_t ysz = symbolic ? sizeof(int32_t) * (size_t)n : es * (size_t)n * d;
+      CU(ctx->stage_Y.reserve(ysz));
       CU(ctx->stage_W.reserve(es * (size_t)n));
       CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
-      CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, s));
       CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
       off = ctx->stage_off.p;
       Y = ctx->stage_Y.p;
@@ -1061,8 +1120,9 @@ ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void
     }
   }
   CU(ctx->asg_cx.reserve(es * (size_t)K * m * (d + 1)));
-  CU(cudaMemcpyAsync(ctx->asg_cx.p, x, es * (size_t)K * m * d, h2d, s));
+  CU(cudaMemcpyAsync(ctx->asg_cx.p, x, symbolic ? sizeof(int32_t) * (size_t)K * m : es * (size_t)K * m * d, h2d, s));
   CU(cudaMemcpyAsync((char*)ctx->asg_cx.p + es * (size_t)K * m * d, w, es * (size_t)K * m, h2d, s));
+  if (symbolic) CU(ctx->asg_tab.reserve(8 * (size_t)ctx->tab_V * ctx->tab_V));
   CU(ctx->asg_x.reserve(8 * ((size_t)K * m * d + (size_t)K * m + (size_t)K * d)));
   CU(ctx->asg_lab.reserve(sizeof(int32_t) * (N > 0 ? N : 1)));
   CU(ctx->asg_best.reserve(sizeof(double) * (N > 0 ? N : 1)));
@@ -1087,7 +1147,8 @@ ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void
   double* xb = wc + (size_t)K * m;
   const void* wdev = (const char*)ctx->asg_cx.p + es * (size_t)K * m * d;
   if (assign_launch(b->dtype == AD2_F64, static_cast<const int64_t*>(off), N, Y, W, ctx->asg_cx.p, wdev, K, m, d,
-                    (int)hs[0], xc, wc, xb, ctx->asg_lab.as<int32_t>(), ctx->asg_best.as<double>(), scal + 1, err,
+                    (int)hs[0], xc, wc, xb, symbolic ? ctx->asg_cx.as<int32_t>() : nullptr, ctx->tab.p, ctx->tab_V,
+                    ctx->asg_tab.as<double>(), ctx->asg_lab.as<int32_t>(), ctx->asg_best.as<double>(), scal + 1, err,
                     optin, s) != 0)
     return ctx->fail(AD2_ERR_ARG, "assign: workspace does not fit");
   CHK(launch_check(ctx, "k_assign"));
@@ -1100,7 +1161,18 @@ ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void
   CU(cudaStreamSynchronize(s));
   if (n_exact_out) *n_exact_out = (int64_t)hs[1];
   if (hs[2] & 1) return ctx->fail(AD2_ERR_NONFINITE, "assign: a transport solve did not terminate");
+  if (hs[2] & 4) return ctx->fail(AD2_ERR_ARG, "assign: a symbol id outside [0, V) of the cost table");
   return AD2_OK;
+}
+
+ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
+                      double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+  return assign_impl(ctx, b, x, w, labels_out, w2_out, where, n_exact_out, false);
+}
+
+ad2_status ad2_assign_symbolic(ad2_ctx ctx, const ad2_batch* b, const int32_t* xs, const void* w, int32_t* labels_out,
+                               double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+  return assign_impl(ctx, b, xs, w, labels_out, w2_out, where, n_exact_out, true);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1146,10 +1218,11 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
     if (host) {
       n = static_cast<const int64_t*>(b->offsets)[N];
       CU(ctx->cl_off.reserve(sizeof(int64_t) * (N + 1)));
-      CU(ctx->cl_Y.reserve(es * (size_t)n * d));
+      const size_t ysz = prm->cost_mode == AD2_COST_TABLE ? sizeof(int32_t) * (size_t)n : es * (size_t)n * d;
+      CU(ctx->cl_Y.reserve(ysz));
       CU(ctx->cl_W.reserve(es * (size_t)n));
       CU(cudaMemcpyAsync(ctx->cl_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
-      CU(cudaMemcpyAsync(ctx->cl_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->cl_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, s));
       CU(cudaMemcpyAsync(ctx->cl_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
       bd.offsets = ctx->cl_off.as<int64_t>();
       bd.supports = ctx->cl_Y.p;
@@ -1182,7 +1255,8 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
     if (obj_out) CHK(ad2_objective(ctx, obj_out + (size_t)r * K));
     CHK(ad2_get_centroids(ctx, ctx->cl_x.p, ctx->cl_w.p, AD2_DEVICE));
     // assignment against the new centroids (identical on every rank)
-    CHK(ad2_assign(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE, nullptr));
+    CHK(assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE, nullptr,
+                    prm->cost_mode == AD2_COST_TABLE));
     CU(cudaMemsetAsync(ctx->cl_cnt.p, 0, sizeof(unsigned long long) * ((size_t)K + 1), s));
     if (N > 0) {
       k_label_diff<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ctx->cl_lab.as<int32_t>(), ctx->cl_lab2.as<int32_t>(),

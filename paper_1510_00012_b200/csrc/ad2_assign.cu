@@ -184,6 +184,7 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
 }
 
 // centroids to fp64: weights renormalised by their (sequential) fp64 sum, weighted means
+// (x == nullptr: symbolic supports, weights only)
 template <typename T>
 __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, int K, int m, int d,
                               double* __restrict__ xc, double* __restrict__ wc, double* __restrict__ xb) {
@@ -196,6 +197,7 @@ __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, 
   }
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) wc[(int64_t)c * m + i] = (double)w[(int64_t)c * m + i] / tot;
+  if (!x) return;
   for (int e = threadIdx.x; e < m * d; e += blockDim.x) xc[(int64_t)c * m * d + e] = (double)x[(int64_t)c * m * d + e];
   __syncthreads();
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
@@ -215,10 +217,14 @@ __global__ void k_assign_mk(const int64_t* __restrict__ off, int64_t N, unsigned
   else atomicMax(mkmax, (unsigned long long)mk);
 }
 
+// Dtab != nullptr: symbolic supports — Y and xs hold int32 symbol ids, the cost is the
+// table entry D[xs_ci][y_j] (fp64 copy), and there is no vector-space mean bound (all bounds 0:
+// centroids are visited in index order, the relaxed-marginal bounds still prune).
 template <typename T>
 __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __restrict__ Y,
                          const T* __restrict__ Wt, const double* __restrict__ xc, const double* __restrict__ wc,
-                         const double* __restrict__ xb, AsgLay L, int32_t* __restrict__ labels,
+                         const double* __restrict__ xb, const int32_t* __restrict__ xs, const double* __restrict__ Dtab,
+                         int V, AsgLay L, int32_t* __restrict__ labels,
                          double* __restrict__ best_out, unsigned long long* __restrict__ n_exact, int* err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,19 +247,22 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   s = wsum(s);
   for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
   __syncwarp();
-  for (int t = lane; t < d; t += 32) {
-    double a = 0.0;
-    for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
-    yb[t] = a;
-  }
+  const int32_t* Ysym = reinterpret_cast<const int32_t*>(Y) + o0;
+  if (!Dtab)
+    for (int t = lane; t < d; t += 32) {
+      double a = 0.0;
+      for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
+      yb[t] = a;
+    }
   for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
   __syncwarp();
   for (int c = lane; c < K; c += 32) {              // |mean_c - mean_k|^2 <= W^2
     double a = 0.0;
-    for (int t = 0; t < d; ++t) {
-      const double df = xb[(int64_t)c * d + t] - yb[t];
-      a += df * df;
-    }
+    if (!Dtab)
+      for (int t = 0; t < d; ++t) {
+        const double df = xb[(int64_t)c * d + t] - yb[t];
+        a += df * df;
+      }
     LB[c] = a;
   }
   __syncwarp();
@@ -288,9 +297,15 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     for (int e = lane; e < m * mk; e += 32) {
       const int i = e / mk, j = e - i * mk;
       double a = 0.0;
-      for (int t = 0; t < d; ++t) {
-        const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
-        a += df * df;
+      if (Dtab) {
+        const int sa = xs[(int64_t)cs * m + i], sb = Ysym[j];
+        if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
+        else a = Dtab[(int64_t)sa * V + sb];
+      } else {
+        for (int t = 0; t < d; ++t) {
+          const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
+          a += df * df;
+        }
       }
       C[e] = a;
     }
@@ -336,11 +351,24 @@ size_t assign_warp_bytes(int m, int mkmax, int K, int d) {
 }
 
 // x, w: device centroids in the batch dtype; all pointers device
+template <typename T>
+__global__ void k_to_f64(const T* __restrict__ a, double* __restrict__ b, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+
+// symbolic (xs != nullptr): x unused, Y / xs int32 ids, table D [V][V] in the batch dtype
 int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
                   const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
+                  const int32_t* xs, const void* D, int V, double* Dtab,
                   int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s) {
-  if (f64) k_assign_prep<double><<<K, 128, 0, s>>>((const double*)x, (const double*)w, K, m, d, xc, wc, xb);
-  else k_assign_prep<float><<<K, 128, 0, s>>>((const float*)x, (const float*)w, K, m, d, xc, wc, xb);
+  if (f64) k_assign_prep<double><<<K, 128, 0, s>>>(xs ? nullptr : (const double*)x, (const double*)w, K, m, d, xc, wc, xb);
+  else k_assign_prep<float><<<K, 128, 0, s>>>(xs ? nullptr : (const float*)x, (const float*)w, K, m, d, xc, wc, xb);
+  if (xs) {
+    const int64_t nv = (int64_t)V * V;
+    if (f64) k_to_f64<double><<<(unsigned)((nv + 255) / 256), 256, 0, s>>>((const double*)D, Dtab, nv);
+    else k_to_f64<float><<<(unsigned)((nv + 255) / 256), 256, 0, s>>>((const float*)D, Dtab, nv);
+  }
   if (N == 0) return 0;
   AsgLay L;
   L.make(m, mkmax, K, d);
@@ -351,12 +379,12 @@ int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const v
   const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
   if (f64) {
     cudaFuncSetAttribute(k_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_assign<double><<<grid, 32 * wpc, sm, s>>>(off, N, (const double*)Y, (const double*)Wt, xc, wc, xb, L, labels,
-                                                best, n_exact, err);
+    k_assign<double><<<grid, 32 * wpc, sm, s>>>(off, N, (const double*)Y, (const double*)Wt, xc, wc, xb, xs,
+                                                xs ? Dtab : nullptr, V, L, labels, best, n_exact, err);
   } else {
     cudaFuncSetAttribute(k_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_assign<float><<<grid, 32 * wpc, sm, s>>>(off, N, (const float*)Y, (const float*)Wt, xc, wc, xb, L, labels,
-                                               best, n_exact, err);
+    k_assign<float><<<grid, 32 * wpc, sm, s>>>(off, N, (const float*)Y, (const float*)Wt, xc, wc, xb, xs,
+                                               xs ? Dtab : nullptr, V, L, labels, best, n_exact, err);
   }
   return 0;
 }

@@ -725,6 +725,54 @@ static __global__ void k_member_cluster(const int64_t* __restrict__ item_mb, con
   for (int64_t s = item_mb[it]; s < item_mb[it + 1]; ++s) mem_cl[s] = item_cl[it];
 }
 
+// Symbolic supports: member symbol ids into the sorted layout, and the cost from the
+// table, C_ij = D[xs_i, ys_j] (cached; rows >= m are 0) with optional per-item sums for rho.
+// err bit ERR_SYMBOL: an id outside [0, V).
+constexpr int ERR_SYMBOL = 4;
+static __global__ void k_gather_sym(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
+                                    const int64_t* __restrict__ dst_off, const int32_t* __restrict__ ys_src,
+                                    int32_t* __restrict__ ys, int64_t N) {
+  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= N) return;
+  const int64_t k = order[s];
+  const int64_t so = src_off[k], dsto = dst_off[s];
+  const int mk = (int)(src_off[k + 1] - so);
+  for (int j = lane; j < mk; j += 32) ys[dsto + j] = ys_src[so + j];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_cost_table(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+             const int32_t* __restrict__ item_cl, const int32_t* __restrict__ ys, const int32_t* __restrict__ xs,
+             const T* __restrict__ D, int V, T* __restrict__ Cc, double* __restrict__ psum, int m, int ld, int* err) {
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int64_t p0 = off[item_mb[item]], p1 = off[item_mb[item + 1]];
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t e = (int64_t)threadIdx.x; e < (p1 - p0) * ld; e += blockDim.x) {
+    const int64_t p = e / ld;
+    const int i = (int)(e - p * ld);
+    T v = T(0);
+    if (i < m) {
+      const int a = xs[(int64_t)c * m + i], b = ys[p0 + p];
+      if (a < 0 || a >= V || b < 0 || b >= V) bad = true;
+      else v = D[(int64_t)a * V + b];
+    }
+    Cc[ld * p0 + e] = v;
+    acc += (double)v;
+  }
+  if (bad) atomicOr(err, ERR_SYMBOL);
+  if (psum) {
+    for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+    __shared__ double sh[4];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) psum[item] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+  }
+}
+
 // per-cluster sum of per-member doubles over the cluster's sorted members [cstart[c], cstart[c+1]):
 // fixed strided order per thread, then a fixed-shape tree -> deterministic
 static __global__ void k_dsum_members(const double* __restrict__ pm, const int64_t* __restrict__ cstart,

@@ -389,3 +389,63 @@ def make_random(N: int, m: int, d: int, K: int = 1, mk_range=(1, 8), seed: int =
     b = Bundle(f"random_N{N}_m{m}_d{d}_K{K}", d, m, K, off, Y, W, labels, x0, w0, dtype,
                Schedule(T=T, tau=tau, rule=rule))
     return _cast(b)
+
+
+@dataclass
+class SymbolicBundle:
+    """Members over a fixed symbol set with a symbol-to-symbol cost table."""
+    name: str
+    V: int
+    m: int
+    K: int
+    D: np.ndarray            # [V][V] cost table
+    offsets: np.ndarray      # [N+1]
+    ids: np.ndarray          # [n] int32 symbol ids
+    weights: np.ndarray      # [n]
+    labels: np.ndarray       # [N] int32
+    xs0: np.ndarray          # [K][m] int32 centroid symbols
+    w0: np.ndarray           # [K][m]
+    dtype: str = "f32"
+    sched: Schedule = field(default_factory=lambda: Schedule(T=30, tau=10))
+
+    @property
+    def N(self) -> int:
+        return len(self.offsets) - 1
+
+
+def make_symbolic(N: int = 600, K: int = 5, m: int = 16, V: int = 400, mk_range=(5, 40), seed: int = 0,
+                  dtype: str = "f32") -> SymbolicBundle:
+    """Seeded stand-in for the paper's symbolic data (protein n-gram histograms, P:892-893,
+    dataset missing): V = 400 symbols (dipeptide-like), each with a random 6-D profile; the cost
+    table is the L1 distance between profiles (non-Euclidean, non-negative).  K latent groups
+    each prefer a random 60-symbol subset (Zipf over it, 20 % background); a member draws
+    m_k ~ U{mk_range} distinct symbols from its group's law, weights Dirichlet(1).  Labels are
+    random; each centroid starts from m distinct symbols of its first member's group law."""
+    ck = 200
+    rs = lambda p: _rng(seed, ck, p)
+    prof = rs(_P_CENTRES).uniform(0.0, 1.0, size=(V, 6))
+    D = np.abs(prof[:, None, :] - prof[None, :, :]).sum(-1)
+    g = rs(_P_COMP)
+    laws = []
+    for _ in range(K):
+        fav = g.choice(V, 60, replace=False)
+        p = np.full(V, 0.2 / V)
+        p[fav] += 0.8 * (1.0 / np.arange(1, 61)) / (1.0 / np.arange(1, 61)).sum()
+        laws.append(p / p.sum())
+    lo, hi = mk_range
+    sizes = rs(_P_SIZES).integers(lo, hi + 1, size=N).astype(np.int64)
+    off = _offsets(sizes)
+    grp = rs(_P_SAMPLE).integers(0, K, size=N)
+    rn = rs(_P_NOISE)
+    ids = np.concatenate([rn.choice(V, int(sizes[k]), replace=False, p=laws[grp[k]]) for k in range(N)])
+    W = _dirichlet_ragged((seed, ck, _P_WEIGHTS), 1.0, off)
+    labels = rs(_P_PERM).integers(0, K, size=N).astype(np.int32)
+    for c in range(K):                                   # no empty cluster
+        labels[c % N] = c
+    xs0 = np.stack([rs(_P_INIT).choice(V, m, replace=False, p=laws[grp[int(np.nonzero(labels == c)[0][0])]])
+                    for c in range(K)]).astype(np.int32)
+    w0 = np.full((K, m), 1.0 / m)
+    ft = np.float64 if dtype == "f64" else np.float32
+    return SymbolicBundle(f"symbolic_V{V}_N{N}_K{K}_m{m}", V, m, K, np.ascontiguousarray(D, ft),
+                          np.ascontiguousarray(off, np.int64), np.ascontiguousarray(ids, np.int32),
+                          np.ascontiguousarray(W, ft), labels, xs0, np.ascontiguousarray(w0, ft), dtype)
