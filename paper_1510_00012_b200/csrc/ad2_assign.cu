@@ -29,7 +29,7 @@ namespace ad2a {
 
 struct AsgLay {
   int m, mk, V, K, d;
-  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, bytes;
+  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, oCf, olog, bytes;
   __host__ __device__ void make(int m_, int mk_, int K_, int d_) {
     m = m_, mk = mk_, K = K_, d = d_;
     V = m + mk;
@@ -51,6 +51,8 @@ struct AsgLay {
     oLB = take(8 * (size_t)K);
     osolv = take(4 * (size_t)((K + 31) / 32));
     oyb = take(8 * (size_t)d);
+    oCf = take(4 * (size_t)m * mk);
+    olog = take(4 * (size_t)V);
     bytes = o;
   }
 };
@@ -183,6 +185,119 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
   return wsum(acc);
 }
 
+// Dual lower bound and primal upper bound on W^2 for one pair (C in smem, fp64).  A log-domain
+// Sinkhorn run (fp32, eps-scaling from max C down to 1e-3 mean C) gives
+// approximate potentials f (24 iterations); two c-transforms in fp64 make them dual-feasible
+// (v_j = min_i C_ij - u_i, u_i = min_j C_ij - v_j, so u_i + v_j <= C_ij), hence
+// LB = sum_i a_i u_i + sum_j b_j v_j <= W^2 (Kantorovich duality).  The Sinkhorn plan rounded
+// onto the transport polytope (row scaling to <= a, column scaling to <= b, rank-one
+// correction, Altschuler et al.) is feasible, hence UB = <C, P> >= W^2.  Uses F as scratch.
+__device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double& lb,
+                            double& ub) {
+  const int m = L.m;
+  const double* C = reinterpret_cast<const double*>(ws + L.oC);
+  double* P = reinterpret_cast<double*>(ws + L.oF);
+  double* u = reinterpret_cast<double*>(ws + L.opi);          // [m] then v at u + m
+  double* v = u + m;
+  float* fs = reinterpret_cast<float*>(ws + L.odist);         // f [m], g [mk] (fp32 potentials)
+  float* gs = fs + m;
+  float* Cf = reinterpret_cast<float*>(ws + L.oCf);            // fp32 copy of C
+  float* la = reinterpret_cast<float*>(ws + L.olog);           // log a [m], log b [mk]
+  float* lbv = la + m;
+  const double* b = reinterpret_cast<const double*>(ws + L.oom);
+  double cmax = 0.0, csum = 0.0;
+  for (int e = lane; e < m * mk; e += 32) {
+    cmax = fmax(cmax, C[e]);
+    csum += C[e];
+    Cf[e] = (float)C[e];
+  }
+  for (int i = lane; i < m; i += 32) la[i] = __logf((float)a[i] + 1e-38f);
+  for (int j = lane; j < mk; j += 32) lbv[j] = __logf((float)b[j] + 1e-38f);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  csum = wsum(csum);
+  const float eps_f = (float)fmax(1e-3 * csum / (double)(m * mk), 1e-30);
+  float eps = (float)fmax(cmax, 1e-30);
+  for (int i = lane; i < m; i += 32) fs[i] = 0.f;
+  for (int j = lane; j < mk; j += 32) gs[j] = 0.f;
+  __syncwarp();
+  __syncwarp();
+  for (int it = 0; it < 24; ++it) {
+    eps = fmaxf(eps_f, eps * 0.5f);
+    const float ie = 1.f / eps;
+    for (int j = lane; j < mk; j += 32) {            // g_j = -eps LSE_i(log a_i + (f_i - C_ij)/eps)
+      float mx = -CUDART_INF_F;
+      for (int i = 0; i < m; ++i) mx = fmaxf(mx, la[i] + (fs[i] - Cf[i * mk + j]) * ie);
+      float sm = 0.f;
+      for (int i = 0; i < m; ++i) sm += __expf(la[i] + (fs[i] - Cf[i * mk + j]) * ie - mx);
+      gs[j] = -eps * (mx + __logf(sm));
+    }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {             // f_i = -eps LSE_j(log b_j + (g_j - C_ij)/eps)
+      float mx = -CUDART_INF_F;
+      for (int j = 0; j < mk; ++j) mx = fmaxf(mx, lbv[j] + (gs[j] - Cf[i * mk + j]) * ie);
+      float sm = 0.f;
+      for (int j = 0; j < mk; ++j) sm += __expf(lbv[j] + (gs[j] - Cf[i * mk + j]) * ie - mx);
+      fs[i] = -eps * (mx + __logf(sm));
+    }
+    __syncwarp();
+  }
+  // dual-feasible potentials by two fp64 c-transforms
+  for (int j = lane; j < mk; j += 32) {
+    double mn = CUDART_INF;
+    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j] - (double)fs[i]);
+    v[j] = mn;
+  }
+  __syncwarp();
+  double acc = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double mn = CUDART_INF;
+    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j] - v[j]);
+    u[i] = mn;
+    acc += a[i] * mn;
+  }
+  for (int j = lane; j < mk; j += 32) acc += b[j] * v[j];
+  lb = wsum(acc);
+  // primal: Sinkhorn plan, rounded onto the transport polytope
+  const float ie = 1.f / eps;
+  for (int e = lane; e < m * mk; e += 32) {
+    const int i = e / mk, j = e - i * mk;
+    P[e] = (double)__expf((fs[i] + gs[j] - (float)C[e]) * ie) * a[i] * b[j];
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {              // rows scaled down to <= a_i
+    double r = 0.0;
+    for (int j = 0; j < mk; ++j) r += P[i * mk + j];
+    const double x = r > a[i] ? a[i] / r : 1.0;
+    for (int j = 0; j < mk; ++j) P[i * mk + j] *= x;
+  }
+  __syncwarp();
+  for (int j = lane; j < mk; j += 32) {             // columns scaled down to <= b_j
+    double c = 0.0;
+    for (int i = 0; i < m; ++i) c += P[i * mk + j];
+    const double y = c > b[j] ? b[j] / c : 1.0;
+    for (int i = 0; i < m; ++i) P[i * mk + j] *= y;
+    v[j] = b[j] - c * y;                            // column deficit
+  }
+  __syncwarp();
+  double dr = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double r = 0.0;
+    for (int j = 0; j < mk; ++j) r += P[i * mk + j];
+    u[i] = fmax(a[i] - r, 0.0);                     // row deficit
+    dr += u[i];
+  }
+  dr = wsum(dr);
+  __syncwarp();
+  double cu = 0.0;
+  for (int e = lane; e < m * mk; e += 32) {
+    const int i = e / mk, j = e - i * mk;
+    const double pe = P[e] + (dr > 0.0 ? u[i] * fmax(v[j], 0.0) / dr : 0.0);
+    cu += C[e] * pe;
+  }
+  ub = wsum(cu);
+}
+
 // centroids to fp64: weights renormalised by their (sequential) fp64 sum, weighted means
 // (x == nullptr: symbolic supports, weights only)
 template <typename T>
@@ -267,9 +382,67 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   }
   __syncwarp();
   const double shrink = 1.0 - 1e-12;               // fp64 rounding margin on the bounds
+  const double grow = 1.0 + 1e-9;                  // margin on the rounded-plan upper bound
   double best = CUDART_INF;
   int bc = -1;
   unsigned nsolve = 0;
+  // phase A: candidates in increasing mean-bound order while the mean bound is below the best
+  // upper bound: sharpen each bound (relaxed marginals, Sinkhorn dual) and collect upper bounds
+  double ubest = CUDART_INF;
+  for (int visit = 0; visit < K; ++visit) {
+    __syncwarp();
+    double lb = CUDART_INF;
+    int cs = K;
+    for (int c = lane; c < K; c += 32)
+      if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
+        lb = LB[c];
+        cs = c;
+      }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
+      if (ol < lb || (ol == lb && oc < cs)) {
+        lb = ol;
+        cs = oc;
+      }
+    }
+    if (cs >= K || lb * shrink > ubest) break;      // every remaining centroid has W^2 > ubest
+    const double* xk = xc + (int64_t)cs * m * d;
+    for (int e = lane; e < m * mk; e += 32) {
+      const int i = e / mk, j = e - i * mk;
+      double a = 0.0;
+      if (Dtab) {
+        const int sa = xs[(int64_t)cs * m + i], sb = Ysym[j];
+        if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
+        else a = Dtab[(int64_t)sa * V + sb];
+      } else {
+        for (int t = 0; t < d; ++t) {
+          const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
+          a += df * df;
+        }
+      }
+      C[e] = a;
+    }
+    __syncwarp();
+    const double* wn = wc + (int64_t)cs * m;
+    double dlb, dub;
+    dual_bounds(L, ws, wn, mk, lane, dlb, dub);
+    ubest = fmin(ubest, dub * grow);
+    if (lane == 0) {
+      LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
+      solved[cs >> 5] |= 1u << (cs & 31);           // visited in phase A
+    }
+    __syncwarp();
+  }
+  // phase B: only phase-A centroids can win (the others have mean bound > ubest); exact solves
+  // in increasing sharpened-bound order until the bound exceeds the best exact W^2
+  for (int c = lane; c < K; c += 32) {
+    const bool vis = (solved[c >> 5] >> (c & 31)) & 1u;
+    if (!vis) LB[c] = CUDART_INF;
+  }
+  for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
+  __syncwarp();
   for (int visit = 0; visit < K; ++visit) {
     __syncwarp();                                   // C / solved of the previous visit consumed
     double lb = CUDART_INF;
