@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <new>
 #include <string>
@@ -608,7 +609,8 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const int64_t per_pass = variant == 3 ? (int64_t)wide_npair(wcfg) : (int64_t)NWARP * (32 / mp);
     const int64_t want = N / (per_pass * 6 * (int64_t)sms);          // >= ~6 CTAs per SM slot
-    passes = (int)std::max<int64_t>(4, std::min<int64_t>(32, want));
+    passes = (int)std::max<int64_t>(8, std::min<int64_t>(32, want));
+    if (const char* e = getenv("AD2_PASSES")) passes = std::max(1, atoi(e));   // tuning knob (bench experiments)
   }
   const int64_t per_item = variant == 3 ? (int64_t)wide_npair(wcfg) * passes
                            : variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
