@@ -581,18 +581,24 @@ k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
              const int32_t* __restrict__ item_cl, const int64_t* __restrict__ warm_src,
              const T* __restrict__ om, const T* __restrict__ w, const T* __restrict__ Qold,
              T* __restrict__ dst, T* __restrict__ L, int m, int ld) {
+  // warp per member, lane = row i (rows in chunks of 32), one column per step: coalesced rows
   const int item = blockIdx.x;
   const int c = item_cl[item];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k = item_mb[item] + warp; k < item_mb[item + 1]; k += 4) {
     const int64_t o0 = off[k];
-    const int64_t ne = (int64_t)ld * (off[k + 1] - o0);
+    const int mk = (int)(off[k + 1] - o0);
     const int64_t base = (int64_t)ld * o0;
     const int64_t src = warm_src ? warm_src[k] : -1;
-    for (int64_t e = lane; e < ne; e += 32) {
-      const int j = (int)(e / ld), i = (int)(e - (int64_t)j * ld);
-      dst[base + e] = (src >= 0) ? Qold[src + e] : (i < m ? w[(int64_t)c * m + i] * om[o0 + j] : T(0));
-      L[base + e] = T(0);
+    for (int r0 = 0; r0 < ld; r0 += 32) {
+      const int i = r0 + lane;
+      if (i >= ld) break;
+      const T wi = i < m ? w[(int64_t)c * m + i] : T(0);
+      for (int j = 0; j < mk; ++j) {
+        const int64_t e = (int64_t)j * ld + i;
+        dst[base + e] = (src >= 0) ? Qold[src + e] : wi * om[o0 + j];
+        L[base + e] = T(0);
+      }
     }
   }
 }

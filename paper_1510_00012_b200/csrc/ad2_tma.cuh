@@ -461,6 +461,8 @@ k_badmm_tma(const IterArgs<T> a) {
 // objective).  P == nullptr: sum of C (Eq.rho numerator); otherwise sum of C .* Pi1
 // (surrogate objective).  Accumulated in double per member; the cluster sums are
 // formed in a fixed order by k_dsum_members.
+template <typename T> __host__ __device__ constexpr int cost_member_warps() { return sizeof(T) == 8 ? 2 : 4; }
+
 template <typename T, int DP>
 __global__ void __launch_bounds__(128)
 k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restrict__ mem_cl,
@@ -471,54 +473,65 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
   using T2 = typename PR::t;
   constexpr int E = 16 / (int)sizeof(T);
   constexpr int DY = (DP == 4) ? 4 : DP + E;
+  constexpr int MKX = 32;                            // variant 2: m_k <= 32, ld <= 32
+  // the member's Y rows and (objective) its Pi1 block, staged by coalesced 16-byte loads
+  constexpr int NW = cost_member_warps<T>();
+  __shared__ __align__(16) T sY[NW][MKX * DY];
+  __shared__ __align__(16) T sP[NW][MKX * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+  const int64_t sidx = (int64_t)blockIdx.x * NW + warp;
   if (sidx >= N) return;
   const int c = mem_cl[sidx];
-  T2 nx2[DP / 2], msk2[DP / 2];                      // -x_i (difference form); mask only for DP == 4
-  double acc = 0.0;
-  for (int r0 = 0; r0 < m; r0 += 32) {
-    const int i = r0 + lane;
-    const bool rowok = i < m;
-#pragma unroll
-    for (int t = 0; t < DP / 2; ++t) {
-      const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
-      const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
-      nx2[t] = PR::make(-v0, -v1);
-      msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+  const int64_t o0 = off[sidx];
+  const int mk = (int)(off[sidx + 1] - o0);
+  {
+    const V* src = reinterpret_cast<const V*>(Y + o0 * DY);
+    V* dst = reinterpret_cast<V*>(sY[warp]);
+    for (int e = lane; e < mk * DY / E; e += 32) dst[e] = __ldg(src + e);
+    if (P) {
+      const V* ps = reinterpret_cast<const V*>(P + (int64_t)ld * o0);
+      V* pd = reinterpret_cast<V*>(sP[warp]);
+      for (int e = lane; e < mk * ld / E; e += 32) pd[e] = __ldcs(ps + e);
     }
-    const int64_t o0 = off[sidx];
-    const int mk = (int)(off[sidx + 1] - o0);
-    T s = T(0);
-    for (int j0 = 0; j0 < mk; j0 += 4) {
-      T2 c2[4];
-      T pv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = (j0 + u < mk) ? j0 + u : mk - 1;
-        const T* yj = Y + (o0 + j) * DY;
-        c2[u] = PR::make(T(0), T(0));
-#pragma unroll
-        for (int tt = 0; tt < DP / E; ++tt) {
-          const V v = __ldg(reinterpret_cast<const V*>(yj + tt * E));
-#pragma unroll
-          for (int u2 = 0; u2 < E / 2; ++u2) {
-            const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
-            // y - x on the real coordinates: for DP >= 16 the slots [d, DP) of a Y row are 0 (and
-            // |y|^2 sits at DP), for DP == 4 the |y|^2 slot is inside the row and is masked
-            T2 df = PR::add(yv, nx2[tt * (E / 2) + u2]);
-            if constexpr (DP == 4) df = PR::mul(df, msk2[tt * (E / 2) + u2]);
-            c2[u] = PR::fma(df, df, c2[u]);
-          }
-        }
-        pv[u] = (P && rowok) ? P[(int64_t)ld * (o0 + j) + i] : T(1);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * pv[u];
-    }
-    acc += (double)s;
   }
+  T2 nx2[DP / 2], msk2[DP / 2];                      // -x_i (difference form); mask only for DP == 4
+  const int i = lane;
+  const bool rowok = i < m;
+#pragma unroll
+  for (int t = 0; t < DP / 2; ++t) {
+    const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
+    const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
+    nx2[t] = PR::make(-v0, -v1);
+    msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+  }
+  __syncwarp();
+  T s = T(0);
+  for (int j0 = 0; j0 < mk; j0 += 4) {
+    T2 c2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = (j0 + u < mk) ? j0 + u : mk - 1;
+      const T* yj = sY[warp] + j * DY;
+      c2[u] = PR::make(T(0), T(0));
+#pragma unroll
+      for (int tt = 0; tt < DP / E; ++tt) {
+        const V v = *reinterpret_cast<const V*>(yj + tt * E);
+#pragma unroll
+        for (int u2 = 0; u2 < E / 2; ++u2) {
+          const T2 yv = reinterpret_cast<const T2*>(&v)[u2];
+          // y - x on the real coordinates: for DP >= 16 the slots [d, DP) of a Y row are 0 (and
+          // |y|^2 sits at DP), for DP == 4 the |y|^2 slot is inside the row and is masked
+          T2 df = PR::add(yv, nx2[tt * (E / 2) + u2]);
+          if constexpr (DP == 4) df = PR::mul(df, msk2[tt * (E / 2) + u2]);
+          c2[u] = PR::fma(df, df, c2[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * (P ? sP[warp][(j0 + u) * ld + i] : T(1));
+  }
+  double acc = (double)s;
   for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
   if (lane == 0) pm[sidx] = acc;
 }

@@ -77,7 +77,8 @@ template <>
 void launch_cost_member<double>(int dp, const int64_t* off, int64_t N, const int32_t* mem_cl, const double* Y,
                              const double* x, const double* P, double* pm, int m, int d, int ld, cudaStream_t s) {
   if (N == 0) return;
-  const unsigned g = (unsigned)((N + 3) / 4);
-  if (dp <= 4) k_cost_member<double, 4><<<g, 128, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
-  else k_cost_member<double, 16><<<g, 128, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
+  constexpr int NW = cost_member_warps<double>();
+  const unsigned g = (unsigned)((N + NW - 1) / NW);
+  if (dp <= 4) k_cost_member<double, 4><<<g, 32 * NW, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
+  else k_cost_member<double, 16><<<g, 32 * NW, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
 }
