@@ -192,8 +192,32 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
 // LB = sum_i a_i u_i + sum_j b_j v_j <= W^2 (Kantorovich duality).  The Sinkhorn plan rounded
 // onto the transport polytope (row scaling to <= a, column scaling to <= b, rank-one
 // correction, Altschuler et al.) is feasible, hence UB = <C, P> >= W^2.  Uses F as scratch.
-__device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double& lb,
-                            double& ub) {
+// dual-feasible potentials from fs by two fp64 c-transforms -> Kantorovich lower bound
+__device__ double ctrans_lb(int m, int mk, const double* C, const float* fs, const double* a, const double* b,
+                            double* u, double* v, int lane) {
+  for (int j = lane; j < mk; j += 32) {
+    double mn = CUDART_INF;
+    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j] - (double)fs[i]);
+    v[j] = mn;
+  }
+  __syncwarp();
+  double acc = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double mn = CUDART_INF;
+    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j] - v[j]);
+    u[i] = mn;
+    acc += a[i] * mn;
+  }
+  for (int j = lane; j < mk; j += 32) acc += b[j] * v[j];
+  const double r = wsum(acc);
+  __syncwarp();
+  return r;
+}
+
+// prune_at: if an intermediate lower bound (after 8 / 16 iterations) already exceeds it, return
+// early with ub = +inf (the candidate cannot win)
+__device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double prune_at,
+                            double& lb, double& ub) {
   const int m = L.m;
   const double* C = reinterpret_cast<const double*>(ws + L.oC);
   double* P = reinterpret_cast<double*>(ws + L.oF);
@@ -241,23 +265,16 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
       fs[i] = -eps * (mx + __logf(sm));
     }
     __syncwarp();
+    if (it == 7 || it == 15) {                      // early exit for clearly worse centroids
+      const double l = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
+      if (l * (1.0 - 1e-12) > prune_at) {
+        lb = l;
+        ub = CUDART_INF;
+        return;
+      }
+    }
   }
-  // dual-feasible potentials by two fp64 c-transforms
-  for (int j = lane; j < mk; j += 32) {
-    double mn = CUDART_INF;
-    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j] - (double)fs[i]);
-    v[j] = mn;
-  }
-  __syncwarp();
-  double acc = 0.0;
-  for (int i = lane; i < m; i += 32) {
-    double mn = CUDART_INF;
-    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j] - v[j]);
-    u[i] = mn;
-    acc += a[i] * mn;
-  }
-  for (int j = lane; j < mk; j += 32) acc += b[j] * v[j];
-  lb = wsum(acc);
+  lb = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
   // primal: Sinkhorn plan, rounded onto the transport polytope
   const float ie = 1.f / eps;
   for (int e = lane; e < m * mk; e += 32) {
@@ -427,7 +444,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     __syncwarp();
     const double* wn = wc + (int64_t)cs * m;
     double dlb, dub;
-    dual_bounds(L, ws, wn, mk, lane, dlb, dub);
+    dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
     ubest = fmin(ubest, dub * grow);
     if (lane == 0) {
       LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
