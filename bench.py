@@ -267,39 +267,28 @@ def run_ours(args, rank, world, local_rank):
 
 # ------------------------------------------------------------------------------------------ oracle
 
-def oracle_sample(b: wl.Bundle, budget_s: float):
-    """A bounded sample of the workload for the oracle: the first members of cluster 0, sized so
-    T iterations take about budget_s on this host (estimated from a 1-iteration probe)."""
+def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, n_clusters=None):
+    """The fp64 oracle (Alg. 4 as written, OpenMP over members) on a bounded sample of the same
+    workload: whole clusters 0, 1, ... with the full schedule until about budget_s of host time
+    (or exactly n_clusters when given, for repeatable reference steps)."""
     import oracle
-    mem = np.nonzero(b.labels == 0)[0]
     s = b.sched
-    # probe with the full schedule on a growing prefix until it takes >= 1 s, then scale to budget_s
-    n_try = min(len(mem), 500)
-    while True:
-        sub = b.subset(mem[:n_try])
+    t_all, entries, members, c = 0.0, 0, 0, 0
+    while c < b.K:
+        mem = np.nonzero(b.labels == c)[0]
+        sub = b.subset(mem)
         t = time.time()
-        oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
+        oracle.badmm_centroid(b.x0[c], b.w0[c], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
                               s.eps, 1e-5, want_state=False)
-        dt = time.time() - t
-        if dt >= 1.0 or n_try >= len(mem):
+        t_all += time.time() - t
+        entries += b.m * sub.n
+        members += sub.N
+        c += 1
+        if (n_clusters is not None and c >= n_clusters) or (n_clusters is None and t_all >= budget_s):
             break
-        n_try = min(len(mem), n_try * 4)
-    take = int(min(len(mem), max(50, n_try * budget_s / max(dt, 1e-3))))
-    return b.subset(mem[:take]), take
-
-
-def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, sub=None):
-    import oracle
-    s = b.sched
-    if sub is None:
-        sub, _ = oracle_sample(b, budget_s)
-    t = time.time()
-    oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0, s.eps,
-                          1e-5, want_state=False)
-    dt = time.time() - t
-    return {"value": b.m * sub.n * s.T / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"cluster 0 of {b.name}: first {sub.N} members ({b.m * sub.n} plan entries), T={s.T}, "
-                      f"tau={s.tau}, fp64, {dt:.1f}s"}
+    return {"value": entries * s.T / t_all, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"clusters 0..{c - 1} of {b.name}: {members} members ({entries} plan entries), T={s.T}, "
+                      f"tau={s.tau}, fp64, {t_all:.1f}s", "n_clusters": c}
 
 
 def run_reference(args, rank, world):
@@ -307,11 +296,13 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     b = load_bundle(args.workload, 0, 1, lambda: None)
-    sub, _ = oracle_sample(b, args.cpu_budget / max(1, args.steps + args.warmup) * 2)
-    for _ in range(args.warmup):
-        cpu_baseline(b, sub=sub)
+    # each reference step: the same bounded sample (whole clusters), sized so the run stays short
+    probe = cpu_baseline(b, budget_s=max(2.0, args.cpu_budget / max(1, args.steps + args.warmup)))
+    nc = probe["n_clusters"]
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_baseline(b, n_clusters=nc)
     t = time.time()
-    vals = [cpu_baseline(b, sub=sub) for _ in range(args.steps)]
+    vals = [cpu_baseline(b, n_clusters=nc) for _ in range(args.steps)]
     ms = (time.time() - t) / max(1, args.steps) * 1e3
     v = float(np.mean([x["value"] for x in vals]))
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
