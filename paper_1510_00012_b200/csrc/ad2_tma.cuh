@@ -193,13 +193,17 @@ k_badmm_tma(const IterArgs<T> a) {
   };
   int64_t cp0 = 0, cp1 = 0;
   int cnp = pass_pts(0, cp0, cp1);
+  // the geometry of pass t+1 is loaded one pass ahead (its offsets are on the critical path of
+  // the ring placement): pass t uses (np0, nnp) loaded during pass t-1
+  int64_t np0 = 0, np1 = 0;
+  int nnp = pass_pts(1, np0, np1);
   int cbase = 0;                                       // ring offset of the current pass
   if (lane == 0 && cnp > 0) issue(0, 0, cp0, cnp);
 
   for (int t = 0; cnp > 0; ++t) {
     // place pass t+1 behind pass t (or at the ring start) while t computes
-    int64_t np0 = 0, np1 = 0;
-    const int nnp = pass_pts(t + 1, np0, np1);
+    int64_t fp0 = 0, fp1 = 0;
+    const int fnp = pass_pts(t + 2, fp0, fp1);          // consumed next pass
     const int csize = (2 * MP + DY) * slot(cnp), nsize = (2 * MP + DY) * slot(nnp);
     int nbase = -1;
     if (nnp > 0) {
@@ -426,6 +430,9 @@ k_badmm_tma(const IterArgs<T> a) {
     cnp = nnp;
     cp0 = np0;
     cp1 = np1;
+    nnp = fnp;
+    np0 = fp0;
+    np1 = fp1;
   }
   if (lane == 0) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);

@@ -105,11 +105,13 @@ k_badmm_wide(const IterArgs<float> a) {
   int cnp = member(0, cp0);
   int cbase = 0;
   if (leader && cnp > 0) issue(0, 0, cp0, cnp);
+  int64_t np0 = 0;                                 // geometry of pass t+1, loaded one pass ahead
+  int nnp = member(1, np0);
 
   for (int t = 0; cnp > 0; ++t) {
     // place pass t+1 beside pass t (alternating ring start / ring end) while t computes
-    int64_t np0 = 0;
-    const int nnp = member(t + 1, np0);
+    int64_t fp0 = 0;
+    const int fnp = member(t + 2, fp0);            // consumed next pass
     const int csize = (2 * WMP + third) * cnp, nsize = (2 * WMP + third) * nnp;
     int nbase = -1;
     if (nnp > 0) {
@@ -266,6 +268,8 @@ k_badmm_wide(const IterArgs<float> a) {
     cbase = nbase;
     cnp = nnp;
     cp0 = np0;
+    nnp = fnp;
+    np0 = fp0;
   }
   if (leader) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);
