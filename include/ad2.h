@@ -202,6 +202,17 @@ ad2_status ad2_set_profiling(ad2_ctx ctx, int enable);
 ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64_t *n_launches,
                          double *step_ms);
 
+/* Centroid initialisation (§V, Eq.merge; part of SURVEY.md §8(f) NEXT #2):
+ * for every cluster c the caller picks a member pick[c] (host int64 [K], index into the batch;
+ * the paper picks one at random among the cluster's members with at least m support points), and
+ * its support (weights renormalised in fp64) is reduced to m points by repeatedly merging the pair
+ * minimising w_i w_j |x_i - x_j|^2 / (w_i + w_j) into its weighted mean (ties: lowest (i, j));
+ * a member with fewer than m points has its heaviest point split in halves (reading X19).
+ * Runs in fp64 on the device; x0_out [K][m][d], w0_out [K][m] (batch dtype) in `where` memory.
+ * batch->K, m, d give the shapes; its labels are ignored.  Synchronous. */
+ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch *batch, const int64_t *pick, void *x0_out, void *w0_out,
+                          ad2_mem where);
+
 /* The AD2 outer loop (Alg. 1, P:259-266 with Alg. 4 as the centroid update; SURVEY.md §8(f)
  * NEXT #2), on the device: the shard is staged once and stays on this GPU; each
  * round r = ad2_barycenter_init (round 0 cold; later rounds warm-start Pi^(2) for members whose

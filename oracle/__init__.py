@@ -55,6 +55,7 @@ def lib():
             d, i, p, i64 = C.c_double, C.c_int, C.c_void_p, C.c_int64
             L.ad2o_assign.argtypes = [i, i, i, p, p, i, p, p, p, p, p, p]
             L.ad2o_badmm_table.argtypes = [i, i, p, p, p, p, p, p, i, p, p, i, i, d, d, d, p, p, p, p, p]
+            L.ad2o_merge.argtypes = [i, i, p, p, i, p, p]
             L.ad2o_cost.argtypes = [i, i, i, p, p, p]
             L.ad2o_rho.argtypes = [i, i, p, i, p, p, d, p]
             L.ad2o_rho.restype = d
@@ -357,3 +358,13 @@ def badmm_table(xs, w0, offsets, ys, omega, D, T, rule=0, rho0=2.0, eps=1e-16, w
         for name, cat in (("Pi1", Pi1), ("Pi2", Pi2), ("Lam", Lam)):
             res.mats[name] = [cat[bounds[k]:bounds[k + 1]].reshape(m, sizes[k]) for k in range(N)]
     return res
+
+
+def merge(y, w, m):
+    """Eq.merge initialisation of a centroid with m points from one member."""
+    y, w = _f64(y), _f64(w)
+    mk, d = y.shape
+    x = np.empty((m, d))
+    wo = np.empty(m)
+    lib().ad2o_merge(mk, d, _ptr(y), _ptr(w), m, _ptr(x), _ptr(wo))
+    return x, wo

@@ -220,3 +220,63 @@ void ad2o_assign(int K, int m, int d, const double *x, const double *w, int N, c
     }
     free(wn);
 }
+
+/* Centroid initialisation (§V, Eq.merge): from a chosen member's support
+ * (y [mk][d], weights w renormalised to sum 1), recursively merge the pair (i, j), i < j,
+ * minimising w_i w_j |x_i - x_j|^2 / (w_i + w_j) (first pair in (i, j) order on ties) into
+ * x = (w_i x_i + w_j x_j) / (w_i + w_j) with weight w_i + w_j, kept at position i (j removed,
+ * the later points move up), until m points remain.  With fewer than m points (reading X19,
+ * SPEC's fallback): repeatedly split the heaviest point (first on ties) into two copies of half
+ * its weight, the copy appended at the end.  Outputs xout [m][d], wout [m] (sum 1). */
+void ad2o_merge(int mk, int d, const double *y, const double *w_in, int m, double *xout, double *wout)
+{
+    int cap = mk > m ? mk : m;
+    double *x = (double *)malloc(sizeof(double) * (size_t)cap * d);
+    double *w = (double *)malloc(sizeof(double) * (size_t)cap);
+    double s = 0.0;
+    for (int j = 0; j < mk; ++j) s += w_in[j];
+    for (int j = 0; j < mk; ++j) {
+        w[j] = w_in[j] / s;
+        for (int t = 0; t < d; ++t) x[j * d + t] = y[j * d + t];
+    }
+    int n = mk;
+    while (n > m) {
+        double best = INFINITY;
+        int bi = 0, bj = 1;
+        for (int i = 0; i < n; ++i)
+            for (int j = i + 1; j < n; ++j) {
+                double dd = 0.0;
+                for (int t = 0; t < d; ++t) {
+                    double df = x[i * d + t] - x[j * d + t];
+                    dd += df * df;
+                }
+                double c = w[i] * w[j] * dd / (w[i] + w[j]);
+                if (c < best) { best = c; bi = i; bj = j; }
+            }
+        double wb = w[bi] + w[bj];
+        for (int t = 0; t < d; ++t) x[bi * d + t] = (w[bi] * x[bi * d + t] + w[bj] * x[bj * d + t]) / wb;
+        w[bi] = wb;
+        for (int j = bj; j < n - 1; ++j) {
+            w[j] = w[j + 1];
+            for (int t = 0; t < d; ++t) x[j * d + t] = x[(j + 1) * d + t];
+        }
+        --n;
+    }
+    while (n < m) {
+        int h = 0;
+        for (int j = 1; j < n; ++j)
+            if (w[j] > w[h]) h = j;
+        w[h] *= 0.5;
+        w[n] = w[h];
+        for (int t = 0; t < d; ++t) x[n * d + t] = x[h * d + t];
+        ++n;
+    }
+    double tot = 0.0;
+    for (int i = 0; i < m; ++i) tot += w[i];
+    for (int i = 0; i < m; ++i) {
+        wout[i] = w[i] / tot;
+        for (int t = 0; t < d; ++t) xout[i * d + t] = x[i * d + t];
+    }
+    free(x);
+    free(w);
+}

@@ -60,7 +60,7 @@ class Info(C.Structure):
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
            "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
-           "ad2_set_cost_table", "ad2_cluster", "ad2_sync",
+           "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_sync",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
     L.ad2_set_cost_table.argtypes = [p, p, i32, C.c_int, C.c_int]
     L.ad2_cluster.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), C.POINTER(Loop), p, p, p, C.POINTER(i32),
                               p, p]
+    L.ad2_merge_init.argtypes = [p, C.POINTER(Batch), p, p, p, C.c_int]
     L.ad2_sync.argtypes = [p]
     L.ad2_last_error.argtypes = [p]
     L.ad2_last_error.restype = C.c_char_p
@@ -330,6 +331,22 @@ class Context:
         self._chk(self.L.ad2_assign_symbolic(self.h, C.byref(b), _ptr(xs), _ptr(w), lab.ctypes.data, w2.ctypes.data,
                                              HOST, C.byref(n_exact)))
         return lab, w2, int(n_exact.value)
+
+    def merge_init(self, offsets, supports, weights, pick, K: int, m: int, mem: str = "device",
+                   dtype: Optional[str] = None):
+        """ad2_merge_init: Eq.merge centroids from the picked members; returns host (x0, w0)."""
+        if dtype is None:
+            dtype = "f64" if str(getattr(weights, "dtype", "")) in ("float64", "torch.float64") else "f32"
+        d = int(supports.shape[1])
+        N = int(offsets.shape[0]) - 1
+        b = Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, d, int(m), int(K), N,
+                  _ptr(offsets), _ptr(supports), _ptr(weights), None)
+        pk = np.ascontiguousarray(pick, np.int64)
+        ft = np.float64 if dtype == "f64" else np.float32
+        x0 = np.zeros((int(K), int(m), d), ft)
+        w0 = np.zeros((int(K), int(m)), ft)
+        self._chk(self.L.ad2_merge_init(self.h, C.byref(b), pk.ctypes.data, x0.ctypes.data, w0.ctypes.data, HOST))
+        return x0, w0
 
     def sync(self):
         self._chk(self.L.ad2_sync(self.h))

@@ -1297,6 +1297,75 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
   return ret;
 }
 
+// ------------------------------------------------------------------------------------------
+// centroid initialisation by Eq.merge
+// ------------------------------------------------------------------------------------------
+int merge_init_launch(int f64, const int64_t* off, const void* Y, const void* Wt, const int64_t* pick, int K, int m,
+                      int d, int cap, void* x0, void* w0, int optin, cudaStream_t s);
+void pick_sizes_launch(const int64_t* off, const int64_t* pick, int K, int64_t N, int64_t* mk, int* err, cudaStream_t s);
+
+ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch* b, const int64_t* pick, void* x0_out, void* w0_out,
+                          ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!b || !pick || !x0_out || !w0_out) return ctx->fail(AD2_ERR_ARG, "merge_init: null argument");
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
+  if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
+  if (where != AD2_DEVICE && where != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "where");
+  if (b->d < 1 || b->m < 1 || b->K < 1 || b->n_members < 1 || !b->offsets || !b->supports || !b->weights)
+    return ctx->fail(AD2_ERR_ARG, "merge_init: shape / batch arrays");
+  CHK(set_dev(ctx));
+  cudaStream_t s = ctx->stream;
+  const int64_t N = b->n_members;
+  const int d = b->d, m = b->m, K = b->K;
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  const void* off = b->offsets;
+  const void* Y = b->supports;
+  const void* W = b->weights;
+  if (b->mem == AD2_HOST) {
+    const int64_t n = static_cast<const int64_t*>(b->offsets)[N];
+    CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
+    CU(ctx->stage_Y.reserve(es * (size_t)n * d));
+    CU(ctx->stage_W.reserve(es * (size_t)n));
+    CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+    off = ctx->stage_off.p;
+    Y = ctx->stage_Y.p;
+    W = ctx->stage_W.p;
+  }
+  CU(ctx->asg_scal.reserve(64));
+  CU(ctx->asg_x.reserve(sizeof(int64_t) * 2 * (size_t)K + es * (size_t)K * m * (d + 1)));
+  int64_t* dpick = ctx->asg_x.as<int64_t>();
+  int64_t* dmk = dpick + K;
+  void* x0 = (char*)ctx->asg_x.p + sizeof(int64_t) * 2 * (size_t)K;
+  void* w0 = (char*)x0 + es * (size_t)K * m * d;
+  int* err = ctx->asg_scal.as<int>();
+  CU(cudaMemsetAsync(err, 0, sizeof(int), s));
+  CU(cudaMemcpyAsync(dpick, pick, sizeof(int64_t) * K, cudaMemcpyHostToDevice, s));
+  pick_sizes_launch(static_cast<const int64_t*>(off), dpick, K, N, dmk, err, s);
+  CHK(launch_check(ctx, "k_pick_sizes"));
+  std::vector<int64_t> hmk(K);
+  int herr = 0;
+  CU(cudaMemcpyAsync(hmk.data(), dmk, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (herr & 8) return ctx->fail(AD2_ERR_ARG, "merge_init: a picked member index is outside [0, N)");
+  int64_t cap = m;
+  for (int c = 0; c < K; ++c) cap = std::max(cap, hmk[c]);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (merge_init_launch(b->dtype == AD2_F64, static_cast<const int64_t*>(off), Y, W, dpick, K, m, d, (int)cap, x0, w0,
+                        optin, s) != 0)
+    return ctx->fail(AD2_ERR_ARG, "merge_init: a picked member (m_k = %lld, d = %d) exceeds shared memory",
+                     (long long)cap, d);
+  CHK(launch_check(ctx, "k_merge_init"));
+  const cudaMemcpyKind kind = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(x0_out, x0, es * (size_t)K * m * d, kind, s));
+  CU(cudaMemcpyAsync(w0_out, w0, es * (size_t)K * m, kind, s));
+  CU(cudaStreamSynchronize(s));
+  return AD2_OK;
+}
+
 ad2_status ad2_sync(ad2_ctx ctx) {
   if (!ctx) return AD2_ERR_ARG;
   CHK(set_dev(ctx));

@@ -583,3 +583,136 @@ void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int*
   if (N == 0) return;
   k_assign_mk<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(off, N, mkmax, err);
 }
+
+// ------------------------------------------------------------------------------------------
+// Centroid initialisation by Eq.merge: one warp per cluster c takes the chosen
+// member pick[c] (renormalised weights, fp64) and merges the pair (i < j) minimising
+// w_i w_j |x_i - x_j|^2 / (w_i + w_j) (lowest (i, j) on ties) into the weighted mean at i (j
+// removed, later points move up) until m remain; with fewer than m points the heaviest point
+// (lowest index on ties) is split into two halves, the copy appended (reading X19).
+// ------------------------------------------------------------------------------------------
+namespace ad2a {
+__global__ void k_pick_sizes(const int64_t* __restrict__ off, const int64_t* __restrict__ pick, int K, int64_t N,
+                             int64_t* __restrict__ mk, int* __restrict__ err) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  const int64_t k = pick[c];
+  if (k < 0 || k >= N) {
+    atomicOr(err, 8);
+    mk[c] = 0;
+    return;
+  }
+  mk[c] = off[k + 1] - off[k];
+}
+
+template <typename T>
+__global__ void k_merge_init(const int64_t* __restrict__ off, const T* __restrict__ Y, const T* __restrict__ Wt,
+                             const int64_t* __restrict__ pick, int m, int d, int cap, T* __restrict__ x0,
+                             T* __restrict__ w0) {
+  extern __shared__ __align__(16) double msm[];
+  double* x = msm;                                  // [cap][d]
+  double* w = msm + (size_t)cap * d;                // [cap]
+  const int c = blockIdx.x, lane = threadIdx.x;
+  const int64_t k = pick[c];
+  const int64_t o0 = off[k];
+  const int mk = (int)(off[k + 1] - o0);
+  double s = 0.0;
+  if (lane == 0)
+    for (int j = 0; j < mk; ++j) s += (double)Wt[o0 + j];
+  s = __shfl_sync(0xffffffffu, s, 0);
+  for (int j = lane; j < mk; j += 32) w[j] = (double)Wt[o0 + j] / s;
+  for (int e = lane; e < mk * d; e += 32) x[e] = (double)Y[o0 * d + e];
+  __syncwarp();
+  int n = mk;
+  while (n > m) {
+    double best = CUDART_INF;
+    int bp = 1 << 30;
+    const int np = n * (n - 1) / 2;
+    for (int p = lane; p < np; p += 32) {           // pair p -> (i, j), i < j, in (i, j) order
+      int i = 0, rem = p;
+      while (rem >= n - 1 - i) {
+        rem -= n - 1 - i;
+        ++i;
+      }
+      const int j = i + 1 + rem;
+      // uncontracted IEEE operations in the oracle's order: identical decisions
+      double dd = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double df = __dsub_rn(x[i * d + t], x[j * d + t]);
+        dd = __dadd_rn(dd, __dmul_rn(df, df));
+      }
+      const double cst = __ddiv_rn(__dmul_rn(__dmul_rn(w[i], w[j]), dd), __dadd_rn(w[i], w[j]));
+      if (cst < best) {                             // pairs of a lane ascend: first minimum kept
+        best = cst;
+        bp = p;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ob < best || (ob == best && op < bp)) {
+        best = ob;
+        bp = op;
+      }
+    }
+    int bi = 0, rem = bp;
+    while (rem >= n - 1 - bi) {
+      rem -= n - 1 - bi;
+      ++bi;
+    }
+    const int bj = bi + 1 + rem;
+    const double wb = w[bi] + w[bj];
+    __syncwarp();
+    for (int t = lane; t < d; t += 32)
+      x[bi * d + t] = __ddiv_rn(__dadd_rn(__dmul_rn(w[bi], x[bi * d + t]), __dmul_rn(w[bj], x[bj * d + t])), wb);
+    __syncwarp();
+    if (lane == 0) {
+      w[bi] = wb;
+      for (int j = bj; j < n - 1; ++j) {
+        w[j] = w[j + 1];
+        for (int t = 0; t < d; ++t) x[j * d + t] = x[(j + 1) * d + t];
+      }
+    }
+    --n;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    while (n < m) {
+      int h = 0;
+      for (int j = 1; j < n; ++j)
+        if (w[j] > w[h]) h = j;
+      w[h] *= 0.5;
+      w[n] = w[h];
+      for (int t = 0; t < d; ++t) x[n * d + t] = x[h * d + t];
+      ++n;
+    }
+    double tot = 0.0;
+    for (int i = 0; i < m; ++i) tot += w[i];
+    for (int i = 0; i < m; ++i) w[i] = w[i] / tot;
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) w0[(int64_t)c * m + i] = (T)w[i];
+  for (int e = lane; e < m * d; e += 32) x0[(int64_t)c * m * d + e] = (T)x[e];
+}
+}  // namespace ad2a
+
+int merge_init_launch(int f64, const int64_t* off, const void* Y, const void* Wt, const int64_t* pick, int K, int m,
+                      int d, int cap, void* x0, void* w0, int optin, cudaStream_t s) {
+  const size_t sm = sizeof(double) * ((size_t)cap * d + cap);
+  if (sm > (size_t)optin) return -1;
+  if (f64) {
+    cudaFuncSetAttribute(k_merge_init<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_merge_init<double><<<K, 32, sm, s>>>(off, (const double*)Y, (const double*)Wt, pick, m, d, cap, (double*)x0,
+                                          (double*)w0);
+  } else {
+    cudaFuncSetAttribute(k_merge_init<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_merge_init<float><<<K, 32, sm, s>>>(off, (const float*)Y, (const float*)Wt, pick, m, d, cap, (float*)x0,
+                                         (float*)w0);
+  }
+  return 0;
+}
+
+void pick_sizes_launch(const int64_t* off, const int64_t* pick, int K, int64_t N, int64_t* mk, int* err, cudaStream_t s) {
+  k_pick_sizes<<<(K + 127) / 128, 128, 0, s>>>(off, pick, K, N, mk, err);
+}

@@ -132,3 +132,34 @@ def test_cluster_loop_fp32_stops_on_stable_labels():
     lab, _, _ = ctx.assign(a["offsets"], a["supports"], a["weights"], torch.from_numpy(x).cuda(),
                            torch.from_numpy(w).cuda())
     np.testing.assert_array_equal(lab, res["labels"])
+
+
+# ------------------------------------------------------------------ Eq.merge initialisation
+
+@pytest.mark.parametrize("cfg,N,K,dtype", [(2, 600, 10, "f32"), (3, 400, 6, "f64"), (4, 120, 5, "f32")])
+def test_merge_init_matches_oracle(cfg, N, K, dtype):
+    """ad2_merge_init (fp64 on the device, uncontracted operations in the oracle's order) against
+    oracle.merge on the same picks: identical merge decisions, values to fp64 rounding (the cast
+    to the batch dtype at the end)."""
+    from paper_1510_00012_b200 import ad2
+    b = wl.make_config(cfg, N=N, K=K, dtype=dtype)
+    rng = np.random.default_rng(cfg)
+    sizes = np.diff(b.offsets)
+    pick = []
+    for c in range(b.K):
+        mem = np.nonzero(b.labels == c)[0]
+        big = mem[sizes[mem] >= b.m]
+        pick.append(int(rng.choice(big)) if len(big) else int(mem[0]))   # small members exercise the split
+    ctx = ad2.Context(0)
+    for mem_kind in ("host", "device"):
+        if mem_kind == "device":
+            a = to_dev(b, torch_cuda())
+            x0, w0 = ctx.merge_init(a["offsets"], a["supports"], a["weights"], pick, b.K, b.m, dtype=dtype)
+        else:
+            x0, w0 = ctx.merge_init(b.offsets, b.supports, b.weights, pick, b.K, b.m, mem="host", dtype=dtype)
+        for c, k in enumerate(pick):
+            y, w = b.member(k)
+            ox, ow = oracle.merge(y, w, b.m)
+            tol = 1e-14 if dtype == "f64" else 1e-6
+            np.testing.assert_allclose(w0[c], ow, rtol=tol, atol=tol * 1e-3)
+            np.testing.assert_allclose(x0[c], ox, rtol=tol, atol=tol * np.abs(ox).max())

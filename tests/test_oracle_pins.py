@@ -531,3 +531,43 @@ def test_symbolic_support_is_never_updated_and_marginals_hold():
     for k in range(N):
         np.testing.assert_allclose(res.mats["Pi1"][k].sum(0), om[off[k]:off[k + 1]], rtol=1e-12)  # P1 columns
         np.testing.assert_allclose(res.mats["Pi2"][k].sum(1), res.w, rtol=1e-10, atol=1e-15)     # P1 rows
+
+
+# ---------------------------------------------------------------- Eq.merge initialisation
+
+def test_merge_init_pins():
+    """Eq.merge: each step merges the pair minimising w_i w_j |x_i-x_j|^2/(w_i+w_j) (brute force
+    over the pairs in the test) into the weighted mean; mass and mean are preserved; one merge
+    moves the distribution by W^2(P, P') <= w_i|x_i - xb|^2 + w_j|x_j - xb|^2, which for
+    the merged pair equals the merge cost; m >= m_k leaves the points (fallback splits)."""
+    rng = np.random.default_rng(41)
+    y = rng.normal(0, 2, (7, 3))
+    w = rng.dirichlet(np.ones(7))
+    # one merge, by brute force
+    best, bi, bj = np.inf, -1, -1
+    for i in range(7):
+        for j in range(i + 1, 7):
+            c = w[i] * w[j] * ((y[i] - y[j]) ** 2).sum() / (w[i] + w[j])
+            if c < best:
+                best, bi, bj = c, i, j
+    x6, w6 = oracle.merge(y, w, 6)
+    xb = (w[bi] * y[bi] + w[bj] * y[bj]) / (w[bi] + w[bj])
+    keep = [k for k in range(7) if k not in (bi, bj)]
+    np.testing.assert_allclose(x6[bi], xb, rtol=1e-14)
+    assert w6[bi] == pytest.approx(w[bi] + w[bj], rel=1e-14)
+    others = [k for k in range(6) if k != bi]
+    np.testing.assert_allclose(x6[others], y[keep], rtol=0, atol=0)
+    W = oracle.w2sq(y, w, x6, w6)
+    bound = w[bi] * ((y[bi] - xb) ** 2).sum() + w[bj] * ((y[bj] - xb) ** 2).sum()
+    assert W <= bound + 1e-12 and bound == pytest.approx(best, rel=1e-12)
+    # full reduction: mass and mean preserved
+    x3, w3 = oracle.merge(y, w, 3)
+    assert w3.sum() == pytest.approx(1.0, abs=1e-15)
+    np.testing.assert_allclose(w3 @ x3, w @ y, rtol=1e-12, atol=1e-12)
+    # m >= m_k: the member itself (m = m_k) and heaviest-point splitting (m > m_k)
+    x7, w7 = oracle.merge(y, w, 7)
+    np.testing.assert_allclose(x7, y, atol=0)
+    x9, w9 = oracle.merge(y, w, 9)
+    h = int(np.argmax(w))
+    assert w9[h] == pytest.approx(w[h] / 2) and w9[7] == pytest.approx(w[h] / 2)
+    np.testing.assert_allclose(x9[7], y[h], atol=0)
