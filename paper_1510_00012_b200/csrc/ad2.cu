@@ -1130,9 +1130,9 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
   CU(ctx->asg_best.reserve(sizeof(double) * (N > 0 ? N : 1)));
   CU(ctx->asg_scal.reserve(64));
   CU(cudaMemsetAsync(ctx->asg_scal.p, 0, 64, s));
-  unsigned long long* scal = ctx->asg_scal.as<unsigned long long>();   // [0] mkmax [1] n_exact [2] err
+  unsigned long long* scal = ctx->asg_scal.as<unsigned long long>();   // [0] mkmax [1] n_exact [2] err [3] visits
   int* err = reinterpret_cast<int*>(scal + 2);
-  unsigned long long hs[3] = {0, 0, 0};
+  unsigned long long hs[4] = {0, 0, 0, 0};
   if (N > 0) {
     assign_mkmax(static_cast<const int64_t*>(off), N, scal, err, s);
     CHK(launch_check(ctx, "k_assign_mk"));
@@ -1162,6 +1162,8 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
   CU(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   if (n_exact_out) *n_exact_out = (int64_t)hs[1];
+  if (getenv("AD2_ASSIGN_STATS"))
+    fprintf(stderr, "[ad2_assign] N=%lld K=%d exact=%llu sinkhorn_candidates=%llu\n", (long long)N, K, hs[1], hs[3]);
   if (hs[2] & 1) return ctx->fail(AD2_ERR_NONFINITE, "assign: a transport solve did not terminate");
   if (hs[2] & 4) return ctx->fail(AD2_ERR_ARG, "assign: a symbol id outside [0, V) of the cost table");
   return AD2_OK;

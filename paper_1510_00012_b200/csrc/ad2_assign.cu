@@ -29,7 +29,7 @@ namespace ad2a {
 
 struct AsgLay {
   int m, mk, V, K, d;
-  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, oCf, olog, bytes;
+  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, oCf, olog, oys, bytes;
   __host__ __device__ void make(int m_, int mk_, int K_, int d_) {
     m = m_, mk = mk_, K = K_, d = d_;
     V = m + mk;
@@ -53,6 +53,7 @@ struct AsgLay {
     oyb = take(8 * (size_t)d);
     oCf = take(4 * (size_t)m * mk);
     olog = take(4 * (size_t)V);
+    oys = take(8 * (size_t)mk * d);                   // the member's points in fp64
     bytes = o;
   }
 };
@@ -265,7 +266,7 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
       fs[i] = -eps * (mx + __logf(sm));
     }
     __syncwarp();
-    if (it == 7 || it == 15) {                      // early exit for clearly worse centroids
+    if (it == 3 || it == 7 || it == 15) {           // early exit for clearly worse centroids
       const double l = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
       if (l * (1.0 - 1e-12) > prune_at) {
         lb = l;
@@ -313,6 +314,46 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
     cu += C[e] * pe;
   }
   ub = wsum(cu);
+}
+
+// C_ij = |x_ci - y_j|^2 in fp64 (difference form) with lane = centroid row: x_i is held in
+// registers 16 coordinates at a time, the member's points ys are broadcast from shared memory;
+// symbolic supports read the table instead.
+__device__ void build_cost(const AsgLay& L, unsigned char* ws, const double* __restrict__ xk, int mk, int lane,
+                           const int32_t* xs_c, const int32_t* Ysym, const double* Dtab, int V, int* err) {
+  const int m = L.m, d = L.d;
+  double* C = reinterpret_cast<double*>(ws + L.oC);
+  const double* ys = reinterpret_cast<const double*>(ws + L.oys);
+  if (Dtab) {
+    for (int e = lane; e < m * mk; e += 32) {
+      const int i = e / mk, j = e - i * mk;
+      const int sa = xs_c[i], sb = Ysym[j];
+      double a = 0.0;
+      if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
+      else a = Dtab[(int64_t)sa * V + sb];
+      C[e] = a;
+    }
+    return;
+  }
+  for (int i = lane; i < m; i += 32) {
+    for (int t0 = 0; t0 < d; t0 += 16) {
+      double xr[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) xr[t] = (t0 + t < d) ? xk[(int64_t)i * d + t0 + t] : 0.0;
+      const int tn = d - t0 < 16 ? d - t0 : 16;
+      for (int j = 0; j < mk; ++j) {
+        const double* yj = ys + j * d + t0;
+        double a = (t0 == 0) ? 0.0 : C[i * mk + j];
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < tn) {
+            const double df = xr[t] - yj[t];
+            a += df * df;
+          }
+        C[i * mk + j] = a;
+      }
+    }
+  }
 }
 
 // centroids to fp64: weights renormalised by their (sequential) fp64 sum, weighted means
@@ -380,6 +421,10 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
   __syncwarp();
   const int32_t* Ysym = reinterpret_cast<const int32_t*>(Y) + o0;
+  if (!Dtab) {
+    double* ys = reinterpret_cast<double*>(ws + L.oys);
+    for (int e = lane; e < mk * d; e += 32) ys[e] = (double)Yk[e];
+  }
   if (!Dtab)
     for (int t = lane; t < d; t += 32) {
       double a = 0.0;
@@ -402,7 +447,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   const double grow = 1.0 + 1e-9;                  // margin on the rounded-plan upper bound
   double best = CUDART_INF;
   int bc = -1;
-  unsigned nsolve = 0;
+  unsigned nsolve = 0, nvisit = 0;
   // phase A: candidates in increasing mean-bound order while the mean bound is below the best
   // upper bound: sharpen each bound (relaxed marginals, Sinkhorn dual) and collect upper bounds
   double ubest = CUDART_INF;
@@ -425,26 +470,12 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
       }
     }
     if (cs >= K || lb * shrink > ubest) break;      // every remaining centroid has W^2 > ubest
-    const double* xk = xc + (int64_t)cs * m * d;
-    for (int e = lane; e < m * mk; e += 32) {
-      const int i = e / mk, j = e - i * mk;
-      double a = 0.0;
-      if (Dtab) {
-        const int sa = xs[(int64_t)cs * m + i], sb = Ysym[j];
-        if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
-        else a = Dtab[(int64_t)sa * V + sb];
-      } else {
-        for (int t = 0; t < d; ++t) {
-          const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
-          a += df * df;
-        }
-      }
-      C[e] = a;
-    }
+    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err);
     __syncwarp();
     const double* wn = wc + (int64_t)cs * m;
     double dlb, dub;
     dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
+    ++nvisit;
     ubest = fmin(ubest, dub * grow);
     if (lane == 0) {
       LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
@@ -483,22 +514,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     if (lbs > best || (lbs == best && cs > bc)) break;            // no remaining centroid can win
     if (lane == 0) solved[cs >> 5] |= 1u << (cs & 31);
     // cost matrix C_ij = |x_ci - y_j|^2, difference form in fp64
-    const double* xk = xc + (int64_t)cs * m * d;
-    for (int e = lane; e < m * mk; e += 32) {
-      const int i = e / mk, j = e - i * mk;
-      double a = 0.0;
-      if (Dtab) {
-        const int sa = xs[(int64_t)cs * m + i], sb = Ysym[j];
-        if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
-        else a = Dtab[(int64_t)sa * V + sb];
-      } else {
-        for (int t = 0; t < d; ++t) {
-          const double df = xk[(int64_t)i * d + t] - (double)Yk[(int64_t)j * d + t];
-          a += df * df;
-        }
-      }
-      C[e] = a;
-    }
+    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err);
     __syncwarp();
     // relaxed-marginal lower bounds
     const double* wn = wc + (int64_t)cs * m;
@@ -527,6 +543,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     labels[k] = bc;
     if (best_out) best_out[k] = best;
     atomicAdd(n_exact, (unsigned long long)nsolve);
+    atomicAdd(n_exact + 2, (unsigned long long)nvisit);   // scal[3]: phase-A candidates (statistics)
   }
 }
 
