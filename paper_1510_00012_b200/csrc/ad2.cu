@@ -977,16 +977,20 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
     CU(ctx->tmp_out.reserve(bytes));
     dst = ctx->tmp_out.p;
   }
+  // variant 2 keeps Lambda pre-scaled by kx (ad2_tma.cuh): undo it on read-back
+  const bool lam_scaled = which == AD2_LAMBDA && ctx->variant == 2;
   if (ctx->N > 0) {
     const unsigned grid = (unsigned)((ctx->N + 3) / 4);
     if (ctx->dtype == AD2_F64)
       k_scatter_plans<double><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                              ctx->d_orig_off.as<int64_t>(), (const double*)src->p,
-                                                             (double*)dst, ctx->N, ctx->m, ctx->ld);
+                                                             (double*)dst, ctx->N, ctx->m, ctx->ld, ctx->mem_cl.as<int32_t>(),
+                                                             lam_scaled ? ctx->kx.as<double>() : nullptr);
     else
       k_scatter_plans<float><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                             ctx->d_orig_off.as<int64_t>(), (const float*)src->p,
-                                                            (float*)dst, ctx->N, ctx->m, ctx->ld);
+                                                            (float*)dst, ctx->N, ctx->m, ctx->ld, ctx->mem_cl.as<int32_t>(),
+                                                            lam_scaled ? ctx->kx.as<float>() : nullptr);
     CHK(launch_check(ctx, "k_scatter_plans"));
   }
   if (where == AD2_HOST) {

@@ -35,12 +35,15 @@ template <> struct Num<float> {
   static __device__ __forceinline__ void st(float* p, float v) { __stcs(p, v); }
   // fp32 normalisations: MUFU reciprocal based quotient (<= 2 ulp), far inside the fp32 parity bar
   static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+  // kx * rho for kx = log2(e)/rho: the scale of a pre-scaled Lambda's dual step
+  static __device__ __forceinline__ float kappa() { return 1.4426950408889634f; }
 };
 template <> struct Num<double> {
   static __device__ __forceinline__ double ex(double a) { return exp(a); }
   static __device__ __forceinline__ double ld(const double* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(double* p, double v) { __stcs(p, v); }
   static __device__ __forceinline__ double div(double a, double b) { return a / b; }
+  static __device__ __forceinline__ double kappa() { return 1.0; }
 };
 
 template <typename T>
@@ -607,7 +610,8 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
                 const int64_t* __restrict__ orig_off, const T* __restrict__ src, T* __restrict__ dst,
-                int64_t N, int m, int ld) {
+                int64_t N, int m, int ld, const int32_t* __restrict__ mem_cl, const T* __restrict__ unscale) {
+  // unscale != nullptr: divide by unscale[cluster] (the pre-scaled Lambda of variant 2)
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
@@ -615,9 +619,10 @@ k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ o
   const int64_t ne = (int64_t)m * (off[s + 1] - off[s]);
   const T* a = src + (int64_t)ld * off[s];
   T* b = dst + (int64_t)m * orig_off[k];
+  const T sc = unscale ? unscale[mem_cl[s]] : T(1);
   for (int64_t e = lane; e < ne; e += 32) {
     const int64_t j = e / m, i = e - j * m;
-    b[e] = a[j * ld + i];
+    b[e] = unscale ? a[j * ld + i] / sc : a[j * ld + i];
   }
 }
 

@@ -134,8 +134,13 @@ k_badmm_tma(const IterArgs<T> a) {
   const T rho = a.rho[c];
   const T eps_r = rowok ? a.eps : T(0);
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
-  const T2 kx2 = PR::make(kx, kx), nkx2 = PR::make(-kx, -kx), rho2 = PR::make(rho, rho);
-  const T2 nrho2 = PR::make(-rho, -rho), eps2 = PR::make(eps_r, eps_r);
+  // Lambda is stored pre-scaled, L' = Lambda * kx (kx = log2(e)/rho for fp32, 1/rho for fp64), so
+  // exp(Lambda/rho) = ex(L') and Eq.badmm2 becomes L' += kappa (Pi1 - Pi2) with kappa = kx * rho
+  // (log2(e) or 1); ad2_get_plans divides by kx on read-back
+  (void)rho;
+  const T kap = N::kappa();
+  const T2 nkx2 = PR::make(-kx, -kx), rho2 = PR::make(kap, kap);
+  const T2 nrho2 = PR::make(-kap, -kap), eps2 = PR::make(eps_r, eps_r);
   // cost C_ij = (|x_i|^2 + |y_j|^2) + sum_t (-2 x_it) y_jt, coordinates taken in pairs
   T2 xn2[DP / 2];
   T xx = T(0);
@@ -265,8 +270,7 @@ k_badmm_tma(const IterArgs<T> a) {
         if constexpr (MODE == P1ONLY) {
           q2[jp] = p2[jp];                                             // Pi2^(0)
         } else {
-          const T2 ar = PR::mul(l2[jp], kx2);
-          const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
+          const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
           q2[jp] = PR::mul(p2[jp], e);
           racc[h] = PR::add(racc[h], q2[jp]);
         }
@@ -338,7 +342,7 @@ k_badmm_tma(const IterArgs<T> a) {
             l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
           }
           const T2 cst = PR::make(c2[2 * h].x + c2[2 * h].y, c2[2 * h + 1].x + c2[2 * h + 1].y);
-          const T2 ar = PR::mul(PR::add(cst, l2[jp]), nkx2);
+          const T2 ar = PR::fma(cst, nkx2, PR::make(-l2[jp].x, -l2[jp].y));   // -(C kx + L')
           const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
           p2[jp] = PR::fma(q, e, eps2);                                    // pt2 (column j >= m_k: finite)
         }
@@ -389,8 +393,7 @@ k_badmm_tma(const IterArgs<T> a) {
           const int jp = 2 * jb + h, j = 2 * jp;
           const T2 fj = (E == 4) ? fp[h] : *reinterpret_cast<const T2*>(&fbuf[seg * MK + j]);
           p2[jp] = PR::mul(p2[jp], fj);
-          const T2 ar = PR::mul(l2[jp], kx2);
-          const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
+          const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
           racc2[h] = PR::fma(p2[jp], e, racc2[h]);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
