@@ -978,7 +978,7 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
     dst = ctx->tmp_out.p;
   }
   // variant 2 keeps Lambda pre-scaled by kx (ad2_tma.cuh): undo it on read-back
-  const bool lam_scaled = which == AD2_LAMBDA && ctx->variant == 2;
+  const bool lam_scaled = which == AD2_LAMBDA && (ctx->variant == 2 || ctx->variant == 3);
   if (ctx->N > 0) {
     const unsigned grid = (unsigned)((ctx->N + 3) / 4);
     if (ctx->dtype == AD2_F64)

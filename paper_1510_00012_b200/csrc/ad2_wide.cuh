@@ -64,8 +64,11 @@ k_badmm_wide(const IterArgs<float> a) {
   const float kx = a.kx[c], rho = a.rho[c];
   const float eps_r = rowok ? a.eps : 0.f;
   const float wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + ig] : 0.f;
-  const float2 kx2 = make_float2(kx, kx), nkx2 = make_float2(-kx, -kx);
-  const float2 rho2 = make_float2(rho, rho), nrho2 = make_float2(-rho, -rho);
+  // Lambda pre-scaled: L' = Lambda kx (kx = log2(e)/rho), dual step kappa = kx rho = log2(e)
+  (void)rho;
+  const float kap = N::kappa();
+  const float2 nkx2 = make_float2(-kx, -kx);
+  const float2 rho2 = make_float2(kap, kap), nrho2 = make_float2(-kap, -kap);
   const float2 eps2 = make_float2(eps_r, eps_r);
   float accw = 0.f, accm = 0.f;
   float2 accx[(MODE == P2ONLY) ? DP / 2 : 1];                     // coordinate pairs (FFMA2)
@@ -133,8 +136,8 @@ k_badmm_wide(const IterArgs<float> a) {
     float* const Ls = Ps + WMP * mk;
     const float* const Cs = Ls + WMP * mk;                         // C (P2ONLY: Y rows, stride dy)
 
-    // ---- sweep A (phase 2 of iteration t-1): pe = Pi1 exp(Lambda/rho) (Eq.badmmc1b without eps),
-    //      row mass r = sum_j pe_j + m_k eps; Ps <- pe, Ls <- Lambda + rho Pi1
+    // ---- sweep A (phase 2 of iteration t-1): row mass r = sum_j Pi1 exp(Lambda/rho) + m_k eps
+    //      (Eq.badmmc1b; Lambda is stored pre-scaled, L' = Lambda kx, so exp(Lambda/rho) = ex(L'))
     float f = 0.f;
     if constexpr (MODE != P1ONLY) {
       float2 racc = make_float2(0.f, 0.f);
@@ -144,33 +147,24 @@ k_badmm_wide(const IterArgs<float> a) {
         const int e0 = j * WMP + ig, e1 = e0 + WMP;
         const float2 p = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
         const float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
-        const float2 ar = __fmul2_rn(l, kx2);
-        const float2 q = __fmul2_rn(p, make_float2(N::ex(ar.x), N::ex(ar.y)));
-        const float2 lp = __ffma2_rn(rho2, p, l);
-        racc = __fadd2_rn(racc, q);
-        Ps[e0] = q.x;
-        Ls[e0] = lp.x;
-        if (v1) {
-          Ps[e1] = q.y;
-          Ls[e1] = lp.y;
-        }
+        racc = __ffma2_rn(p, make_float2(N::ex(l.x), N::ex(l.y)), racc);
       }
       const float r = (racc.x + racc.y) + (float)mk * eps_r;
-      f = rowok ? wi / r : 0.f;                                      // Eq.badmmc1: w_i / row mass
+      f = rowok ? __fdividef(wi, r) : 0.f;                           // Eq.badmmc1: w_i / row mass
     }
     const float2 f2 = make_float2(f, f), ef2 = make_float2(eps_r * f, eps_r * f);
 
     if constexpr (MODE == P2ONLY) {
-      // ---- sweep B2: Pi2 = (pe + eps) w_i / r (Eq.badmmc1), Lambda -= rho Pi2 (Eq.badmm2),
+      // ---- sweep B2: Pi2 = (pe + eps) w_i / r (Eq.badmmc1), L' += kappa (Pi1 - Pi2) (Eq.badmm2),
       //      support-update partials sum_j pi2_ij y_j, sum_j pi2_ij (Eq.updatex, X5)
 #pragma unroll 2
       for (int j = 0; j < mk; ++j) {
         const int e0 = j * WMP + ig;
-        const float q = fmaf(Ps[e0], f, eps_r * f);
+        const float p = Ps[e0], l = Ls[e0];
+        const float q = fmaf(p * N::ex(l), f, eps_r * f);
         const float2 q2 = make_float2(q, q);
-        const float l = fmaf(-rho, q, Ls[e0]);
         Ps[e0] = q;
-        Ls[e0] = l;
+        Ls[e0] = fmaf(-kap, q, fmaf(kap, p, l));
         accm += q;
         const float* yj = Cs + j * dy;
 #pragma unroll
@@ -185,20 +179,22 @@ k_badmm_wide(const IterArgs<float> a) {
       fence_proxy_async_smem();
       pair_sync(bar_id);
     } else {
-      // ---- sweep B: (FUSED) Pi2 = (pe + eps) f, Lambda^{n+1} = (Lambda + rho Pi1) - rho Pi2;
-      //      pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b) -> Ps
+      // ---- sweep B: (FUSED) Pi2 = (Pi1 exp(Lambda/rho) + eps) f (Eq.badmmc1, pe recomputed),
+      //      L' += kappa (Pi1 - Pi2) (Eq.badmm2); pt2 = Pi2 exp(-(C + Lambda)/rho) + eps
+      //      (Eq.badmmc0b) = Pi2 ex(-(C kx + L')) + eps -> Ps
 #pragma unroll 4
       for (int j = 0; j < mk; j += 2) {
         const bool v1 = j + 1 < mk;
         const int e0 = j * WMP + ig, e1 = e0 + WMP;
-        float2 q = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
+        const float2 p = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
         float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
         const float2 cst = make_float2(Cs[e0], v1 ? Cs[e1] : 0.f);
+        float2 q = p;                                                  // P1ONLY: Pi2^(0)
         if constexpr (MODE == FUSED) {
-          q = __ffma2_rn(q, f2, ef2);
-          l = __ffma2_rn(nrho2, q, l);
+          q = __ffma2_rn(__fmul2_rn(p, make_float2(N::ex(l.x), N::ex(l.y))), f2, ef2);
+          l = __ffma2_rn(nrho2, q, __ffma2_rn(rho2, p, l));
         }
-        const float2 ar = __fmul2_rn(__fadd2_rn(cst, l), nkx2);
+        const float2 ar = __ffma2_rn(cst, nkx2, make_float2(-l.x, -l.y));
         const float2 pt = __ffma2_rn(q, make_float2(N::ex(ar.x), N::ex(ar.y)), eps2);
         Ps[e0] = pt.x;
         if (MODE == FUSED) Ls[e0] = l.x;
@@ -221,7 +217,7 @@ k_badmm_wide(const IterArgs<float> a) {
           s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
         }
         const float s = (s0.x + s0.y) + (s1.x + s1.y);
-        fbuf[jc] = om_j / s;                                           // Eq.badmmc0: w_j^(k) / colsum
+        fbuf[jc] = __fdividef(om_j, s);                                // Eq.badmmc0: w_j^(k) / colsum
       }
       pair_sync(bar_id);
       // ---- sweep C: Pi1 = pt2 * factor_j -> Ps; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row mass
@@ -234,8 +230,7 @@ k_badmm_wide(const IterArgs<float> a) {
         const float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
         const float2 fj = make_float2(fbuf[j], v1 ? fbuf[j + 1] : 0.f);
         const float2 p1 = __fmul2_rn(pt, fj);
-        const float2 ar = __fmul2_rn(l, kx2);
-        racc = __ffma2_rn(p1, make_float2(N::ex(ar.x), N::ex(ar.y)), racc);
+        racc = __ffma2_rn(p1, make_float2(N::ex(l.x), N::ex(l.y)), racc);
         Ps[e0] = p1.x;
         if (v1) Ps[e1] = p1.y;
       }
@@ -248,7 +243,7 @@ k_badmm_wide(const IterArgs<float> a) {
       pair_sync(bar_id);
       R = Rw[0] + Rw[1];
       if (rowok) {
-        const float wt = r2 / R;                                       // normalised row mass
+        const float wt = __fdividef(r2, R);                            // normalised row mass
         accw += (a.rule == 1) ? sqrtf(wt) : wt;
         bad |= !isfinite(wt);
       }
