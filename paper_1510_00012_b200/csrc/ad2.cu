@@ -105,7 +105,7 @@ struct ad2_ctx_s {
   int d = 0, m = 0, K = 0, rule = 0;
   double rho0 = 2.0, eps = 1e-16;
   int64_t N = 0, n = 0, n_items = 0;
-  int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;
+  int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;   // wcfg: rows per member block of variant 3
   int cost_mode = 0;                 // ad2_cost_mode
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
@@ -232,12 +232,11 @@ static size_t tma_bytes(ad2_dtype dt, int mp, int nch, int dp) {
 template <typename T, int MP>
 void launch_warp(int variant, int mode, int nch, int dp, const IterArgs<T>& a, int64_t n_items, cudaStream_t s);
 // variant 3 (inst_f32_wide.cu)
-int wide_cfg();
 int wide_npair(int cfg);
 size_t wide_cta_bytes(int cfg);
 void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s);
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
-                      float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
+                      float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s);
 void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
                     float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
 
@@ -316,7 +315,7 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
     if (ctx->variant == 3) {
       launch_cost_tile(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
                        ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
-                       with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->n_items, s);
+                       with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->ld, ctx->n_items, s);
       return launch_check(ctx, "k_cost_tile");
     }
   }
@@ -546,8 +545,11 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
 
   // ---- kernel variant
   //   2: TMA-staged fused warp kernel, cost recomputed in-kernel (m <= 32, m_k <= MK, d <= 16)
-  //   1: fused warp kernel with direct loads and a cost cache (m <= 32, m_k <= MK, d <= 64, fp32)
-  //   0: generic one-thread-per-member kernels (anything else)
+  //   3: TMA-staged warp-group kernel (ad2_wide.cuh) with a cost cache, fp32, m <= 64, m_k <= 64,
+  //      d <= 64 when variant 2 does not fit: one warp per member (ld 32) for m <= 32, a warp
+  //      pair (ld 64) for m <= 64; also every symbolic (cost-table) round with those sizes
+  //   0: generic one-thread-per-member kernels (anything else, e.g. fp64 with m > 32)
+  //   (1: the direct-load warp kernel with a cost cache is no longer selected)
   int variant = 0, mp = 0, nch = 0, dp = 0;
   const int E = (int)(16 / es);
   for (int cand : {8, 16, 32}) {
@@ -556,48 +558,35 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
       if (d <= 16) {
         variant = 2;
         dp = d <= 3 ? 4 : 16;
-      } else if (b->dtype == AD2_F32 && d <= 64) {
-        variant = 1;
-        dp = 64;
-      } else {
-        break;
+        mp = cand;
+        nch = mkmax <= cand ? 1 : 2;
       }
-      mp = cand;
-      nch = mkmax <= cand ? 1 : 2;
       break;
     }
   }
   if (variant == 2) {                       // the staged pipeline must fit the SM's shared memory
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-    if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) {
-      if (b->dtype == AD2_F32 && d <= 64) {
-        variant = 1;
-        dp = d <= 4 ? 4 : (d <= 16 ? 16 : 64);
-      } else {
-        variant = 0;
-      }
-    }
+    if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) variant = 0;
   }
-  //   3: warp-pair fused kernel (ad2_wide.cuh) with a cost cache for m <= 64, m_k <= 64, d <= 64, fp32
-  //      (taken when none of the above fits)
   int wcfg = 0;
   if (variant == 0 && b->dtype == AD2_F32 && m <= 64 && mkmax <= 64 && d <= 64) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-    wcfg = wide_cfg();
-    if (wide_cta_bytes(wcfg) <= (size_t)optin) {
+    const int wm = m <= 32 ? 32 : 64;
+    if (wide_cta_bytes(wm) <= (size_t)optin) {
       variant = 3;
-      mp = 64;
+      wcfg = wm;
+      mp = wm;
       nch = 1;
       dp = d <= 16 ? 16 : 64;
     }
   }
-  if (prm->cost_mode == AD2_COST_TC_BF16 && variant != 3)
+  if (prm->cost_mode == AD2_COST_TC_BF16 && !(variant == 3 && mp == 64))
     return ctx->fail(AD2_ERR_ARG, "cost_mode 1 (bf16 tensor-core cost) needs the cached-cost warp-pair kernel "
-                     "(fp32, m <= 64, m_k <= 64, d <= 64, and m > 32, m_k > 32 or d > 16)");
+                     "(fp32, 32 < m <= 64, m_k <= 64, d <= 64)");
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
-  // variant 3: blocks padded to 64 rows; Y rows padded with zeros to a multiple of 4
+  // variant 3: blocks padded to WM (32 / 64) rows; Y rows padded with zeros to a multiple of 4
   const int ld = (variant == 2 || variant == 3) ? mp : m;
   const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : (variant == 3 ? (d + 3) / 4 * 4 : d);
   if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");

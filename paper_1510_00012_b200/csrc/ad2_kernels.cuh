@@ -70,20 +70,7 @@ struct IterArgs {
   T eps;
 };
 
-// ---------------------------------------------------------------------------------------------
-// Fused warp-per-member iteration kernel.  One warp holds G = 32/MP members at once, lane
-// (seg, i) = row i of member seg; a row lives in registers (MK = MP*NCH columns, predicated to
-// j < m_k).  Row sums are lane-local; column sums use a transpose-reduce butterfly inside the
-// MP-lane segment (MP-1 shuffles per MP columns).
-//
-//   MODE P1ONLY (first iteration of a step): Pi2 = Q, Lambda = L ->
-//            Eq.badmmc0b/c0 -> P = Pi1;  Eq.badmmc1b row masses -> pw
-//   MODE FUSED  (iterations 2..n): phase 2 of iteration t-1 (Eq.badmmc1 with the consensus w
-//            of t-1, Eq.badmm2) then phase 1 of iteration t; P, L rewritten in place.
-//            pt^(1) of t-1 is recomputed from (Pi1, Lambda^{t-2}) instead of being stored.
-//   MODE P2ONLY (end of a step): phase 2 only -> Q = Pi2, L = Lambda, and the support-update
-//            partials sum_j pi2_ij y_j, sum_j pi2_ij -> px.
-// ---------------------------------------------------------------------------------------------
+// 16-byte vectors of the element type (shared-memory tiles, staged rows)
 template <typename T> struct Vec16;
 template <> struct Vec16<float> {
   using type = float4;
@@ -93,180 +80,6 @@ template <> struct Vec16<double> {
   using type = double2;
   static __device__ __forceinline__ double hsum(double2 v) { return v.x + v.y; }
 };
-
-template <typename T, int MP, int NCH, int MODE, int DP>
-__global__ void __launch_bounds__(NWARP * 32)
-k_badmm_warp(const IterArgs<T> a) {
-  using N = Num<T>;
-  using V = typename Vec16<T>::type;
-  constexpr int G = 32 / MP;
-  constexpr int MK = MP * NCH;
-  constexpr int E = 16 / (int)sizeof(T);      // elements per 16-byte shared-memory chunk
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seg = lane / MP, i = lane - seg * MP;
-  const int item = blockIdx.x;
-  const int c = a.item_cl[item];
-  const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
-  const int m = a.m;
-  const bool rowok = i < m;
-  const T kx = a.kx[c];
-  const T rho = a.rho[c];
-  const T eps = a.eps;
-  const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
-  T accw = T(0);
-  T accm = T(0);
-  T accx[DP];
-#pragma unroll
-  for (int t = 0; t < DP; ++t) accx[t] = T(0);
-  bool bad = false;
-
-  for (int64_t k0 = mb + (int64_t)warp * G; k0 < me; k0 += NWARP * G) {   // warp-uniform
-    const int64_t k = k0 + seg;
-    const bool has = k < me;
-    const int64_t o0 = has ? a.off[k] : 0;
-    const int mk = has ? (int)(a.off[k + 1] - o0) : 0;
-    const int64_t base = (int64_t)m * o0 + i;
-    T p[MK], l[MK], q[MK];
-#pragma unroll
-    for (int j = 0; j < MK; ++j) {
-      const bool ok = rowok && j < mk;
-      const int64_t e = base + (int64_t)j * m;
-      p[j] = ok ? N::ld((MODE == P1ONLY ? a.Q : a.P) + e) : T(0);
-      l[j] = ok ? N::ld(a.L + e) : T(0);
-    }
-    if constexpr (MODE == P1ONLY) {
-#pragma unroll
-      for (int j = 0; j < MK; ++j) q[j] = p[j];            // Pi2^(0)
-    } else {
-      // ---- phase 2 of the previous iteration: pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b),
-      //      Pi2 = pt1 / rowsum * w_i (Eq.badmmc1), Lambda += rho (Pi1 - Pi2) (Eq.badmm2)
-      T r = T(0);
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        q[j] = ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
-        r += q[j];
-      }
-      const T f = (has && rowok) ? wi / r : T(0);
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        q[j] = q[j] * f;
-        if (ok) l[j] = l[j] + rho * (p[j] - q[j]);
-      }
-    }
-    if constexpr (MODE == P2ONLY) {
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        const int64_t e = base + (int64_t)j * m;
-        if (ok) { N::st(a.Q + e, q[j]); N::st(a.L + e, l[j]); }
-      }
-      // support-update partials (Eq.updatex with X5): sum_j pi2_ij y_j and sum_j pi2_ij
-      const T* yk = a.Y + o0 * a.d;
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        if (j < mk) {                                      // q[j] = 0 on invalid rows
-          accm += q[j];
-#pragma unroll
-          for (int t = 0; t < DP; ++t)
-            if (t < a.d) accx[t] += q[j] * __ldg(yk + (int64_t)j * a.d + t);
-        }
-      }
-    } else {
-      // ---- phase 1: pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b)
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        const T cst = ok ? N::ld(a.Cc + base + (int64_t)j * m) : T(0);
-        p[j] = ok ? q[j] * N::ex(-(cst + l[j]) * kx) + eps : T(0);
-      }
-      // column sums over the m rows through a per-warp shared tile (row u = column u of a
-      // chunk, 16-byte chunks XOR-swizzled by u so both the scalar writes and the vector
-      // reads are bank-conflict free); lane (seg, u) sums column u of its member.
-      __shared__ __align__(16) T s_tile[NWARP][MP][32];
-      __shared__ __align__(16) T s_f[NWARP][G][MK];
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < MP; ++u)
-          s_tile[warp][u][(((lane / E) ^ (u & 7)) * E) + (lane % E)] = p[ch * MP + u];
-        __syncwarp();
-        T s = T(0);
-#pragma unroll
-        for (int cc = 0; cc < MP / E; ++cc) {
-          const V v = *reinterpret_cast<const V*>(&s_tile[warp][i][((seg * (MP / E) + cc) ^ (i & 7)) * E]);
-          s += Vec16<T>::hsum(v);
-        }
-        const int jc = ch * MP + i;
-        // Eq.badmmc0: Pi1_ij = pt2_ij / colsum_j * w_j^(k)
-        s_f[warp][seg][jc] = (jc < mk) ? __ldg(a.om + o0 + jc) / s : T(0);
-      }
-      __syncwarp();
-      T r2 = T(0);
-#pragma unroll
-      for (int jj = 0; jj < MK; jj += E) {
-        const V fv = *reinterpret_cast<const V*>(&s_f[warp][seg][jj]);
-        const T* fe = reinterpret_cast<const T*>(&fv);
-#pragma unroll
-        for (int u = 0; u < E; ++u) {
-          const int j = jj + u;
-          const bool ok = rowok && j < mk;
-          p[j] = p[j] * fe[u];
-          // Eq.badmmc1b with Lambda^n (X4): pt1 = Pi1 exp(Lambda/rho) + eps; row mass
-          r2 += ok ? p[j] * N::ex(l[j] * kx) + eps : T(0);
-        }
-      }
-      T R = r2;
-#pragma unroll
-      for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
-      if (has && rowok) {
-        const T wt = r2 / R;
-        accw += (a.rule == 1) ? sqrt(wt) : wt;
-        bad |= !isfinite(wt);
-      }
-#pragma unroll
-      for (int j = 0; j < MK; ++j) {
-        const bool ok = rowok && j < mk;
-        const int64_t e = base + (int64_t)j * m;
-        if (ok) {
-          N::st(a.P + e, p[j]);
-          if (MODE == FUSED) N::st(a.L + e, l[j]);
-        }
-      }
-    }
-  }
-  if (bad) atomicOr(a.err, ERR_NONFINITE);
-
-  // fixed-order combination of the warps' / segments' per-row accumulators -> item partial
-  if constexpr (MODE != P2ONLY) {
-    __shared__ T sw[NWARP * G][MP];
-    sw[warp * G + seg][i] = accw;
-    __syncthreads();
-    if (threadIdx.x < m) {
-      T s = T(0);
-#pragma unroll
-      for (int u = 0; u < NWARP * G; ++u) s += sw[u][threadIdx.x];
-      a.pw[(int64_t)item * m + threadIdx.x] = s;
-    }
-  } else {
-    __shared__ T sx[NWARP * G][MP][DP + 1];
-#pragma unroll
-    for (int t = 0; t < DP; ++t) sx[warp * G + seg][i][t] = accx[t];
-    sx[warp * G + seg][i][DP] = accm;
-    __syncthreads();
-    const int d = a.d;
-    for (int v = threadIdx.x; v < m * (d + 1); v += NWARP * 32) {
-      const int ii = v / (d + 1), t = v - ii * (d + 1);
-      const int tt = (t == d) ? DP : t;
-      T s = T(0);
-#pragma unroll
-      for (int u = 0; u < NWARP * G; ++u) s += sx[u][ii][tt];
-      a.px[(int64_t)item * m * (d + 1) + v] = s;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------------------------
 // Generic iteration kernel: any m, m_k, d.  One thread per member (work item = 1 member), state

@@ -1,9 +1,9 @@
 // ad2_wide.cuh — fused B-ADMM iteration kernel for 32 < m <= 64 (variant 3, fp32): a warp PAIR
 // per member.  Modified B-ADMM of AD2-clustering (arXiv 1510.00012, Alg. 4).
 //
-// Member blocks have WMP = 64 rows (ld = 64, rows >= m zero) and m_k <= WMK = 64 columns.  Lane
-// i of warp h of a pair owns centroid row 32h + i for EVERY column of the member, so row sums are
-// lane-local.  The state does not live in registers (a 64-column row would need ~200): the pass
+// Member blocks have WM = 64 (or 32, one warp per member) rows (ld = WM, rows >= m zero) and
+// m_k <= WMK = 64 columns.  Lane i of warp h of a group owns centroid row 32h + i for EVERY
+// column of the member, so row sums are lane-local.  The state does not live in registers (a 64-column row would need ~200): the pass
 // region [P | L | C] of one member is staged by three cp.async.bulk loads into a per-pair ring and
 // the iteration is three column sweeps over shared memory (each entry's intermediate is written
 // back in place), plus a column-sum step in which lane j of the pair reads column j's 64 rows
@@ -23,32 +23,36 @@
 
 namespace ad2k {
 
-constexpr int WMP = 64;     // rows of a member block (ld)
 constexpr int WMK = 64;     // largest m_k
 
-template <int NPAIR, int RING_KB>
+// WM = rows of a member block (ld) = 32 x warps per member group; NPAIR groups per CTA
+template <int WM, int NPAIR, int RING_KB>
 struct WideLayout {
-  static constexpr int RING = RING_KB * 1024 / 4;               // floats per pair
+  static constexpr int RING = RING_KB * 1024 / 4;               // floats per group
   // [ring | fbuf[WMK] | Rw[4] | 2 mbarriers]
   static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + WMK + 4) + 16) + 127) / 128 * 128;
   static constexpr size_t CTA_BYTES = NPAIR * PAIR_BYTES;
-  static_assert(RING >= 3 * WMP * WMK, "ring must hold the largest pass");
+  static_assert(RING >= 3 * WM * WMK, "ring must hold the largest pass");
   static_assert(CTA_BYTES <= 227 * 1024, "shared memory");
 };
 
-__device__ __forceinline__ void pair_sync(int id) {
-  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+template <int WM>
+__device__ __forceinline__ void group_sync(int id) {
+  if constexpr (WM == 64) asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+  else __syncwarp();
 }
 
-template <int NPAIR, int RING_KB, int MODE, int DP>
-__global__ void __launch_bounds__(NPAIR * 64, 1)
+template <int WM, int NPAIR, int RING_KB, int MODE, int DP>
+__global__ void __launch_bounds__(NPAIR * WM, 1)
 k_badmm_wide(const IterArgs<float> a) {
-  using Lay = WideLayout<NPAIR, RING_KB>;
+  constexpr int WMP = WM;
+  constexpr int GW = WM / 32;                                      // warps per member group
+  using Lay = WideLayout<WM, NPAIR, RING_KB>;
   using N = Num<float>;
   constexpr int RING = Lay::RING;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = warp >> 1, h = warp & 1;
+  const int pair = warp / GW, h = warp % GW;
   float* const ring = reinterpret_cast<float*>(smem_raw + (size_t)pair * Lay::PAIR_BYTES);
   float* const fbuf = ring + RING;                                 // Eq.badmmc0 column factors
   float* const Rw = fbuf + WMK;                                    // per-warp row-mass totals
@@ -83,7 +87,7 @@ k_badmm_wide(const IterArgs<float> a) {
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  pair_sync(bar_id);
+  group_sync<WM>(bar_id);
 
   auto member = [&](int t, int64_t& p0) -> int {                  // pair-uniform
     const int64_t k = mb + pair + (int64_t)t * NPAIR;
@@ -131,6 +135,7 @@ k_badmm_wide(const IterArgs<float> a) {
     const int mk = cnp;
     const int jc = ig;                 // the column this lane sums (jc < mk)
     const float om_j = (MODE != P2ONLY && jc < mk) ? __ldg(a.om + cp0 + jc) : 0.f;
+    const float om_j2 = (MODE != P2ONLY && WM == 32 && jc + 32 < mk) ? __ldg(a.om + cp0 + jc + 32) : 0.f;
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     float* const Ps = ring + cbase;
     float* const Ls = Ps + WMP * mk;
@@ -177,7 +182,7 @@ k_badmm_wide(const IterArgs<float> a) {
         }
       }
       fence_proxy_async_smem();
-      pair_sync(bar_id);
+      group_sync<WM>(bar_id);
     } else {
       // ---- sweep B: (FUSED) Pi2 = (Pi1 exp(Lambda/rho) + eps) f (Eq.badmmc1, pe recomputed),
       //      L' += kappa (Pi1 - Pi2) (Eq.badmm2); pt2 = Pi2 exp(-(C + Lambda)/rho) + eps
@@ -203,23 +208,27 @@ k_badmm_wide(const IterArgs<float> a) {
           if (MODE == FUSED) Ls[e1] = l.y;
         }
       }
-      pair_sync(bar_id);
+      group_sync<WM>(bar_id);
       // ---- column sums over the 64 rows (Eq.badmmc0 denominators): lane jc reads its column in
       //      16 chunks of 4 rows, starting at chunk jc mod 16 (4 lanes per bank quad: no conflicts)
-      if (jc < mk) {
-        const float* col = Ps + jc * WMP;
-        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int chn = (u + jc) & 15;
-          const float4 v = *reinterpret_cast<const float4*>(col + 4 * chn);
-          s0 = __fadd2_rn(s0, make_float2(v.x, v.y));
-          s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
+      for (int cj = 0; cj < WMK / WM; ++cj) {                          // WM = 32: two columns per lane
+        const int jcc = jc + cj * WM;
+        if (jcc < mk) {
+          const float* col = Ps + jcc * WMP;
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < WM / 4; ++u) {
+            const int chn = (u + jcc) & (WM / 4 - 1);
+            const float4 v = *reinterpret_cast<const float4*>(col + 4 * chn);
+            s0 = __fadd2_rn(s0, make_float2(v.x, v.y));
+            s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
+          }
+          const float s = (s0.x + s0.y) + (s1.x + s1.y);
+          fbuf[jcc] = __fdividef(cj ? om_j2 : om_j, s);                // Eq.badmmc0: w_j^(k) / colsum
         }
-        const float s = (s0.x + s0.y) + (s1.x + s1.y);
-        fbuf[jc] = __fdividef(om_j, s);                                // Eq.badmmc0: w_j^(k) / colsum
       }
-      pair_sync(bar_id);
+      group_sync<WM>(bar_id);
       // ---- sweep C: Pi1 = pt2 * factor_j -> Ps; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row mass
       float2 racc = make_float2(0.f, 0.f);
 #pragma unroll 4
@@ -238,10 +247,14 @@ k_badmm_wide(const IterArgs<float> a) {
       float R = r2;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
-      if (lane == 0) Rw[h] = R;
       fence_proxy_async_smem();
-      pair_sync(bar_id);
-      R = Rw[0] + Rw[1];
+      if constexpr (WM == 64) {
+        if (lane == 0) Rw[h] = R;
+        group_sync<WM>(bar_id);
+        R = Rw[0] + Rw[1];
+      } else {
+        __syncwarp();
+      }
       if (rowok) {
         const float wt = __fdividef(r2, R);                            // normalised row mass
         accw += (a.rule == 1) ? sqrtf(wt) : wt;
@@ -294,7 +307,7 @@ template <int DMAX>
 __global__ void __launch_bounds__(256)
 k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
             const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
-            float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
+            float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy, int ld) {
   __shared__ __align__(16) float xs[DMAX][68];       // x_c^T (coordinate-major, padded rows)
   __shared__ __align__(16) float ys[DMAX][68];       // chunk of 64 points, coordinate-major
   __shared__ float xx[64], yy[64];
@@ -352,7 +365,7 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int j = 4 * tj + v;
-      if (j < np) {
+      if (j < np && 4 * ti < ld) {
         float4 o;
         float* oe = reinterpret_cast<float*>(&o);
 #pragma unroll
@@ -363,7 +376,7 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
           oe[u] = cv;
           s += cv;
         }
-        *reinterpret_cast<float4*>(Cc + (q0 + j) * 64 + 4 * ti) = o;
+        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + 4 * ti) = o;
       }
     }
     acc += (double)s;

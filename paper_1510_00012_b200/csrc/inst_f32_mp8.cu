@@ -1,7 +1,6 @@
 // inst_f32_mp8.cu — explicit instantiations of the fused B-ADMM iteration kernels for
 // T=float, MP=8 (split per (dtype, MP) so nvcc compiles the template set in parallel).
 //   variant 2: k_badmm_tma  (TMA-staged, cost recomputed; ad2_tma.cuh)
-//   variant 1: k_badmm_warp (direct loads, cached cost; ad2_kernels.cuh)
 #include "ad2_tma.cuh"
 
 namespace ad2k {
@@ -22,23 +21,11 @@ static void go_tma(int mode, const IterArgs<float>& a, int64_t n_items, cudaStre
   else k_badmm_tma<float, 8, NCH, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
 }
 
-template <int NCH, int DP>
-static void go_warp(int mode, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
-  dim3 g((unsigned)n_items), b(NWARP * 32);
-  if (mode == P1ONLY) k_badmm_warp<float, 8, NCH, P1ONLY, 1><<<g, b, 0, s>>>(a);
-  else if (mode == FUSED) k_badmm_warp<float, 8, NCH, FUSED, 1><<<g, b, 0, s>>>(a);
-  else k_badmm_warp<float, 8, NCH, P2ONLY, DP><<<g, b, 0, s>>>(a);
-}
-
 template <int NCH>
 static void go_nch(int variant, int mode, int dp, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
   if (variant == 2) {
     if (dp <= 4) go_tma<NCH, 4>(mode, a, n_items, s);
     else go_tma<NCH, 16>(mode, a, n_items, s);
-  } else {
-    if (dp <= 4) go_warp<NCH, 4>(mode, a, n_items, s);
-    else if (dp <= 16) go_warp<NCH, 16>(mode, a, n_items, s);
-    else go_warp<NCH, 64>(mode, a, n_items, s);
   }
 }
 

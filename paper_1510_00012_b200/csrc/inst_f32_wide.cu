@@ -7,55 +7,52 @@
 
 namespace ad2k {
 
-// (pairs per CTA, ring KB per pair): 0 = (2, 80) one CTA / SM with 4 warps; 1 = (3, 64) 6 warps;
-// 2 = (4, 48) 8 warps (single-buffered: a ring that holds exactly one largest pass)
-template <int NPAIR, int RKB, int DP>
+// (rows per member WM, groups per CTA, ring KB per group): WM = 64 -> (4, 48), one CTA / SM of 8
+// warps with single-pass rings; WM = 32 -> (8, 24), one warp per member, 8 warps / SM
+template <int WM, int NPAIR, int RKB, int DP>
 static void go_wide(int mode, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
-  using Lay = WideLayout<NPAIR, RKB>;
+  using Lay = WideLayout<WM, NPAIR, RKB>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_badmm_wide<NPAIR, RKB, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
-    cudaFuncSetAttribute(k_badmm_wide<NPAIR, RKB, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
-    cudaFuncSetAttribute(k_badmm_wide<NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     attr = true;
   }
-  dim3 g((unsigned)n_items), b(NPAIR * 64);
-  if (mode == P1ONLY) k_badmm_wide<NPAIR, RKB, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
-  else if (mode == FUSED) k_badmm_wide<NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
-  else k_badmm_wide<NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  dim3 g((unsigned)n_items), b(NPAIR * WM);
+  if (mode == P1ONLY) k_badmm_wide<WM, NPAIR, RKB, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == FUSED) k_badmm_wide<WM, NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else k_badmm_wide<WM, NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+}
+
+template <int WM, int NPAIR, int RKB>
+static void go_wide_d(int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
+  if (d <= 16) go_wide<WM, NPAIR, RKB, 16>(mode, a, n_items, s);
+  else go_wide<WM, NPAIR, RKB, 64>(mode, a, n_items, s);
 }
 
 }  // namespace ad2k
 
 using namespace ad2k;
 
-int wide_cfg() {
-  const char* e = getenv("AD2_WIDE_CFG");
-  return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
-}
-int wide_npair(int cfg) { return cfg == 1 ? 3 : cfg == 2 ? 4 : 2; }
-size_t wide_cta_bytes(int cfg) {
-  return cfg == 1 ? WideLayout<3, 64>::CTA_BYTES : cfg == 2 ? WideLayout<4, 48>::CTA_BYTES : WideLayout<2, 80>::CTA_BYTES;
+// cfg = rows per member block (32 or 64)
+int wide_cfg() { return 64; }
+int wide_npair(int wm) { return wm == 32 ? 8 : 4; }
+size_t wide_cta_bytes(int wm) {
+  return wm == 32 ? WideLayout<32, 8, 24>::CTA_BYTES : WideLayout<64, 4, 48>::CTA_BYTES;
 }
 
-template <int NPAIR, int RKB>
-static void go_wide_d(int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
-  if (d <= 16) go_wide<NPAIR, RKB, 16>(mode, a, n_items, s);
-  else go_wide<NPAIR, RKB, 64>(mode, a, n_items, s);
-}
-
-void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
+void launch_wide(int wm, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
-  if (cfg == 1) go_wide_d<3, 64>(mode, d, a, n_items, s);
-  else if (cfg == 2) go_wide_d<4, 48>(mode, d, a, n_items, s);
-  else go_wide_d<2, 80>(mode, d, a, n_items, s);
+  if (wm == 32) go_wide_d<32, 8, 24>(mode, d, a, n_items, s);
+  else go_wide_d<64, 4, 48>(mode, d, a, n_items, s);
 }
 
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
-                      float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
+                      float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
-  if (d <= 16) k_cost_tile<16><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
-  else k_cost_tile<64><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
+  if (d <= 16) k_cost_tile<16><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
+  else k_cost_tile<64><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
 }
 
 void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,

@@ -94,9 +94,7 @@ def expected_variant(m, mkmax, d, dtype="f32"):
     fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
     if fits and d <= 16:
         return 2
-    if fits and dtype == "f32" and d <= 64:
-        return 1
-    if dtype == "f32" and m <= 64 and mkmax <= 64:
+    if dtype == "f32" and m <= 64 and mkmax <= 64 and d <= 64:
         return 3
     return 0
 
@@ -104,14 +102,18 @@ def expected_variant(m, mkmax, d, dtype="f32"):
 @pytest.mark.parametrize("m,mk,d", [(6, (1, 40), 2), (32, (30, 64), 16), (48, (4, 32), 16), (8, (1, 16), 3),
                                     (12, (10, 32), 5), (20, (1, 32), 7), (32, (1, 4), 16), (3, (1, 3), 1),
                                     (64, (20, 64), 64), (64, (1, 64), 5), (33, (1, 63), 9), (64, (1, 3), 64),
-                                    (40, (60, 64), 64), (64, (1, 80), 3)])
+                                    (40, (60, 64), 64), (64, (1, 80), 3), (32, (1, 64), 32), (16, (1, 30), 24),
+                                    (20, (30, 64), 5), (32, (10, 20), 64)])
 def test_fp32_ragged_shapes(m, mk, d):
     """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
     two-chunk column sums, tiny m_k, the warp-pair kernel (32 < m <= 64 or 32 < m_k <= 64, cached
     cost from the tiled cost build), and the generic kernel (m_k > 64)."""
     b = wl.make_random(500, m, d, K=4, mk_range=mk, seed=7 + m, dtype="f32", T=1, tau=1)
     ctx, _ = compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
-    assert ctx.info()["variant"] == expected_variant(m, int(b.sizes.max()), d)
+    v = expected_variant(m, int(b.sizes.max()), d)
+    assert ctx.info()["variant"] == v
+    if v == 3:                                        # one warp per member (ld 32) or a warp pair (ld 64)
+        assert ctx.info()["mp"] == (32 if m <= 32 else 64)
     compare_round(b, T=12, tau=4, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False)
 
 
