@@ -159,10 +159,16 @@ def run_ours(args, rank, world, local_rank):
              x0=t(b.x0), w0=t(b.w0))
     obj_box = {}
 
+    sched_ev = []                                      # events around step/update (SURVEY.md §8(d) metric)
+
     def step(arr, mem):
         ctx.init(arr["offsets"], arr["supports"], arr["weights"], arr["labels"], arr["x0"], arr["w0"], b.K, b.m,
                  s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype, cost_mode=args.cost_mode)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         ad2.run_schedule(ctx, T, tau)
+        e1.record(stream)
+        sched_ev.append((e0, e1))
         obj_box["obj"] = ctx.objective()               # device -> host read of the result (syncs)
 
     def timed(fn, K, W):
@@ -189,6 +195,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_profiling(True)          # event nodes around every iteration kernel (live, in-graph)
     with ClockSampler(local_rank) as clk:
         ms, launches = timed(lambda: step(D, "device"), args.steps, args.warmup)
+    sched_ms = float(np.mean([a.elapsed_time(z) for a, z in sched_ev[-args.steps:]]))
     launch_ms, step_graph_ms = ctx.prof_read()
     info = ctx.info()
     value = entries_total * T / (ms / 1e3)
@@ -257,6 +264,9 @@ def run_ours(args, rank, world, local_rank):
                      "iteration_kernels_share_of_step": iter_share},
         "iter_only": {"value": entries_total * T / ((np.sum(launch_ms) * T / max(1, len(launch_ms) - 1)) / 1e3),
                       "note": "iteration kernels only (event-timed), excluding consensus/init/objective"},
+        "steps_and_updates": {"value": entries_total * T / (sched_ms / 1e3), "ms": sched_ms,
+                              "note": "SURVEY.md 8(d) definition: ad2_badmm_step + ad2_update_support only "
+                                      "(value above is the whole round incl. init and objective)"},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
