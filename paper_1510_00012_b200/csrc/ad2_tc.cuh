@@ -12,8 +12,8 @@
 //   D = A B^T in TMEM (128 lanes = points x 64 fp32 columns = centroid rows), 4 MMAs of K = 16,
 // then each thread reads its point's 64 accumulators (tcgen05.ld 32x32b) and writes the 64
 // costs (256 contiguous bytes) with |x_i|^2 and |y_p|^2 added in fp32 and the result clamped
-// at 0.  bf16 operands bound the error by |dC| <= 2^-7 |x_i| |y_j| (+ fp32 rounding); the fp32
-// FMA build (k_cost_tile) stays the parity default, this one is params->cost_mode = 1.
+// at 0.  bf16 operands bound the error by |dC| <= 2^-7 |x_i| |y_j| (+ fp32 rounding): this one
+// is params->cost_mode = 1; the parity default is the fp32 FFMA2 tile build (k_cost_tile).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -170,6 +170,193 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
     }
     acc += (double)s;
     // TMEM and the A tile are reused by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  }
+  if (psum) {
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) psum[item] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+}  // namespace ad2k
+
+namespace ad2k {
+
+// ---------------------------------------------------------------------------------------------
+// fp32-accurate tensor-core cost build: 3 x TF32 (tcgen05.mma kind::tf32).  Each operand is split
+// into hi = tf32(v) and lo = tf32(v - hi) (11 + 11 significant bits), and
+//   x . y = x_hi.y_hi + x_hi.y_lo + x_lo.y_hi   (+ x_lo.y_lo, ~2^-22 relative, dropped)
+// is accumulated in fp32 in TMEM: 24 MMAs (3 terms x K = 64 in steps of 8) per 128-point tile.
+// Operands are K-major with the 128-byte swizzle: a 64-element fp32 row spans two 128-byte
+// K-blocks, stored as two [rows][128 B] tiles.  Experimental (AD2_COST_TC32=1): measured on
+// config 4 the accumulation leaves ~2e-6 absolute error (C of coincident points ~1.7e-6), outside
+// the fp32 parity bar, so the FFMA2 tile kernel stays the cost_mode-0 default.
+// ---------------------------------------------------------------------------------------------
+// instruction descriptor, kind::tf32: D fp32, A/B tf32 (format 2), K-major, N = 64, M = 128
+constexpr uint32_t TC32_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+// byte offset of fp32 element (row r, k) in a tile of R rows x 64 k: K-block kb = k / 32 of
+// R x 128 bytes, 8-row swizzle atoms of 1024 bytes, 16-byte chunks XOR-swizzled by the row
+__device__ __forceinline__ uint32_t tc32_off(int R, int r, int k) {
+  const int kb = k >> 5, kin = k & 31;
+  const int chunk = (kin >> 2) ^ (r & 7);
+  return (uint32_t)(kb * R * 128 + (r >> 3) * 1024 + (r & 7) * 128 + chunk * 16 + (kin & 3) * 4);
+}
+
+__device__ __forceinline__ float tf32_rna(float v) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+  return __uint_as_float(u);
+}
+
+__global__ void __launch_bounds__(128)
+k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+            const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
+            float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  // the 128-byte swizzle needs 1024-byte aligned atoms: align the dynamic region by hand
+  unsigned char* tsm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* sAh = tsm;                          // 128 x 64 fp32 = 32 KB each
+  unsigned char* sAl = tsm + 32768;
+  unsigned char* sBh = tsm + 65536;                  // 64 x 64 fp32 = 16 KB each
+  unsigned char* sBl = tsm + 81920;
+  __shared__ float xx[64], yy[128];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ double red[4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(tc_smem(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // B = x_c split into tf32 hi / lo (rows >= m and coordinates >= d are zero); |x_i|^2 in fp32
+  for (int v = tid; v < 64 * 16; v += 128) {
+    const int r = v >> 4, k0 = (v & 15) * 4;
+    float4 h, l;
+    float* he = reinterpret_cast<float*>(&h);
+    float* le = reinterpret_cast<float*>(&l);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float val = (r < m && k0 + u < d) ? x[((int64_t)c * m + r) * d + k0 + u] : 0.f;
+      he[u] = tf32_rna(val);
+      le[u] = tf32_rna(val - he[u]);
+    }
+    *reinterpret_cast<float4*>(sBh + tc32_off(64, r, k0)) = h;
+    *reinterpret_cast<float4*>(sBl + tc32_off(64, r, k0)) = l;
+  }
+  if (tid < 64) {
+    float s = 0.f;
+    for (int k = 0; k < d; ++k) {
+      const float v = tid < m ? x[((int64_t)c * m + tid) * d + k] : 0.f;
+      s = fmaf(v, v, s);
+    }
+    xx[tid] = s;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  uint32_t phase = 0;
+  for (int64_t q0 = p_beg; q0 < p_end; q0 += 128) {
+    const int np = (int)((p_end - q0) < 128 ? (p_end - q0) : 128);
+    // A = Y tile split into tf32 hi / lo: 16 threads per point row, 4 coordinates each
+    for (int v = tid; v < 128 * 16; v += 128) {
+      const int r = v >> 4, k0 = (v & 15) * 4;
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < np && k0 < d) f = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0
+      float s = fmaf(f.x, f.x, fmaf(f.y, f.y, fmaf(f.z, f.z, f.w * f.w)));
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((v & 15) == 0) yy[r] = s;
+      const float4 h = make_float4(tf32_rna(f.x), tf32_rna(f.y), tf32_rna(f.z), tf32_rna(f.w));
+      const float4 l = make_float4(tf32_rna(f.x - h.x), tf32_rna(f.y - h.y), tf32_rna(f.z - h.z), tf32_rna(f.w - h.w));
+      *reinterpret_cast<float4*>(sAh + tc32_off(128, r, k0)) = h;
+      *reinterpret_cast<float4*>(sAl + tc32_off(128, r, k0)) = l;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned char* As[3] = {sAh, sAh, sAl};
+      const unsigned char* Bs[3] = {sBh, sBl, sBh};
+      int first = 1;
+#pragma unroll
+      for (int term = 0; term < 3; ++term) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {             // K = 8 tf32 (32 bytes) per MMA
+          const int kb = kk >> 2, kin = kk & 3;
+          const uint64_t da = tc_desc_sw128(tc_smem(As[term] + kb * 128 * 128)) + (uint64_t)(2 * kin);
+          const uint64_t db = tc_desc_sw128(tc_smem(Bs[term] + kb * 64 * 128)) + (uint64_t)(2 * kin);
+          const uint32_t accum = first ? 0u : 1u;
+          first = 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(TC32_IDESC), "r"(accum));
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       tc_smem(&mbar))
+                   : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\nTW%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra.uni TW%=;\n}" ::"r"(tc_smem(&mbar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int p = 32 * warp + lane;
+    const float yp = yy[p];
+    float s = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * h);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (p < np) {
+        float4* dst = reinterpret_cast<float4*>(Cc + (q0 + p) * 64 + 32 * h);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 32 * h + 4 * u + e;
+            const float dot = __uint_as_float(r[4 * u + e]);
+            o[e] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yp), 0.f) : 0.f;
+            s += o[e];
+          }
+          dst[u] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
+    acc += (double)s;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
   }

@@ -60,3 +60,16 @@ void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, 
   if (n_items == 0) return;
   k_cost_tc<<<(unsigned)n_items, 128, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
 }
+
+// fp32-accurate 3 x TF32 tensor-core cost build (ld 64)
+void launch_cost_tc32(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                      float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
+  if (n_items == 0) return;
+  constexpr int SMEM = 98304 + 1024;             // + alignment slack
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_cost_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  k_cost_tc32<<<(unsigned)n_items, 128, SMEM, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
+}
