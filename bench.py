@@ -133,7 +133,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------------ ours
 
-def run_ours(args, rank, world, local_rank):
+def run_ours(args, rank, world, local_rank, dist_on=False):
     import torch
     import torch.distributed as dist
     from paper_1510_00012_b200 import ad2
@@ -141,17 +141,17 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    barrier = (lambda: dist.barrier(device_ids=[local_rank])) if world > 1 else (lambda: None)
+    barrier = (lambda: dist.barrier(device_ids=[local_rank])) if dist_on else (lambda: None)
     b = load_bundle(args.workload, rank, world, barrier)
     s = b.sched
     T, tau = s.T, s.tau
     bounds = shard_bounds(b.offsets, world)
-    mine = b.subset(np.arange(bounds[rank], bounds[rank + 1])) if world > 1 else b
+    mine = b.subset(np.arange(bounds[rank], bounds[rank + 1])) if dist_on else b
     entries_local = mine.entries()
     entries_total = b.entries()
     stream = torch.cuda.current_stream(dev)
     ctx = ad2.Context(local_rank, stream.cuda_stream)
-    if world > 1:
+    if dist_on:
         bootstrap_nccl(ctx)
 
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -186,7 +186,7 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         ms = e0.elapsed_time(e1) / K
         launches = ctx.info()["launches"] - l0
-        if world > 1:
+        if dist_on:
             x = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             ms = float(x.item())
@@ -335,6 +335,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cost-mode", type=int, default=0, help="0: fp32 cost build, 1: bf16 tcgen05 (cached-cost kernels)")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU path (torch.distributed + NCCL communicator in libad2) even with 1 rank")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -342,13 +344,18 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    dist_on = world > 1 or args.dist
+    if dist_on:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
-    if world > 1:
+    run_ours(args, rank, world, local_rank, dist_on)
+    if dist_on:
         import torch.distributed as dist
         dist.destroy_process_group()
 
