@@ -163,3 +163,24 @@ def test_merge_init_matches_oracle(cfg, N, K, dtype):
             tol = 1e-14 if dtype == "f64" else 1e-6
             np.testing.assert_allclose(w0[c], ow, rtol=tol, atol=tol * 1e-3)
             np.testing.assert_allclose(x0[c], ox, rtol=tol, atol=tol * np.abs(ox).max())
+
+
+def test_next_row_api_errors():
+    """Argument errors of the NEXT-row entry points are reported, not crashed on."""
+    from paper_1510_00012_b200 import ad2
+    b = wl.make_random(20, 4, 2, K=3, mk_range=(2, 5), seed=2, dtype="f32")
+    ctx = ad2.Context(0)
+    bad_off = b.offsets.copy()
+    bad_off[3] = bad_off[2]                                   # a member with m_k = 0
+    with pytest.raises(ad2.AD2Error, match="ARG"):
+        ctx.assign(bad_off, b.supports, b.weights, b.x0, b.w0, mem="host")
+    with pytest.raises(ad2.AD2Error, match="ARG"):
+        ctx.merge_init(b.offsets, b.supports, b.weights, [0, 1, 99], b.K, b.m, mem="host")
+    with pytest.raises(ad2.AD2Error, match="ARG"):              # loop parameters
+        ctx.cluster(b.offsets, b.supports, b.weights, b.labels, b.x0, b.w0, b.K, b.m, 0, 1, 1, mem="host")
+    with pytest.raises(ad2.AD2Error, match="ARG"):              # symbolic round without a cost table
+        ctx.init(b.offsets, np.zeros(int(b.offsets[-1]), np.int32), b.weights, b.labels,
+                 np.zeros((b.K, b.m), np.int32), b.w0, b.K, b.m, mem="host", dtype="f32", cost_mode=ad2.COST_TABLE)
+    # the context still works after the errors
+    lab, w2, _ = ctx.assign(b.offsets, b.supports, b.weights, b.x0, b.w0, mem="host")
+    assert (lab >= 0).all() and (lab < b.K).all() and np.isfinite(w2).all()
