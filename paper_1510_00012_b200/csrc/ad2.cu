@@ -205,6 +205,7 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.x = ctx->x.as<T>();
   a.ld = ctx->ld;
   a.dy = ctx->dy;
+  a.xext = (ctx->variant == 3 && ctx->d > 64) ? 1 : 0;
   a.rho = ctx->rho.as<T>();
   a.kx = ctx->kx.as<T>();
   a.pw = ctx->pw.as<T>();
@@ -239,6 +240,10 @@ void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl
                       float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s);
 void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
                     float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
+void launch_cost_tile_big(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                          float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s);
+void launch_xpart(const int64_t* off, const int64_t* imb, const float* Q, const float* Y, float* px, int m, int d,
+                  int dy, int ld, int parts, int64_t n_items, cudaStream_t s);
 void launch_cost_tc32(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
                       float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s);
 
@@ -324,6 +329,12 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
                        ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
                        with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->n_items, s);
       return launch_check(ctx, "k_cost_tc32");
+    }
+    if (ctx->variant == 3 && ctx->d > 64) {
+      launch_cost_tile_big(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
+                           ctx->Y.as<float>(), ctx->x.as<float>(), ctx->Cc.as<float>(),
+                           with_sum ? ctx->pd.as<double>() : nullptr, ctx->m, ctx->d, ctx->dy, ctx->ld, ctx->n_items, s);
+      return launch_check(ctx, "k_cost_tile_big");
     }
     if (ctx->variant == 3) {
       launch_cost_tile(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
@@ -583,7 +594,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) variant = 0;
   }
   int wcfg = 0;
-  if (variant == 0 && b->dtype == AD2_F32 && m <= 64 && mkmax <= 64 && d <= 64) {
+  if (variant == 0 && b->dtype == AD2_F32 && m <= 64 && mkmax <= 64) {   // any d (d > 64: k_xpart)
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
     const int wm = m <= 32 ? 32 : 64;
@@ -595,7 +606,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
       dp = d <= 16 ? 16 : 64;
     }
   }
-  if (prm->cost_mode == AD2_COST_TC_BF16 && !(variant == 3 && mp == 64))
+  if (prm->cost_mode == AD2_COST_TC_BF16 && !(variant == 3 && mp == 64 && d <= 64))
     return ctx->fail(AD2_ERR_ARG, "cost_mode 1 (bf16 tensor-core cost) needs the cached-cost warp-pair kernel "
                      "(fp32, 32 < m <= 64, m_k <= 64, d <= 64)");
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
@@ -900,6 +911,13 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
 template <typename T>
 static ad2_status update_support_T(ad2_ctx ctx) {
   cudaStream_t s = ctx->stream;
+  if constexpr (sizeof(T) == 4) {
+    if (ctx->variant == 3 && ctx->d > 64) {     // x partials from the Pi2 blocks (the step skipped them)
+      launch_xpart(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->Q.as<float>(), ctx->Y.as<float>(),
+                   ctx->px.as<float>(), ctx->m, ctx->d, ctx->dy, ctx->ld, ctx->parts, ctx->n_items, s);
+      CHK(launch_check(ctx, "k_xpart"));
+    }
+  }
   k_xsum<T><<<ctx->K, 256, 0, s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->d, ctx->Sx.as<T>());
   CHK(launch_check(ctx, "k_xsum"));
   CHK(allreduce(ctx, ctx->Sx.p, (size_t)ctx->K * ctx->m * (ctx->d + 1), nccl_t(ctx), s));

@@ -67,6 +67,7 @@ struct IterArgs {
   int m, d, rule;
   int ld;                  // leading dimension of a member block (rows; >= m)
   int dy;                  // row stride of Y (>= d, zero-padded)
+  int xext;                // 1: the x partials come from k_xpart (d > 64), P2ONLY skips them
   T eps;
 };
 

@@ -97,14 +97,17 @@ k_badmm_wide(const IterArgs<float> a) {
   };
   // pass region [P | L | C] (P2ONLY: [P | L | Y], the supports for the x partials); dy % 4 == 0
   const int dy = a.dy;
-  const int third = (MODE == P2ONLY) ? dy : WMP;                   // floats per point of the 3rd array
+  // P2ONLY with external x partials (d > 64, k_xpart) stages no supports
+  const int third = (MODE == P2ONLY) ? (a.xext ? 0 : dy) : WMP;    // floats per point of the 3rd array
   auto issue = [&](int t, int base, int64_t p0, int np) {          // leader only
     const uint32_t bp = (uint32_t)(WMP * np * 4), b3 = (uint32_t)(third * np * 4);
     float* st = ring + base;
     mbar_expect_tx(&bar[t & 1], 2 * bp + b3);
     tma_load(st, src_plan + (int64_t)WMP * p0, bp, &bar[t & 1]);
     tma_load(st + WMP * np, a.L + (int64_t)WMP * p0, bp, &bar[t & 1]);
-    if (MODE == P2ONLY) tma_load(st + 2 * WMP * np, a.Y + (int64_t)dy * p0, b3, &bar[t & 1]);
+    if (MODE == P2ONLY) {
+      if (b3) tma_load(st + 2 * WMP * np, a.Y + (int64_t)dy * p0, b3, &bar[t & 1]);
+    }
     else tma_load(st + 2 * WMP * np, a.Cc + (int64_t)WMP * p0, b3, &bar[t & 1]);
   };
 
@@ -170,6 +173,7 @@ k_badmm_wide(const IterArgs<float> a) {
         const float2 q2 = make_float2(q, q);
         Ps[e0] = q;
         Ls[e0] = fmaf(-kap, q, fmaf(kap, p, l));
+        if (a.xext) continue;
         accm += q;
         const float* yj = Cs + j * dy;
 #pragma unroll
@@ -288,7 +292,7 @@ k_badmm_wide(const IterArgs<float> a) {
   if constexpr (MODE != P2ONLY) {
     if (rowok) a.pw[part * m + ig] = accw;
   } else {
-    if (rowok) {
+    if (rowok && !a.xext) {
       float* px = a.px + (part * m + ig) * (d + 1);
       px[d] = accm;
 #pragma unroll
@@ -389,6 +393,156 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
       double t = 0.0;
       for (int w = 0; w < 8; ++w) t += red[w];
       psum[item] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// d > 64 (the paper's document embeddings, d = 300-400) for the cached-cost kernels
+// ---------------------------------------------------------------------------------------------
+// Cost build C_ij = |x_i|^2 + |y_j|^2 - 2 x_i.y_j with the coordinates in chunks of 64:
+// per chunk of 64 points, X_c^T and the points' coordinates are staged 64 dims at a time and the
+// 4 x 4 register tiles accumulate across the dim chunks; |x|^2, |y|^2 in fp32.  Rows >= m are 0,
+// rows >= ld not written; per-item double sums for rho.  One CTA (256 threads) per work item.
+__global__ void __launch_bounds__(256)
+k_cost_tile_big(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
+                const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
+                float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy, int ld) {
+  __shared__ __align__(16) float xs[64][68];
+  __shared__ __align__(16) float ys[64][68];
+  __shared__ float xx[64], yy[64];
+  __shared__ double red[8];
+  const int item = blockIdx.x;
+  const int c = item_cl[item];
+  const int tid = threadIdx.x;
+  const int ti = tid & 15, tj = tid >> 4;
+  if (tid < 64) {
+    float s = 0.f;
+    if (tid < m)
+      for (int t = 0; t < d; ++t) {
+        const float v = x[((int64_t)c * m + tid) * d + t];
+        s = fmaf(v, v, s);
+      }
+    xx[tid] = s;
+  }
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  for (int64_t q0 = p_beg; q0 < p_end; q0 += 64) {
+    const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
+    float2 a2[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) a2[u][v] = make_float2(0.f, 0.f);
+    float ysq = 0.f;                                   // |y|^2 of point tid (tid < 64)
+    for (int t0 = 0; t0 < d; t0 += 64) {
+      __syncthreads();                                 // previous chunk consumed
+      for (int v = tid; v < 64 * 64; v += 256) {
+        const int t = v >> 6, i = v & 63;
+        xs[t][i] = (i < m && t0 + t < d) ? x[((int64_t)c * m + i) * d + t0 + t] : 0.f;
+        const int j = v >> 6, tt = v & 63;
+        ys[tt][j] = (j < np && t0 + tt < d) ? Y[(q0 + j) * dy + t0 + tt] : 0.f;
+      }
+      __syncthreads();
+      if (tid < 64)
+        for (int t = 0; t < 64; ++t) ysq = fmaf(ys[t][tid], ys[t][tid], ysq);
+#pragma unroll 4
+      for (int t = 0; t < 64; ++t) {
+        const float4 xv = *reinterpret_cast<const float4*>(&xs[t][4 * ti]);
+        const float4 yv = *reinterpret_cast<const float4*>(&ys[t][4 * tj]);
+        const float2 x01 = make_float2(xv.x, xv.y), x23 = make_float2(xv.z, xv.w);
+        const float ya[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float2 y2 = make_float2(ya[v], ya[v]);
+          a2[0][v] = __ffma2_rn(x01, y2, a2[0][v]);
+          a2[1][v] = __ffma2_rn(x23, y2, a2[1][v]);
+        }
+      }
+    }
+    if (tid < 64) yy[tid] = ysq;
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = 4 * tj + v;
+      if (j < np && 4 * ti < ld) {
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = 4 * ti + u;
+          const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
+          o[u] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yy[j]), 0.f) : 0.f;
+          s += o[u];
+        }
+        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + 4 * ti) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    acc += (double)s;
+  }
+  if (psum) {
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      psum[item] = t;
+    }
+  }
+}
+
+// Support-update partials for d > 64 (Eq.updatex, X5): px[item*parts][i][t] = sum over the
+// item's points j of Pi2_ij y_jt, px[..][i][d] = sum_j Pi2_ij, from the Pi2 blocks (Q,
+// column-major, ld rows, contiguous over the item's points) and the supports.  Tiles of 64 rows x
+// 64 coordinates, points in chunks of 32 staged in shared memory, 4 x 4 register tiles; the
+// item's other part rows are zeroed (k_xsum adds all parts).  One CTA (256 threads) per item.
+__global__ void __launch_bounds__(256)
+k_xpart(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb, const float* __restrict__ Q,
+        const float* __restrict__ Y, float* __restrict__ px, int m, int d, int dy, int ld, int parts) {
+  __shared__ __align__(16) float qs[32][68];           // [point][row]
+  __shared__ __align__(16) float ys[32][68];           // [point][coordinate]
+  const int item = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int ti = tid & 15, tj = tid >> 4;               // rows 4ti.., coordinates 4tj..
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  float* out = px + (int64_t)item * parts * m * (d + 1);
+  for (int e = tid + m * (d + 1); e < parts * m * (d + 1); e += 256) out[e] = 0.f;   // parts 1..
+  for (int t0 = 0; t0 < d + 1; t0 += 64) {              // the last chunk holds the mass column d
+    float a[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) a[u][v] = 0.f;
+    for (int64_t q0 = p_beg; q0 < p_end; q0 += 32) {
+      const int np = (int)((p_end - q0) < 32 ? (p_end - q0) : 32);
+      __syncthreads();
+      for (int v = tid; v < 32 * 64; v += 256) {
+        const int j = v >> 6, r = v & 63;
+        qs[j][r] = (j < np && r < m) ? Q[(q0 + j) * ld + r] : 0.f;
+        const int t = t0 + r;
+        ys[j][r] = (j < np) ? (t < d ? Y[(q0 + j) * dy + t] : (t == d ? 1.f : 0.f)) : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const float4 qv = *reinterpret_cast<const float4*>(&qs[j][4 * ti]);
+        const float4 yv = *reinterpret_cast<const float4*>(&ys[j][4 * tj]);
+        const float qa[4] = {qv.x, qv.y, qv.z, qv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) a[u][v] = fmaf(qa[u], ya[v], a[u][v]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = 4 * ti + u;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int t = t0 + 4 * tj + v;
+        if (i < m && t <= d) out[(int64_t)i * (d + 1) + t] = a[u][v];
+      }
     }
   }
 }

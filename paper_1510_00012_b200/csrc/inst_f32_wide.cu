@@ -73,3 +73,15 @@ void launch_cost_tc32(const int64_t* off, const int64_t* imb, const int32_t* icl
   }
   k_cost_tc32<<<(unsigned)n_items, 128, SMEM, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
 }
+
+void launch_cost_tile_big(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
+                          float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s) {
+  if (n_items == 0) return;
+  k_cost_tile_big<<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
+}
+
+void launch_xpart(const int64_t* off, const int64_t* imb, const float* Q, const float* Y, float* px, int m, int d,
+                  int dy, int ld, int parts, int64_t n_items, cudaStream_t s) {
+  if (n_items == 0) return;
+  k_xpart<<<(unsigned)n_items, 256, 0, s>>>(off, imb, Q, Y, px, m, d, dy, ld, parts);
+}

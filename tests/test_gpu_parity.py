@@ -94,7 +94,7 @@ def expected_variant(m, mkmax, d, dtype="f32"):
     fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
     if fits and d <= 16:
         return 2
-    if dtype == "f32" and m <= 64 and mkmax <= 64 and d <= 64:
+    if dtype == "f32" and m <= 64 and mkmax <= 64:      # any d (d > 64: external x partials)
         return 3
     return 0
 
@@ -103,7 +103,8 @@ def expected_variant(m, mkmax, d, dtype="f32"):
                                     (12, (10, 32), 5), (20, (1, 32), 7), (32, (1, 4), 16), (3, (1, 3), 1),
                                     (64, (20, 64), 64), (64, (1, 64), 5), (33, (1, 63), 9), (64, (1, 3), 64),
                                     (40, (60, 64), 64), (64, (1, 80), 3), (32, (1, 64), 32), (16, (1, 30), 24),
-                                    (20, (30, 64), 5), (32, (10, 20), 64)])
+                                    (20, (30, 64), 5), (32, (10, 20), 64), (48, (4, 40), 130), (64, (20, 64), 100),
+                                    (20, (1, 50), 300)])
 def test_fp32_ragged_shapes(m, mk, d):
     """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
     two-chunk column sums, tiny m_k, the warp-pair kernel (32 < m <= 64 or 32 < m_k <= 64, cached
