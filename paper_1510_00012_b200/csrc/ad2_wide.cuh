@@ -38,7 +38,8 @@ struct WideLayout {
 
 template <int WM>
 __device__ __forceinline__ void group_sync(int id) {
-  if constexpr (WM == 64) asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+  if constexpr (WM == 128) asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+  else if constexpr (WM == 64) asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
   else __syncwarp();
 }
 
@@ -216,7 +217,7 @@ k_badmm_wide(const IterArgs<float> a) {
       // ---- column sums over the 64 rows (Eq.badmmc0 denominators): lane jc reads its column in
       //      16 chunks of 4 rows, starting at chunk jc mod 16 (4 lanes per bank quad: no conflicts)
 #pragma unroll
-      for (int cj = 0; cj < WMK / WM; ++cj) {                          // WM = 32: two columns per lane
+      for (int cj = 0; cj < (WMK + WM - 1) / WM; ++cj) {               // WM = 32: two columns per lane
         const int jcc = jc + cj * WM;
         if (jcc < mk) {
           const float* col = Ps + jcc * WMP;
@@ -252,10 +253,10 @@ k_badmm_wide(const IterArgs<float> a) {
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
       fence_proxy_async_smem();
-      if constexpr (WM == 64) {
+      if constexpr (WM >= 64) {
         if (lane == 0) Rw[h] = R;
         group_sync<WM>(bar_id);
-        R = Rw[0] + Rw[1];
+        R = (WM == 128) ? (Rw[0] + Rw[1]) + (Rw[2] + Rw[3]) : Rw[0] + Rw[1];
       } else {
         __syncwarp();
       }
@@ -320,9 +321,13 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
   const int c = item_cl[item];
   const int tid = threadIdx.x;
   const int ti = tid & 15, tj = tid >> 4;              // rows 4ti..4ti+3, points 4tj..4tj+3
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  for (int rb = 0; rb < ld; rb += 64) {                // row blocks of 64 (ld = 128 for m > 64)
+  __syncthreads();
   for (int v = tid; v < DMAX * 64; v += 256) {
     const int t = v >> 6, i = v & 63;
-    xs[t][i] = (i < m && t < d) ? x[((int64_t)c * m + i) * d + t] : 0.f;
+    xs[t][i] = (rb + i < m && t < d) ? x[((int64_t)c * m + rb + i) * d + t] : 0.f;
   }
   __syncthreads();
   if (tid < 64) {
@@ -330,8 +335,6 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
     for (int t = 0; t < d; ++t) s = fmaf(xs[t][tid], xs[t][tid], s);
     xx[tid] = s;
   }
-  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
-  double acc = 0.0;
   for (int64_t q0 = p_beg; q0 < p_end; q0 += 64) {
     const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
     __syncthreads();                                   // previous chunk consumed
@@ -369,21 +372,22 @@ k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int j = 4 * tj + v;
-      if (j < np && 4 * ti < ld) {
+      if (j < np && rb + 4 * ti < ld) {
         float4 o;
         float* oe = reinterpret_cast<float*>(&o);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int i = 4 * ti + u;
+          const int i = rb + 4 * ti + u;
           const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
-          const float cv = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yy[j]), 0.f) : 0.f;
+          const float cv = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i - rb] + yy[j]), 0.f) : 0.f;
           oe[u] = cv;
           s += cv;
         }
-        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + 4 * ti) = o;
+        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + rb + 4 * ti) = o;
       }
     }
     acc += (double)s;
+  }
   }
   if (psum) {
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -416,17 +420,19 @@ k_cost_tile_big(const int64_t* __restrict__ off, const int64_t* __restrict__ ite
   const int c = item_cl[item];
   const int tid = threadIdx.x;
   const int ti = tid & 15, tj = tid >> 4;
+  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  double acc = 0.0;
+  for (int rb = 0; rb < ld; rb += 64) {                // row blocks of 64 (ld = 128 for m > 64)
+  __syncthreads();
   if (tid < 64) {
     float s = 0.f;
-    if (tid < m)
+    if (rb + tid < m)
       for (int t = 0; t < d; ++t) {
-        const float v = x[((int64_t)c * m + tid) * d + t];
+        const float v = x[((int64_t)c * m + rb + tid) * d + t];
         s = fmaf(v, v, s);
       }
     xx[tid] = s;
   }
-  const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
-  double acc = 0.0;
   for (int64_t q0 = p_beg; q0 < p_end; q0 += 64) {
     const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
     float2 a2[2][4];
@@ -439,7 +445,7 @@ k_cost_tile_big(const int64_t* __restrict__ off, const int64_t* __restrict__ ite
       __syncthreads();                                 // previous chunk consumed
       for (int v = tid; v < 64 * 64; v += 256) {
         const int t = v >> 6, i = v & 63;
-        xs[t][i] = (i < m && t0 + t < d) ? x[((int64_t)c * m + i) * d + t0 + t] : 0.f;
+        xs[t][i] = (rb + i < m && t0 + t < d) ? x[((int64_t)c * m + rb + i) * d + t0 + t] : 0.f;
         const int j = v >> 6, tt = v & 63;
         ys[tt][j] = (j < np && t0 + tt < d) ? Y[(q0 + j) * dy + t0 + tt] : 0.f;
       }
@@ -466,19 +472,20 @@ k_cost_tile_big(const int64_t* __restrict__ off, const int64_t* __restrict__ ite
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int j = 4 * tj + v;
-      if (j < np && 4 * ti < ld) {
+      if (j < np && rb + 4 * ti < ld) {
         float o[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int i = 4 * ti + u;
+          const int i = rb + 4 * ti + u;
           const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
-          o[u] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yy[j]), 0.f) : 0.f;
+          o[u] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i - rb] + yy[j]), 0.f) : 0.f;
           s += o[u];
         }
-        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + 4 * ti) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + rb + 4 * ti) = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
     acc += (double)s;
+  }
   }
   if (psum) {
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -508,6 +515,7 @@ k_xpart(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb, co
   const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
   float* out = px + (int64_t)item * parts * m * (d + 1);
   for (int e = tid + m * (d + 1); e < parts * m * (d + 1); e += 256) out[e] = 0.f;   // parts 1..
+  for (int rb = 0; rb < ld; rb += 64)                    // row blocks of 64 (ld = 128 for m > 64)
   for (int t0 = 0; t0 < d + 1; t0 += 64) {              // the last chunk holds the mass column d
     float a[4][4];
 #pragma unroll
@@ -519,7 +527,7 @@ k_xpart(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb, co
       __syncthreads();
       for (int v = tid; v < 32 * 64; v += 256) {
         const int j = v >> 6, r = v & 63;
-        qs[j][r] = (j < np && r < m) ? Q[(q0 + j) * ld + r] : 0.f;
+        qs[j][r] = (j < np && rb + r < m) ? Q[(q0 + j) * ld + rb + r] : 0.f;
         const int t = t0 + r;
         ys[j][r] = (j < np) ? (t < d ? Y[(q0 + j) * dy + t] : (t == d ? 1.f : 0.f)) : 0.f;
       }
@@ -537,7 +545,7 @@ k_xpart(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb, co
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int i = 4 * ti + u;
+      const int i = rb + 4 * ti + u;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int t = t0 + 4 * tj + v;

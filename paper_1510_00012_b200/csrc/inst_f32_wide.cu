@@ -37,15 +37,17 @@ using namespace ad2k;
 
 // cfg = rows per member block (32 or 64)
 int wide_cfg() { return 64; }
-int wide_npair(int wm) { return wm == 32 ? 8 : 4; }
+int wide_npair(int wm) { return wm == 32 ? 8 : wm == 64 ? 4 : 2; }
 size_t wide_cta_bytes(int wm) {
-  return wm == 32 ? WideLayout<32, 8, 24>::CTA_BYTES : WideLayout<64, 4, 48>::CTA_BYTES;
+  return wm == 32 ? WideLayout<32, 8, 24>::CTA_BYTES
+                  : wm == 64 ? WideLayout<64, 4, 48>::CTA_BYTES : WideLayout<128, 2, 96>::CTA_BYTES;
 }
 
 void launch_wide(int wm, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
   if (wm == 32) go_wide_d<32, 8, 24>(mode, d, a, n_items, s);
-  else go_wide_d<64, 4, 48>(mode, d, a, n_items, s);
+  else if (wm == 64) go_wide_d<64, 4, 48>(mode, d, a, n_items, s);
+  else go_wide_d<128, 2, 96>(mode, d, a, n_items, s);
 }
 
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,

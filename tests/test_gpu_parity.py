@@ -94,7 +94,7 @@ def expected_variant(m, mkmax, d, dtype="f32"):
     fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
     if fits and d <= 16:
         return 2
-    if dtype == "f32" and m <= 64 and mkmax <= 64:      # any d (d > 64: external x partials)
+    if dtype == "f32" and m <= 128 and mkmax <= 64:     # any d (d > 64: external x partials)
         return 3
     return 0
 
@@ -104,7 +104,7 @@ def expected_variant(m, mkmax, d, dtype="f32"):
                                     (64, (20, 64), 64), (64, (1, 64), 5), (33, (1, 63), 9), (64, (1, 3), 64),
                                     (40, (60, 64), 64), (64, (1, 80), 3), (32, (1, 64), 32), (16, (1, 30), 24),
                                     (20, (30, 64), 5), (32, (10, 20), 64), (48, (4, 40), 130), (64, (20, 64), 100),
-                                    (20, (1, 50), 300)])
+                                    (20, (1, 50), 300), (100, (20, 64), 5), (96, (1, 40), 300), (128, (10, 64), 16)])
 def test_fp32_ragged_shapes(m, mk, d):
     """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
     two-chunk column sums, tiny m_k, the warp-pair kernel (32 < m <= 64 or 32 < m_k <= 64, cached
@@ -114,7 +114,7 @@ def test_fp32_ragged_shapes(m, mk, d):
     v = expected_variant(m, int(b.sizes.max()), d)
     assert ctx.info()["variant"] == v
     if v == 3:                                        # one warp per member (ld 32) or a warp pair (ld 64)
-        assert ctx.info()["mp"] == (32 if m <= 32 else 64)
+        assert ctx.info()["mp"] == (32 if m <= 32 else (64 if m <= 64 else 128))
     compare_round(b, T=12, tau=4, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False)
 
 
