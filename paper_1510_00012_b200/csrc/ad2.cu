@@ -594,13 +594,14 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) variant = 0;
   }
   int wcfg = 0;
-  if (variant == 0 && b->dtype == AD2_F32 && m <= 128 && mkmax <= 64) {   // any d (d > 64: k_xpart)
+  if (variant == 0 && b->dtype == AD2_F32 && m <= 128 && mkmax <= 128) {   // any d (d > 64: k_xpart)
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
     const int wm = m <= 32 ? 32 : (m <= 64 ? 64 : 128);
-    if (wide_cta_bytes(wm) <= (size_t)optin) {
+    const int cfg = wm + (mkmax > 64 ? 1 : 0);          // m_k <= 64 or <= 128 instantiation
+    if (wide_cta_bytes(cfg) <= (size_t)optin) {
       variant = 3;
-      wcfg = wm;
+      wcfg = cfg;
       mp = wm;
       nch = 1;
       dp = d <= 16 ? 16 : 64;

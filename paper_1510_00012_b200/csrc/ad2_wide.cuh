@@ -2,7 +2,7 @@
 // per member.  Modified B-ADMM of AD2-clustering (arXiv 1510.00012, Alg. 4).
 //
 // Member blocks have WM = 64 (or 32, one warp per member) rows (ld = WM, rows >= m zero) and
-// m_k <= WMK = 64 columns.  Lane i of warp h of a group owns centroid row 32h + i for EVERY
+// m_k <= MKX (64 or 128) columns.  Lane i of warp h of a group owns centroid row 32h + i for EVERY
 // column of the member, so row sums are lane-local.  The state does not live in registers (a 64-column row would need ~200): the pass
 // region [P | L | C] of one member is staged by three cp.async.bulk loads into a per-pair ring and
 // the iteration is three column sweeps over shared memory (each entry's intermediate is written
@@ -23,16 +23,15 @@
 
 namespace ad2k {
 
-constexpr int WMK = 64;     // largest m_k
-
-// WM = rows of a member block (ld) = 32 x warps per member group; NPAIR groups per CTA
-template <int WM, int NPAIR, int RING_KB>
+// WM = rows of a member block (ld) = 32 x warps per member group; MKX = largest m_k; NPAIR groups
+// per CTA, each with a ring of RING_KB
+template <int WM, int MKX, int NPAIR, int RING_KB>
 struct WideLayout {
   static constexpr int RING = RING_KB * 1024 / 4;               // floats per group
-  // [ring | fbuf[WMK] | Rw[4] | 2 mbarriers]
-  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + WMK + 4) + 16) + 127) / 128 * 128;
+  // [ring | fbuf[MKX] | Rw[4] | 2 mbarriers]
+  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + MKX + 4) + 16) + 127) / 128 * 128;
   static constexpr size_t CTA_BYTES = NPAIR * PAIR_BYTES;
-  static_assert(RING >= 3 * WM * WMK, "ring must hold the largest pass");
+  static_assert(RING >= 3 * WM * MKX, "ring must hold the largest pass");
   static_assert(CTA_BYTES <= 227 * 1024, "shared memory");
 };
 
@@ -43,12 +42,13 @@ __device__ __forceinline__ void group_sync(int id) {
   else __syncwarp();
 }
 
-template <int WM, int NPAIR, int RING_KB, int MODE, int DP>
+template <int WM, int MKX, int NPAIR, int RING_KB, int MODE, int DP>
 __global__ void __launch_bounds__(NPAIR * WM, 1)
 k_badmm_wide(const IterArgs<float> a) {
   constexpr int WMP = WM;
+  constexpr int WMK = MKX;
   constexpr int GW = WM / 32;                                      // warps per member group
-  using Lay = WideLayout<WM, NPAIR, RING_KB>;
+  using Lay = WideLayout<WM, MKX, NPAIR, RING_KB>;
   using N = Num<float>;
   constexpr int RING = Lay::RING;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -139,7 +139,10 @@ k_badmm_wide(const IterArgs<float> a) {
     const int mk = cnp;
     const int jc = ig;                 // the column this lane sums (jc < mk)
     const float om_j = (MODE != P2ONLY && jc < mk) ? __ldg(a.om + cp0 + jc) : 0.f;
-    const float om_j2 = (MODE != P2ONLY && WM == 32 && jc + 32 < mk) ? __ldg(a.om + cp0 + jc + 32) : 0.f;
+    float om_jc[(MKX + WM - 1) / WM];               // w^(k)_j of the columns this lane sums
+#pragma unroll
+    for (int cj = 0; cj < (MKX + WM - 1) / WM; ++cj)
+      om_jc[cj] = (MODE != P2ONLY && jc + cj * WM < mk) ? __ldg(a.om + cp0 + jc + cj * WM) : 0.f;
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     float* const Ps = ring + cbase;
     float* const Ls = Ps + WMP * mk;
@@ -230,7 +233,7 @@ k_badmm_wide(const IterArgs<float> a) {
             s1 = __fadd2_rn(s1, make_float2(v.z, v.w));
           }
           const float s = (s0.x + s0.y) + (s1.x + s1.y);
-          fbuf[jcc] = __fdividef(cj ? om_j2 : om_j, s);                // Eq.badmmc0: w_j^(k) / colsum
+          fbuf[jcc] = __fdividef(om_jc[cj], s);                          // Eq.badmmc0: w_j^(k) / colsum
         }
       }
       group_sync<WM>(bar_id);

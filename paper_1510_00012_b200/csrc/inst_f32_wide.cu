@@ -7,47 +7,61 @@
 
 namespace ad2k {
 
-// (rows per member WM, groups per CTA, ring KB per group): WM = 64 -> (4, 48), one CTA / SM of 8
-// warps with single-pass rings; WM = 32 -> (8, 24), one warp per member, 8 warps / SM
-template <int WM, int NPAIR, int RKB, int DP>
+// instantiations (rows per member WM, largest m_k MKX, groups per CTA, ring KB per group):
+//   (32, 64, 8, 24) (64, 64, 4, 48) (128, 64, 2, 96) (32, 128, 4, 48) (64, 128, 2, 96) (128, 128, 1, 192)
+template <int WM, int MKX, int NPAIR, int RKB, int DP>
 static void go_wide(int mode, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
-  using Lay = WideLayout<WM, NPAIR, RKB>;
+  using Lay = WideLayout<WM, MKX, NPAIR, RKB>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
-    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
-    cudaFuncSetAttribute(k_badmm_wide<WM, NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     attr = true;
   }
   dim3 g((unsigned)n_items), b(NPAIR * WM);
-  if (mode == P1ONLY) k_badmm_wide<WM, NPAIR, RKB, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
-  else if (mode == FUSED) k_badmm_wide<WM, NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
-  else k_badmm_wide<WM, NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  if (mode == P1ONLY) k_badmm_wide<WM, MKX, NPAIR, RKB, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == FUSED) k_badmm_wide<WM, MKX, NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
 }
 
-template <int WM, int NPAIR, int RKB>
+template <int WM, int MKX, int NPAIR, int RKB>
 static void go_wide_d(int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
-  if (d <= 16) go_wide<WM, NPAIR, RKB, 16>(mode, a, n_items, s);
-  else go_wide<WM, NPAIR, RKB, 64>(mode, a, n_items, s);
+  if (d <= 16) go_wide<WM, MKX, NPAIR, RKB, 16>(mode, a, n_items, s);
+  else go_wide<WM, MKX, NPAIR, RKB, 64>(mode, a, n_items, s);
 }
 
 }  // namespace ad2k
 
 using namespace ad2k;
 
-// cfg = rows per member block (32 or 64)
-int wide_cfg() { return 64; }
-int wide_npair(int wm) { return wm == 32 ? 8 : wm == 64 ? 4 : 2; }
-size_t wide_cta_bytes(int wm) {
-  return wm == 32 ? WideLayout<32, 8, 24>::CTA_BYTES
-                  : wm == 64 ? WideLayout<64, 4, 48>::CTA_BYTES : WideLayout<128, 2, 96>::CTA_BYTES;
+// kernel configuration id: wm (32 / 64 / 128) + (mkx == 128 ? 1 : 0)
+int wide_npair(int cfg) {
+  const int wm = cfg & ~1, big = cfg & 1;
+  if (!big) return wm == 32 ? 8 : wm == 64 ? 4 : 2;
+  return wm == 32 ? 4 : wm == 64 ? 2 : 1;
+}
+size_t wide_cta_bytes(int cfg) {
+  switch (cfg) {
+    case 32: return WideLayout<32, 64, 8, 24>::CTA_BYTES;
+    case 64: return WideLayout<64, 64, 4, 48>::CTA_BYTES;
+    case 128: return WideLayout<128, 64, 2, 96>::CTA_BYTES;
+    case 33: return WideLayout<32, 128, 4, 48>::CTA_BYTES;
+    case 65: return WideLayout<64, 128, 2, 96>::CTA_BYTES;
+    default: return WideLayout<128, 128, 1, 192>::CTA_BYTES;
+  }
 }
 
-void launch_wide(int wm, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
+void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
-  if (wm == 32) go_wide_d<32, 8, 24>(mode, d, a, n_items, s);
-  else if (wm == 64) go_wide_d<64, 4, 48>(mode, d, a, n_items, s);
-  else go_wide_d<128, 2, 96>(mode, d, a, n_items, s);
+  switch (cfg) {
+    case 32: go_wide_d<32, 64, 8, 24>(mode, d, a, n_items, s); break;
+    case 64: go_wide_d<64, 64, 4, 48>(mode, d, a, n_items, s); break;
+    case 128: go_wide_d<128, 64, 2, 96>(mode, d, a, n_items, s); break;
+    case 33: go_wide_d<32, 128, 4, 48>(mode, d, a, n_items, s); break;
+    case 65: go_wide_d<64, 128, 2, 96>(mode, d, a, n_items, s); break;
+    default: go_wide_d<128, 128, 1, 192>(mode, d, a, n_items, s); break;
+  }
 }
 
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,

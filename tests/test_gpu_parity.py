@@ -94,7 +94,7 @@ def expected_variant(m, mkmax, d, dtype="f32"):
     fits = [mp for mp in (8, 16, 32) if m <= mp and mkmax <= (32 if mp == 32 else 2 * mp)]
     if fits and d <= 16:
         return 2
-    if dtype == "f32" and m <= 128 and mkmax <= 64:     # any d (d > 64: external x partials)
+    if dtype == "f32" and m <= 128 and mkmax <= 128:    # any d (d > 64: external x partials)
         return 3
     return 0
 
@@ -104,11 +104,13 @@ def expected_variant(m, mkmax, d, dtype="f32"):
                                     (64, (20, 64), 64), (64, (1, 64), 5), (33, (1, 63), 9), (64, (1, 3), 64),
                                     (40, (60, 64), 64), (64, (1, 80), 3), (32, (1, 64), 32), (16, (1, 30), 24),
                                     (20, (30, 64), 5), (32, (10, 20), 64), (48, (4, 40), 130), (64, (20, 64), 100),
-                                    (20, (1, 50), 300), (100, (20, 64), 5), (96, (1, 40), 300), (128, (10, 64), 16)])
+                                    (20, (1, 50), 300), (100, (20, 64), 5), (96, (1, 40), 300), (128, (10, 64), 16),
+                                    (100, (50, 100), 300), (64, (60, 128), 16), (20, (1, 120), 3), (8, (100, 140), 2)])
 def test_fp32_ragged_shapes(m, mk, d):
     """Covers the TMA kernel's G = 4 / 2 / 1 member packings, padded rows (m < MP), the
-    two-chunk column sums, tiny m_k, the warp-pair kernel (32 < m <= 64 or 32 < m_k <= 64, cached
-    cost from the tiled cost build), and the generic kernel (m_k > 64)."""
+    two-chunk column sums, tiny m_k, the cached-cost warp-group kernel (one warp per member for
+    m <= 32, a pair for m <= 64, four warps for m <= 128; m_k up to 128; any d, with the external
+    x partials for d > 64), and the generic kernel (m_k > 128)."""
     b = wl.make_random(500, m, d, K=4, mk_range=mk, seed=7 + m, dtype="f32", T=1, tau=1)
     ctx, _ = compare_round(b, T=1, tau=1, rtol_plan=1e-5, rtol_x=1e-5, atol_w=1e-6)
     v = expected_variant(m, int(b.sizes.max()), d)
