@@ -27,9 +27,18 @@
 
 namespace ad2a {
 
+// row stride of the fp32 cost copy used by the Sinkhorn sweeps: a multiple of 4 floats with an odd
+// number of 16-byte groups, so lane-per-row LDS.128 reads are conflict-free (and lane-per-column
+// scalar reads are consecutive)
+__host__ __device__ inline int ldf_of(int mk) {
+  int l = (mk + 3) & ~3;
+  if (((l >> 2) & 1) == 0) l += 4;
+  return l;
+}
+
 struct AsgLay {
   int m, mk, V, K, d;
-  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, oCf, olog, oys, bytes;
+  size_t oC, oF, opi, odist, oprev, odone, oarem, obrem, oom, oLB, osolv, oyb, oCf, olog, olb, oAb, oBb, oys, bytes;
   __host__ __device__ void make(int m_, int mk_, int K_, int d_) {
     m = m_, mk = mk_, K = K_, d = d_;
     V = m + mk;
@@ -39,8 +48,9 @@ struct AsgLay {
       o += (b + 15) & ~(size_t)15;
       return r;
     };
-    oC = take(8 * (size_t)m * mk);
-    oF = take(8 * (size_t)m * mk);
+    oC = take(8 * (size_t)m * (mk | 1));       // rows padded to an odd stride (bank-conflict-free columns)
+    oF = take(8 * (size_t)m * (mk | 1) > 4 * (size_t)m * ldf_of(mk) ? 8 * (size_t)m * (mk | 1)
+                                                                    : 4 * (size_t)m * ldf_of(mk));
     opi = take(8 * (size_t)V);
     odist = take(8 * (size_t)V);
     oprev = take(4 * (size_t)V);
@@ -51,12 +61,21 @@ struct AsgLay {
     oLB = take(8 * (size_t)K);
     osolv = take(4 * (size_t)((K + 31) / 32));
     oyb = take(8 * (size_t)d);
-    oCf = take(4 * (size_t)m * mk);
-    olog = take(4 * (size_t)V);
+    oCf = oF;                                         // fp32 copy of C (Sinkhorn only) aliases the flows
+    olog = take(4 * (size_t)m);                       // Sinkhorn: log a [m]
+    olb = take(4 * (size_t)(mk + 4));                  // log b [m_k] (+ padding)
+    oAb = take(4 * (size_t)m);                         // per-iteration row terms (base 2)
+    oBb = take(4 * (size_t)(mk + 4));                  // per-iteration column terms (base 2)
     oys = take(8 * (size_t)mk * d);                   // the member's points in fp64
     bytes = o;
   }
 };
+
+__device__ __forceinline__ float ex2f(float a) {      // MUFU 2^a (flush-to-zero)
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -64,11 +83,26 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+// order-preserving map of fp64 onto uint64 (negative values flip every bit, others the sign bit)
+__device__ __forceinline__ unsigned long long okey(double x) {
+  const long long b = __double_as_longlong(x);
+  return (unsigned long long)(b ^ ((b >> 63) | (long long)0x8000000000000000ull));
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
+}
+
 // exact W^2 by successive shortest paths; C row-major m x mk in smem; returns the cost of the
 // final plan.  err bit 1: no augmenting path / iteration cap (should not happen on a balanced
 // problem).
-__device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, int mk, int lane, int* err) {
-  const int m = L.m, V = m + mk;
+// warm: start from the dual-feasible potentials (u, v) that dual_bounds(duals_only) left in the
+// pi region (pi_i = -u_i, pi_{m+j} = v_j, so every forward reduced cost C_ij - u_i - v_j >= 0);
+// with near-optimal duals each Dijkstra reaches a sink over (near-)tight arcs in a few steps.
+// The optimum does not depend on the starting potentials, only their feasibility.
+__device__ __noinline__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, int mk, int lane, int* err,
+                         bool warm, unsigned long long* stats) {
+  unsigned naug = 0, nstep = 0;
+  const int m = L.m, V = m + mk, ld = mk | 1;
   const double* C = reinterpret_cast<const double*>(ws + L.oC);
   double* F = reinterpret_cast<double*>(ws + L.oF);
   double* pi = reinterpret_cast<double*>(ws + L.opi);
@@ -79,8 +113,12 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
   double* brem = reinterpret_cast<double*>(ws + L.obrem);
   const double* om = reinterpret_cast<const double*>(ws + L.oom);
   const double tiny = 1e-14;
-  for (int e = lane; e < m * mk; e += 32) F[e] = 0.0;
-  for (int v = lane; v < V; v += 32) pi[v] = 0.0;
+  for (int e = lane; e < m * ld; e += 32) F[e] = 0.0;
+  if (warm) {
+    for (int i = lane; i < m; i += 32) pi[i] = -pi[i];
+  } else {
+    for (int v = lane; v < V; v += 32) pi[v] = 0.0;
+  }
   for (int i = lane; i < m; i += 32) arem[i] = wn[i];
   for (int j = lane; j < mk; j += 32) brem[j] = om[j];
   __syncwarp();
@@ -94,33 +132,60 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
       if (lane == 0) atomicOr(err, 1);
       break;
     }
-    for (int v = lane; v < V; v += 32) {
-      done[v] = 0;
-      prev[v] = -1;
-      dist[v] = (v < m && arem[v] > tiny) ? 0.0 : CUDART_INF;
+    // every source with supply left is at distance 0: settle them all at once and relax their
+    // forward arcs in one pass (lane = sink), instead of one Dijkstra step per source
+    for (int i = lane; i < m; i += 32) {
+      const bool act = arem[i] > tiny;
+      done[i] = act;
+      prev[i] = -1;
+      dist[i] = act ? 0.0 : CUDART_INF;
+    }
+    for (int j = lane; j < mk; j += 32) {
+      double bd = CUDART_INF;
+      int bi = -1;
+      const double pj = pi[m + j];
+      #pragma unroll 1
+      for (int i = 0; i < m; ++i)
+        if (arem[i] > tiny) {
+          const double nd = C[i * ld + j] + pi[i] - pj;
+          if (nd < bd) {
+            bd = nd;
+            bi = i;
+          }
+        }
+      done[m + j] = 0;
+      prev[m + j] = bi;
+      dist[m + j] = bd;
     }
     __syncwarp();
     int t = -1;
     double dt = CUDART_INF;
     for (int step = 0; step < V; ++step) {
-      double bd = CUDART_INF;
+      // warp argmin of dist over unsettled nodes: order-preserving 64-bit keys, one shuffle
+      // pair per round; the lowest lane holding the minimum key supplies the node (deterministic)
+      unsigned long long key = ~0ull;
       int bv = V;
       for (int v = lane; v < V; v += 32)
-        if (!done[v] && dist[v] < bd) {
-          bd = dist[v];
-          bv = v;
+        if (!done[v]) {
+          const unsigned long long kv = okey(dist[v]);
+          if (kv < key) {
+            key = kv;
+            bv = v;
+          }
         }
+      unsigned long long km = key;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        if (od < bd || (od == bd && ov < bv)) {
-          bd = od;
-          bv = ov;
-        }
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, km, o);
+        km = ok < km ? ok : km;
       }
+      if (km == ~0ull) break;
+      const int src = __ffs(__ballot_sync(0xffffffffu, key == km)) - 1;
+      bv = __shfl_sync(0xffffffffu, bv, src);
+      const double bd = okey_inv(km);
       if (bv >= V || !(bd < CUDART_INF)) break;
       if (lane == 0) done[bv] = 1;
+      ++nstep;
       if (bv >= m && brem[bv - m] > tiny) {         // the nearest sink with demand left
         t = bv;
         dt = bd;
@@ -131,8 +196,8 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
       if (bv >= m) {                                // sink j: reverse arcs j -> i carrying flow
         const int j = bv - m;
         for (int i = lane; i < m; i += 32)
-          if (!done[i] && F[i * mk + j] > 0.0) {
-            const double nd = bd - C[i * mk + j] + pi[bv] - pi[i];
+          if (!done[i] && F[i * ld + j] > 0.0) {
+            const double nd = bd - C[i * ld + j] + pi[bv] - pi[i];
             if (nd < dist[i]) {
               dist[i] = nd;
               prev[i] = bv;
@@ -143,7 +208,7 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
         for (int j = lane; j < mk; j += 32) {
           const int v = m + j;
           if (!done[v]) {
-            const double nd = bd + C[i * mk + j] + pi[i] - pi[v];
+            const double nd = bd + C[i * ld + j] + pi[i] - pi[v];
             if (nd < dist[v]) {
               dist[v] = nd;
               prev[v] = i;
@@ -157,6 +222,7 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
       if (lane == 0) atomicOr(err, 1);
       break;
     }
+    ++naug;
     for (int v = lane; v < V; v += 32) pi[v] += done[v] ? dist[v] : dt;   // reduced costs stay >= 0
     __syncwarp();
     if (lane == 0) {
@@ -164,7 +230,7 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
       int v = t;
       while (prev[v] >= 0) {
         const int u = prev[v];
-        if (u >= m) del = fmin(del, F[v * mk + (u - m)]);
+        if (u >= m) del = fmin(del, F[v * ld + (u - m)]);
         v = u;
       }
       const int s = v;
@@ -172,8 +238,8 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
       v = t;
       while (prev[v] >= 0) {
         const int u = prev[v];
-        if (u < m) F[u * mk + (v - m)] += del;
-        else F[v * mk + (u - m)] -= del;
+        if (u < m) F[u * ld + (v - m)] += del;
+        else F[v * ld + (u - m)] -= del;
         v = u;
       }
       arem[s] -= del;
@@ -181,8 +247,14 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
     }
     __syncwarp();
   }
+  if (lane == 0) {                                  // statistics: augmentations, Dijkstra steps
+    atomicAdd(stats, (unsigned long long)naug);
+    atomicAdd(stats + 1, (unsigned long long)nstep);
+  }
   double acc = 0.0;
-  for (int e = lane; e < m * mk; e += 32) acc += F[e] * C[e];
+#pragma unroll 1
+  for (int i = 0; i < m; ++i)
+    for (int j = lane; j < mk; j += 32) acc += F[i * ld + j] * C[i * ld + j];
   return wsum(acc);
 }
 
@@ -194,18 +266,21 @@ __device__ double ssp_w2(const AsgLay& L, unsigned char* ws, const double* wn, i
 // onto the transport polytope (row scaling to <= a, column scaling to <= b, rank-one
 // correction, Altschuler et al.) is feasible, hence UB = <C, P> >= W^2.  Uses F as scratch.
 // dual-feasible potentials from fs by two fp64 c-transforms -> Kantorovich lower bound
-__device__ double ctrans_lb(int m, int mk, const double* C, const float* fs, const double* a, const double* b,
+__device__ __noinline__ double ctrans_lb(int m, int mk, const double* C, const float* fs, const double* a, const double* b,
                             double* u, double* v, int lane) {
+  const int ld = mk | 1;
   for (int j = lane; j < mk; j += 32) {
     double mn = CUDART_INF;
-    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j] - (double)fs[i]);
+    #pragma unroll 1
+    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j] - (double)fs[i]);
     v[j] = mn;
   }
   __syncwarp();
   double acc = 0.0;
   for (int i = lane; i < m; i += 32) {
     double mn = CUDART_INF;
-    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j] - v[j]);
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j] - v[j]);
     u[i] = mn;
     acc += a[i] * mn;
   }
@@ -215,29 +290,80 @@ __device__ double ctrans_lb(int m, int mk, const double* C, const float* fs, con
   return r;
 }
 
+// Kantorovich lower bound from zero potentials by two fp64 c-transforms, in both orders
+// (v_j = min_i C_ij, u_i = min_j C_ij - v_j; and the mirror), each dual-feasible — at least the
+// relaxed-marginal bounds sum_j b_j min_i C_ij and sum_i a_i min_j C_ij, for O(m m_k) work.
+__device__ __noinline__ double zero_ctrans_lb(int m, int mk, const double* C, const double* a, const double* b, double* u,
+                                 double* v, int lane) {
+  const int ld = mk | 1;
+  for (int j = lane; j < mk; j += 32) {
+    double mn = CUDART_INF;
+    #pragma unroll 1
+    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j]);
+    v[j] = mn;
+  }
+  for (int i = lane; i < m; i += 32) {
+    double mn = CUDART_INF;
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j]);
+    u[i] = mn;
+  }
+  __syncwarp();
+  double a1 = 0.0, a2 = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    double mn = CUDART_INF;
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j] - v[j]);
+    a1 += a[i] * mn;
+    a2 += a[i] * u[i];
+  }
+  for (int j = lane; j < mk; j += 32) {
+    double mn = CUDART_INF;
+    #pragma unroll 1
+    for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j] - u[i]);
+    a1 += b[j] * v[j];
+    a2 += b[j] * mn;
+  }
+  const double r = fmax(wsum(a1), wsum(a2));
+  __syncwarp();
+  return r;
+}
+
 // prune_at: if an intermediate lower bound (after 8 / 16 iterations) already exceeds it, return
 // early with ub = +inf (the candidate cannot win)
-__device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double prune_at,
-                            double& lb, double& ub) {
-  const int m = L.m;
+// duals_only: stop after the lower bound, leaving the dual-feasible (u, v) in the pi region
+__device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double prune_at,
+                            double& lb, double& ub, bool duals_only = false) {
+  const int m = L.m, ld = mk | 1;
   const double* C = reinterpret_cast<const double*>(ws + L.oC);
   double* P = reinterpret_cast<double*>(ws + L.oF);
   double* u = reinterpret_cast<double*>(ws + L.opi);          // [m] then v at u + m
   double* v = u + m;
   float* fs = reinterpret_cast<float*>(ws + L.odist);         // f [m], g [mk] (fp32 potentials)
   float* gs = fs + m;
-  float* Cf = reinterpret_cast<float*>(ws + L.oCf);            // fp32 copy of C
-  float* la = reinterpret_cast<float*>(ws + L.olog);           // log a [m], log b [mk]
-  float* lbv = la + m;
+  float* Cf = reinterpret_cast<float*>(ws + L.oCf);            // fp32 copy of C, row stride ldf
+  float* la = reinterpret_cast<float*>(ws + L.olog);           // log a [m]
+  float* lbv = reinterpret_cast<float*>(ws + L.olb);           // log b [m_k]
+  float* Ab = reinterpret_cast<float*>(ws + L.oAb);            // (log a_i + f_i / eps) log2 e
+  float* Bb = reinterpret_cast<float*>(ws + L.oBb);            // (log b_j + g_j / eps) log2 e; -inf pad
   const double* b = reinterpret_cast<const double*>(ws + L.oom);
+  const int ldf = ldf_of(mk), nq = (mk + 3) >> 2;
   double cmax = 0.0, csum = 0.0;
-  for (int e = lane; e < m * mk; e += 32) {
-    cmax = fmax(cmax, C[e]);
-    csum += C[e];
-    Cf[e] = (float)C[e];
-  }
+#pragma unroll 1
+  for (int i = 0; i < m; ++i)
+    for (int j = lane; j < ldf; j += 32) {
+      float cf = 0.f;
+      if (j < mk) {
+        const double c = C[i * ld + j];
+        cmax = fmax(cmax, c);
+        csum += c;
+        cf = (float)c;
+      }
+      Cf[i * ldf + j] = cf;
+    }
   for (int i = lane; i < m; i += 32) la[i] = __logf((float)a[i] + 1e-38f);
   for (int j = lane; j < mk; j += 32) lbv[j] = __logf((float)b[j] + 1e-38f);
+  for (int j = mk + lane; j < 4 * nq; j += 32) Bb[j] = -CUDART_INF_F;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
   csum = wsum(csum);
@@ -246,24 +372,40 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
   for (int i = lane; i < m; i += 32) fs[i] = 0.f;
   for (int j = lane; j < mk; j += 32) gs[j] = 0.f;
   __syncwarp();
-  __syncwarp();
+  const float L2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
   for (int it = 0; it < 24; ++it) {
     eps = fmaxf(eps_f, eps * 0.5f);
-    const float ie = 1.f / eps;
-    for (int j = lane; j < mk; j += 32) {            // g_j = -eps LSE_i(log a_i + (f_i - C_ij)/eps)
+    const float ie = 1.f / eps, iel = ie * L2E;
+    // g_j = -eps LSE_i(log a_i + (f_i - C_ij)/eps), in base 2: t_ij = Ab_i - C_ij iel
+    for (int i = lane; i < m; i += 32) Ab[i] = (la[i] + fs[i] * ie) * L2E;
+    __syncwarp();
+    for (int j = lane; j < mk; j += 32) {
       float mx = -CUDART_INF_F;
-      for (int i = 0; i < m; ++i) mx = fmaxf(mx, la[i] + (fs[i] - Cf[i * mk + j]) * ie);
+      for (int i = 0; i < m; ++i) mx = fmaxf(mx, fmaf(-Cf[i * ldf + j], iel, Ab[i]));
       float sm = 0.f;
-      for (int i = 0; i < m; ++i) sm += __expf(la[i] + (fs[i] - Cf[i * mk + j]) * ie - mx);
-      gs[j] = -eps * (mx + __logf(sm));
+      for (int i = 0; i < m; ++i) sm += ex2f(fmaf(-Cf[i * ldf + j], iel, Ab[i]) - mx);
+      gs[j] = -eps * LN2 * (mx + __log2f(sm));
     }
     __syncwarp();
-    for (int i = lane; i < m; i += 32) {             // f_i = -eps LSE_j(log b_j + (g_j - C_ij)/eps)
+    // f_i = -eps LSE_j(log b_j + (g_j - C_ij)/eps): lane = row, four columns per LDS.128
+    for (int j = lane; j < mk; j += 32) Bb[j] = (lbv[j] + gs[j] * ie) * L2E;
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+      const float4* cr = reinterpret_cast<const float4*>(Cf + i * ldf);
+      const float4* br = reinterpret_cast<const float4*>(Bb);
       float mx = -CUDART_INF_F;
-      for (int j = 0; j < mk; ++j) mx = fmaxf(mx, lbv[j] + (gs[j] - Cf[i * mk + j]) * ie);
-      float sm = 0.f;
-      for (int j = 0; j < mk; ++j) sm += __expf(lbv[j] + (gs[j] - Cf[i * mk + j]) * ie - mx);
-      fs[i] = -eps * (mx + __logf(sm));
+      for (int q = 0; q < nq; ++q) {
+        const float4 c4 = cr[q], b4 = br[q];
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaf(-c4.x, iel, b4.x), fmaf(-c4.y, iel, b4.y)),
+                             fmaxf(fmaf(-c4.z, iel, b4.z), fmaf(-c4.w, iel, b4.w))));
+      }
+      float s0 = 0.f, s1 = 0.f;
+      for (int q = 0; q < nq; ++q) {
+        const float4 c4 = cr[q], b4 = br[q];
+        s0 += ex2f(fmaf(-c4.x, iel, b4.x) - mx) + ex2f(fmaf(-c4.y, iel, b4.y) - mx);
+        s1 += ex2f(fmaf(-c4.z, iel, b4.z) - mx) + ex2f(fmaf(-c4.w, iel, b4.w) - mx);
+      }
+      fs[i] = -eps * LN2 * (mx + __log2f(s0 + s1));
     }
     __syncwarp();
     if (it == 3 || it == 7 || it == 15) {           // early exit for clearly worse centroids
@@ -276,41 +418,53 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
     }
   }
   lb = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
+  if (duals_only) {
+    ub = CUDART_INF;
+    return;
+  }
   // primal: Sinkhorn plan, rounded onto the transport polytope
   const float ie = 1.f / eps;
-  for (int e = lane; e < m * mk; e += 32) {
-    const int i = e / mk, j = e - i * mk;
-    P[e] = (double)__expf((fs[i] + gs[j] - (float)C[e]) * ie) * a[i] * b[j];
-  }
+#pragma unroll 1
+  for (int i = 0; i < m; ++i)
+    for (int j = lane; j < mk; j += 32)
+      P[i * ld + j] = (double)__expf((fs[i] + gs[j] - (float)C[i * ld + j]) * ie) * a[i] * b[j];
   __syncwarp();
   for (int i = lane; i < m; i += 32) {              // rows scaled down to <= a_i
     double r = 0.0;
-    for (int j = 0; j < mk; ++j) r += P[i * mk + j];
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) r += P[i * ld + j];
     const double x = r > a[i] ? a[i] / r : 1.0;
-    for (int j = 0; j < mk; ++j) P[i * mk + j] *= x;
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) P[i * ld + j] *= x;
   }
   __syncwarp();
   for (int j = lane; j < mk; j += 32) {             // columns scaled down to <= b_j
     double c = 0.0;
-    for (int i = 0; i < m; ++i) c += P[i * mk + j];
+    #pragma unroll 1
+    for (int i = 0; i < m; ++i) c += P[i * ld + j];
     const double y = c > b[j] ? b[j] / c : 1.0;
-    for (int i = 0; i < m; ++i) P[i * mk + j] *= y;
+    #pragma unroll 1
+    for (int i = 0; i < m; ++i) P[i * ld + j] *= y;
     v[j] = b[j] - c * y;                            // column deficit
   }
   __syncwarp();
   double dr = 0.0;
   for (int i = lane; i < m; i += 32) {
     double r = 0.0;
-    for (int j = 0; j < mk; ++j) r += P[i * mk + j];
+    #pragma unroll 1
+    for (int j = 0; j < mk; ++j) r += P[i * ld + j];
     u[i] = fmax(a[i] - r, 0.0);                     // row deficit
     dr += u[i];
   }
   dr = wsum(dr);
   __syncwarp();
   double cu = 0.0;
-  for (int e = lane; e < m * mk; e += 32) {
-    const int i = e / mk, j = e - i * mk;
-    const double pe = P[e] + (dr > 0.0 ? u[i] * fmax(v[j], 0.0) / dr : 0.0);
+  const double idr = dr > 0.0 ? 1.0 / dr : 0.0;
+#pragma unroll 1
+  for (int i = 0; i < m; ++i)
+    for (int j = lane; j < mk; j += 32) {
+    const int e = i * ld + j;
+    const double pe = P[e] + u[i] * fmax(v[j], 0.0) * idr;
     cu += C[e] * pe;
   }
   ub = wsum(cu);
@@ -319,14 +473,16 @@ __device__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a,
 // C_ij = |x_ci - y_j|^2 in fp64 (difference form) with lane = centroid row: x_i is held in
 // registers 16 coordinates at a time, the member's points ys are broadcast from shared memory;
 // symbolic supports read the table instead.
-__device__ void build_cost(const AsgLay& L, unsigned char* ws, const double* __restrict__ xk, int mk, int lane,
+__device__ __noinline__ void build_cost(const AsgLay& L, unsigned char* ws, const double* __restrict__ xk, int mk, int lane,
                            const int32_t* xs_c, const int32_t* Ysym, const double* Dtab, int V, int* err) {
-  const int m = L.m, d = L.d;
+  const int m = L.m, d = L.d, ld = mk | 1;
   double* C = reinterpret_cast<double*>(ws + L.oC);
   const double* ys = reinterpret_cast<const double*>(ws + L.oys);
   if (Dtab) {
-    for (int e = lane; e < m * mk; e += 32) {
-      const int i = e / mk, j = e - i * mk;
+#pragma unroll 1
+    for (int i = 0; i < m; ++i)
+      for (int j = lane; j < mk; j += 32) {
+      const int e = i * ld + j;
       const int sa = xs_c[i], sb = Ysym[j];
       double a = 0.0;
       if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
@@ -341,16 +497,17 @@ __device__ void build_cost(const AsgLay& L, unsigned char* ws, const double* __r
 #pragma unroll
       for (int t = 0; t < 16; ++t) xr[t] = (t0 + t < d) ? xk[(int64_t)i * d + t0 + t] : 0.0;
       const int tn = d - t0 < 16 ? d - t0 : 16;
+      #pragma unroll 1
       for (int j = 0; j < mk; ++j) {
         const double* yj = ys + j * d + t0;
-        double a = (t0 == 0) ? 0.0 : C[i * mk + j];
+        double a = (t0 == 0) ? 0.0 : C[i * ld + j];
 #pragma unroll
         for (int t = 0; t < 16; ++t)
           if (t < tn) {
             const double df = xr[t] - yj[t];
             a += df * df;
           }
-        C[i * mk + j] = a;
+        C[i * ld + j] = a;
       }
     }
   }
@@ -365,6 +522,7 @@ __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, 
   __shared__ double tot;
   if (threadIdx.x == 0) {
     double s = 0.0;
+    #pragma unroll 1
     for (int i = 0; i < m; ++i) s += (double)w[(int64_t)c * m + i];
     tot = s;
   }
@@ -375,6 +533,7 @@ __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, 
   __syncthreads();
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
     double s = 0.0;
+    #pragma unroll 1
     for (int i = 0; i < m; ++i) s += wc[(int64_t)c * m + i] * xc[((int64_t)c * m + i) * d + t];
     xb[(int64_t)c * d + t] = s;
   }
@@ -401,9 +560,14 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
                          double* __restrict__ best_out, unsigned long long* __restrict__ n_exact, int* err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (k >= N) return;
   unsigned char* ws = smem + (size_t)warp * L.bytes;
+  // persistent warps: members are taken from a global counter (n_exact[5]) one at a time, so
+  // a warp with cheap members moves on instead of idling until its block's slowest warp ends
+  for (;;) {
+  unsigned long long kq = 0;
+  if (lane == 0) kq = atomicAdd(n_exact + 5, 1ull);
+  const int64_t k = (int64_t)__shfl_sync(0xffffffffu, kq, 0);
+  if (k >= N) break;
   const int m = L.m, K = L.K, d = L.d;
   double* C = reinterpret_cast<double*>(ws + L.oC);
   double* om = reinterpret_cast<double*>(ws + L.oom);
@@ -411,7 +575,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   unsigned* solved = reinterpret_cast<unsigned*>(ws + L.osolv);
   double* yb = reinterpret_cast<double*>(ws + L.oyb);
   const int64_t o0 = off[k];
-  const int mk = (int)(off[k + 1] - o0);
+  const int mk = (int)(off[k + 1] - o0), ld = mk | 1;
   const T* Yk = Y + o0 * d;
 
   // member weights renormalised in fp64 (O1), member mean
@@ -428,6 +592,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   if (!Dtab)
     for (int t = lane; t < d; t += 32) {
       double a = 0.0;
+      #pragma unroll 1
       for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
       yb[t] = a;
     }
@@ -474,8 +639,16 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     __syncwarp();
     const double* wn = wc + (int64_t)cs * m;
     double dlb, dub;
-    dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
-    ++nvisit;
+    const double zlb = zero_ctrans_lb(m, mk, C, wn, om, reinterpret_cast<double*>(ws + L.opi),
+                                      reinterpret_cast<double*>(ws + L.opi) + m, lane);
+    if (zlb * shrink > ubest) {                      // cannot win: no Sinkhorn run
+      dlb = zlb;
+      dub = CUDART_INF;
+    } else {
+      dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
+      dlb = fmax(dlb, zlb);
+      ++nvisit;
+    }
     ubest = fmin(ubest, dub * grow);
     if (lane == 0) {
       LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
@@ -521,17 +694,21 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     double l1 = 0.0, l2 = 0.0;
     for (int j = lane; j < mk; j += 32) {
       double mn = CUDART_INF;
-      for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * mk + j]);
+      #pragma unroll 1
+      for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j]);
       l1 += om[j] * mn;
     }
     for (int i = lane; i < m; i += 32) {
       double mn = CUDART_INF;
-      for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * mk + j]);
+      #pragma unroll 1
+      for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j]);
       l2 += wn[i] * mn;
     }
     const double lbr = fmax(wsum(l1), wsum(l2)) * shrink;
     if (lbr > best || (lbr == best && cs > bc)) continue;
-    const double W = ssp_w2(L, ws, wn, mk, lane, err);
+    double dlb, dub;
+    dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
+    const double W = ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
     ++nsolve;
     if (W < best || (W == best && cs < bc)) {
       best = W;
@@ -544,6 +721,8 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     if (best_out) best_out[k] = best;
     atomicAdd(n_exact, (unsigned long long)nsolve);
     atomicAdd(n_exact + 2, (unsigned long long)nvisit);   // scal[3]: phase-A candidates (statistics)
+  }
+  __syncwarp();
   }
 }
 
@@ -579,11 +758,20 @@ int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const v
   if (N == 0) return 0;
   AsgLay L;
   L.make(m, mkmax, K, d);
-  int wpc = (int)((size_t)(optin - 1024) / L.bytes);
-  if (wpc < 1) return -1;
-  if (wpc > 8) wpc = 8;
-  const size_t sm = (size_t)wpc * L.bytes;
-  const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
+  // one warp per block (independent workspaces), as many resident blocks as shared memory allows
+  // (at most 16 per SM: the register limit), a persistent grid of SMs x blocks per SM
+  if (L.bytes + 1024 > (size_t)optin) return -1;
+  int dev = 0, nsm = 0, smem_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  int bps = (int)((size_t)smem_sm / (L.bytes + 1024));
+  bps = bps < 1 ? 1 : (bps > 16 ? 16 : bps);
+  const int wpc = 1;
+  const size_t sm = L.bytes;
+  int64_t nb = (int64_t)nsm * bps;
+  if (nb > N) nb = N;
+  const unsigned grid = (unsigned)nb;
   if (f64) {
     cudaFuncSetAttribute(k_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_assign<double><<<grid, 32 * wpc, sm, s>>>(off, N, (const double*)Y, (const double*)Wt, xc, wc, xb, xs,
