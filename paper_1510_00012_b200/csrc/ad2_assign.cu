@@ -258,6 +258,203 @@ __device__ __noinline__ double ssp_w2(const AsgLay& L, unsigned char* ws, const 
   return wsum(acc);
 }
 
+// The same successive-shortest-path solve with the Dijkstra state in registers: lane l owns
+// sources l + 32q and sinks l + 32q (q < Q, so m, m_k <= 32 Q); distances, settled flags and the
+// own potentials live in registers, the node argmin is a 64-bit order-preserving key reduced by
+// two 32-bit warp reductions (high word, then low word among the lanes holding the minimum high
+// word) and the lowest such lane supplies the node.  Only prev (for the path walk), pi (broadcast
+// of the settled node's potential) and the plan F stay in shared memory.  Warm start, bulk settle
+// of the sources with supply and the augmentation step are those of ssp_w2.
+template <int Q>
+__device__ __noinline__ double ssp_reg(const AsgLay& L, unsigned char* ws, const double* wn, int mk, int lane,
+                                       int* err, unsigned long long* stats) {
+  const int m = L.m, V = m + mk, ld = mk | 1;
+  const double* C = reinterpret_cast<const double*>(ws + L.oC);
+  double* F = reinterpret_cast<double*>(ws + L.oF);
+  double* pi = reinterpret_cast<double*>(ws + L.opi);
+  int* prev = reinterpret_cast<int*>(ws + L.oprev);
+  double* arem = reinterpret_cast<double*>(ws + L.oarem);
+  double* brem = reinterpret_cast<double*>(ws + L.obrem);
+  const double* om = reinterpret_cast<const double*>(ws + L.oom);
+  const double tiny = 1e-14;
+  unsigned naug = 0, nstep = 0;
+  for (int e = lane; e < m * ld; e += 32) F[e] = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    pi[i] = -pi[i];                                  // warm start: pi_i = -u_i, pi_{m+j} = v_j
+    arem[i] = wn[i];
+  }
+  for (int j = lane; j < mk; j += 32) brem[j] = om[j];
+  __syncwarp();
+  double ps[Q], pk[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = lane + 32 * q, j = lane + 32 * q;
+    ps[q] = i < m ? pi[i] : 0.0;
+    pk[q] = j < mk ? pi[m + j] : 0.0;
+  }
+  const int cap = 8 * V + 256;
+  for (int it = 0;; ++it) {
+    bool hs = false, hd = false;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      hs |= i < m && arem[i] > tiny;
+      hd |= i < mk && brem[i] > tiny;
+    }
+    if (!__any_sync(0xffffffffu, hs) || !__any_sync(0xffffffffu, hd)) break;
+    if (it >= cap) {
+      if (lane == 0) atomicOr(err, 1);
+      break;
+    }
+    double ds[Q], dk[Q];
+    unsigned dn = 0;                                 // settled: bit q source, bit Q + q sink
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      const bool act = i < m && arem[i] > tiny;
+      ds[q] = act ? 0.0 : CUDART_INF;
+      if (act || i >= m) dn |= 1u << q;
+      if (i < m) prev[i] = -1;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      double bd = CUDART_INF;
+      int bi = -1;
+      if (j < mk) {
+#pragma unroll 1
+        for (int i = 0; i < m; ++i)
+          if (arem[i] > tiny) {
+            const double nd = C[i * ld + j] + pi[i] - pk[q];
+            if (nd < bd) {
+              bd = nd;
+              bi = i;
+            }
+          }
+        prev[m + j] = bi;
+      } else {
+        dn |= 1u << (Q + q);
+      }
+      dk[q] = bd;
+    }
+    int t = -1;
+    double dt = CUDART_INF;
+    for (int step = 0; step < V; ++step) {
+      unsigned long long key = ~0ull;
+      int cand = V;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (!((dn >> q) & 1u)) {
+          const unsigned long long kv = okey(ds[q]);
+          if (kv < key) {
+            key = kv;
+            cand = lane + 32 * q;
+          }
+        }
+        if (!((dn >> (Q + q)) & 1u)) {
+          const unsigned long long kv = okey(dk[q]);
+          if (kv < key) {
+            key = kv;
+            cand = m + lane + 32 * q;
+          }
+        }
+      }
+      const unsigned hi = (unsigned)(key >> 32);
+      const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+      const unsigned lo = hi == mh ? (unsigned)key : 0xffffffffu;
+      const unsigned ml = __reduce_min_sync(0xffffffffu, lo);
+      if (mh == 0xffffffffu && ml == 0xffffffffu) break;
+      const unsigned ball = __ballot_sync(0xffffffffu, hi == mh && lo == ml);
+      const int bv = __shfl_sync(0xffffffffu, cand, __ffs(ball) - 1);
+      const double bd = okey_inv(((unsigned long long)mh << 32) | ml);
+      if (bv >= V || !(bd < CUDART_INF)) break;
+      ++nstep;
+      const bool snk = bv >= m;
+      const int nid = snk ? bv - m : bv;
+      if ((nid & 31) == lane) dn |= 1u << ((snk ? Q : 0) + (nid >> 5));
+      if (snk && brem[nid] > tiny) {                 // the nearest sink with demand left
+        t = bv;
+        dt = bd;
+        break;
+      }
+      const double pb = pi[bv];
+      if (snk) {                                     // reverse arcs j -> i carrying flow
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = lane + 32 * q;
+          if (!((dn >> q) & 1u) && F[i * ld + nid] > 0.0) {
+            const double nd = bd - C[i * ld + nid] + pb - ps[q];
+            if (nd < ds[q]) {
+              ds[q] = nd;
+              prev[i] = bv;
+            }
+          }
+        }
+      } else {                                       // forward arcs i -> j
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int j = lane + 32 * q;
+          if (!((dn >> (Q + q)) & 1u)) {
+            const double nd = bd + C[nid * ld + j] + pb - pk[q];
+            if (nd < dk[q]) {
+              dk[q] = nd;
+              prev[m + j] = nid;
+            }
+          }
+        }
+      }
+    }
+    if (t < 0) {
+      if (lane == 0) atomicOr(err, 1);
+      break;
+    }
+    ++naug;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {                   // reduced costs stay >= 0
+      const int i = lane + 32 * q;
+      if (i < m) {
+        ps[q] += ((dn >> q) & 1u) ? ds[q] : dt;
+        pi[i] = ps[q];
+      }
+      if (i < mk) {
+        pk[q] += ((dn >> (Q + q)) & 1u) ? dk[q] : dt;
+        pi[m + i] = pk[q];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double del = brem[t - m];
+      int v = t;
+      while (prev[v] >= 0) {
+        const int u = prev[v];
+        if (u >= m) del = fmin(del, F[v * ld + (u - m)]);
+        v = u;
+      }
+      const int s0 = v;
+      del = fmin(del, arem[s0]);
+      v = t;
+      while (prev[v] >= 0) {
+        const int u = prev[v];
+        if (u < m) F[u * ld + (v - m)] += del;
+        else F[v * ld + (u - m)] -= del;
+        v = u;
+      }
+      arem[s0] -= del;
+      brem[t - m] -= del;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(stats, (unsigned long long)naug);
+    atomicAdd(stats + 1, (unsigned long long)nstep);
+  }
+  double acc = 0.0;
+#pragma unroll 1
+  for (int i = 0; i < m; ++i)
+    for (int j = lane; j < mk; j += 32) acc += F[i * ld + j] * C[i * ld + j];
+  return wsum(acc);
+}
+
 // Dual lower bound and primal upper bound on W^2 for one pair (C in smem, fp64).  A log-domain
 // Sinkhorn run (fp32, eps-scaling from max C down to 1e-3 mean C) gives
 // approximate potentials f (24 iterations); two c-transforms in fp64 make them dual-feasible
@@ -708,7 +905,11 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     if (lbr > best || (lbr == best && cs > bc)) continue;
     double dlb, dub;
     dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
-    const double W = ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
+    const int qn = ((m > mk ? m : mk) + 31) >> 5;
+    const double W = qn <= 1   ? ssp_reg<1>(L, ws, wn, mk, lane, err, n_exact + 3)
+                     : qn <= 2 ? ssp_reg<2>(L, ws, wn, mk, lane, err, n_exact + 3)
+                     : qn <= 4 ? ssp_reg<4>(L, ws, wn, mk, lane, err, n_exact + 3)
+                               : ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
     ++nsolve;
     if (W < best || (W == best && cs < bc)) {
       best = W;

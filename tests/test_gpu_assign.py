@@ -69,6 +69,13 @@ def test_assign_ragged_and_edge_shapes(m, mk, d, K, dtype):
         assert (lab == 0).all()
 
 
+@pytest.mark.parametrize("m,mk,d,K,dtype", [(100, (60, 128), 3, 3, "f32"),     # 4 nodes per lane and side
+                                             (20, (120, 140), 2, 2, "f64")])    # m_k > 128: shared-memory SSP
+def test_assign_large_supports(m, mk, d, K, dtype):
+    b = wl.make_random(12, m, d, K=K, mk_range=mk, seed=11 + m, dtype=dtype)
+    check_assign(b, b.x0, b.w0)
+
+
 def test_assign_identity_and_duplicate_centroids():
     """Members equal to centroid c get c with W^2 = 0; a duplicated centroid ties to the lower index."""
     rng = np.random.default_rng(5)
