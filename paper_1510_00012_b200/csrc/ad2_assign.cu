@@ -49,8 +49,10 @@ struct AsgLay {
       return r;
     };
     oC = take(8 * (size_t)m * (mk | 1));       // rows padded to an odd stride (bank-conflict-free columns)
-    oF = take(8 * (size_t)m * (mk | 1) > 4 * (size_t)m * ldf_of(mk) ? 8 * (size_t)m * (mk | 1)
-                                                                    : 4 * (size_t)m * ldf_of(mk));
+    size_t fb = 8 * (size_t)m * (mk | 1);                 // flows; also the fp32 cost copy and
+    if (4 * (size_t)m * ldf_of(mk) > fb) fb = 4 * (size_t)m * ldf_of(mk);   // the staged member
+    if (8 * (size_t)mk * d > fb) fb = 8 * (size_t)mk * d;                    // points (aliases)
+    oF = take(fb);
     opi = take(8 * (size_t)V);
     odist = take(8 * (size_t)V);
     oprev = take(4 * (size_t)V);
@@ -66,7 +68,7 @@ struct AsgLay {
     olb = take(4 * (size_t)(mk + 4));                  // log b [m_k] (+ padding)
     oAb = take(4 * (size_t)m);                         // per-iteration row terms (base 2)
     oBb = take(4 * (size_t)(mk + 4));                  // per-iteration column terms (base 2)
-    oys = take(8 * (size_t)mk * d);                   // the member's points in fp64
+    oys = oF;                                         // the member's points in fp64, staged per build_cost
     bytes = o;
   }
 };
@@ -316,20 +318,54 @@ __device__ __noinline__ double ssp_reg(const AsgLay& L, unsigned char* ws, const
       if (act || i >= m) dn |= 1u << q;
       if (i < m) prev[i] = -1;
     }
+    // the sources with supply left, compacted in index order (ballot prefix counts)
+    int* act = reinterpret_cast<int*>(ws + L.odone);
+    int nact = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      const bool a_ = i < m && arem[i] > tiny;
+      const unsigned bal = __ballot_sync(0xffffffffu, a_);
+      if (a_) act[nact + __popc(bal & ((1u << lane) - 1u))] = i;
+      nact += __popc(bal);
+    }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int j = lane + 32 * q;
       double bd = CUDART_INF;
       int bi = -1;
       if (j < mk) {
+        // four independent running minima (sources t = r mod 4), merged lowest index first
+        double b4[4] = {CUDART_INF, CUDART_INF, CUDART_INF, CUDART_INF};
+        int i4[4] = {-1, -1, -1, -1};
+        int t = 0;
 #pragma unroll 1
-        for (int i = 0; i < m; ++i)
-          if (arem[i] > tiny) {
+        for (; t + 4 <= nact; t += 4) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int i = act[t + r];
             const double nd = C[i * ld + j] + pi[i] - pk[q];
-            if (nd < bd) {
-              bd = nd;
-              bi = i;
+            if (nd < b4[r]) {
+              b4[r] = nd;
+              i4[r] = i;
             }
+          }
+        }
+#pragma unroll 1
+        for (; t < nact; ++t) {
+          const int i = act[t];
+          const double nd = C[i * ld + j] + pi[i] - pk[q];
+          if (nd < b4[0]) {
+            b4[0] = nd;
+            i4[0] = i;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (b4[r] < bd || (b4[r] == bd && i4[r] >= 0 && i4[r] < bi)) {
+            bd = b4[r];
+            bi = i4[r];
           }
         prev[m + j] = bi;
       } else {
@@ -670,11 +706,13 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
 // C_ij = |x_ci - y_j|^2 in fp64 (difference form) with lane = centroid row: x_i is held in
 // registers 16 coordinates at a time, the member's points ys are broadcast from shared memory;
 // symbolic supports read the table instead.
+template <typename T>
 __device__ __noinline__ void build_cost(const AsgLay& L, unsigned char* ws, const double* __restrict__ xk, int mk, int lane,
-                           const int32_t* xs_c, const int32_t* Ysym, const double* Dtab, int V, int* err) {
+                           const int32_t* xs_c, const int32_t* Ysym, const double* Dtab, int V, int* err,
+                           const T* __restrict__ Yk) {
   const int m = L.m, d = L.d, ld = mk | 1;
   double* C = reinterpret_cast<double*>(ws + L.oC);
-  const double* ys = reinterpret_cast<const double*>(ws + L.oys);
+  double* ys = reinterpret_cast<double*>(ws + L.oys);
   if (Dtab) {
 #pragma unroll 1
     for (int i = 0; i < m; ++i)
@@ -688,6 +726,8 @@ __device__ __noinline__ void build_cost(const AsgLay& L, unsigned char* ws, cons
     }
     return;
   }
+  for (int e = lane; e < mk * d; e += 32) ys[e] = (double)Yk[e];   // ys shares the flows' region
+  __syncwarp();
   for (int i = lane; i < m; i += 32) {
     for (int t0 = 0; t0 < d; t0 += 16) {
       double xr[16];
@@ -782,10 +822,6 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
   __syncwarp();
   const int32_t* Ysym = reinterpret_cast<const int32_t*>(Y) + o0;
-  if (!Dtab) {
-    double* ys = reinterpret_cast<double*>(ws + L.oys);
-    for (int e = lane; e < mk * d; e += 32) ys[e] = (double)Yk[e];
-  }
   if (!Dtab)
     for (int t = lane; t < d; t += 32) {
       double a = 0.0;
@@ -832,7 +868,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
       }
     }
     if (cs >= K || lb * shrink > ubest) break;      // every remaining centroid has W^2 > ubest
-    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err);
+    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
     __syncwarp();
     const double* wn = wc + (int64_t)cs * m;
     double dlb, dub;
@@ -884,7 +920,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     if (lbs > best || (lbs == best && cs > bc)) break;            // no remaining centroid can win
     if (lane == 0) solved[cs >> 5] |= 1u << (cs & 31);
     // cost matrix C_ij = |x_ci - y_j|^2, difference form in fp64
-    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err);
+    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
     __syncwarp();
     // relaxed-marginal lower bounds
     const double* wn = wc + (int64_t)cs * m;
