@@ -161,9 +161,11 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
 
     sched_ev = []                                      # events around step/update (SURVEY.md §8(d) metric)
 
-    def step(arr, mem):
+    def step(arr, mem, after_init=None):
         ctx.init(arr["offsets"], arr["supports"], arr["weights"], arr["labels"], arr["x0"], arr["w0"], b.K, b.m,
                  s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype, cost_mode=args.cost_mode)
+        if after_init is not None:
+            after_init()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ad2.run_schedule(ctx, T, tau)
@@ -229,16 +231,31 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
         xo = torch.empty(b.x0.shape, dtype=H["x0"].dtype).pin_memory()
         wo = torch.empty(b.w0.shape, dtype=H["w0"].dtype).pin_memory()
 
+        # pipelined like a stream of batches: during timed step i (i < K) the next step's inputs are
+        # copied on the library's copy stream (ad2_prefetch) while step i computes; the warm-up
+        # step prefetches nothing, so every timed step's own host->device copy is inside the
+        # timed region (step 1's synchronously, steps 2..K's overlapped with steps 1..K-1)
+        k_e2e = max(1, min(args.steps, 3))
+        calls = {"n": 0}
+
+        def prefetch_next():
+            c = calls["n"]
+            if 1 <= c < k_e2e:
+                ctx.prefetch(H["offsets"], H["supports"], H["weights"], H["labels"], dtype=b.dtype,
+                             cost_mode=args.cost_mode)
+
         def step_host():
-            step(H, "host")
+            step(H, "host", prefetch_next)
             ctx.centroids_into(xo, wo, mem="host")
+            calls["n"] += 1
 
         ctx.set_profiling(False)
-        ms_e2e, _ = timed(step_host, max(1, min(args.steps, 3)), 1)
+        ms_e2e, _ = timed(step_host, k_e2e, 1)
         h2d = sum(v.numel() * v.element_size() for v in H.values())
         d2h = xo.numel() * xo.element_size() + wo.numel() * wo.element_size() + 2 * 8 * b.K
         e2e = {"value": entries_total * T / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_overlap": "next step's inputs prefetched during the current step (ad2_prefetch)"}
 
     if rank != 0:
         return

@@ -142,6 +142,16 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch *batch, const ad2_pa
                                const void *x0, const void *w0, const uint8_t *warm_mask,
                                double *rho_out);
 
+/* Host-batch prefetch (pipelining a stream of rounds): enqueue the host->device copies of a host
+ * batch (batch->mem == AD2_HOST; offsets, labels, supports, weights) on an internal copy stream,
+ * so they overlap whatever the context's stream is running (e.g. the current round).  The next
+ * ad2_barycenter_init with the same four host pointers and sizes uses those copies instead of
+ * copying again (it waits for them on its stream); any other init discards them.  The host
+ * arrays must stay valid and unchanged until that init returns (page-locked memory for an
+ * asynchronous copy).  cost_mode tells the layout of `supports` (AD2_COST_TABLE: int32 symbol
+ * ids).  Asynchronous; no state change besides the staging buffers. */
+ad2_status ad2_prefetch(ad2_ctx ctx, const ad2_batch *batch, ad2_cost_mode cost_mode);
+
 /* n_iters >= 0 B-ADMM iterations at fixed x (a4-a8), then the support-update partial sums of
  * the final Pi^(2) are formed for ad2_update_support.  Asynchronous (one CUDA graph per n). */
 ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters);

@@ -60,7 +60,7 @@ class Info(C.Structure):
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
            "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
-           "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_sync",
+           "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_prefetch", "ad2_sync",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH):
     L.ad2_cluster.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), C.POINTER(Loop), p, p, p, C.POINTER(i32),
                               p, p]
     L.ad2_merge_init.argtypes = [p, C.POINTER(Batch), p, p, p, C.c_int]
+    L.ad2_prefetch.argtypes = [p, C.POINTER(Batch), C.c_int]
     L.ad2_sync.argtypes = [p]
     L.ad2_last_error.argtypes = [p]
     L.ad2_last_error.restype = C.c_char_p
@@ -189,6 +190,17 @@ class Context:
         self._offsets = offsets
         self._offsets_host = None
         return rho
+
+    def prefetch(self, offsets, supports, weights, labels, dtype: Optional[str] = None, cost_mode: int = 0):
+        """ad2_prefetch: start the host->device copies of a host batch on the context's copy stream;
+        the next init(..., mem="host") with the same arrays uses them (pinned arrays overlap)."""
+        if dtype is None:
+            dt = getattr(weights, "dtype", None)
+            dtype = "f64" if str(dt) in ("float64", "torch.float64") else "f32"
+        d = 1 if (cost_mode == COST_TABLE or len(supports.shape) == 1) else int(supports.shape[1])
+        b = Batch(F64 if dtype == "f64" else F32, HOST, d, 1, 1, int(len(labels)), _ptr(offsets), _ptr(supports),
+                  _ptr(weights), _ptr(labels))
+        self._chk(self.L.ad2_prefetch(self.h, C.byref(b), int(cost_mode)))
 
     @property
     def offsets_host(self) -> np.ndarray:

@@ -79,6 +79,10 @@ struct DBuf {
   }
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
+static void dbuf_swap(DBuf& a, DBuf& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.cap, b.cap);
+}
 
 struct StepGraph {
   cudaGraphExec_t exec = nullptr;
@@ -122,6 +126,15 @@ struct ad2_ctx_s {
   DBuf stage_lab, mem_cl, pm;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
+  // ad2_prefetch: a second set of host-batch staging buffers, filled on a copy stream while the
+  // previous round computes; the next init with the same host arrays swaps them in
+  cudaStream_t pfs = nullptr;
+  cudaEvent_t pf_done = nullptr, stage_rel = nullptr;
+  DBuf pf_off, pf_lab, pf_Y, pf_W;
+  bool pf_valid = false;
+  const void *pf_k_off = nullptr, *pf_k_lab = nullptr, *pf_k_Y = nullptr, *pf_k_W = nullptr;
+  int64_t pf_N = 0;
+  size_t pf_ysz = 0, pf_wsz = 0;
   DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal, asg_tab;   // assignment step scratch
   DBuf cl_lab, cl_lab2, cl_x, cl_w, cl_warm, cl_cnt, cl_off, cl_Y, cl_W;   // outer loop (ad2_cluster)
   // symbolic supports: cost table D [V][V] (dtype tab_dtype), sorted member ids, centroid ids
@@ -138,6 +151,12 @@ struct ad2_ctx_s {
     clear_graphs();
     if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
     if (cap) cudaStreamDestroy(cap);
+    if (pfs) {
+      cudaStreamSynchronize(pfs);
+      cudaStreamDestroy(pfs);
+    }
+    if (pf_done) cudaEventDestroy(pf_done);
+    if (stage_rel) cudaEventDestroy(stage_rel);
   }
   void clear_graphs() {
     for (auto& kv : graphs) delete kv.second;
@@ -448,6 +467,46 @@ void ad2_destroy(ad2_ctx ctx) {
   delete ctx;
 }
 
+ad2_status ad2_prefetch(ad2_ctx ctx, const ad2_batch* b, ad2_cost_mode cost_mode) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!b || b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "prefetch: needs a host batch");
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "prefetch: dtype");
+  if (b->d < 1 || b->n_members < 0 || b->n_members > INT32_MAX) return ctx->fail(AD2_ERR_ARG, "prefetch: shape");
+  const int64_t N = b->n_members;
+  ctx->pf_valid = false;
+  if (N == 0) return AD2_OK;
+  if (!b->offsets || !b->supports || !b->weights || !b->labels) return ctx->fail(AD2_ERR_ARG, "prefetch: null array");
+  const int64_t n = static_cast<const int64_t*>(b->offsets)[N];
+  if (n < 0) return ctx->fail(AD2_ERR_ARG, "prefetch: offsets[N] < 0");
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  const size_t ysz = (cost_mode == AD2_COST_TABLE ? sizeof(int32_t) : es * (size_t)b->d) * (size_t)n;
+  CHK(set_dev(ctx));
+  if (!ctx->pfs) {
+    CU(cudaStreamCreateWithFlags(&ctx->pfs, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&ctx->pf_done, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->stage_rel, cudaEventDisableTiming));
+  }
+  CU(ctx->pf_off.reserve(sizeof(int64_t) * (N + 1)));
+  CU(ctx->pf_lab.reserve(sizeof(int32_t) * N));
+  CU(ctx->pf_Y.reserve(ysz));
+  CU(ctx->pf_W.reserve(es * (size_t)n));
+  CU(cudaStreamWaitEvent(ctx->pfs, ctx->stage_rel, 0));      // the previous init is done with them
+  CU(cudaMemcpyAsync(ctx->pf_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, ctx->pfs));
+  CU(cudaMemcpyAsync(ctx->pf_lab.p, b->labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice, ctx->pfs));
+  CU(cudaMemcpyAsync(ctx->pf_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, ctx->pfs));
+  CU(cudaMemcpyAsync(ctx->pf_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, ctx->pfs));
+  CU(cudaEventRecord(ctx->pf_done, ctx->pfs));
+  ctx->pf_valid = true;
+  ctx->pf_k_off = b->offsets;
+  ctx->pf_k_lab = b->labels;
+  ctx->pf_k_Y = b->supports;
+  ctx->pf_k_W = b->weights;
+  ctx->pf_N = N;
+  ctx->pf_ysz = ysz;
+  ctx->pf_wsz = es * (size_t)n;
+  return AD2_OK;
+}
+
 ad2_status ad2_nccl_unique_id(void* id_out) {
   if (!id_out) return AD2_ERR_ARG;
   if (!nccl_load()) return AD2_ERR_NCCL;
@@ -525,11 +584,30 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   // ---- index arrays on the device (host batches are staged), validated before any state change
   const int64_t* off_in = static_cast<const int64_t*>(b->offsets);
   const int32_t* lab_in = b->labels;
+  // a matching ad2_prefetch (same host arrays and sizes) already copied the batch: swap it in
+  bool prefetched = false;
+  if (host && N > 0 && ctx->pf_valid) {
+    const int64_t n_h = static_cast<const int64_t*>(b->offsets)[N];
+    const size_t ysz_h = (table ? sizeof(int32_t) : es * (size_t)d) * (size_t)n_h;
+    prefetched = ctx->pf_k_off == b->offsets && ctx->pf_k_lab == b->labels && ctx->pf_k_Y == b->supports &&
+                 ctx->pf_k_W == b->weights && ctx->pf_N == N && ctx->pf_ysz == ysz_h &&
+                 ctx->pf_wsz == es * (size_t)n_h;
+    ctx->pf_valid = false;
+    if (prefetched) {
+      CU(cudaStreamWaitEvent(s, ctx->pf_done, 0));
+      dbuf_swap(ctx->stage_off, ctx->pf_off);
+      dbuf_swap(ctx->stage_lab, ctx->pf_lab);
+      dbuf_swap(ctx->stage_Y, ctx->pf_Y);
+      dbuf_swap(ctx->stage_W, ctx->pf_W);
+    }
+  }
   if (host && N > 0) {
-    CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
-    CU(ctx->stage_lab.reserve(sizeof(int32_t) * N));
-    CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->stage_lab.p, b->labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    if (!prefetched) {
+      CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
+      CU(ctx->stage_lab.reserve(sizeof(int32_t) * N));
+      CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->stage_lab.p, b->labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    }
     off_in = ctx->stage_off.as<int64_t>();
     lab_in = ctx->stage_lab.as<int32_t>();
   }
@@ -760,10 +838,12 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   const void* Wsrc = b->weights;
   const size_t ysz = table ? sizeof(int32_t) * (size_t)n : es * (size_t)n * d;   // symbolic: int32 ids
   if (host && N > 0) {
-    CU(ctx->stage_Y.reserve(ysz));
-    CU(ctx->stage_W.reserve(es * (size_t)n));
-    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+    if (!prefetched) {
+      CU(ctx->stage_Y.reserve(ysz));
+      CU(ctx->stage_W.reserve(es * (size_t)n));
+      CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, ysz, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+    }
     Ysrc = ctx->stage_Y.p;
     Wsrc = ctx->stage_W.p;
   }
@@ -793,6 +873,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     CU(cudaMemcpyAsync(ctx->x.p, x0, es * (size_t)K * m * d, h2d, s));
   }
   CU(cudaMemcpyAsync(ctx->w.p, w0, es * (size_t)K * m, h2d, s));
+  if (host && ctx->stage_rel) CU(cudaEventRecord(ctx->stage_rel, s));   // staging buffers consumed
 
   // ---- Pi^(2),0 and Lambda = 0 (warm: new Pi2 built in P from the old Q, then swapped)
   if (warm) {
