@@ -146,7 +146,7 @@ __device__ __noinline__ double ssp_w2(const AsgLay& L, unsigned char* ws, const 
       double bd = CUDART_INF;
       int bi = -1;
       const double pj = pi[m + j];
-      #pragma unroll 1
+#pragma unroll 1
       for (int i = 0; i < m; ++i)
         if (arem[i] > tiny) {
           const double nd = C[i * ld + j] + pi[i] - pj;
@@ -504,7 +504,7 @@ __device__ __noinline__ double ctrans_lb(int m, int mk, const double* C, const f
   const int ld = mk | 1;
   for (int j = lane; j < mk; j += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j] - (double)fs[i]);
     v[j] = mn;
   }
@@ -512,7 +512,7 @@ __device__ __noinline__ double ctrans_lb(int m, int mk, const double* C, const f
   double acc = 0.0;
   for (int i = lane; i < m; i += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j] - v[j]);
     u[i] = mn;
     acc += a[i] * mn;
@@ -531,13 +531,13 @@ __device__ __noinline__ double zero_ctrans_lb(int m, int mk, const double* C, co
   const int ld = mk | 1;
   for (int j = lane; j < mk; j += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j]);
     v[j] = mn;
   }
   for (int i = lane; i < m; i += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j]);
     u[i] = mn;
   }
@@ -545,14 +545,14 @@ __device__ __noinline__ double zero_ctrans_lb(int m, int mk, const double* C, co
   double a1 = 0.0, a2 = 0.0;
   for (int i = lane; i < m; i += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j] - v[j]);
     a1 += a[i] * mn;
     a2 += a[i] * u[i];
   }
   for (int j = lane; j < mk; j += 32) {
     double mn = CUDART_INF;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j] - u[i]);
     a1 += b[j] * v[j];
     a2 += b[j] * mn;
@@ -664,19 +664,19 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
   __syncwarp();
   for (int i = lane; i < m; i += 32) {              // rows scaled down to <= a_i
     double r = 0.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) r += P[i * ld + j];
     const double x = r > a[i] ? a[i] / r : 1.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) P[i * ld + j] *= x;
   }
   __syncwarp();
   for (int j = lane; j < mk; j += 32) {             // columns scaled down to <= b_j
     double c = 0.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) c += P[i * ld + j];
     const double y = c > b[j] ? b[j] / c : 1.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) P[i * ld + j] *= y;
     v[j] = b[j] - c * y;                            // column deficit
   }
@@ -684,7 +684,7 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
   double dr = 0.0;
   for (int i = lane; i < m; i += 32) {
     double r = 0.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = 0; j < mk; ++j) r += P[i * ld + j];
     u[i] = fmax(a[i] - r, 0.0);                     // row deficit
     dr += u[i];
@@ -696,10 +696,10 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
 #pragma unroll 1
   for (int i = 0; i < m; ++i)
     for (int j = lane; j < mk; j += 32) {
-    const int e = i * ld + j;
-    const double pe = P[e] + u[i] * fmax(v[j], 0.0) * idr;
-    cu += C[e] * pe;
-  }
+      const int e = i * ld + j;
+      const double pe = P[e] + u[i] * fmax(v[j], 0.0) * idr;
+      cu += C[e] * pe;
+    }
   ub = wsum(cu);
 }
 
@@ -717,13 +717,13 @@ __device__ __noinline__ void build_cost(const AsgLay& L, unsigned char* ws, cons
 #pragma unroll 1
     for (int i = 0; i < m; ++i)
       for (int j = lane; j < mk; j += 32) {
-      const int e = i * ld + j;
-      const int sa = xs_c[i], sb = Ysym[j];
-      double a = 0.0;
-      if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
-      else a = Dtab[(int64_t)sa * V + sb];
-      C[e] = a;
-    }
+        const int e = i * ld + j;
+        const int sa = xs_c[i], sb = Ysym[j];
+        double a = 0.0;
+        if (sa < 0 || sa >= V || sb < 0 || sb >= V) atomicOr(err, 4);
+        else a = Dtab[(int64_t)sa * V + sb];
+        C[e] = a;
+      }
     return;
   }
   for (int e = lane; e < mk * d; e += 32) ys[e] = (double)Yk[e];   // ys shares the flows' region
@@ -734,7 +734,7 @@ __device__ __noinline__ void build_cost(const AsgLay& L, unsigned char* ws, cons
 #pragma unroll
       for (int t = 0; t < 16; ++t) xr[t] = (t0 + t < d) ? xk[(int64_t)i * d + t0 + t] : 0.0;
       const int tn = d - t0 < 16 ? d - t0 : 16;
-      #pragma unroll 1
+#pragma unroll 1
       for (int j = 0; j < mk; ++j) {
         const double* yj = ys + j * d + t0;
         double a = (t0 == 0) ? 0.0 : C[i * ld + j];
@@ -759,7 +759,7 @@ __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, 
   __shared__ double tot;
   if (threadIdx.x == 0) {
     double s = 0.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) s += (double)w[(int64_t)c * m + i];
     tot = s;
   }
@@ -770,7 +770,7 @@ __global__ void k_assign_prep(const T* __restrict__ x, const T* __restrict__ w, 
   __syncthreads();
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
     double s = 0.0;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = 0; i < m; ++i) s += wc[(int64_t)c * m + i] * xc[((int64_t)c * m + i) * d + t];
     xb[(int64_t)c * d + t] = s;
   }
@@ -801,165 +801,165 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
   // persistent warps: members are taken from a global counter (n_exact[5]) one at a time, so
   // a warp with cheap members moves on instead of idling until its block's slowest warp ends
   for (;;) {
-  unsigned long long kq = 0;
-  if (lane == 0) kq = atomicAdd(n_exact + 5, 1ull);
-  const int64_t k = (int64_t)__shfl_sync(0xffffffffu, kq, 0);
-  if (k >= N) break;
-  const int m = L.m, K = L.K, d = L.d;
-  double* C = reinterpret_cast<double*>(ws + L.oC);
-  double* om = reinterpret_cast<double*>(ws + L.oom);
-  double* LB = reinterpret_cast<double*>(ws + L.oLB);
-  unsigned* solved = reinterpret_cast<unsigned*>(ws + L.osolv);
-  double* yb = reinterpret_cast<double*>(ws + L.oyb);
-  const int64_t o0 = off[k];
-  const int mk = (int)(off[k + 1] - o0), ld = mk | 1;
-  const T* Yk = Y + o0 * d;
+    unsigned long long kq = 0;
+    if (lane == 0) kq = atomicAdd(n_exact + 5, 1ull);
+    const int64_t k = (int64_t)__shfl_sync(0xffffffffu, kq, 0);
+    if (k >= N) break;
+    const int m = L.m, K = L.K, d = L.d;
+    double* C = reinterpret_cast<double*>(ws + L.oC);
+    double* om = reinterpret_cast<double*>(ws + L.oom);
+    double* LB = reinterpret_cast<double*>(ws + L.oLB);
+    unsigned* solved = reinterpret_cast<unsigned*>(ws + L.osolv);
+    double* yb = reinterpret_cast<double*>(ws + L.oyb);
+    const int64_t o0 = off[k];
+    const int mk = (int)(off[k + 1] - o0), ld = mk | 1;
+    const T* Yk = Y + o0 * d;
 
-  // member weights renormalised in fp64 (O1), member mean
-  double s = 0.0;
-  for (int j = lane; j < mk; j += 32) s += (double)Wt[o0 + j];
-  s = wsum(s);
-  for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
-  __syncwarp();
-  const int32_t* Ysym = reinterpret_cast<const int32_t*>(Y) + o0;
-  if (!Dtab)
-    for (int t = lane; t < d; t += 32) {
-      double a = 0.0;
-      #pragma unroll 1
-      for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
-      yb[t] = a;
-    }
-  for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
-  __syncwarp();
-  for (int c = lane; c < K; c += 32) {              // |mean_c - mean_k|^2 <= W^2
-    double a = 0.0;
+    // member weights renormalised in fp64 (O1), member mean
+    double s = 0.0;
+    for (int j = lane; j < mk; j += 32) s += (double)Wt[o0 + j];
+    s = wsum(s);
+    for (int j = lane; j < mk; j += 32) om[j] = (double)Wt[o0 + j] / s;
+    __syncwarp();
+    const int32_t* Ysym = reinterpret_cast<const int32_t*>(Y) + o0;
     if (!Dtab)
-      for (int t = 0; t < d; ++t) {
-        const double df = xb[(int64_t)c * d + t] - yb[t];
-        a += df * df;
+      for (int t = lane; t < d; t += 32) {
+        double a = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
+        yb[t] = a;
       }
-    LB[c] = a;
-  }
-  __syncwarp();
-  const double shrink = 1.0 - 1e-12;               // fp64 rounding margin on the bounds
-  const double grow = 1.0 + 1e-9;                  // margin on the rounded-plan upper bound
-  double best = CUDART_INF;
-  int bc = -1;
-  unsigned nsolve = 0, nvisit = 0;
-  // phase A: candidates in increasing mean-bound order while the mean bound is below the best
-  // upper bound: sharpen each bound (relaxed marginals, Sinkhorn dual) and collect upper bounds
-  double ubest = CUDART_INF;
-  for (int visit = 0; visit < K; ++visit) {
+    for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
     __syncwarp();
-    double lb = CUDART_INF;
-    int cs = K;
-    for (int c = lane; c < K; c += 32)
-      if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
-        lb = LB[c];
-        cs = c;
-      }
+    for (int c = lane; c < K; c += 32) {              // |mean_c - mean_k|^2 <= W^2
+      double a = 0.0;
+      if (!Dtab)
+        for (int t = 0; t < d; ++t) {
+          const double df = xb[(int64_t)c * d + t] - yb[t];
+          a += df * df;
+        }
+      LB[c] = a;
+    }
+    __syncwarp();
+    const double shrink = 1.0 - 1e-12;               // fp64 rounding margin on the bounds
+    const double grow = 1.0 + 1e-9;                  // margin on the rounded-plan upper bound
+    double best = CUDART_INF;
+    int bc = -1;
+    unsigned nsolve = 0, nvisit = 0;
+    // phase A: candidates in increasing mean-bound order while the mean bound is below the best
+    // upper bound: sharpen each bound (relaxed marginals, Sinkhorn dual) and collect upper bounds
+    double ubest = CUDART_INF;
+    for (int visit = 0; visit < K; ++visit) {
+      __syncwarp();
+      double lb = CUDART_INF;
+      int cs = K;
+      for (int c = lane; c < K; c += 32)
+        if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
+          lb = LB[c];
+          cs = c;
+        }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
-      if (ol < lb || (ol == lb && oc < cs)) {
-        lb = ol;
-        cs = oc;
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
+        if (ol < lb || (ol == lb && oc < cs)) {
+          lb = ol;
+          cs = oc;
+        }
       }
+      if (cs >= K || lb * shrink > ubest) break;      // every remaining centroid has W^2 > ubest
+      build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
+      __syncwarp();
+      const double* wn = wc + (int64_t)cs * m;
+      double dlb, dub;
+      const double zlb = zero_ctrans_lb(m, mk, C, wn, om, reinterpret_cast<double*>(ws + L.opi),
+                                        reinterpret_cast<double*>(ws + L.opi) + m, lane);
+      if (zlb * shrink > ubest) {                      // cannot win: no Sinkhorn run
+        dlb = zlb;
+        dub = CUDART_INF;
+      } else {
+        dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
+        dlb = fmax(dlb, zlb);
+        ++nvisit;
+      }
+      ubest = fmin(ubest, dub * grow);
+      if (lane == 0) {
+        LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
+        solved[cs >> 5] |= 1u << (cs & 31);           // visited in phase A
+      }
+      __syncwarp();
     }
-    if (cs >= K || lb * shrink > ubest) break;      // every remaining centroid has W^2 > ubest
-    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
+    // phase B: only phase-A centroids can win (the others have mean bound > ubest); exact solves
+    // in increasing sharpened-bound order until the bound exceeds the best exact W^2
+    for (int c = lane; c < K; c += 32) {
+      const bool vis = (solved[c >> 5] >> (c & 31)) & 1u;
+      if (!vis) LB[c] = CUDART_INF;
+    }
+    for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
     __syncwarp();
-    const double* wn = wc + (int64_t)cs * m;
-    double dlb, dub;
-    const double zlb = zero_ctrans_lb(m, mk, C, wn, om, reinterpret_cast<double*>(ws + L.opi),
-                                      reinterpret_cast<double*>(ws + L.opi) + m, lane);
-    if (zlb * shrink > ubest) {                      // cannot win: no Sinkhorn run
-      dlb = zlb;
-      dub = CUDART_INF;
-    } else {
-      dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
-      dlb = fmax(dlb, zlb);
-      ++nvisit;
+    for (int visit = 0; visit < K; ++visit) {
+      __syncwarp();                                   // C / solved of the previous visit consumed
+      double lb = CUDART_INF;
+      int cs = K;
+      for (int c = lane; c < K; c += 32)
+        if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
+          lb = LB[c];
+          cs = c;
+        }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
+        if (ol < lb || (ol == lb && oc < cs)) {
+          lb = ol;
+          cs = oc;
+        }
+      }
+      if (cs >= K) break;
+      const double lbs = lb * shrink;
+      if (lbs > best || (lbs == best && cs > bc)) break;            // no remaining centroid can win
+      if (lane == 0) solved[cs >> 5] |= 1u << (cs & 31);
+      // cost matrix C_ij = |x_ci - y_j|^2, difference form in fp64
+      build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
+      __syncwarp();
+      // relaxed-marginal lower bounds
+      const double* wn = wc + (int64_t)cs * m;
+      double l1 = 0.0, l2 = 0.0;
+      for (int j = lane; j < mk; j += 32) {
+        double mn = CUDART_INF;
+#pragma unroll 1
+        for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j]);
+        l1 += om[j] * mn;
+      }
+      for (int i = lane; i < m; i += 32) {
+        double mn = CUDART_INF;
+#pragma unroll 1
+        for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j]);
+        l2 += wn[i] * mn;
+      }
+      const double lbr = fmax(wsum(l1), wsum(l2)) * shrink;
+      if (lbr > best || (lbr == best && cs > bc)) continue;
+      double dlb, dub;
+      dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
+      const int qn = ((m > mk ? m : mk) + 31) >> 5;
+      const double W = qn <= 1   ? ssp_reg<1>(L, ws, wn, mk, lane, err, n_exact + 3)
+                       : qn <= 2 ? ssp_reg<2>(L, ws, wn, mk, lane, err, n_exact + 3)
+                       : qn <= 4 ? ssp_reg<4>(L, ws, wn, mk, lane, err, n_exact + 3)
+                                 : ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
+      ++nsolve;
+      if (W < best || (W == best && cs < bc)) {
+        best = W;
+        bc = cs;
+      }
+      __syncwarp();
     }
-    ubest = fmin(ubest, dub * grow);
     if (lane == 0) {
-      LB[cs] = fmax(lb, dlb);                       // sharpened bound (cs stays unsolved)
-      solved[cs >> 5] |= 1u << (cs & 31);           // visited in phase A
+      labels[k] = bc;
+      if (best_out) best_out[k] = best;
+      atomicAdd(n_exact, (unsigned long long)nsolve);
+      atomicAdd(n_exact + 2, (unsigned long long)nvisit);   // scal[3]: phase-A candidates (statistics)
     }
     __syncwarp();
-  }
-  // phase B: only phase-A centroids can win (the others have mean bound > ubest); exact solves
-  // in increasing sharpened-bound order until the bound exceeds the best exact W^2
-  for (int c = lane; c < K; c += 32) {
-    const bool vis = (solved[c >> 5] >> (c & 31)) & 1u;
-    if (!vis) LB[c] = CUDART_INF;
-  }
-  for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
-  __syncwarp();
-  for (int visit = 0; visit < K; ++visit) {
-    __syncwarp();                                   // C / solved of the previous visit consumed
-    double lb = CUDART_INF;
-    int cs = K;
-    for (int c = lane; c < K; c += 32)
-      if (!((solved[c >> 5] >> (c & 31)) & 1u) && LB[c] < lb) {
-        lb = LB[c];
-        cs = c;
-      }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const double ol = __shfl_xor_sync(0xffffffffu, lb, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, cs, o);
-      if (ol < lb || (ol == lb && oc < cs)) {
-        lb = ol;
-        cs = oc;
-      }
-    }
-    if (cs >= K) break;
-    const double lbs = lb * shrink;
-    if (lbs > best || (lbs == best && cs > bc)) break;            // no remaining centroid can win
-    if (lane == 0) solved[cs >> 5] |= 1u << (cs & 31);
-    // cost matrix C_ij = |x_ci - y_j|^2, difference form in fp64
-    build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
-    __syncwarp();
-    // relaxed-marginal lower bounds
-    const double* wn = wc + (int64_t)cs * m;
-    double l1 = 0.0, l2 = 0.0;
-    for (int j = lane; j < mk; j += 32) {
-      double mn = CUDART_INF;
-      #pragma unroll 1
-      for (int i = 0; i < m; ++i) mn = fmin(mn, C[i * ld + j]);
-      l1 += om[j] * mn;
-    }
-    for (int i = lane; i < m; i += 32) {
-      double mn = CUDART_INF;
-      #pragma unroll 1
-      for (int j = 0; j < mk; ++j) mn = fmin(mn, C[i * ld + j]);
-      l2 += wn[i] * mn;
-    }
-    const double lbr = fmax(wsum(l1), wsum(l2)) * shrink;
-    if (lbr > best || (lbr == best && cs > bc)) continue;
-    double dlb, dub;
-    dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
-    const int qn = ((m > mk ? m : mk) + 31) >> 5;
-    const double W = qn <= 1   ? ssp_reg<1>(L, ws, wn, mk, lane, err, n_exact + 3)
-                     : qn <= 2 ? ssp_reg<2>(L, ws, wn, mk, lane, err, n_exact + 3)
-                     : qn <= 4 ? ssp_reg<4>(L, ws, wn, mk, lane, err, n_exact + 3)
-                               : ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
-    ++nsolve;
-    if (W < best || (W == best && cs < bc)) {
-      best = W;
-      bc = cs;
-    }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    labels[k] = bc;
-    if (best_out) best_out[k] = best;
-    atomicAdd(n_exact, (unsigned long long)nsolve);
-    atomicAdd(n_exact + 2, (unsigned long long)nvisit);   // scal[3]: phase-A candidates (statistics)
-  }
-  __syncwarp();
   }
 }
 
