@@ -467,8 +467,8 @@ k_badmm_tma(const IterArgs<T> a) {
 
 // Row-wise cost sums for variant 2 (no C cache), one warp per sorted member -> pm[s]: lane i
 // holds x_i, the member's Y rows (stride DY) are broadcast 16-byte loads, and the cost is the
-// difference form sum_t (y_jt - x_it)^2 (no cancellation: these are the reported rho and
-// objective).  P == nullptr: sum of C (Eq.rho numerator); otherwise sum of C .* Pi1
+// difference form sum_t (y_jt - x_it)^2 (no cancellation: the reported objective).
+// P == nullptr: sum of C (Eq.rho numerator) in closed form; otherwise sum of C .* Pi1
 // (surrogate objective).  Accumulated in double per member; the cluster sums are
 // formed in a fixed order by k_dsum_members.
 template <typename T> __host__ __device__ constexpr int cost_member_warps() { return sizeof(T) == 8 ? 2 : 4; }
@@ -489,8 +489,12 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
   __shared__ __align__(16) T sY[NW][MKX * DY];
   __shared__ __align__(16) T sP[NW][MKX * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t sidx = (int64_t)blockIdx.x * NW + warp;
-  if (sidx >= N) return;
+  // grid-stride over the sorted members (a few resident CTAs per SM instead of N / NW short
+  // CTAs, whose launch and teardown bounded the kernel); x_i is reloaded only when the cluster
+  // changes (members are sorted by cluster)
+  T2 nx2[DP / 2], msk2[DP / 2];                      // -x_i (difference form); mask only for DP == 4
+  int c_prev = -1;
+  for (int64_t sidx = (int64_t)blockIdx.x * NW + warp; sidx < N; sidx += (int64_t)gridDim.x * NW) {
   const int c = mem_cl[sidx];
   const int64_t o0 = off[sidx];
   const int mk = (int)(off[sidx + 1] - o0);
@@ -504,17 +508,50 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
       for (int e = lane; e < mk * ld / E; e += 32) pd[e] = __ldcs(ps + e);
     }
   }
-  T2 nx2[DP / 2], msk2[DP / 2];                      // -x_i (difference form); mask only for DP == 4
   const int i = lane;
   const bool rowok = i < m;
+  if (c != c_prev) {
 #pragma unroll
-  for (int t = 0; t < DP / 2; ++t) {
-    const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
-    const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
-    nx2[t] = PR::make(-v0, -v1);
-    msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+    for (int t = 0; t < DP / 2; ++t) {
+      const T v0 = (rowok && 2 * t < d) ? x[((int64_t)c * m + i) * d + 2 * t] : T(0);
+      const T v1 = (rowok && 2 * t + 1 < d) ? x[((int64_t)c * m + i) * d + 2 * t + 1] : T(0);
+      nx2[t] = PR::make(-v0, -v1);
+      msk2[t] = PR::make(2 * t < d ? T(1) : T(0), 2 * t + 1 < d ? T(1) : T(0));
+    }
+    c_prev = c;
   }
   __syncwarp();
+  if (!P) {
+    // Eq.rho numerator in closed form, in fp64 (products of fp32 values are exact there):
+    //   sum_ij |x_i - y_j|^2 = m_k sum_i |x_i|^2 + m sum_j |y_j|^2 - 2 sum_i x_i . (sum_j y_j)
+    // O((m + m_k) d) per member instead of O(m m_k d); the cancellation costs no more than a few
+    // digits of fp64 (|x|^2, |y|^2 within a small factor of the cost on these workloads)
+    __shared__ double sSy[NW][16];
+    double q = 0.0;                                   // lane t < d: sum_j y_jt^2, then sum_j y_jt
+    if (lane < d && lane < 16) {
+      double sy = 0.0;
+      for (int j = 0; j < mk; ++j) {
+        const double v = (double)sY[warp][j * DY + lane];
+        sy += v;
+        q = fma(v, v, q);
+      }
+      sSy[warp][lane] = sy;
+    }
+    __syncwarp();
+    double xi2 = 0.0, xdot = 0.0;                     // lane i < m: |x_i|^2 and x_i . sum_j y_j
+#pragma unroll
+    for (int t = 0; t < DP / 2; ++t) {                // nx2 = -x_i (0 past d and for rows >= m)
+      const double x0 = -(double)nx2[t].x, x1 = -(double)nx2[t].y;
+      xi2 = fma(x0, x0, fma(x1, x1, xi2));
+      if (2 * t < d) xdot = fma(x0, sSy[warp][2 * t], xdot);
+      if (2 * t + 1 < d) xdot = fma(x1, sSy[warp][2 * t + 1], xdot);
+    }
+    double acc = (double)mk * xi2 - 2.0 * xdot + (double)m * q;
+    for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
+    if (lane == 0) pm[sidx] = acc;
+    __syncwarp();                                   // sY / sSy reused by the next member
+    continue;
+  }
   T s = T(0);
   for (int j0 = 0; j0 < mk; j0 += 4) {
     T2 c2[4];
@@ -544,6 +581,8 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
   double acc = (double)s;
   for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
   if (lane == 0) pm[sidx] = acc;
+  __syncwarp();
+  }
 }
 
 }  // namespace ad2k

@@ -66,7 +66,16 @@ void launch_cost_member<float>(int dp, const int64_t* off, int64_t N, const int3
                              const float* x, const float* P, double* pm, int m, int d, int ld, cudaStream_t s) {
   if (N == 0) return;
   constexpr int NW = cost_member_warps<float>();
-  const unsigned g = (unsigned)((N + NW - 1) / NW);
+  static int grid_cap = 0;                             // resident CTAs (grid-stride kernel)
+  if (!grid_cap) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cost_member<float, 16>, 32 * NW, 0);
+    grid_cap = nsm * (per > 0 ? per : 1);
+  }
+  const int64_t need = (N + NW - 1) / NW;
+  const unsigned g = (unsigned)(need < grid_cap ? need : grid_cap);
   if (dp <= 4) k_cost_member<float, 4><<<g, 32 * NW, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
   else k_cost_member<float, 16><<<g, 32 * NW, 0, s>>>(off, N, mem_cl, Y, x, P, pm, m, d, ld);
 }
