@@ -1239,7 +1239,7 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
   CU(cudaMemsetAsync(ctx->asg_scal.p, 0, 64, s));
   unsigned long long* scal = ctx->asg_scal.as<unsigned long long>();   // [0] mkmax [1] n_exact [2] err [3] visits
   int* err = reinterpret_cast<int*>(scal + 2);
-  unsigned long long hs[6] = {0, 0, 0, 0, 0, 0};   // [4] augmentations [5] Dijkstra steps
+  unsigned long long hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // [4] augmentations [5] Dijkstra steps [7] Sinkhorn its
   if (N > 0) {
     assign_mkmax(static_cast<const int64_t*>(off), N, scal, err, s);
     CHK(launch_check(ctx, "k_assign_mk"));
@@ -1270,8 +1270,8 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
   CU(cudaStreamSynchronize(s));
   if (n_exact_out) *n_exact_out = (int64_t)hs[1];
   if (getenv("AD2_ASSIGN_STATS"))
-    fprintf(stderr, "[ad2_assign] N=%lld K=%d exact=%llu sinkhorn_candidates=%llu augmentations=%llu steps=%llu\n",
-            (long long)N, K, hs[1], hs[3], hs[4], hs[5]);
+    fprintf(stderr, "[ad2_assign] N=%lld K=%d exact=%llu sinkhorn_candidates=%llu sinkhorn_iterations=%llu "
+            "augmentations=%llu steps=%llu\n", (long long)N, K, hs[1], hs[3], hs[7], hs[4], hs[5]);
   if (hs[2] & 1) return ctx->fail(AD2_ERR_NONFINITE, "assign: a transport solve did not terminate");
   if (hs[2] & 4) return ctx->fail(AD2_ERR_ARG, "assign: a symbol id outside [0, V) of the cost table");
   return AD2_OK;

@@ -566,7 +566,7 @@ __device__ __noinline__ double zero_ctrans_lb(int m, int mk, const double* C, co
 // early with ub = +inf (the candidate cannot win)
 // duals_only: stop after the lower bound, leaving the dual-feasible (u, v) in the pi region
 __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, const double* a, int mk, int lane, double prune_at,
-                            double& lb, double& ub, bool duals_only = false) {
+                            double& lb, double& ub, bool duals_only = false, unsigned long long* iters = nullptr) {
   const int m = L.m, ld = mk | 1;
   const double* C = reinterpret_cast<const double*>(ws + L.oC);
   double* P = reinterpret_cast<double*>(ws + L.oF);
@@ -601,7 +601,7 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
   for (int o = 16; o >= 1; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
   csum = wsum(csum);
   const float eps_f = (float)fmax(1e-3 * csum / (double)(m * mk), 1e-30);
-  float eps = (float)fmax(cmax, 1e-30);
+  float eps = (float)fmax(0.25 * cmax, 1e-30);          // first iteration at cmax / 8
   for (int i = lane; i < m; i += 32) fs[i] = 0.f;
   for (int j = lane; j < mk; j += 32) gs[j] = 0.f;
   __syncwarp();
@@ -641,16 +641,18 @@ __device__ __noinline__ void dual_bounds(const AsgLay& L, unsigned char* ws, con
       fs[i] = -eps * LN2 * (mx + __log2f(s0 + s1));
     }
     __syncwarp();
-    if (it == 3 || it == 7 || it == 15) {           // early exit for clearly worse centroids
+    if (it == 1 || it == 3 || it == 7 || it == 15) {   // early exit for clearly worse centroids
       const double l = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
       if (l * (1.0 - 1e-12) > prune_at) {
         lb = l;
         ub = CUDART_INF;
+        if (iters && lane == 0) atomicAdd(iters, (unsigned long long)(it + 1));
         return;
       }
     }
   }
   lb = ctrans_lb(m, mk, C, fs, a, b, u, v, lane);
+  if (iters && lane == 0) atomicAdd(iters, 24ull);
   if (duals_only) {
     ub = CUDART_INF;
     return;
@@ -878,7 +880,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
         dlb = zlb;
         dub = CUDART_INF;
       } else {
-        dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub);
+        dual_bounds(L, ws, wn, mk, lane, ubest, dlb, dub, false, n_exact + 6);   // [7]: Sinkhorn iterations
         dlb = fmax(dlb, zlb);
         ++nvisit;
       }
