@@ -586,13 +586,14 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   const int32_t* lab_in = b->labels;
   // a matching ad2_prefetch (same host arrays and sizes) already copied the batch: swap it in
   bool prefetched = false;
-  if (host && N > 0 && ctx->pf_valid) {
+  const bool pf_pending = ctx->pf_valid;
+  ctx->pf_valid = false;                            // any init consumes or discards a prefetch
+  if (host && N > 0 && pf_pending) {
     const int64_t n_h = static_cast<const int64_t*>(b->offsets)[N];
     const size_t ysz_h = (table ? sizeof(int32_t) : es * (size_t)d) * (size_t)n_h;
     prefetched = ctx->pf_k_off == b->offsets && ctx->pf_k_lab == b->labels && ctx->pf_k_Y == b->supports &&
                  ctx->pf_k_W == b->weights && ctx->pf_N == N && ctx->pf_ysz == ysz_h &&
                  ctx->pf_wsz == es * (size_t)n_h;
-    ctx->pf_valid = false;
     if (prefetched) {
       CU(cudaStreamWaitEvent(s, ctx->pf_done, 0));
       dbuf_swap(ctx->stage_off, ctx->pf_off);

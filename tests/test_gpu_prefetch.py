@@ -90,3 +90,25 @@ def test_prefetch_argument_errors():
     assert ctx.L.ad2_prefetch(ctx.h, None, 0) == 1                 # AD2_ERR_ARG: no batch
     ctx.prefetch(b.offsets[:1], b.supports[:0], b.weights[:0], b.labels[:0], dtype=b.dtype)   # N = 0: no-op
     ctx.close()
+
+
+def test_any_init_discards_a_pending_prefetch():
+    """A prefetch not consumed by the next init is dropped: a later host init of the same (since
+    rewritten) arrays copies them again instead of using the stale staged copy."""
+    torch = torch_cuda()
+    b = wl.make_config(2, N=1200, K=3)
+    H = host_arrays(b, torch)
+    ctx = ad2.Context(0)
+    ctx.prefetch(H["offsets"], H["supports"], H["weights"], H["labels"], dtype=b.dtype)
+    dev = {k: v.cuda() for k, v in H.items()}
+    ctx.init(dev["offsets"], dev["supports"], dev["weights"], dev["labels"], dev["x0"], dev["w0"], b.K, b.m,
+             b.sched.rho0, b.sched.eps, b.sched.rule, dtype=b.dtype)          # device init: discards it
+    torch.cuda.synchronize()
+    H["supports"].mul_(1.5)                                                       # same pointers, new data
+    x, _, o = run_round(ctx, H, b)
+    ref = ad2.Context(0)
+    x0, _, o0 = run_round(ref, H, b)
+    np.testing.assert_array_equal(x, x0)
+    np.testing.assert_array_equal(o, o0)
+    ctx.close()
+    ref.close()
