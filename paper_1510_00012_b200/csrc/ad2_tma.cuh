@@ -321,7 +321,7 @@ k_badmm_tma(const IterArgs<T> a) {
         if (4 * jb >= mkw) break;
         T2 c2[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) c2[u] = PR::make(xx + Ys[(4 * jb + u) * DY + YYI], T(0));
+        for (int u = 0; u < 4; ++u) c2[u] = PR::make(xx, Ys[(4 * jb + u) * DY + YYI]);   // (|x|^2, |y|^2) + dot pairs
 #pragma unroll
         for (int tt = 0; tt < DP / E; ++tt) {
           V v[4];
