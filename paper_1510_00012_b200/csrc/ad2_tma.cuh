@@ -358,7 +358,8 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * jb + u, jt = j - ch * MP;
             const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
-            if (PAD || j < mkw) tile[jt * 32 + ((((lane / E) ^ (jt & 7))) * E) + (lane % E)] = v;   // P slot bound
+            // swizzle ((lane / E) ^ (jt & 7)) * E + lane % E == lane ^ ((jt & 7) * E) (E a power of 2)
+            if (PAD || j < mkw) tile[jt * 32 + (lane ^ ((jt & 7) * E))] = v;   // P slot bound
           }
         }
         __syncwarp();
@@ -368,7 +369,7 @@ k_badmm_tma(const IterArgs<T> a) {
           T2 sp[MP / E];
 #pragma unroll
           for (int cc = 0; cc < MP / E; ++cc) {
-            const V v = *reinterpret_cast<const V*>(&tile[i * 32 + ((seg * (MP / E) + cc) ^ (i & 7)) * E]);
+            const V v = *reinterpret_cast<const V*>(&tile[i * 32 + (((seg * (MP / E) + cc) * E) ^ ((i & 7) * E))]);
             const T2* v2 = reinterpret_cast<const T2*>(&v);
             sp[cc] = (E == 4) ? PR::add(v2[0], v2[(E == 4) ? 1 : 0]) : v2[0];
           }
