@@ -245,10 +245,12 @@ k_badmm_tma(const IterArgs<T> a) {
     T* const Ls = st + MP * cns + MP * rel;
     const T* const Ys = st + 2 * MP * cns + DY * rel;
     if constexpr (PAD) {
-      for (int j = mk; j < cns; ++j) {                 // padding columns: p = Lambda = 0
-        Ps[j * MP + i] = T(0);
-        Ls[j * MP + i] = T(0);
-      }
+#pragma unroll
+      for (int u = 0; u < 3; ++u)                      // padding columns (at most 3): p = Lambda = 0
+        if (mk + u < cns) {
+          Ps[(mk + u) * MP + i] = T(0);
+          Ls[(mk + u) * MP + i] = T(0);
+        }
     }
     T* const tile = (G == 1) ? st : tile_sep;          // G == 1: reuse this pass's P slot
 
