@@ -313,9 +313,30 @@ def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, n_clusters=None):
         c += 1
         if (n_clusters is not None and c >= n_clusters) or (n_clusters is None and t_all >= budget_s):
             break
-    return {"value": entries * s.T / t_all, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"clusters 0..{c - 1} of {b.name}: {members} members ({entries} plan entries), T={s.T}, "
-                      f"tau={s.tau}, fp64, {t_all:.1f}s", "n_clusters": c}
+    out = {"value": entries * s.T / t_all, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+           "sample": f"clusters 0..{c - 1} of {b.name}: {members} members ({entries} plan entries), T={s.T}, "
+                     f"tau={s.tau}, fp64, {t_all:.1f}s", "n_clusters": c, "cpu_model": cpu_model()}
+    if n_clusters is None:
+        # the 1-thread rate on the first members of cluster 0, ~2 s
+        mem = np.nonzero(b.labels == 0)[0]
+        k = max(1, min(len(mem), int(len(mem) * min(1.0, 2.0 / max(t_all / c, 1e-3)) / max(1, oracle.max_threads()))))
+        sub = b.subset(mem[:k])
+        t = time.time()
+        oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
+                              s.eps, 1e-5, nthreads=1, want_state=False)
+        out["value_1thread"] = b.m * sub.n * s.T / (time.time() - t)
+        out["sample_1thread"] = f"first {k} members of cluster 0, 1 thread"
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank, world):
