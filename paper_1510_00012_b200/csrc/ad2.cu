@@ -428,6 +428,9 @@ const char* ad2_status_string(ad2_status s) {
 const char* ad2_last_error(ad2_ctx ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
 
 
+// the variant-2 kernel with 32-row blocks keeps P, Q, L in the pair layout (blk_idx)
+static bool pair_layout(ad2_ctx ctx) { return ctx->variant == 2 && ctx->ld == 32; }
+
 static ad2_status set_dev(ad2_ctx ctx) {
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return ctx->fail(AD2_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
@@ -550,7 +553,7 @@ static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
   k_init_plans<T><<<(unsigned)ctx->n_items, 128, 0, ctx->stream>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
       warm ? ctx->d_warm.as<int64_t>() : nullptr, ctx->om.as<T>(), ctx->w.as<T>(), ctx->Q.as<T>(), dst,
-      ctx->L.as<T>(), ctx->m, ctx->ld);
+      ctx->L.as<T>(), ctx->m, ctx->ld, pair_layout(ctx));
 }
 
 // warm_dev: warm_mask is a device array (the outer loop's label-diff mask, always "some warm")
@@ -1089,12 +1092,14 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
       k_scatter_plans<double><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                              ctx->d_orig_off.as<int64_t>(), (const double*)src->p,
                                                              (double*)dst, ctx->N, ctx->m, ctx->ld, ctx->mem_cl.as<int32_t>(),
-                                                             lam_scaled ? ctx->kx.as<double>() : nullptr);
+                                                             lam_scaled ? ctx->kx.as<double>() : nullptr,
+                                                             which != AD2_COST && pair_layout(ctx));
     else
       k_scatter_plans<float><<<grid, 128, 0, ctx->stream>>>(ctx->d_order.as<int32_t>(), ctx->d_off.as<int64_t>(),
                                                             ctx->d_orig_off.as<int64_t>(), (const float*)src->p,
                                                             (float*)dst, ctx->N, ctx->m, ctx->ld, ctx->mem_cl.as<int32_t>(),
-                                                            lam_scaled ? ctx->kx.as<float>() : nullptr);
+                                                            lam_scaled ? ctx->kx.as<float>() : nullptr,
+                                                            which != AD2_COST && pair_layout(ctx));
     CHK(launch_check(ctx, "k_scatter_plans"));
   }
   if (where == AD2_HOST) {

@@ -390,6 +390,16 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
   for (int j = lane; j < mk; j += 32) om[dsto + j] = Wsrc[so + j] / tot;
 }
 
+// Offset of entry (i, j) in a member's plan block (leading dimension ld >= m).  The column-major
+// layout puts (i, j) at j ld + i; the "pair layout" of the variant-2 kernel with 32-row blocks
+// interleaves columns 2q and 2q+1 by row ((i, 2q) at 2q ld + 2i, (i, 2q+1) at 2q ld + 2i + 1),
+// so a lane moves both with one 8-byte access; an odd m_k's last column keeps j ld + i.  Both
+// layouts fill exactly ld m_k elements per member.
+__host__ __device__ __forceinline__ int64_t blk_idx(int i, int j, int mk, int ld, bool pair) {
+  if (!pair || j >= (mk & ~1)) return (int64_t)j * ld + i;
+  return (int64_t)(j & ~1) * ld + 2 * i + (j & 1);
+}
+
 // Pi^(2),0 = w_i w_j^(k) or, for warm members, the cached block;
 // Lambda = 0.  Writes the new Pi2 into `dst` (a buffer distinct from the warm source).
 template <typename T>
@@ -397,7 +407,7 @@ __global__ void __launch_bounds__(128)
 k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
              const int32_t* __restrict__ item_cl, const int64_t* __restrict__ warm_src,
              const T* __restrict__ om, const T* __restrict__ w, const T* __restrict__ Qold,
-             T* __restrict__ dst, T* __restrict__ L, int m, int ld) {
+             T* __restrict__ dst, T* __restrict__ L, int m, int ld, bool pair) {
   // warp per member, lane = row i (rows in chunks of 32), one column per step: coalesced rows
   const int item = blockIdx.x;
   const int c = item_cl[item];
@@ -412,7 +422,7 @@ k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
       if (i >= ld) break;
       const T wi = i < m ? w[(int64_t)c * m + i] : T(0);
       for (int j = 0; j < mk; ++j) {
-        const int64_t e = (int64_t)j * ld + i;
+        const int64_t e = blk_idx(i, j, mk, ld, pair);
         dst[base + e] = (src >= 0) ? Qold[src + e] : wi * om[o0 + j];
         L[base + e] = T(0);
       }
@@ -424,19 +434,22 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_scatter_plans(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
                 const int64_t* __restrict__ orig_off, const T* __restrict__ src, T* __restrict__ dst,
-                int64_t N, int m, int ld, const int32_t* __restrict__ mem_cl, const T* __restrict__ unscale) {
+                int64_t N, int m, int ld, const int32_t* __restrict__ mem_cl, const T* __restrict__ unscale,
+                bool pair) {
   // unscale != nullptr: divide by unscale[cluster] (the pre-scaled Lambda of variant 2)
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= N) return;
   const int64_t k = order[s];
-  const int64_t ne = (int64_t)m * (off[s + 1] - off[s]);
+  const int mk = (int)(off[s + 1] - off[s]);
+  const int64_t ne = (int64_t)m * mk;
   const T* a = src + (int64_t)ld * off[s];
   T* b = dst + (int64_t)m * orig_off[k];
   const T sc = unscale ? unscale[mem_cl[s]] : T(1);
   for (int64_t e = lane; e < ne; e += 32) {
     const int64_t j = e / m, i = e - j * m;
-    b[e] = unscale ? a[j * ld + i] / sc : a[j * ld + i];
+    const int64_t q = blk_idx((int)i, (int)j, mk, ld, pair);
+    b[e] = unscale ? a[q] / sc : a[q];
   }
 }
 

@@ -245,12 +245,27 @@ k_badmm_tma(const IterArgs<T> a) {
     T* const Ls = st + MP * cns + MP * rel;
     const T* const Ys = st + 2 * MP * cns + DY * rel;
     if constexpr (PAD) {
+      // G == 1 blocks use the pair layout (blk_idx, ad2_kernels.cuh): columns 2q, 2q+1 interleaved
+      // by row, so a lane moves both with one 8-byte access; an odd m_k's last column arrives in the
+      // single-column layout and is rewritten here as the pair (m_k - 1, pad) with a zero partner
+      const bool odd = mk & 1;
+      T px = T(0), lx = T(0);
+      if (odd) {
+        px = Ps[(mk - 1) * MP + i];
+        lx = Ls[(mk - 1) * MP + i];
+      }
 #pragma unroll
       for (int u = 0; u < 3; ++u)                      // padding columns (at most 3): p = Lambda = 0
         if (mk + u < cns) {
           Ps[(mk + u) * MP + i] = T(0);
           Ls[(mk + u) * MP + i] = T(0);
         }
+      __syncwarp();
+      if (odd) {
+        *reinterpret_cast<T2*>(Ps + (mk - 1) * MP + 2 * i) = PR::make(px, T(0));
+        *reinterpret_cast<T2*>(Ls + (mk - 1) * MP + 2 * i) = PR::make(lx, T(0));
+      }
+      __syncwarp();
     }
     T* const tile = (G == 1) ? st : tile_sep;          // G == 1: reuse this pass's P slot
 
@@ -264,11 +279,16 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int jp = 2 * jb + h, j = 2 * jp;
-        const bool v0 = PAD || j < mk, v1 = PAD || j + 1 < mk;
-        const T pa = Ps[j * MP + i], pb = Ps[(j + 1) * MP + i];
-        const T la = Ls[j * MP + i], lb = Ls[(j + 1) * MP + i];
-        p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
-        l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
+        if constexpr (PAD) {                           // pair layout: one 8-byte load per pair
+          p2[jp] = *reinterpret_cast<const T2*>(Ps + j * MP + 2 * i);
+          l2[jp] = *reinterpret_cast<const T2*>(Ls + j * MP + 2 * i);
+        } else {
+          const bool v0 = j < mk, v1 = j + 1 < mk;
+          const T pa = Ps[j * MP + i], pb = Ps[(j + 1) * MP + i];
+          const T la = Ls[j * MP + i], lb = Ls[(j + 1) * MP + i];
+          p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
+          l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
+        }
         if constexpr (MODE == P1ONLY) {
           q2[jp] = p2[jp];                                             // Pi2^(0)
         } else {
@@ -294,11 +314,15 @@ k_badmm_tma(const IterArgs<T> a) {
           const int jp = 2 * jb + h, j = 2 * jp;
           const T2 q = PR::fma(q2[jp], f2, ef2);                        // Pi2 = (pe + eps) w_i / r
           const T2 l = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));  // Eq.badmm2
+          if constexpr (PAD) {
+            *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = q;
+            *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l;
+          }
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             const T qv = u ? q.y : q.x, lv = u ? l.y : l.x;
-            if (PAD || jj < mk) {          // packed blocks (G > 1): no tail writes
+            if (!PAD && jj < mk) {           // packed blocks (G > 1): no tail writes
               Ps[jj * MP + i] = qv;
               Ls[jj * MP + i] = lv;
             }
@@ -398,12 +422,17 @@ k_badmm_tma(const IterArgs<T> a) {
           p2[jp] = PR::mul(p2[jp], fj);
           const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
           racc2[h] = PR::fma(p2[jp], e, racc2[h]);
+          if constexpr (PAD) {
+            *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = p2[jp];
+            if (MODE == FUSED) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
+          } else {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int jj = j + u;
-            if (PAD || jj < mk) {          // packed blocks (G > 1): no tail writes
-              Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
-              if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+            for (int u = 0; u < 2; ++u) {
+              const int jj = j + u;
+              if (jj < mk) {                 // packed blocks (G > 1): no tail writes
+                Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
+                if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+              }
             }
           }
         }
@@ -416,6 +445,16 @@ k_badmm_tma(const IterArgs<T> a) {
         const T wt = N::div(r2, R);                                      // normalised row mass
         accw += (a.rule == 1) ? sqrt(wt) : wt;
         bad |= !isfinite(wt);
+      }
+    }
+    if constexpr (PAD) {                               // an odd m_k's last column back to its
+      if (mk & 1) {                                    // single-column layout for the store
+        __syncwarp();
+        const T px = Ps[(mk - 1) * MP + 2 * i];
+        const T lx = (MODE != P1ONLY) ? Ls[(mk - 1) * MP + 2 * i] : T(0);
+        __syncwarp();
+        Ps[(mk - 1) * MP + i] = px;
+        if (MODE != P1ONLY) Ls[(mk - 1) * MP + i] = lx;
       }
     }
     // results leave by bulk stores from the same slots
@@ -579,7 +618,7 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * (P ? sP[warp][(j0 + u) * ld + i] : T(1));
+      if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * sP[warp][blk_idx(i, j0 + u, mk, ld, ld == 32)];
   }
   double acc = (double)s;
   for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
