@@ -161,6 +161,8 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
 
     sched_ev = []                                      # events around step/update (SURVEY.md §8(d) metric)
 
+    prof_box = {"arm": False}
+
     def step(arr, mem, after_init=None):
         ctx.init(arr["offsets"], arr["supports"], arr["weights"], arr["labels"], arr["x0"], arr["w0"], b.K, b.m,
                  s.rho0, s.eps, s.rule, mem=mem, dtype=b.dtype, cost_mode=args.cost_mode)
@@ -168,12 +170,14 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
             after_init()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ad2.run_schedule(ctx, T, tau)
+        arm = prof_box["arm"]
+        prof_box["arm"] = False
+        ad2.run_schedule(ctx, T, tau, before_last_step=(lambda: ctx.set_profiling(2)) if arm else None)
         e1.record(stream)
         sched_ev.append((e0, e1))
         obj_box["obj"] = ctx.objective()               # device -> host read of the result (syncs)
 
-    def timed(fn, K, W):
+    def timed(fn, K, W, before_last=None):
         for _ in range(W):
             fn()
         barrier()
@@ -181,7 +185,9 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = ctx.info()["launches"]
         e0.record(stream)
-        for _ in range(K):
+        for k in range(K):
+            if before_last is not None and k == K - 1:
+                before_last()
             fn()
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -194,9 +200,13 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
             ms = float(x.item())
         return ms, launches
 
-    ctx.set_profiling(True)          # event nodes around every iteration kernel (live, in-graph)
+    # the iteration kernels of the LAST step(tau) of the last timed round run with event-record nodes
+    # around every launch (live, in-graph, inside the timed region); the other steps run the
+    # plain graph, so the instrumentation costs the timed region almost nothing
+    ctx.set_profiling(0)
     with ClockSampler(local_rank) as clk:
-        ms, launches = timed(lambda: step(D, "device"), args.steps, args.warmup)
+        ms, launches = timed(lambda: step(D, "device"), args.steps, args.warmup,
+                             before_last=lambda: prof_box.update(arm=True))
     sched_ms = float(np.mean([a.elapsed_time(z) for a, z in sched_ev[-args.steps:]]))
     launch_ms, step_graph_ms = ctx.prof_read()
     info = ctx.info()
@@ -238,9 +248,11 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
         k_e2e = max(1, args.steps)
         calls = {"n": 0}
 
+        use_pf = not os.environ.get("AD2_BENCH_NO_PREFETCH")
+
         def prefetch_next():
             c = calls["n"]
-            if 1 <= c < k_e2e:
+            if use_pf and 1 <= c < k_e2e:
                 ctx.prefetch(H["offsets"], H["supports"], H["weights"], H["labels"], dtype=b.dtype,
                              cost_mode=args.cost_mode)
 
@@ -249,7 +261,7 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
             ctx.centroids_into(xo, wo, mem="host")
             calls["n"] += 1
 
-        ctx.set_profiling(False)
+        ctx.set_profiling(0)
         ms_e2e, _ = timed(step_host, k_e2e, 1)
         h2d = sum(v.numel() * v.element_size() for v in H.values())
         d2h = xo.numel() * xo.element_size() + wo.numel() * wo.element_size() + 2 * 8 * b.K

@@ -203,11 +203,13 @@ ad2_status ad2_get_rho(ad2_ctx ctx, double *rho_out);
 
 ad2_status ad2_get_info(ad2_ctx ctx, ad2_info *info);
 
-/* Kernel timing: when enabled, every B-ADMM iteration-kernel launch of later steps is bracketed
- * by CUDA events on the launching stream (event-record nodes inside the step graph).
- * ad2_prof_read fills launch_ms[0..min(capacity, n)-1] with the durations (ms) of the most
- * recent step's launches in order [first (phase 1 only), fused x (n_iters-1), last (phase 2
- * only)], *n_launches = n_iters + 1, and *step_ms = first start to last end.  Synchronises. */
+/* Kernel timing: enable = 1 brackets every B-ADMM iteration-kernel launch of later steps by CUDA
+ * events on the launching stream (event-record nodes inside the step graph); enable = 2 does so
+ * for the next ad2_badmm_step call only (later steps run the plain graph: no timing overhead);
+ * 0 turns it off.  Other values: AD2_ERR_ARG.  ad2_prof_read fills
+ * launch_ms[0..min(capacity, n)-1] with the durations (ms) of the most recent profiled step's
+ * launches in order [first (phase 1 only), fused x (n_iters-1), last (phase 2 only)],
+ * *n_launches = n_iters + 1, and *step_ms = first start to last end.  Synchronises. */
 ad2_status ad2_set_profiling(ad2_ctx ctx, int enable);
 ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64_t *n_launches,
                          double *step_ms);

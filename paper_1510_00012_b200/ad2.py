@@ -260,11 +260,12 @@ class Context:
         self._chk(self.L.ad2_get_info(self.h, C.byref(i)))
         return {f: getattr(i, f) for f, _ in Info._fields_}
 
-    def set_profiling(self, enable: bool):
-        self._chk(self.L.ad2_set_profiling(self.h, 1 if enable else 0))
+    def set_profiling(self, enable):
+        """ad2_set_profiling: False/0 off, True/1 every later step, 2 the next step only."""
+        self._chk(self.L.ad2_set_profiling(self.h, int(enable)))
 
     def prof_read(self):
-        """(per-launch ms of the last step's iteration kernels, step ms)."""
+        """(per-launch ms of the last profiled step's iteration kernels, step ms)."""
         buf = np.zeros(4096)
         n, step = C.c_int64(), C.c_double()
         self._chk(self.L.ad2_prof_read(self.h, buf.ctypes.data, len(buf), C.byref(n), C.byref(step)))
@@ -364,11 +365,14 @@ class Context:
         self._chk(self.L.ad2_sync(self.h))
 
 
-def run_schedule(ctx: Context, T: int, tau: int):
-    """Alg. 4's schedule (reading X6): step(tau); update_support() per full tau block."""
+def run_schedule(ctx: Context, T: int, tau: int, before_last_step=None):
+    """Alg. 4's schedule (reading X6): step(tau); update_support() per full tau block.
+    before_last_step: called before the last step call (e.g. ctx.set_profiling(2))."""
     done = 0
     while done < T:
         n = min(tau, T - done)
+        if before_last_step is not None and done + n >= T:
+            before_last_step()
         ctx.step(n)
         done += n
         if n == tau:

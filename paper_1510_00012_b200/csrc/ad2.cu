@@ -142,9 +142,10 @@ struct ad2_ctx_s {
   int tab_V = 0, tab_dtype = -1;
   bool table = false;                // the current round uses AD2_COST_TABLE
 
-  std::map<int, StepGraph*> graphs;
-  bool prof = false;
-  StepGraph* last_graph = nullptr;
+  std::map<int, StepGraph*> graphs;  // key 2 n + (profiled)
+  int prof = 0;                      // 0 off, 1 every step, 2 the next step only (ad2_set_profiling)
+  bool prof_pending = false;
+  StepGraph* last_graph = nullptr;   // the most recent profiled step graph (ad2_prof_read)
   int64_t launches = 0;
 
   ~ad2_ctx_s() {
@@ -934,11 +935,11 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
 }
 
 // one step = n iterations of Alg. 4 at fixed x, captured once per n into a CUDA graph
-static ad2_status capture_step(ad2_ctx ctx, int n, StepGraph** out) {
+static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, StepGraph** out) {
   StepGraph* g = new StepGraph();
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
-  if (ctx->prof) {
+  if (prof) {
     g->ev.resize(2 * (size_t)n + 2);
     for (auto& e : g->ev) CU(cudaEventCreate(&e));
   }
@@ -946,9 +947,9 @@ static ad2_status capture_step(ad2_ctx ctx, int n, StepGraph** out) {
   ad2_status st = AD2_OK;
   for (int t = 0; t <= n && st == AD2_OK; ++t) {
     const int mode = t == 0 ? P1ONLY : (t == n ? P2ONLY : FUSED);
-    if (ctx->prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
+    if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
     st = launch_iter(ctx, mode, s);
-    if (ctx->prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
+    if (prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
     if (st == AD2_OK && t < n) st = consensus(ctx, s);
   }
   cudaGraph_t graph = nullptr;
@@ -980,17 +981,22 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "step before init");
   if (n_iters == 0) return AD2_OK;
   CHK(set_dev(ctx));
-  auto it = ctx->graphs.find(n_iters);
+  const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
+  const int key = 2 * n_iters + (prof ? 1 : 0);
+  auto it = ctx->graphs.find(key);
   StepGraph* g = nullptr;
   if (it == ctx->graphs.end()) {
-    CHK(capture_step(ctx, n_iters, &g));
-    ctx->graphs[n_iters] = g;
+    CHK(capture_step(ctx, n_iters, prof, &g));
+    ctx->graphs[key] = g;
   } else {
     g = it->second;
   }
   CU(cudaGraphLaunch(g->exec, ctx->stream));
   ctx->launches += g->nodes;
-  ctx->last_graph = g;
+  if (prof) {
+    ctx->last_graph = g;
+    ctx->prof_pending = false;
+  }
   ctx->state = 2;
   return AD2_OK;
 }
@@ -1142,10 +1148,9 @@ ad2_status ad2_get_info(ad2_ctx ctx, ad2_info* info) {
 
 ad2_status ad2_set_profiling(ad2_ctx ctx, int enable) {
   if (!ctx) return AD2_ERR_ARG;
-  if ((enable != 0) != ctx->prof) {
-    ctx->prof = enable != 0;
-    ctx->clear_graphs();
-  }
+  if (enable < 0 || enable > 2) return ctx->fail(AD2_ERR_ARG, "set_profiling: mode %d", enable);
+  ctx->prof = enable;                 // profiled and plain graphs are cached side by side
+  ctx->prof_pending = enable == 2;
   return AD2_OK;
 }
 
