@@ -11,6 +11,7 @@
 // items of a cluster in item order, so every result is deterministic.
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -421,7 +422,25 @@ k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
       const int i = r0 + lane;
       if (i >= ld) break;
       const T wi = i < m ? w[(int64_t)c * m + i] : T(0);
-      for (int j = 0; j < mk; ++j) {
+      int j = 0;
+      if (pair)                                        // both columns of a pair per access
+        for (; j + 1 < mk; j += 2) {
+          const int64_t e = (int64_t)j * ld + 2 * i;
+          typedef typename std::conditional<sizeof(T) == 4, float2, double2>::type T2;
+          T2 v;
+          if (src >= 0) {
+            v = *reinterpret_cast<const T2*>(Qold + src + e);
+          } else {
+            v.x = wi * om[o0 + j];
+            v.y = wi * om[o0 + j + 1];
+          }
+          *reinterpret_cast<T2*>(dst + base + e) = v;
+          T2 z;
+          z.x = T(0);
+          z.y = T(0);
+          *reinterpret_cast<T2*>(L + base + e) = z;
+        }
+      for (; j < mk; ++j) {
         const int64_t e = blk_idx(i, j, mk, ld, pair);
         dst[base + e] = (src >= 0) ? Qold[src + e] : wi * om[o0 + j];
         L[base + e] = T(0);
