@@ -123,7 +123,8 @@ struct ad2_ctx_s {
   DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm, d_pos_of;
   DBuf d_off_old, d_pos_of_old;      // previous round's layout (warm starts)
   DBuf lay_keys, lay_keys2, lay_iota, lay_sz, lay_cnt, lay_pts, lay_cstart, lay_scal, lay_cub, lay_warm;
-  DBuf stage_lab, mem_cl, pm;
+  DBuf stage_lab, mem_cl, pm, xsum;  // xsum: per-cluster sum x_i, sum |x_i|^2 (fp64, Eq.rho in k_gather)
+  bool rho_in_gather = false;
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
   // ad2_prefetch: a second set of host-batch staging buffers, filled on a copy stream while the
@@ -327,7 +328,7 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
     return launch_check(ctx, "k_cost_table");
   }
   if (ctx->variant == 2) {
-    if (!with_sum) return AD2_OK;
+    if (!with_sum || ctx->rho_in_gather) return AD2_OK;   // the gather formed the rho numerators
     launch_cost_member<T>(ctx->dp, ctx->d_off.as<int64_t>(), ctx->N, ctx->mem_cl.as<int32_t>(), ctx->Y.as<T>(),
                           ctx->x.as<T>(), nullptr, ctx->pm.as<double>(), ctx->m, ctx->d, ctx->ld, s);
     return launch_check(ctx, "k_cost_member");
@@ -540,12 +541,15 @@ ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void* unique
 }
 
 template <typename T>
-static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, double wtol) {
+static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, double wtol, bool rho_sums) {
   if (ctx->N == 0) return;
+  // rho_sums (variant 2, vector supports): the per-member Eq.rho numerators come out of this pass
+  if (rho_sums) k_xsums<T><<<ctx->K, 32, 0, ctx->stream>>>(ctx->x.as<T>(), ctx->m, ctx->d, ctx->xsum.as<double>());
   k_gather<T><<<(unsigned)((ctx->N + 3) / 4), 128, 0, ctx->stream>>>(
       ctx->d_order.as<int32_t>(), ctx->d_orig_off.as<int64_t>(), ctx->d_off.as<int64_t>(), (const T*)Ysrc,
       (const T*)Wsrc, ctx->Y.as<T>(), ctx->om.as<T>(), ctx->N, ctx->d, ctx->dy, ctx->variant == 2 ? (ctx->dp == 4 ? 3 : 16) : -1, wtol,
-      ctx->d_err.as<int>());
+      ctx->d_err.as<int>(), rho_sums ? ctx->xsum.as<double>() : nullptr, ctx->mem_cl.as<int32_t>(), ctx->m,
+      rho_sums ? ctx->pm.as<double>() : nullptr);
 }
 
 template <typename T>
@@ -854,11 +858,12 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   }
   const double wtol = b->dtype == AD2_F64 ? 1e-6 : 1e-5;
   ctx->table = table;
+  ctx->rho_in_gather = false;
   if (table) {                      // weights only through k_gather (d = 0); ids gathered separately
     const int d_save = ctx->d;
     ctx->d = 0;
-    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
-    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
+    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol, false);
+    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol, false);
     ctx->d = d_save;
     if (N > 0) CHK(launch_check(ctx, "k_gather"));
     CU(ctx->ysym.reserve(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)));
@@ -872,10 +877,15 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     CU(cudaMemcpyAsync(ctx->xsym.p, x0, sizeof(int32_t) * (size_t)K * m, h2d, s));
     CU(cudaMemsetAsync(ctx->x.p, 0, es * (size_t)K * m * d, s));
   } else {
-    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol);
-    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol);
-    if (N > 0) CHK(launch_check(ctx, "k_gather"));
     CU(cudaMemcpyAsync(ctx->x.p, x0, es * (size_t)K * m * d, h2d, s));
+    ctx->rho_in_gather = ctx->variant == 2;
+    if (ctx->rho_in_gather) {
+      CU(ctx->xsum.reserve(sizeof(double) * (size_t)K * (d + 1)));
+      CU(ctx->pm.reserve(sizeof(double) * (size_t)(N > 0 ? N : 1)));
+    }
+    if (b->dtype == AD2_F64) launch_gather<double>(ctx, Ysrc, Wsrc, wtol, ctx->rho_in_gather);
+    else launch_gather<float>(ctx, Ysrc, Wsrc, wtol, ctx->rho_in_gather);
+    if (N > 0) CHK(launch_check(ctx, "k_gather"));
   }
   CU(cudaMemcpyAsync(ctx->w.p, w0, es * (size_t)K * m, h2d, s));
   if (host && ctx->stage_rel) CU(cudaEventRecord(ctx->stage_rel, s));   // staging buffers consumed

@@ -355,7 +355,8 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
          const int64_t* __restrict__ dst_off, const T* __restrict__ Ysrc, const T* __restrict__ Wsrc,
-         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, int yy_col, double wtol, int* err) {
+         T* __restrict__ Y, T* __restrict__ om, int64_t N, int d, int dy, int yy_col, double wtol, int* err,
+         const double* __restrict__ xsum, const int32_t* __restrict__ mem_cl, int m, double* __restrict__ pm) {
   // warp per member, lane per support point: the point's row [y, 0.., |y|^2 at yy_col, 0..]
   const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -366,9 +367,16 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
   // coordinates: the member's source block is contiguous, read lane-strided (coalesced)
   const T* srcb = Ysrc + so * d;
   T* dstb = Y + dsto * dy;
+  // (with pm: the Eq.rho numerator of the member in the same pass, fp64, closed form:
+  //  sum_ij |x_i - y_j|^2 = m_k sum_i |x_i|^2 + sum_jt (m y_jt^2 - 2 (sum_i x_it) y_jt), the cluster's
+  //  sums from k_xsums; fp32 inputs are exact in fp64)
+  const double* xs = pm ? xsum + (int64_t)mem_cl[s] * (d + 1) : nullptr;
+  double racc = 0.0;
   for (int e = lane; e < mk * d; e += 32) {
     const int j = e / d, t = e - j * d;
-    dstb[(int64_t)j * dy + t] = srcb[e];
+    const T v = srcb[e];
+    dstb[(int64_t)j * dy + t] = v;
+    if (pm) racc += (double)v * fma((double)m, (double)v, -2.0 * xs[t]);
   }
   // zero padding and the |y|^2 column (sequential in t, like the oracle's sum): lane per point
   if (dy > d)
@@ -380,6 +388,10 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
         for (int t = 0; t < d; ++t) yy += src[t] * src[t];
       for (int t = d; t < dy; ++t) dst[t] = (t == yy_col) ? yy : T(0);
     }
+  if (pm) {                                         // Eq.rho numerator (X1)
+    for (int h = 16; h >= 1; h >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, h);
+    if (lane == 0) pm[s] = (double)mk * xs[d] + racc;
+  }
   double sum = 0.0;
   for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
   for (int h = 16; h >= 1; h >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, h);
@@ -389,6 +401,24 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
     for (int j = 0; j < mk; ++j) tot += Wsrc[so + j];
   tot = __shfl_sync(0xffffffffu, tot, 0);
   for (int j = lane; j < mk; j += 32) om[dsto + j] = Wsrc[so + j] / tot;
+}
+
+// per cluster: sum_i x_i (d values) and sum_i |x_i|^2 in fp64 (the Eq.rho numerator in k_gather)
+template <typename T>
+__global__ void k_xsums(const T* __restrict__ x, int m, int d, double* __restrict__ out) {
+  const int c = blockIdx.x, lane = threadIdx.x;
+  double q = 0.0;
+  for (int t = lane; t < d; t += 32) {
+    double sx = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double v = (double)x[((int64_t)c * m + i) * d + t];
+      sx += v;
+      q = fma(v, v, q);
+    }
+    out[(int64_t)c * (d + 1) + t] = sx;
+  }
+  for (int h = 16; h >= 1; h >>= 1) q += __shfl_xor_sync(0xffffffffu, q, h);
+  if (lane == 0) out[(int64_t)c * (d + 1) + d] = q;
 }
 
 // Offset of entry (i, j) in a member's plan block (leading dimension ld >= m).  The column-major

@@ -616,9 +616,24 @@ k_cost_member(const int64_t* __restrict__ off, int64_t N, const int32_t* __restr
         }
       }
     }
+    // Pi1 of the four columns (pair layout for 32-row blocks: one 8-byte read per column pair,
+    // conflict-free; an odd m_k's last column single)
+    T pv[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + 2 * h;
+      if (ld == 32 && j + 1 < mk) {
+        const T2 q = *reinterpret_cast<const T2*>(&sP[warp][j * ld + 2 * i]);
+        pv[2 * h] = q.x;
+        pv[2 * h + 1] = q.y;
+      } else {
+        pv[2 * h] = j < mk ? sP[warp][j * ld + i] : T(0);
+        pv[2 * h + 1] = j + 1 < mk ? sP[warp][(j + 1) * ld + i] : T(0);
+      }
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * sP[warp][blk_idx(i, j0 + u, mk, ld, ld == 32)];
+      if (j0 + u < mk && rowok) s += (c2[u].x + c2[u].y) * pv[u];
   }
   double acc = (double)s;
   for (int h = 16; h >= 1; h >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, h);
