@@ -125,6 +125,7 @@ struct ad2_ctx_s {
   DBuf lay_keys, lay_keys2, lay_iota, lay_sz, lay_cnt, lay_pts, lay_cstart, lay_scal, lay_cub, lay_warm;
   DBuf stage_lab, mem_cl, pm, xsum;  // xsum: per-cluster sum x_i, sum |x_i|^2 (fp64, Eq.rho in k_gather)
   bool rho_in_gather = false;
+  bool fresh = false;                // Pi2^0 / Lambda = 0 not materialised yet (P1INIT pending)
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
   // ad2_prefetch: a second set of host-batch staging buffers, filled on a copy stream while the
@@ -720,6 +721,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   // ---- from here on the previous round's state is replaced (an error leaves the context
   //      needing a fresh init): stable radix sort by cluster, sorted offsets, work items
   ctx->state = 0;
+  ctx->fresh = false;
   ctx->clear_graphs();
   const int64_t old_N = ctx->N;
   const int old_ld = ctx->ld;
@@ -898,6 +900,8 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     std::swap(ctx->P.p, ctx->Q.p);
     std::swap(ctx->P.cap, ctx->Q.cap);
     CU(ctx->P.reserve(es * EL));
+  } else if (pair_layout(ctx)) {
+    ctx->fresh = true;              // cold round: the first step's P1INIT pass forms Pi2^0, Lambda = 0
   } else {
     if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
     else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());
@@ -945,7 +949,7 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
 }
 
 // one step = n iterations of Alg. 4 at fixed x, captured once per n into a CUDA graph
-static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, StepGraph** out) {
+static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, StepGraph** out) {
   StepGraph* g = new StepGraph();
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
@@ -956,7 +960,7 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, StepGraph** out) {
   CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ad2_status st = AD2_OK;
   for (int t = 0; t <= n && st == AD2_OK; ++t) {
-    const int mode = t == 0 ? P1ONLY : (t == n ? P2ONLY : FUSED);
+    const int mode = t == 0 ? (fresh ? P1INIT : P1ONLY) : (t == n ? P2ONLY : FUSED);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
     st = launch_iter(ctx, mode, s);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
@@ -992,17 +996,19 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   if (n_iters == 0) return AD2_OK;
   CHK(set_dev(ctx));
   const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
-  const int key = 2 * n_iters + (prof ? 1 : 0);
+  const bool fresh = ctx->fresh;
+  const int key = 4 * n_iters + (fresh ? 2 : 0) + (prof ? 1 : 0);
   auto it = ctx->graphs.find(key);
   StepGraph* g = nullptr;
   if (it == ctx->graphs.end()) {
-    CHK(capture_step(ctx, n_iters, prof, &g));
+    CHK(capture_step(ctx, n_iters, prof, fresh, &g));
     ctx->graphs[key] = g;
   } else {
     g = it->second;
   }
   CU(cudaGraphLaunch(g->exec, ctx->stream));
   ctx->launches += g->nodes;
+  ctx->fresh = false;
   if (prof) {
     ctx->last_graph = g;
     ctx->prof_pending = false;
@@ -1090,6 +1096,12 @@ ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
   if (which == AD2_PI1 && ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "Pi1 exists after a step");
   CHK(set_dev(ctx));
+  if (ctx->fresh && (which == AD2_PI2 || which == AD2_LAMBDA)) {   // cold round, no step yet
+    if (ctx->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
+    else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());
+    if (ctx->n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
+    ctx->fresh = false;
+  }
   if (which == AD2_COST && ctx->variant == 2) {
     CHK(ctx->dtype == AD2_F64 ? materialise_cost_T<double>(ctx, ctx->stream) : materialise_cost_T<float>(ctx, ctx->stream));
   }

@@ -133,6 +133,9 @@ k_badmm_tma(const IterArgs<T> a) {
   const T kx = a.kx[c];
   const T rho = a.rho[c];
   const T eps_r = rowok ? a.eps : T(0);
+  constexpr bool PH1 = (MODE == P1ONLY || MODE == P1INIT);   // phase 1 only
+  constexpr bool INIT = (MODE == P1INIT);
+  static_assert(!INIT || G == 1, "P1INIT is instantiated for 32-row blocks only");
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
   // Lambda is stored pre-scaled, L' = Lambda * kx (kx = log2(e)/rho for fp32, 1/rho for fp64), so
   // exp(Lambda/rho) = ex(L') and Eq.badmm2 becomes L' += kappa (Pi1 - Pi2) with kappa = kx * rho
@@ -191,10 +194,14 @@ k_badmm_tma(const IterArgs<T> a) {
     const uint32_t by = (uint32_t)(DY * np * (int)sizeof(T));
     const int ns = slot(np);
     T* st = ring + base;
-    mbar_expect_tx(&bar[t & 1], 2 * bp + by);
-    tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + MP * ns, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
-    tma_load(st + 2 * MP * ns, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
+    mbar_expect_tx(&bar[t & 1], INIT ? by : 2 * bp + by);
+    if constexpr (INIT) {
+      tma_load(st + 2 * MP * ns, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
+    } else {
+      tma_load(st, src_plan + (int64_t)MP * p0, bp, &bar[t & 1]);
+      tma_load(st + MP * ns, a.L + (int64_t)MP * p0, bp, &bar[t & 1]);
+      tma_load(st + 2 * MP * ns, a.Y + (int64_t)DY * p0, by, &bar[t & 1]);
+    }
   };
   int64_t cp0 = 0, cp1 = 0;
   int cnp = pass_pts(0, cp0, cp1);
@@ -244,7 +251,7 @@ k_badmm_tma(const IterArgs<T> a) {
     T* const Ps = st + MP * rel;
     T* const Ls = st + MP * cns + MP * rel;
     const T* const Ys = st + 2 * MP * cns + DY * rel;
-    if constexpr (PAD) {
+    if constexpr (PAD && !INIT) {
       // G == 1 blocks use the pair layout (blk_idx, ad2_kernels.cuh): columns 2q, 2q+1 interleaved
       // by row, so a lane moves both with one 8-byte access; an odd m_k's last column arrives in the
       // single-column layout and is rewritten here as the pair (m_k - 1, pad) with a zero partner
@@ -279,7 +286,12 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int jp = 2 * jb + h, j = 2 * jp;
-        if constexpr (PAD) {                           // pair layout: one 8-byte load per pair
+        if constexpr (INIT) {                          // Pi2^0 = w_i w_j^(k), Lambda = 0
+          const T o0v = j < mk ? __ldg(a.om + o0 + j) : T(0);
+          const T o1v = j + 1 < mk ? __ldg(a.om + o0 + j + 1) : T(0);
+          p2[jp] = PR::make(wi * o0v, wi * o1v);
+          l2[jp] = PR::make(T(0), T(0));
+        } else if constexpr (PAD) {                    // pair layout: one 8-byte load per pair
           p2[jp] = *reinterpret_cast<const T2*>(Ps + j * MP + 2 * i);
           l2[jp] = *reinterpret_cast<const T2*>(Ls + j * MP + 2 * i);
         } else {
@@ -289,7 +301,7 @@ k_badmm_tma(const IterArgs<T> a) {
           p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
           l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
         }
-        if constexpr (MODE == P1ONLY) {
+        if constexpr (PH1) {
           q2[jp] = p2[jp];                                             // Pi2^(0)
         } else {
           const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
@@ -299,7 +311,7 @@ k_badmm_tma(const IterArgs<T> a) {
       }
     }
     T f = T(0);
-    if constexpr (MODE != P1ONLY) {
+    if constexpr (!PH1) {
       const T r = (racc[0].x + racc[1].x) + (racc[0].y + racc[1].y) + mkeps;
       f = (has && rowok) ? N::div(wi, r) : T(0);                    // Eq.badmmc1: w_i / rowsum
     }
@@ -424,7 +436,7 @@ k_badmm_tma(const IterArgs<T> a) {
           racc2[h] = PR::fma(p2[jp], e, racc2[h]);
           if constexpr (PAD) {
             *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = p2[jp];
-            if (MODE == FUSED) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
+            if (MODE == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
           } else {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
