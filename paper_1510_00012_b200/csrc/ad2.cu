@@ -126,6 +126,8 @@ struct ad2_ctx_s {
   DBuf stage_lab, mem_cl, pm, xsum;  // xsum: per-cluster sum x_i, sum |x_i|^2 (fp64, Eq.rho in k_gather)
   bool rho_in_gather = false;
   bool fresh = false;                // Pi2^0 / Lambda = 0 not materialised yet (P1INIT pending)
+  bool pending = false;              // the last step ended with P2X: Pi2 and the last Lambda update
+                                     // are not stored; the next step starts with FUSED
   DBuf Y, om, P, Q, L, Cc, x, w, rho, kx, rho_d, pw, px, Sw, Sx, pd, Sd, npts, scr, d_err;
   DBuf stage_off, stage_Y, stage_W, tmp_out;
   // ad2_prefetch: a second set of host-batch staging buffers, filled on a copy stream while the
@@ -562,6 +564,8 @@ static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
       ctx->L.as<T>(), ctx->m, ctx->ld, pair_layout(ctx));
 }
 
+static ad2_status materialise_phase2(ad2_ctx ctx);
+
 // warm_dev: warm_mask is a device array (the outer loop's label-diff mask, always "some warm")
 static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0, const void* w0,
                             const uint8_t* warm_mask, bool warm_dev, double* rho_out) {
@@ -583,6 +587,9 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     return ctx->fail(AD2_ERR_ARG, "cost_mode 2 (symbolic) needs d = 1 (int32 symbol ids) and a cost table of the "
                      "batch dtype (ad2_set_cost_table)");
   CHK(set_dev(ctx));
+  // a warm start reads the previous round's Pi2: store it first if the last step deferred it
+  if (ctx->pending && (warm_mask || warm_dev)) CHK(materialise_phase2(ctx));
+  ctx->pending = false;
   const int64_t N = b->n_members;
   const int d = b->d, m = b->m, K = b->K;
   const size_t es = b->dtype == AD2_F64 ? 8 : 4;
@@ -722,6 +729,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   //      needing a fresh init): stable radix sort by cluster, sorted offsets, work items
   ctx->state = 0;
   ctx->fresh = false;
+  ctx->pending = false;
   ctx->clear_graphs();
   const int64_t old_N = ctx->N;
   const int old_ld = ctx->ld;
@@ -949,7 +957,8 @@ ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params
 }
 
 // one step = n iterations of Alg. 4 at fixed x, captured once per n into a CUDA graph
-static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, StepGraph** out) {
+static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool pending, bool p2x,
+                               StepGraph** out) {
   StepGraph* g = new StepGraph();
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
@@ -960,7 +969,7 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, StepGr
   CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ad2_status st = AD2_OK;
   for (int t = 0; t <= n && st == AD2_OK; ++t) {
-    const int mode = t == 0 ? (fresh ? P1INIT : P1ONLY) : (t == n ? P2ONLY : FUSED);
+    const int mode = t == 0 ? (fresh ? P1INIT : (pending ? FUSED : P1ONLY)) : (t == n ? (p2x ? P2X : P2ONLY) : FUSED);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
     st = launch_iter(ctx, mode, s);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
@@ -996,12 +1005,12 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   if (n_iters == 0) return AD2_OK;
   CHK(set_dev(ctx));
   const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
-  const bool fresh = ctx->fresh;
-  const int key = 4 * n_iters + (fresh ? 2 : 0) + (prof ? 1 : 0);
+  const bool fresh = ctx->fresh, pending = ctx->pending, p2x = pair_layout(ctx);
+  const int key = 8 * n_iters + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
   auto it = ctx->graphs.find(key);
   StepGraph* g = nullptr;
   if (it == ctx->graphs.end()) {
-    CHK(capture_step(ctx, n_iters, prof, fresh, &g));
+    CHK(capture_step(ctx, n_iters, prof, fresh, pending, p2x, &g));
     ctx->graphs[key] = g;
   } else {
     g = it->second;
@@ -1009,6 +1018,7 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   CU(cudaGraphLaunch(g->exec, ctx->stream));
   ctx->launches += g->nodes;
   ctx->fresh = false;
+  ctx->pending = p2x;
   if (prof) {
     ctx->last_graph = g;
     ctx->prof_pending = false;
@@ -1090,12 +1100,22 @@ ad2_status ad2_get_centroids(ad2_ctx ctx, void* x, void* w, ad2_mem where) {
   return AD2_OK;
 }
 
+// a step that ended with P2X left Pi2 and the last Lambda update unstored: store them now with a
+// P2ONLY pass (phase 2 does not read x, so this is exact after update_support too)
+static ad2_status materialise_phase2(ad2_ctx ctx) {
+  if (!ctx->pending) return AD2_OK;
+  CHK(launch_iter(ctx, P2ONLY, ctx->stream));
+  ctx->pending = false;
+  return AD2_OK;
+}
+
 ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
   if (!ctx) return AD2_ERR_ARG;
   if (!out || which < 0 || which > 3) return ctx->fail(AD2_ERR_ARG, "get_plans args");
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
   if (which == AD2_PI1 && ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "Pi1 exists after a step");
   CHK(set_dev(ctx));
+  if (which == AD2_PI2 || which == AD2_LAMBDA) CHK(materialise_phase2(ctx));
   if (ctx->fresh && (which == AD2_PI2 || which == AD2_LAMBDA)) {   // cold round, no step yet
     if (ctx->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
     else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());

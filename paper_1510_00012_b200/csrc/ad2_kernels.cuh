@@ -19,7 +19,9 @@ namespace ad2k {
 
 // P1INIT: P1ONLY at the start of a cold round (32-row variant-2 blocks only): Pi2^0 = w_i w_j^(k)
 // and Lambda = 0 are formed in registers instead of being written by k_init_plans and read back
-enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3 };
+// P2X: P2ONLY without the stores (the support-update partials only); the next step starts with a
+// FUSED pass that recomputes the same phase 2 (32-row variant-2 blocks only)
+enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4 };
 enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2 };
 
 constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels

@@ -156,9 +156,12 @@ k_badmm_tma(const IterArgs<T> a) {
     xn2[t] = PR::make(T(-2) * v0, T(-2) * v1);
   }
   T accw = T(0), accm = T(0);
-  T accx[(MODE == P2ONLY) ? DP : 1];
+  constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);     // phase 2 only (+ x partials)
+  constexpr bool NOSTORE = (MODE == P2X);
+  static_assert(!NOSTORE || G == 1, "P2X is instantiated for 32-row blocks only");
+  T accx[PH2 ? DP : 1];
 #pragma unroll
-  for (int t = 0; t < ((MODE == P2ONLY) ? DP : 1); ++t) accx[t] = T(0);
+  for (int t = 0; t < (PH2 ? DP : 1); ++t) accx[t] = T(0);
   bool bad = false;
 
   const T* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
@@ -317,7 +320,7 @@ k_badmm_tma(const IterArgs<T> a) {
     }
     const T2 f2 = PR::make(f, f), ef2 = PR::make(eps_r * f, eps_r * f);
 
-    if constexpr (MODE == P2ONLY) {
+    if constexpr (PH2) {
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
@@ -326,7 +329,7 @@ k_badmm_tma(const IterArgs<T> a) {
           const int jp = 2 * jb + h, j = 2 * jp;
           const T2 q = PR::fma(q2[jp], f2, ef2);                        // Pi2 = (pe + eps) w_i / r
           const T2 l = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));  // Eq.badmm2
-          if constexpr (PAD) {
+          if constexpr (PAD && !NOSTORE) {
             *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = q;
             *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l;
           }
@@ -459,7 +462,7 @@ k_badmm_tma(const IterArgs<T> a) {
         bad |= !isfinite(wt);
       }
     }
-    if constexpr (PAD) {                               // an odd m_k's last column back to its
+    if constexpr (PAD && !NOSTORE) {                   // an odd m_k's last column back to its
       if (mk & 1) {                                    // single-column layout for the store
         __syncwarp();
         const T px = Ps[(mk - 1) * MP + 2 * i];
@@ -474,9 +477,11 @@ k_badmm_tma(const IterArgs<T> a) {
     __syncwarp();
     if (lane == 0) {
       const uint32_t bp = (uint32_t)(MP * cnp * (int)sizeof(T));
-      tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
-      if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cns, bp);
-      bulk_commit();
+      if constexpr (!NOSTORE) {
+        tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
+        if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cns, bp);
+        bulk_commit();
+      }
       if (nnp > 0 && nbase < 0) {    // pass t+1 did not fit beside pass t: issue it now at the ring start
         bulk_wait_read_all();
         issue(t + 1, 0, np0, nnp);
@@ -497,7 +502,7 @@ k_badmm_tma(const IterArgs<T> a) {
   // this warp's partial sums of the item (segments added in a fixed butterfly order); the
   // consensus kernels add the NWARP warp partials of every item in order: no CTA barrier here
   const int64_t part = (int64_t)item * NWARP + warp;
-  if constexpr (MODE != P2ONLY) {
+  if constexpr (!PH2) {
     T sacc = accw;
 #pragma unroll
     for (int h = MP; h < 32; h <<= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, h);
