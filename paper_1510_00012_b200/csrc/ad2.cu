@@ -963,17 +963,26 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
   if (prof) {
-    g->ev.resize(2 * (size_t)n + 2);
+    g->ev.resize(2 * (size_t)(p2x && n >= 2 && !getenv("AD2_NO_FUSEDX") ? n : n + 1));
     for (auto& e : g->ev) CU(cudaEventCreate(&e));
   }
   CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ad2_status st = AD2_OK;
-  for (int t = 0; t <= n && st == AD2_OK; ++t) {
-    const int mode = t == 0 ? (fresh ? P1INIT : (pending ? FUSED : P1ONLY)) : (t == n ? (p2x ? P2X : P2ONLY) : FUSED);
+  // 32-row blocks with n >= 2: the last FUSED pass also forms the support-update partials
+  // (FUSEDX), so the step has n passes and no P2 pass; otherwise n + 1 passes ending with P2X /
+  // P2ONLY.  Phase 2 of the last iteration is then deferred to the next step's first (FUSED) pass.
+  static const bool no_fx = getenv("AD2_NO_FUSEDX") != nullptr;   // A/B knob (bench experiments)
+  const bool fx = p2x && n >= 2 && !no_fx;
+  const int npass = fx ? n : n + 1;
+  for (int t = 0; t < npass && st == AD2_OK; ++t) {
+    int mode;
+    if (t == 0) mode = fresh ? P1INIT : (pending ? FUSED : P1ONLY);
+    else if (t == npass - 1) mode = fx ? FUSEDX : (p2x ? P2X : P2ONLY);
+    else mode = FUSED;
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
     st = launch_iter(ctx, mode, s);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
-    if (st == AD2_OK && t < n) st = consensus(ctx, s);
+    if (st == AD2_OK && (fx || t < n)) st = consensus(ctx, s);
   }
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &graph);

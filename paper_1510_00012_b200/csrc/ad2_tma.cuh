@@ -101,7 +101,7 @@ template <> struct Pr<double> {
 };
 
 template <typename T, int MP, int NCH, int MODE, int DP>
-__global__ void __launch_bounds__(NWARP * 32, 3)
+__global__ void __launch_bounds__(NWARP * 32, MODE == FUSEDX ? 2 : 3)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
@@ -157,11 +157,14 @@ k_badmm_tma(const IterArgs<T> a) {
   }
   T accw = T(0), accm = T(0);
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);     // phase 2 only (+ x partials)
+  constexpr bool XP = (MODE == FUSEDX);                      // FUSED + x partials
+  constexpr int FM = XP ? FUSED : MODE;                      // the mode the sweeps follow
+  static_assert(!XP || G == 1, "FUSEDX is instantiated for 32-row blocks only");
   constexpr bool NOSTORE = (MODE == P2X);
   static_assert(!NOSTORE || G == 1, "P2X is instantiated for 32-row blocks only");
-  T accx[PH2 ? DP : 1];
+  T accx[(PH2 || XP) ? DP : 1];
 #pragma unroll
-  for (int t = 0; t < (PH2 ? DP : 1); ++t) accx[t] = T(0);
+  for (int t = 0; t < ((PH2 || XP) ? DP : 1); ++t) accx[t] = T(0);
   bool bad = false;
 
   const T* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
@@ -378,7 +381,7 @@ k_badmm_tma(const IterArgs<T> a) {
         for (int h = 0; h < 2; ++h) {
           const int jp = 2 * jb + h, j = 2 * jp;
           T2 q = q2[jp];
-          if constexpr (MODE == FUSED) {
+          if constexpr (FM == FUSED) {
             q = PR::fma(q2[jp], f2, ef2);                                 // Pi2 (Eq.badmmc1)
             l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
           }
@@ -439,20 +442,52 @@ k_badmm_tma(const IterArgs<T> a) {
           racc2[h] = PR::fma(p2[jp], e, racc2[h]);
           if constexpr (PAD) {
             *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = p2[jp];
-            if (MODE == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
+            if (FM == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
           } else {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int jj = j + u;
               if (jj < mk) {                 // packed blocks (G > 1): no tail writes
                 Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
-                if (MODE == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+                if (FM == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
               }
             }
           }
         }
       }
       const T r2 = (racc2[0].x + racc2[1].x) + (racc2[0].y + racc2[1].y) + mkeps;
+      if constexpr (XP) {
+        // support-update partials of the Pi2 = (pe + eps) w_i / r that phase 2 of this iteration
+        // will form (Eq.badmmc1): per member sum_j (pe_ij + eps) y_j / r_i and a count of 1 per
+        // row (w_i cancels in Eq.updatex, X5); pe = Pi1 exp(Lambda/rho) recomputed
+        const T ir = (has && rowok) ? N::div(T(1), r2) : T(0);
+        const T2 ir2 = PR::make(ir, ir), eir2 = PR::make(eps_r * ir, eps_r * ir);
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb) {
+          if (4 * jb >= mkw) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jp = 2 * jb + h, j = 2 * jp;
+            const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
+            const T2 sv = PR::fma(PR::mul(p2[jp], e), ir2, eir2);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int jj = j + u;
+              if (jj < mk) {
+                const T qv = u ? sv.y : sv.x;
+#pragma unroll
+                for (int tt = 0; tt < DP / E; ++tt) {
+                  const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
+                  const T* ve = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                  for (int u2 = 0; u2 < E; ++u2) accx[tt * E + u2] += qv * ve[u2];
+                }
+              }
+            }
+          }
+        }
+        if (has && rowok) accm += T(1);
+      }
       T R = r2;
 #pragma unroll
       for (int h = MP / 2; h >= 1; h >>= 1) R += __shfl_xor_sync(0xffffffffu, R, h);
@@ -507,7 +542,8 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
     for (int h = MP; h < 32; h <<= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, h);
     if (seg == 0 && rowok) a.pw[part * m + i] = sacc;
-  } else {
+  }
+  if constexpr (PH2 || XP) {
     T sm_ = accm;
 #pragma unroll
     for (int h = MP; h < 32; h <<= 1) sm_ += __shfl_xor_sync(0xffffffffu, sm_, h);

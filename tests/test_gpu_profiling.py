@@ -21,17 +21,19 @@ def test_profile_next_step_only():
     torch = torch_cuda()
     b = wl.make_config(3, N=500, K=3)
     ctx = _ctx(b, torch)
+    # 32-row blocks: a step of n >= 2 iterations is n passes (the last one forms the x partials)
+    extra = 0 if (ctx.info()["variant"] == 2 and ctx.info()["mp"] == 32) else 1
     ctx.set_profiling(2)
     ctx.step(3)
     ms3, _ = ctx.prof_read()
-    assert len(ms3) == 4 and all(t > 0 for t in ms3)
+    assert len(ms3) == 3 + extra and all(t > 0 for t in ms3)
     ctx.step(5)                                        # plain graph: the profiled step stays the last
     ms, _ = ctx.prof_read()
-    assert len(ms) == 4
+    assert len(ms) == 3 + extra
     ctx.set_profiling(1)
     ctx.step(5)
     ms5, _ = ctx.prof_read()
-    assert len(ms5) == 6
+    assert len(ms5) == 5 + extra
     with pytest.raises(ad2.AD2Error):
         ctx.set_profiling(3)
     ctx.close()
