@@ -163,8 +163,11 @@ k_badmm_tma(const IterArgs<T> a) {
   constexpr bool NOSTORE = (MODE == P2X);
   static_assert(!NOSTORE || G == 1, "P2X is instantiated for 32-row blocks only");
   T accx[(PH2 || XP) ? DP : 1];
+  T accy[XP ? DP : 1];                                        // FUSEDX: the member's sum (pe + eps) y
 #pragma unroll
   for (int t = 0; t < ((PH2 || XP) ? DP : 1); ++t) accx[t] = T(0);
+#pragma unroll
+  for (int t = 0; t < (XP ? DP : 1); ++t) accy[t] = T(0);
   bool bad = false;
 
   const T* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
@@ -439,7 +442,27 @@ k_badmm_tma(const IterArgs<T> a) {
           const T2 fj = (E == 4) ? fp[h] : *reinterpret_cast<const T2*>(&fbuf[seg * MK + j]);
           p2[jp] = PR::mul(p2[jp], fj);
           const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
-          racc2[h] = PR::fma(p2[jp], e, racc2[h]);
+          if constexpr (XP) {
+            // x partials of the coming Pi2 (see below): sum_j (pe_ij + eps) y_j, scaled by 1/r_i later
+            const T2 pe = PR::mul(p2[jp], e);
+            racc2[h] = PR::add(racc2[h], pe);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int jj = j + u;
+              if (jj < mk) {
+                const T qv = (u ? pe.y : pe.x) + eps_r;
+#pragma unroll
+                for (int tt = 0; tt < DP / E; ++tt) {
+                  const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
+                  const T* ve = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                  for (int u2 = 0; u2 < E; ++u2) accy[tt * E + u2] += qv * ve[u2];
+                }
+              }
+            }
+          } else {
+            racc2[h] = PR::fma(p2[jp], e, racc2[h]);
+          }
           if constexpr (PAD) {
             *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = p2[jp];
             if (FM == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
@@ -458,33 +481,13 @@ k_badmm_tma(const IterArgs<T> a) {
       const T r2 = (racc2[0].x + racc2[1].x) + (racc2[0].y + racc2[1].y) + mkeps;
       if constexpr (XP) {
         // support-update partials of the Pi2 = (pe + eps) w_i / r that phase 2 of this iteration
-        // will form (Eq.badmmc1): per member sum_j (pe_ij + eps) y_j / r_i and a count of 1 per
-        // row (w_i cancels in Eq.updatex, X5); pe = Pi1 exp(Lambda/rho) recomputed
+        // will form (Eq.badmmc1): per member sum_j (pe_ij + eps) y_j / r_i (accumulated in the
+        // sweep above) and a count of 1 per row (w_i cancels in Eq.updatex, X5)
         const T ir = (has && rowok) ? N::div(T(1), r2) : T(0);
-        const T2 ir2 = PR::make(ir, ir), eir2 = PR::make(eps_r * ir, eps_r * ir);
 #pragma unroll
-        for (int jb = 0; jb < NB; ++jb) {
-          if (4 * jb >= mkw) break;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int jp = 2 * jb + h, j = 2 * jp;
-            const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
-            const T2 sv = PR::fma(PR::mul(p2[jp], e), ir2, eir2);
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int jj = j + u;
-              if (jj < mk) {
-                const T qv = u ? sv.y : sv.x;
-#pragma unroll
-                for (int tt = 0; tt < DP / E; ++tt) {
-                  const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
-                  const T* ve = reinterpret_cast<const T*>(&v);
-#pragma unroll
-                  for (int u2 = 0; u2 < E; ++u2) accx[tt * E + u2] += qv * ve[u2];
-                }
-              }
-            }
-          }
+        for (int t = 0; t < DP; ++t) {
+          accx[t] += accy[t] * ir;
+          accy[t] = T(0);
         }
         if (has && rowok) accm += T(1);
       }
