@@ -68,6 +68,18 @@ def test_fp64_ragged_shapes_one_and_five_iterations(m, mk, d):
     compare_round(b, T=5, tau=2, rtol_plan=1e-9, rtol_x=1e-9, atol_w=1e-11, rtol_obj=1e-9)
 
 
+@pytest.mark.parametrize("m,mk,d", [(32, (1, 32), 3), (24, (3, 29), 16)])
+def test_fp64_32_row_blocks_step_shapes(m, mk, d):
+    """32-row blocks (pair layout, odd and even m_k): steps of 1 (P2X), 2 and 3 (FUSEDX) and a
+    trailing single step, with the deferred phase 2 stored on read-back, vs the oracle in fp64."""
+    b = wl.make_random(240, m, d, K=3, mk_range=mk, seed=100 + m, dtype="f64", T=1, tau=1)
+    ctx, _ = compare_round(b, T=1, tau=1, rtol_plan=1e-10, rtol_x=1e-10, atol_w=1e-12)
+    info = ctx.info()
+    assert (info["variant"], info["mp"]) == (2, 32), info
+    compare_round(b, T=5, tau=2, rtol_plan=1e-9, rtol_x=1e-9, atol_w=1e-11, rtol_obj=1e-9)
+    compare_round(b, T=9, tau=3, rtol_plan=1e-9, rtol_x=1e-9, atol_w=1e-11, rtol_obj=1e-9)
+
+
 # ------------------------------------------------------------------ fp32
 
 @pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000), (4, 1500)])
