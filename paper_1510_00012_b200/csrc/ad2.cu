@@ -908,7 +908,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     std::swap(ctx->P.p, ctx->Q.p);
     std::swap(ctx->P.cap, ctx->Q.cap);
     CU(ctx->P.reserve(es * EL));
-  } else if (pair_layout(ctx)) {
+  } else if (ctx->variant == 2) {
     ctx->fresh = true;              // cold round: the first step's P1INIT pass forms Pi2^0, Lambda = 0
   } else {
     if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
@@ -1014,7 +1014,7 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   if (n_iters == 0) return AD2_OK;
   CHK(set_dev(ctx));
   const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
-  const bool fresh = ctx->fresh, pending = ctx->pending, p2x = pair_layout(ctx);
+  const bool fresh = ctx->fresh, pending = ctx->pending, p2x = ctx->variant == 2;
   const int key = 8 * n_iters + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
   auto it = ctx->graphs.find(key);
   StepGraph* g = nullptr;

@@ -135,7 +135,6 @@ k_badmm_tma(const IterArgs<T> a) {
   const T eps_r = rowok ? a.eps : T(0);
   constexpr bool PH1 = (MODE == P1ONLY || MODE == P1INIT);   // phase 1 only
   constexpr bool INIT = (MODE == P1INIT);
-  static_assert(!INIT || G == 1, "P1INIT is instantiated for 32-row blocks only");
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
   // Lambda is stored pre-scaled, L' = Lambda * kx (kx = log2(e)/rho for fp32, 1/rho for fp64), so
   // exp(Lambda/rho) = ex(L') and Eq.badmm2 becomes L' += kappa (Pi1 - Pi2) with kappa = kx * rho
@@ -159,9 +158,7 @@ k_badmm_tma(const IterArgs<T> a) {
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);     // phase 2 only (+ x partials)
   constexpr bool XP = (MODE == FUSEDX);                      // FUSED + x partials
   constexpr int FM = XP ? FUSED : MODE;                      // the mode the sweeps follow
-  static_assert(!XP || G == 1, "FUSEDX is instantiated for 32-row blocks only");
   constexpr bool NOSTORE = (MODE == P2X);
-  static_assert(!NOSTORE || G == 1, "P2X is instantiated for 32-row blocks only");
   T accx[(PH2 || XP) ? DP : 1];
   T accy[XP ? DP : 1];                                        // FUSEDX: the member's sum (pe + eps) y
 #pragma unroll
@@ -343,7 +340,7 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             const T qv = u ? q.y : q.x, lv = u ? l.y : l.x;
-            if (!PAD && jj < mk) {           // packed blocks (G > 1): no tail writes
+            if (!PAD && !NOSTORE && jj < mk) {   // packed blocks (G > 1): no tail writes
               Ps[jj * MP + i] = qv;
               Ls[jj * MP + i] = lv;
             }
@@ -472,7 +469,7 @@ k_badmm_tma(const IterArgs<T> a) {
               const int jj = j + u;
               if (jj < mk) {                 // packed blocks (G > 1): no tail writes
                 Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
-                if (FM == FUSED) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+                if (FM == FUSED || INIT) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
               }
             }
           }

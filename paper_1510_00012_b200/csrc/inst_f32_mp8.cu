@@ -13,11 +13,17 @@ static void go_tma(int mode, const IterArgs<float>& a, int64_t n_items, cudaStre
     cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, P1INIT, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, P2X, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_tma<float, 8, NCH, FUSEDX, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     attr = true;
   }
   dim3 g((unsigned)n_items), b(NWARP * 32);
   if (mode == P1ONLY) k_badmm_tma<float, 8, NCH, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else if (mode == FUSED) k_badmm_tma<float, 8, NCH, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == P1INIT) k_badmm_tma<float, 8, NCH, P1INIT, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == P2X) k_badmm_tma<float, 8, NCH, P2X, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == FUSEDX) k_badmm_tma<float, 8, NCH, FUSEDX, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else k_badmm_tma<float, 8, NCH, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
 }
 
