@@ -210,7 +210,7 @@ ad2_status ad2_get_info(ad2_ctx ctx, ad2_info *info);
  * launch_ms[0..min(capacity, n)-1] with the durations (ms) of the most recent profiled step's
  * launches in order [first (phase 1 only), fused x (n_iters-1), last (phase 2 only)],
  * *n_launches = n_iters + 1 (n_iters when the last pass also forms the support-update partials:
- * 32-row blocks and n_iters >= 2), and *step_ms = first start to last end.  Synchronises. */
+ * the variant-2 kernel and n_iters >= 2), and *step_ms = first start to last end.  Synchronises. */
 ad2_status ad2_set_profiling(ad2_ctx ctx, int enable);
 ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64_t *n_launches,
                          double *step_ms);

@@ -17,10 +17,10 @@
 
 namespace ad2k {
 
-// P1INIT: P1ONLY at the start of a cold round (32-row variant-2 blocks only): Pi2^0 = w_i w_j^(k)
+// P1INIT: P1ONLY at the start of a cold round (variant-2 kernel): Pi2^0 = w_i w_j^(k)
 // and Lambda = 0 are formed in registers instead of being written by k_init_plans and read back
 // P2X: P2ONLY without the stores (the support-update partials only); the next step starts with a
-// FUSED pass that recomputes the same phase 2 (32-row variant-2 blocks only)
+// FUSED pass that recomputes the same phase 2 (variant-2 kernel)
 // FUSEDX: FUSED that also forms the support-update partials of the Pi2 its phase 1 implies
 // (x_i = mean over members of sum_j (pe_ij + eps) y_j / r_i, w_i cancels): the last pass of a step
 enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5 };

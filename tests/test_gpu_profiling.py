@@ -21,8 +21,8 @@ def test_profile_next_step_only():
     torch = torch_cuda()
     b = wl.make_config(3, N=500, K=3)
     ctx = _ctx(b, torch)
-    # 32-row blocks: a step of n >= 2 iterations is n passes (the last one forms the x partials)
-    extra = 0 if (ctx.info()["variant"] == 2 and ctx.info()["mp"] == 32) else 1
+    # variant-2 kernel: a step of n >= 2 iterations is n passes (the last one forms the x partials)
+    extra = 0 if ctx.info()["variant"] == 2 else 1
     ctx.set_profiling(2)
     ctx.step(3)
     ms3, _ = ctx.prof_read()
