@@ -81,6 +81,44 @@ def test_pi1_eps_floor_semantics():
     assert np.isnan(Pn).all()
 
 
+def test_pi1_eps_floor_nonuniform_pi2():
+    """X3, Eq.badmmc0b: eps is added AFTER the product Pi2 * exp(...).  With a
+    NON-uniform Pi2 and every exp of a column underflowing, every entry of that column is exactly
+    eps and Eq.badmmc0 gives pi1_ij = w_j / m whatever Pi2 is; eps inside the product
+    (Pi2 * (exp + eps)) would give w_j * Pi2_ij / sum_l Pi2_lj instead.  Column 1 does not
+    underflow and keeps its closed form."""
+    om = np.array([0.2, 0.8])
+    P2 = np.array([[0.05, 0.10], [0.30, 0.20], [0.15, 0.05], [0.01, 0.14]])
+    C = np.array([[1e5, 0.0], [1e5, 1.0], [1e5, 2.0], [1e5, 0.5]])
+    P = oracle.pi1(P2, np.zeros((4, 2)), C, om, 1.0, eps=1e-16)
+    np.testing.assert_allclose(P[:, 0], np.full(4, 0.2 / 4), rtol=1e-15)
+    a = P2[:, 1] * np.exp(-C[:, 1]) + 1e-16
+    np.testing.assert_allclose(P[:, 1], 0.8 * a / a.sum(), rtol=1e-14)
+    # the same through Lambda: a huge dual on a column acts like a huge cost
+    L = np.zeros((4, 2)); L[:, 0] = 1e5
+    P = oracle.pi1(P2, L, np.zeros((4, 2)), om, 1.0, eps=1e-16)
+    np.testing.assert_allclose(P[:, 0], np.full(4, 0.05), rtol=1e-15)
+
+
+def test_pi1_tilde_eps_presence_and_placement():
+    """X3, Eq.badmmc1b: pt1 = pi1 * exp(lambda / rho) + eps.  A row whose exps all
+    underflow (lambda = -1e4 rho) is EXACTLY eps (not 0: eps dropped; not pi1 * eps: eps inside
+    the product), and Eq.badmmc1 then spreads w_i evenly over the row: w_i / m_k."""
+    rho = 0.37
+    P1 = np.array([[0.2, 0.3, 0.05], [0.1, 0.4, 0.25]])
+    L = np.array([[-1e4 * rho] * 3, [0.0, rho * math.log(2.0), -rho * math.log(4.0)]])
+    B = oracle.pi1_tilde(P1, L, rho, eps=1e-16)
+    np.testing.assert_array_equal(B[0], np.full(3, 1e-16))
+    np.testing.assert_allclose(B[1], [0.1 + 1e-16, 0.8 + 1e-16, 0.0625 + 1e-16], rtol=1e-15)
+    w = np.array([0.3, 0.7])
+    P2 = oracle.pi2(B, w)
+    np.testing.assert_allclose(P2[0], np.full(3, 0.1), rtol=1e-15)                 # w_0 / m_k
+    np.testing.assert_allclose(P2[1], 0.7 * np.array([0.1, 0.8, 0.0625]) / 0.9625, rtol=1e-14)
+    # eps = 0: the underflowed row has no mass and Eq.badmmc1 is 0/0
+    with np.errstate(invalid="ignore"):
+        assert np.isnan(oracle.pi2(oracle.pi1_tilde(P1, L, rho, eps=0.0), w)[0]).all()
+
+
 def test_pi1_single_row_and_zero_cost():
     om = np.array([0.1, 0.6, 0.3])
     P = oracle.pi1(np.array([[0.2, 0.5, 0.3]]), np.ones((1, 3)), np.ones((1, 3)) * 3, om, 1.0)
@@ -163,6 +201,77 @@ def test_P1_P2_P3_marginals_simplex_dual_sum(rule):
         np.testing.assert_allclose(P2.sum(1), res.w, rtol=1e-12)                     # P1: rows
         assert (P1 > 0).all() and (P2 > 0).all()
         assert abs(L.sum()) <= 1e-12 * res.rho                                        # P3
+
+
+def test_alg4_one_iteration_hand_values():
+    """ONE iteration of Alg. 4 from the product init, every quantity by hand (two members, N = 2,
+    so that the consensus w differs from each member's row mass and Pi2 != Pi1).
+    x = (0, 1) on a line; both members have y = (0, 1), omega^A = (.3, .7), omega^B = (.6, .4);
+    w0 = (.5, .5).  C = [[0,1],[1,0]] for both, mean entry cost 1/2, so rho = 2 x 1/2 = 1 (X1;
+    the literal Eq.rho's extra 1/N would give 1/2).  Eq.badmmc0b/c0 with Pi2^0 = w0 (x) omega:
+    Pi1_ij = omega_j e^{-C_ij} / (1 + e^-1) (the w0 and omega factors cancel per column).
+    Lambda^0 = 0, so pt1 = Pi1 + eps, r^k_i = row sums, w = (r^A + r^B)/2 (R1, N = 2, the r's are
+    already normalised), Pi2_ij = Pi1_ij w_i / r_i (Eq.badmmc1), Lambda = rho (Pi1 - Pi2)
+    (Eq.badmm2), and the surrogate objective (X14) is
+    (1/N) sum_k <C, Pi1^k> = (1/2)((.7 + .3) + (.4 + .6)) / (e + 1) = 1 / (e + 1)."""
+    e = math.e
+    Y = np.array([[0.0], [1.0], [0.0], [1.0]])
+    om = np.array([0.3, 0.7, 0.6, 0.4])
+    res = oracle.badmm_centroid([[0.0], [1.0]], [0.5, 0.5], [0, 2, 4], Y, om, 1, 10 ** 6, 0, 2.0, 1e-16)
+    assert res.rho == pytest.approx(1.0, rel=1e-15)
+    P1 = {}
+    r = {}
+    for k, (a, b) in enumerate(((0.3, 0.7), (0.6, 0.4))):
+        P1[k] = np.array([[a * e, b], [a, b * e]]) / (e + 1)
+        r[k] = P1[k].sum(1)
+        np.testing.assert_allclose(res.member("Pi1", k), P1[k], rtol=1e-14)
+    w = (r[0] + r[1]) / 2
+    np.testing.assert_allclose(res.w, w, rtol=1e-14)
+    for k in range(2):
+        P2 = P1[k] * (w / r[k])[:, None]
+        np.testing.assert_allclose(res.member("Pi2", k), P2, rtol=1e-14)
+        np.testing.assert_allclose(res.member("Lam", k), 1.0 * (P1[k] - P2), rtol=1e-12, atol=1e-16)
+    assert res.obj == pytest.approx(1.0 / (e + 1.0), rel=1e-14)
+    # a cheaper entry count check of X1 inside Alg. 4 (N = 2, unequal m_k): T = 0 returns rho only
+    r0 = oracle.badmm_centroid([[0.0], [10.0]], [0.5, 0.5], [0, 2, 3], [[1.0], [2.0], [3.0]], [0.4, 0.6, 1.0], 0, 1)
+    assert r0.rho == pytest.approx(2.0 * 208.0 / 6.0, rel=1e-15)
+
+
+def test_alg4_init_product_and_warm_hand_values():
+    """Alg. 4's initialisation (P:686 with P:842-850): a cold member starts from the product
+    Pi2^0_ij = w0_i omega_j, a warm member from its given Pi2.  Same geometry as above (C =
+    [[0,1],[1,0]], rho = 1) with a NON-uniform w0 = (.4, .6); member A warm from
+    Pi2^w = [[.1, .2], [.25, .45]], member B cold.  After one iteration, by Eq.badmmc0b/c0:
+    Pi1_ij = P_ij e^{-C_ij} omega_j / sum_l P_lj e^{-C_lj} with P = Pi2^w (A) or w0 (x) omega (B)."""
+    e1 = math.exp(-1.0)
+    Y = np.array([[0.0], [1.0], [0.0], [1.0]])
+    om = np.array([0.3, 0.7, 0.6, 0.4])
+    Pw = np.array([[0.1, 0.2], [0.25, 0.45]])
+    w0 = np.array([0.4, 0.6])
+    res = oracle.badmm_centroid([[0.0], [1.0]], w0, [0, 2, 4], Y, om, 1, 10 ** 6, 0, 2.0, 1e-16,
+                                warm=[Pw, np.zeros((2, 2))], warm_mask=[1, 0])
+    G = np.array([[1.0, e1], [e1, 1.0]])
+    for k, P in ((0, Pw * G), (1, np.outer(w0, om[2:]) * G)):
+        want = P / P.sum(0) * om[2 * k:2 * k + 2]
+        np.testing.assert_allclose(res.member("Pi1", k), want, rtol=1e-13)
+
+
+@pytest.mark.parametrize("T,tau", [(3, 3), (6, 3)])
+def test_support_update_is_eq_updatex_on_pi2(T, tau):
+    """X5 / Eq.updatex: x_i = 1/(N w_i) sum_k sum_j pi_ij^(k) x_j^(k) holds LITERALLY
+    (with the paper's 1/(N w_i), not the oracle's measured row mass) for the coupling whose rows
+    sum to w_i, i.e. Pi^(2) (Eq.badmmc1).  Right after the support update at t = T (a multiple of
+    tau) the returned Pi2, w and x are the ones the update used."""
+    b = _cluster(N=7, m=4, d=3, seed=29, mk=(2, 6))
+    res = _run(b, T=T, tau=tau)
+    num = np.zeros((b.m, b.d))
+    for k in range(b.N):
+        y, _ = b.member(k)
+        num += res.member("Pi2", k) @ y
+    np.testing.assert_allclose(res.x, num / (b.N * res.w[:, None]), rtol=1e-12, atol=1e-13)
+    # and not for Pi1: its rows do not sum to w_i (the identity would fail visibly)
+    num1 = sum(res.member("Pi1", k) @ b.member(k)[0] for k in range(b.N))
+    assert np.abs(num1 / (b.N * res.w[:, None]) - res.x).max() > 1e-6
 
 
 @pytest.mark.parametrize("n_iter", [1, 5, 25])
@@ -514,6 +623,23 @@ def test_symbolic_table_equals_euclidean_with_fixed_support():
     assert a.obj == pytest.approx(b.obj, rel=1e-12)
     for k in range(N):
         np.testing.assert_allclose(a.mats["Pi1"][k], b.mats["Pi1"][k], rtol=1e-11, atol=1e-16)
+
+
+def test_symbolic_table_orientation_hand():
+    """Symbolic supports: C^(k)_ij = D[centroid symbol x_i][member symbol y_j].  A
+    NON-symmetric table tells the orientation apart.  m = 1 forces Pi1 = omega, so the
+    surrogate objective is sum_j omega_j D[x_0][y_j] and rho = 2 x mean_j D[x_0][y_j]."""
+    D = np.array([[0.0, 1.0, 4.0], [2.0, 0.0, 5.0], [7.0, 3.0, 0.0]])
+    res = oracle.badmm_table([0], [1.0], [0, 2], [1, 2], [0.25, 0.75], D, 3)
+    assert res.rho == pytest.approx(2.0 * (1.0 + 4.0) / 2, rel=1e-15)               # transposed: 9
+    assert res.obj == pytest.approx(0.25 * 1.0 + 0.75 * 4.0, rel=1e-15)              # transposed: 5.75
+    np.testing.assert_allclose(res.mats["Pi1"][0], [[0.25, 0.75]], rtol=1e-15)
+    # m = 2, one member with one point: C = (D[0][1], D[2][1]) = (1, 3), rho = 2 x 2
+    res = oracle.badmm_table([0, 2], [0.5, 0.5], [0, 1], [1], [1.0], D, 0)
+    assert res.rho == pytest.approx(4.0, rel=1e-15)                                  # transposed: 7
+    # N = 2 (X1 inside the symbolic mode): members {1} and {0, 2}: costs 1, 3 | 0, 4, 7, 0 -> 15 / 6
+    res = oracle.badmm_table([0, 2], [0.5, 0.5], [0, 1, 3], [1, 0, 2], [1.0, 0.5, 0.5], D, 0)
+    assert res.rho == pytest.approx(2.0 * 15.0 / 6.0, rel=1e-15)                     # 1/N typo: 2.5
 
 
 def test_symbolic_support_is_never_updated_and_marginals_hold():
