@@ -35,7 +35,6 @@ from paper_1510_00012_b200.sharding import shard_bounds  # noqa: E402
 
 METRIC = "B-ADMM plan-entry-iterations/sec"
 UNIT = "entry-iter/s"
-BYTES_PER_ENTRY = 16          # algorithmic bytes per entry-iteration: r+w Pi-state and Lambda
 CACHE = os.environ.get("AD2_BENCH_CACHE", "/dev/shm/ad2_bench")
 
 
@@ -220,13 +219,17 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     # dominant kernel: the fused iteration kernel (launches 1..n-1 of each step graph)
     fused = launch_ms[1:-1] if len(launch_ms) > 2 else launch_ms
     avg_fused_ms = float(np.mean(fused))
+    # algorithmic bytes per entry-iteration: read + write of the plan state and
+    # Lambda (16 B fp32, 32 B fp64), plus the read of a cached C (variants 3 / 0 keep C in HBM)
+    es = 8 if b.dtype == "f64" else 4
+    bytes_per_entry = 4 * es + (es if info["variant"] in (0, 3) else 0)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = BYTES_PER_ENTRY * entries_local / (avg_fused_ms / 1e3) / 1e9
+    achieved = bytes_per_entry * entries_local / (avg_fused_ms / 1e3) / 1e9
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -293,10 +296,11 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": {3: "k_badmm_wide", 2: "k_badmm_tma", 1: "k_badmm_warp", 0: "k_badmm_generic"}[info["variant"]]
                      + "<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
-                     "bytes_per_entry": BYTES_PER_ENTRY, "entries_per_launch": entries_local,
+                     "bytes_per_entry": bytes_per_entry, "entries_per_launch": entries_local,
                      "avg_launch_ms": avg_fused_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "iteration_kernels_share_of_step": iter_share},
-        "iter_only": {"value": entries_total * T / ((np.sum(launch_ms) * T / max(1, len(launch_ms) - 1)) / 1e3),
+        # the profiled graph is one step(tau) (tau iterations in tau or tau + 1 launches); a round runs T/tau
+        "iter_only": {"value": entries_total * T / ((np.sum(launch_ms) * (T // tau)) / 1e3),
                       "note": "iteration kernels only (event-timed), excluding consensus/init/objective"},
         "steps_and_updates": {"value": entries_total * T / (sched_ms / 1e3), "ms": sched_ms,
                               "note": "SURVEY.md 8(d) definition: ad2_badmm_step + ad2_update_support only "
@@ -311,11 +315,26 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
 
 # ------------------------------------------------------------------------------------------ oracle
 
-def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, n_clusters=None):
+_NCORES = None
+
+
+def host_cores() -> int:
+    """All host cores the oracle's OpenMP runtime offers, read ONCE before any oracle call (a call
+    with nthreads = k sets the OpenMP thread count for the rest of the process)."""
+    global _NCORES
+    if _NCORES is None:
+        import oracle
+        _NCORES = oracle.max_threads()
+    return _NCORES
+
+
+def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, n_clusters=None, one_thread=True):
     """The fp64 oracle (Alg. 4 as written, OpenMP over members) on a bounded sample of the same
     workload: whole clusters 0, 1, ... with the full schedule until about budget_s of host time
-    (or exactly n_clusters when given, for repeatable reference steps)."""
+    (or exactly n_clusters when given, for repeatable reference steps), on every host core; then
+    (one_thread) the 1-thread rate on a small sample."""
     import oracle
+    ncores = host_cores()
     s = b.sched
     t_all, entries, members, c = 0.0, 0, 0, 0
     while c < b.K:
@@ -323,20 +342,20 @@ def cpu_baseline(b: wl.Bundle, budget_s: float = 15.0, n_clusters=None):
         sub = b.subset(mem)
         t = time.time()
         oracle.badmm_centroid(b.x0[c], b.w0[c], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
-                              s.eps, 1e-5, want_state=False)
+                              s.eps, 1e-5, nthreads=ncores, want_state=False)
         t_all += time.time() - t
         entries += b.m * sub.n
         members += sub.N
         c += 1
         if (n_clusters is not None and c >= n_clusters) or (n_clusters is None and t_all >= budget_s):
             break
-    out = {"value": entries * s.T / t_all, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+    out = {"value": entries * s.T / t_all, "unit": UNIT, "cores": ncores, "kind": "oracle",
            "sample": f"clusters 0..{c - 1} of {b.name}: {members} members ({entries} plan entries), T={s.T}, "
                      f"tau={s.tau}, fp64, {t_all:.1f}s", "n_clusters": c, "cpu_model": cpu_model()}
-    if n_clusters is None:
+    if n_clusters is None and one_thread:
         # the 1-thread rate on the first members of cluster 0, ~2 s
         mem = np.nonzero(b.labels == 0)[0]
-        k = max(1, min(len(mem), int(len(mem) * min(1.0, 2.0 / max(t_all / c, 1e-3)) / max(1, oracle.max_threads()))))
+        k = max(1, min(len(mem), int(len(mem) * min(1.0, 2.0 / max(t_all / c, 1e-3)) / max(1, ncores))))
         sub = b.subset(mem[:k])
         t = time.time()
         oracle.badmm_centroid(b.x0[0], b.w0[0], sub.offsets, sub.supports, sub.weights, s.T, s.tau, s.rule, s.rho0,
@@ -362,7 +381,7 @@ def run_reference(args, rank, world):
         return
     b = load_bundle(args.workload, 0, 1, lambda: None)
     # each reference step: the same bounded sample (whole clusters), sized so the run stays short
-    probe = cpu_baseline(b, budget_s=max(2.0, args.cpu_budget / max(1, args.steps + args.warmup)))
+    probe = cpu_baseline(b, budget_s=max(2.0, args.cpu_budget / max(1, args.steps + args.warmup)), one_thread=False)
     nc = probe["n_clusters"]
     for _ in range(max(0, args.warmup - 1)):
         cpu_baseline(b, n_clusters=nc)

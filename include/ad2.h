@@ -111,7 +111,10 @@ typedef struct {
     int64_t n_points;           /* sum_k m_k on this rank */
     int64_t entries;            /* sum_k m * m_k on this rank (plan entries per iteration) */
     int64_t n_items;            /* work items (per-cluster member chunks) */
-    int32_t variant;            /* 2 = TMA-staged fused kernels, 1 = fused warp-per-member (cached C), 0 = generic */
+    int32_t variant;            /* 2 = TMA-staged fused kernel, cost recomputed in-kernel (m <= 32, d <= 16);
+                                   3 = TMA-staged warp / warp-pair / warp-quad kernel with a cost cache (fp32,
+                                   m <= 128, m_k <= 128, any d; configs 4 and symbolic rounds);
+                                   0 = generic one-thread-per-member kernels (anything else) */
     int32_t mp, nch;            /* fused-kernel row tile (8/16/32) and column chunks */
     int32_t nranks, rank;
     int64_t launches;           /* kernels launched by this context so far (graph nodes counted) */
