@@ -36,7 +36,12 @@
  *  - Multi-GPU: one context per GPU/process, each with its own member shard; every
  *    rank calls every function with the same d, m, K, params, x0, w0 and the same schedule.
  *    The per-cluster partial sums (w: K*m per iteration, x: K*m*(d+1) per support update, rho
- *    and objective: K) are summed across ranks by NCCL all-reduce over NVLink.
+ *    and objective: K) are summed across ranks by NCCL all-reduce over NVLink (or by a host
+ *    process group, below).  Errors agree across ranks: ad2_barycenter_init, ad2_objective,
+ *    ad2_sync and ad2_cluster exchange every rank's status before the next collective, so a
+ *    rank-local error (a bad label, weights off the simplex, a non-finite value) makes every
+ *    rank return an error instead of leaving the others waiting in a collective.  A rank with
+ *    no members (n_members = 0) takes part in every collective with zero partial sums.
  */
 #ifndef AD2_H
 #define AD2_H
@@ -133,6 +138,30 @@ ad2_status ad2_nccl_unique_id(void *id_out);
 /* Join an NCCL communicator of `nranks` ranks (this one is `rank`), created from `unique_id`.
  * Must precede ad2_barycenter_init.  nranks == 1 is allowed (all-reduce degenerates to a copy). */
 ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void *unique_id);
+
+/* ---- Host process group: the same cross-rank sums without NCCL --------------------------------
+ * The member-sharded path needs one all-reduce of per-cluster
+ * partial sums per iteration / support update / round.  NCCL needs one GPU per rank; a host
+ * process group serves ranks that are processes on ONE host, e.g. several ranks sharing one GPU
+ * (testing the sharded path on a one-GPU box) or hosts without NCCL.  Ranks share a POSIX
+ * shared-memory segment `name` ("/..."); an all-reduce sums the ranks' buffers in rank order, so
+ * every rank receives the bit-identical sum.  Inside libad2 it runs as a device->host copy, a
+ * host-function node and a host->device copy in the step's CUDA graph (no kernel waits on
+ * another rank).  A barrier that waits longer than AD2_GROUP_TIMEOUT seconds (default 300)
+ * latches a failure: every later libad2 call on an attached context returns AD2_ERR_NCCL.
+ *
+ * ad2_group_open: collective over the `nranks` processes (blocks until all have joined);
+ *   slot_bytes = the largest single all-reduce (>= 8 K m (d + 1) bytes covers libad2's use).
+ * ad2_group_allreduce: in-place sum of `count` host elements (dtype AD2_GROUP_*) over the group.
+ * ad2_attach_group: the context borrows g (g must outlive the context); instead of
+ *   ad2_attach_nccl, before ad2_barycenter_init.
+ * ad2_group_close: unmaps; call after every context using g is destroyed. */
+typedef struct ad2_group_s *ad2_group;
+enum { AD2_GROUP_F32 = 0, AD2_GROUP_F64 = 1, AD2_GROUP_U64 = 2 };
+ad2_status ad2_group_open(ad2_group *out, const char *name, int nranks, int rank, int64_t slot_bytes);
+ad2_status ad2_group_allreduce(ad2_group g, void *host_buf, int64_t count, int32_t dtype);
+ad2_status ad2_attach_group(ad2_ctx ctx, ad2_group g);
+void ad2_group_close(ad2_group g);
 
 /* Start a round (a1-a3 of SURVEY.md §8(a)): copy/sort the batch by cluster, build C, compute
  * rho per cluster (fixed for the round, X2), Lambda = 0, Pi^(2) = product measure or, for

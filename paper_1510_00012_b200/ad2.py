@@ -61,6 +61,7 @@ EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycente
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
            "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
            "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_prefetch", "ad2_sync",
+           "ad2_group_open", "ad2_group_allreduce", "ad2_attach_group", "ad2_group_close",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
@@ -103,8 +104,13 @@ def load_library(path: str = LIB_PATH):
     L.ad2_status_string.restype = C.c_char_p
     L.ad2_destroy.argtypes = [p]
     L.ad2_destroy.restype = None
+    L.ad2_group_open.argtypes = [C.POINTER(p), C.c_char_p, C.c_int, C.c_int, i64]
+    L.ad2_group_allreduce.argtypes = [p, p, i64, i32]
+    L.ad2_attach_group.argtypes = [p, p]
+    L.ad2_group_close.argtypes = [p]
+    L.ad2_group_close.restype = None
     for f in EXPORTS:
-        if f not in ("ad2_last_error", "ad2_status_string", "ad2_destroy"):
+        if f not in ("ad2_last_error", "ad2_status_string", "ad2_destroy", "ad2_group_close"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -131,6 +137,38 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise AD2Error(st, "ncclGetUniqueId failed / NCCL not loadable")
     return buf.raw
+
+
+GROUP_F32, GROUP_F64, GROUP_U64 = 0, 1, 2
+
+
+class Group:
+    """Host process group (ad2_group_open): ranks that are processes on one host sum libad2's
+    per-cluster partials through POSIX shared memory instead of NCCL.  Collective: every rank
+    opens the same `name` ("/...") with the same nranks."""
+
+    def __init__(self, name: str, nranks: int, rank: int, slot_bytes: int = 64 << 20):
+        self.L = load_library()
+        h = C.c_void_p()
+        st = self.L.ad2_group_open(C.byref(h), name.encode(), int(nranks), int(rank), int(slot_bytes))
+        if st != 0:
+            raise AD2Error(st, f"ad2_group_open({name!r}, {nranks}, {rank}) failed")
+        self.h = h
+        self.nranks, self.rank = nranks, rank
+
+    def allreduce(self, a: np.ndarray) -> np.ndarray:
+        """In-place sum of a host array over the group (rank order)."""
+        dt = {np.dtype(np.float32): GROUP_F32, np.dtype(np.float64): GROUP_F64,
+              np.dtype(np.uint64): GROUP_U64}[a.dtype]
+        st = self.L.ad2_group_allreduce(self.h, _ptr(a), a.size, dt)
+        if st != 0:
+            raise AD2Error(st, "ad2_group_allreduce failed")
+        return a
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ad2_group_close(self.h)
+            self.h = None
 
 
 class Context:
@@ -164,6 +202,10 @@ class Context:
 
     def attach_nccl(self, nranks: int, rank: int, unique_id: bytes):
         self._chk(self.L.ad2_attach_nccl(self.h, nranks, rank, C.c_char_p(unique_id)))
+
+    def attach_group(self, group: "Group"):
+        self._chk(self.L.ad2_attach_group(self.h, group.h))
+        self._keep.append(group)                # the group must outlive the context
 
     def init(self, offsets, supports, weights, labels, x0, w0, K: int, m: int, rho0=2.0, eps=1e-16,
              rule=R1, warm_mask=None, mem: str = "device", dtype: Optional[str] = None,

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/ad2.h"
+#include "ad2_group.h"
 #include "ad2_kernels.cuh"
 
 using namespace ad2k;
@@ -84,6 +85,22 @@ static void dbuf_swap(DBuf& a, DBuf& b) {
   std::swap(a.cap, b.cap);
 }
 
+// one cross-rank sum over a host process group (ad2_group.cu), captured as a host-function node
+// between a device->host and a host->device copy of the buffer; lives as long as the context
+struct HostSum {
+  ad2_group g = nullptr;
+  void* host = nullptr;          // pinned staging copy of the device buffer
+  size_t count = 0;
+  int dtype = 0;
+  ~HostSum() {
+    if (host) cudaFreeHost(host);
+  }
+};
+static void CUDART_CB host_sum_fn(void* p) {
+  HostSum* h = static_cast<HostSum*>(p);
+  ad2_group_sum_host(h->g, h->host, h->count, h->dtype);   // a failure is latched in the group
+}
+
 struct StepGraph {
   cudaGraphExec_t exec = nullptr;
   int64_t nodes = 0;
@@ -101,6 +118,9 @@ struct ad2_ctx_s {
   cudaStream_t cap = nullptr;        // private stream used only for graph capture
   std::string msg;
   ncclComm_t comm = nullptr;
+  ad2_group grp = nullptr;           // host process group (borrowed; ad2_attach_group)
+  std::map<std::pair<void*, size_t>, HostSum*> host_sums;
+  DBuf agree_d;
   int nranks = 1, rank = 0;
 
   // round shape
@@ -154,6 +174,7 @@ struct ad2_ctx_s {
 
   ~ad2_ctx_s() {
     clear_graphs();
+    for (auto& kv : host_sums) delete kv.second;
     if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
     if (cap) cudaStreamDestroy(cap);
     if (pfs) {
@@ -200,7 +221,31 @@ static ad2_status launch_check(ad2_ctx ctx, const char* what) {
   return AD2_OK;
 }
 
+// several ranks share the per-cluster sums (NCCL communicator or host process group)
+static bool multi(ad2_ctx ctx) { return ctx->comm != nullptr || ctx->grp != nullptr; }
+
+static ad2_status host_allreduce(ad2_ctx ctx, void* buf, size_t count, ncclDataType_t dt, cudaStream_t s) {
+  const int gt = dt == ncclFloat32 ? AD2_GROUP_F32 : dt == ncclFloat64 ? AD2_GROUP_F64 : AD2_GROUP_U64;
+  const size_t bytes = count * ad2_group_type_size(gt);
+  HostSum*& h = ctx->host_sums[std::make_pair(buf, bytes)];
+  if (!h) {
+    h = new HostSum();
+    h->g = ctx->grp;
+    if (cudaMallocHost(&h->host, bytes ? bytes : 8) != cudaSuccess) {
+      h->host = nullptr;
+      return ctx->fail(AD2_ERR_OOM, "host group: pinned staging of %zu bytes", bytes);
+    }
+  }
+  h->count = count;
+  h->dtype = gt;
+  CU(cudaMemcpyAsync(h->host, buf, bytes, cudaMemcpyDeviceToHost, s));
+  CU(cudaLaunchHostFunc(s, host_sum_fn, h));
+  CU(cudaMemcpyAsync(buf, h->host, bytes, cudaMemcpyHostToDevice, s));
+  return AD2_OK;
+}
+
 static ad2_status allreduce(ad2_ctx ctx, void* buf, size_t count, ncclDataType_t dt, cudaStream_t s) {
+  if (ctx->grp) return host_allreduce(ctx, buf, count, dt, s);
   if (!ctx->comm) return AD2_OK;
   ncclResult_t r = g_nccl.AllReduce(buf, buf, count, dt, ncclSum, ctx->comm, s);
   if (r != ncclSuccess)
@@ -301,7 +346,7 @@ static ad2_status launch_iter(ad2_ctx ctx, int mode, cudaStream_t s) {
 // consensus w: per-cluster sum of item partials, all-reduce across ranks, finalise R1/R2
 template <typename T>
 static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
-  const bool fin = ctx->comm == nullptr;
+  const bool fin = !multi(ctx);
   const size_t sh = sizeof(T) * (size_t)ctx->m;
   k_wsum<T><<<ctx->K, 256, sh + 256 * sizeof(T), s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->Sw.as<T>(),
                                     ctx->w.as<T>(), ctx->rule, fin ? 1 : 0, ctx->d_err.as<int>());
@@ -404,9 +449,41 @@ static ad2_status read_err(ad2_ctx ctx) {
   int h = 0;
   CU(cudaMemcpyAsync(&h, ctx->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (ad2_group_failed(ctx->grp)) return ctx->fail(AD2_ERR_NCCL, "host process group: a collective failed or timed out");
   if (h & ERR_WEIGHTS) return ctx->fail(AD2_ERR_ARG, "member weights off the simplex (|sum-1| > tol)");
   if (h & ERR_NONFINITE) return ctx->fail(AD2_ERR_NONFINITE, "non-finite plan row mass or weight");
   if (h & ERR_SYMBOL) return ctx->fail(AD2_ERR_ARG, "a symbol id outside [0, V) of the cost table");
+  return AD2_OK;
+}
+
+const char* ad2_status_string(ad2_status s);
+
+// Multi-rank runs: every rank returns an error status if any rank hit one (a rank that returned
+// alone would leave the others waiting in the next collective).  A rank with a local error keeps
+// its own status and message; the others return the lowest failing status of another rank.
+// No effect with one rank.
+static ad2_status agree(ad2_ctx ctx, ad2_status local) {
+  if (!multi(ctx) || ctx->nranks <= 1) return local;
+  constexpr int NS = 16;
+  double v[NS] = {0};
+  v[((int)local >= 0 && (int)local < NS) ? (int)local : NS - 1] = 1.0;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return local;
+  if (ctx->grp) {
+    // the stream's earlier collectives (host-function nodes) come first, in the same order on every rank
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || ad2_group_sum_host(ctx->grp, v, NS, AD2_GROUP_F64) != 0)
+      return local != AD2_OK ? local : ctx->fail(AD2_ERR_NCCL, "host process group: status agreement failed");
+  } else {
+    if (ctx->agree_d.reserve(sizeof v) != cudaSuccess ||
+        cudaMemcpyAsync(ctx->agree_d.p, v, sizeof v, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        g_nccl.AllReduce(ctx->agree_d.p, ctx->agree_d.p, NS, ncclFloat64, ncclSum, ctx->comm, ctx->stream) != ncclSuccess ||
+        cudaMemcpyAsync(v, ctx->agree_d.p, sizeof v, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      return local != AD2_OK ? local : ctx->fail(AD2_ERR_NCCL, "NCCL: status agreement failed");
+  }
+  if (local != AD2_OK) return local;
+  for (int k = 1; k < NS; ++k)
+    if (v[k] > 0.0)
+      return ctx->fail((ad2_status)k, "%g other rank(s) failed with: %s", v[k], ad2_status_string((ad2_status)k));
   return AD2_OK;
 }
 
@@ -527,7 +604,7 @@ ad2_status ad2_nccl_unique_id(void* id_out) {
 
 ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void* unique_id) {
   if (!ctx || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return AD2_ERR_ARG;
-  if (ctx->comm) return ctx->fail(AD2_ERR_STATE, "NCCL communicator already attached");
+  if (multi(ctx)) return ctx->fail(AD2_ERR_STATE, "a communicator or group is already attached");
   if (!nccl_load()) return ctx->fail(AD2_ERR_NCCL, "libnccl.so.2 not loadable");
   CHK(set_dev(ctx));
   ncclUniqueId id;
@@ -539,6 +616,16 @@ ad2_status ad2_attach_nccl(ad2_ctx ctx, int nranks, int rank, const void* unique
   }
   ctx->nranks = nranks;
   ctx->rank = rank;
+  ctx->clear_graphs();
+  return AD2_OK;
+}
+
+ad2_status ad2_attach_group(ad2_ctx ctx, ad2_group g) {
+  if (!ctx || !g) return AD2_ERR_ARG;
+  if (multi(ctx)) return ctx->fail(AD2_ERR_STATE, "a communicator or group is already attached");
+  ctx->grp = g;
+  ctx->nranks = ad2_group_size(g);
+  ctx->rank = ad2_group_rank(g);
   ctx->clear_graphs();
   return AD2_OK;
 }
@@ -555,21 +642,45 @@ static void launch_gather(ad2_ctx ctx, const void* Ysrc, const void* Wsrc, doubl
       rho_sums ? ctx->pm.as<double>() : nullptr);
 }
 
+// warm: Pi2 of the warm members from the previous round's Q, stored with ld_src rows per column
+// (pair_src: the pair layout); cold: the product measure
 template <typename T>
-static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst) {
+static void launch_init_plans(ad2_ctx ctx, bool warm, T* dst, int ld_src = 0, bool pair_src = false) {
   if (ctx->n_items == 0) return;
+  if (!warm) {
+    ld_src = ctx->ld;
+    pair_src = pair_layout(ctx);
+  }
   k_init_plans<T><<<(unsigned)ctx->n_items, 128, 0, ctx->stream>>>(
       ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),
       warm ? ctx->d_warm.as<int64_t>() : nullptr, ctx->om.as<T>(), ctx->w.as<T>(), ctx->Q.as<T>(), dst,
-      ctx->L.as<T>(), ctx->m, ctx->ld, pair_layout(ctx));
+      ctx->L.as<T>(), ctx->m, ctx->ld, pair_layout(ctx), ld_src, pair_src);
 }
 
 static ad2_status materialise_phase2(ad2_ctx ctx);
 
 // warm_dev: warm_mask is a device array (the outer loop's label-diff mask, always "some warm")
+// Three phases: validate (no state change: an error leaves the previous round intact), commit
+// (layout and buffers of the new round, rank-local), global (the cross-rank counts and sums, rho).
+// With several ranks, every rank's status is agreed after each of the first two phases (agree),
+// so a rank-local error makes every rank return before the next collective instead of leaving
+// the others waiting in it.
 static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0, const void* w0,
                             const uint8_t* warm_mask, bool warm_dev, double* rho_out) {
   if (!ctx) return AD2_ERR_ARG;
+  // shared by the phases
+  int64_t N = 0, n = 0, mkmax = 0, per_item = 1, n_items = 0;
+  int d = 0, m = 0, K = 0, variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0, ld = 0, dy = 0;
+  size_t es = 4;
+  bool host = false, table = false, warm = false, prefetched = false;
+  cudaMemcpyKind h2d = cudaMemcpyDeviceToDevice;
+  cudaStream_t s = ctx->stream;
+  const int64_t* off_in = nullptr;
+  const int32_t* lab_in = nullptr;
+  unsigned long long* scal = nullptr;
+  std::vector<unsigned long long> hcnt, hpts;
+
+  auto validate = [&]() -> ad2_status {
   if (!b || !prm || !x0 || !w0) return ctx->fail(AD2_ERR_ARG, "null batch/params/x0/w0");
   if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
   if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "mem");
@@ -582,26 +693,35 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
       (prm->cost_mode != AD2_COST_FP32 && prm->cost_mode != AD2_COST_TC_BF16 && prm->cost_mode != AD2_COST_TABLE))
     return ctx->fail(AD2_ERR_ARG, "params rho0=%g eps=%g rule=%d cost_mode=%d", prm->rho0, prm->eps, prm->rule,
                      prm->cost_mode);
-  const bool table = prm->cost_mode == AD2_COST_TABLE;
+  table = prm->cost_mode == AD2_COST_TABLE;
   if (table && (b->d != 1 || ctx->tab_V < 1 || ctx->tab_dtype != (int)b->dtype))
     return ctx->fail(AD2_ERR_ARG, "cost_mode 2 (symbolic) needs d = 1 (int32 symbol ids) and a cost table of the "
                      "batch dtype (ad2_set_cost_table)");
   CHK(set_dev(ctx));
-  // a warm start reads the previous round's Pi2: store it first if the last step deferred it
-  if (ctx->pending && (warm_mask || warm_dev)) CHK(materialise_phase2(ctx));
-  ctx->pending = false;
-  const int64_t N = b->n_members;
-  const int d = b->d, m = b->m, K = b->K;
-  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
-  const bool host = b->mem == AD2_HOST;
-  const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // a warm start reads the previous round's Pi2: store it first if the last step deferred it, or
+  // form Pi2^0 if the previous round was never stepped (a cold variant-2 round forms it in its
+  // first pass).  Both leave the previous round's state intact if this init then fails; the
+  // flags are cleared only once the new round is committed.
+  if (warm_mask || warm_dev) {
+    if (ctx->pending) CHK(materialise_phase2(ctx));
+    if (ctx->fresh && ctx->state >= 1) {
+      if (ctx->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());
+      else launch_init_plans<float>(ctx, false, ctx->Q.as<float>());
+      if (ctx->n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
+      ctx->fresh = false;
+    }
+  }
+  N = b->n_members;
+  d = b->d, m = b->m, K = b->K;
+  es = b->dtype == AD2_F64 ? 8 : 4;
+  host = b->mem == AD2_HOST;
+  h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
 
-  cudaStream_t s = ctx->stream;
   // ---- index arrays on the device (host batches are staged), validated before any state change
-  const int64_t* off_in = static_cast<const int64_t*>(b->offsets);
-  const int32_t* lab_in = b->labels;
+  off_in = static_cast<const int64_t*>(b->offsets);
+  lab_in = b->labels;
   // a matching ad2_prefetch (same host arrays and sizes) already copied the batch: swap it in
-  bool prefetched = false;
+  prefetched = false;
   const bool pf_pending = ctx->pf_valid;
   ctx->pf_valid = false;                            // any init consumes or discards a prefetch
   if (host && N > 0 && pf_pending) {
@@ -631,12 +751,10 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   CU(ctx->lay_cnt.reserve(8 * (size_t)K));
   CU(ctx->lay_pts.reserve(8 * (size_t)K));
   CU(ctx->lay_scal.reserve(64));
-  CU(ctx->lay_cstart.reserve(8 * ((size_t)K + 1)));
   CU(cudaMemsetAsync(ctx->lay_cnt.p, 0, 8 * (size_t)K, s));
   CU(cudaMemsetAsync(ctx->lay_pts.p, 0, 8 * (size_t)K, s));
   CU(cudaMemsetAsync(ctx->lay_scal.p, 0, 64, s));
-  unsigned long long* scal = ctx->lay_scal.as<unsigned long long>();
-  int64_t n = 0, mkmax = 0;
+  scal = ctx->lay_scal.as<unsigned long long>();
   if (N > 0) {
     CU(ctx->lay_keys.reserve(sizeof(int32_t) * N));
     CU(ctx->lay_keys2.reserve(sizeof(int32_t) * N));
@@ -653,7 +771,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     if (hs[0] & 2) return ctx->fail(AD2_ERR_ARG, "a member has m_k < 1 or a label outside [0,%d)", K);
     mkmax = (int64_t)hs[1];
   }
-  const bool warm = warm_mask != nullptr && N > 0;
+  warm = warm_mask != nullptr && N > 0;
   if (warm) {
     bool any = warm_dev;
     if (!warm_dev)
@@ -669,7 +787,6 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   //      pair (ld 64) for m <= 64; also every symbolic (cost-table) round with those sizes
   //   0: generic one-thread-per-member kernels (anything else, e.g. fp64 with m > 32)
   //   (1: the direct-load warp kernel with a cost cache is no longer selected)
-  int variant = 0, mp = 0, nch = 0, dp = 0;
   const int E = (int)(16 / es);
   for (int cand : {8, 16, 32}) {
     if (table) break;                      // symbolic: cost from the table, cached (variants 3 / 0)
@@ -689,7 +806,6 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
     if (tma_bytes(b->dtype, mp, nch, dp) > (size_t)optin) variant = 0;
   }
-  int wcfg = 0;
   if (variant == 0 && b->dtype == AD2_F32 && m <= 128 && mkmax <= 128) {   // any d (d > 64: k_xpart)
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
@@ -708,9 +824,8 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
                      "(fp32, 32 < m <= 64, m_k <= 64, d <= 64)");
   // variant 2: blocks padded to MP rows; Y rows hold [y, |y|^2, 0...] padded to 16 bytes and >= DP
   // variant 3: blocks padded to WM (32 / 64) rows; Y rows padded with zeros to a multiple of 4
-  const int ld = (variant == 2 || variant == 3) ? mp : m;
-  const int dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : (variant == 3 ? (d + 3) / 4 * 4 : d);
-  if (warm && ld != ctx->ld) return ctx->fail(AD2_ERR_ARG, "warm start with a different plan layout");
+  ld = (variant == 2 || variant == 3) ? mp : m;
+  dy = variant == 2 ? (dp == 4 ? 4 : 16 + E) : (variant == 3 ? (d + 3) / 4 * 4 : d);
   // work items: variant 2/1 = one CTA's run of member passes (variant 2 sizes it so the grid still
   // covers every SM a few times), variant 0 = one member
   int passes = ITEM_PASSES;
@@ -722,9 +837,13 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     passes = (int)std::max<int64_t>(8, std::min<int64_t>(32, want));
     if (const char* e = getenv("AD2_PASSES")) passes = std::max(1, atoi(e));   // tuning knob (bench experiments)
   }
-  const int64_t per_item = variant == 3 ? (int64_t)wide_npair(wcfg) * passes
+  per_item = variant == 3 ? (int64_t)wide_npair(wcfg) * passes
                            : variant ? (int64_t)NWARP * (32 / mp) * passes : 1;
 
+  return AD2_OK;
+  };
+
+  auto commit = [&]() -> ad2_status {
   // ---- from here on the previous round's state is replaced (an error leaves the context
   //      needing a fresh init): stable radix sort by cluster, sorted offsets, work items
   ctx->state = 0;
@@ -733,6 +852,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   ctx->clear_graphs();
   const int64_t old_N = ctx->N;
   const int old_ld = ctx->ld;
+  const bool old_pair = pair_layout(ctx);     // layout of the previous round's Q (warm source)
   if (warm) {
     std::swap(ctx->d_off.p, ctx->d_off_old.p);
     std::swap(ctx->d_off.cap, ctx->d_off_old.cap);
@@ -767,16 +887,18 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     CU(cudaMemsetAsync(ctx->d_off.p, 0, sizeof(int64_t), s));
     CU(cudaMemsetAsync(ctx->d_orig_off.p, 0, sizeof(int64_t), s));
   }
+  CU(ctx->lay_cstart.reserve(8 * ((size_t)K + 1)));   // read by the current round's sums: resized only now
   k_layout_items_count<<<1, 1, 0, s>>>(ctx->lay_cnt.as<unsigned long long>(), K, per_item,
                                        ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), scal);
   CHK(launch_check(ctx, "k_layout_items_count"));
-  std::vector<unsigned long long> hcnt(K), hpts(K);
+  hcnt.assign(K, 0);
+  hpts.assign(K, 0);
   unsigned long long hsc[3] = {0, 0, 0};
   CU(cudaMemcpyAsync(hcnt.data(), ctx->lay_cnt.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(hpts.data(), ctx->lay_pts.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(hsc, scal, sizeof hsc, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  const int64_t n_items = (int64_t)hsc[2];
+  n_items = (int64_t)hsc[2];
   CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
   CU(ctx->d_item_cl.reserve(sizeof(int32_t) * (n_items > 0 ? n_items : 1)));
   k_layout_items_fill<<<K, 128, 0, s>>>(ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), K, per_item, N,
@@ -902,8 +1024,8 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
 
   // ---- Pi^(2),0 and Lambda = 0 (warm: new Pi2 built in P from the old Q, then swapped)
   if (warm) {
-    if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, true, ctx->P.as<double>());
-    else launch_init_plans<float>(ctx, true, ctx->P.as<float>());
+    if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, true, ctx->P.as<double>(), old_ld, old_pair);
+    else launch_init_plans<float>(ctx, true, ctx->P.as<float>(), old_ld, old_pair);
     if (n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
     std::swap(ctx->P.p, ctx->Q.p);
     std::swap(ctx->P.cap, ctx->Q.cap);
@@ -916,6 +1038,10 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     if (n_items > 0) CHK(launch_check(ctx, "k_init_plans"));
   }
 
+  return AD2_OK;
+  };
+
+  auto global = [&]() -> ad2_status {
   // ---- global member / point counts per cluster (EMPTY check, rho denominator, 1/N_c)
   std::vector<double> cnts(2 * (size_t)K);
   for (int c = 0; c < K; ++c) {
@@ -942,13 +1068,23 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   CHK(launch_check(ctx, "k_rho"));
   ctx->h_rho.assign(K, 0.0);
   CU(cudaMemcpyAsync(ctx->h_rho.data(), ctx->rho_d.p, sizeof(double) * K, cudaMemcpyDeviceToHost, s));
-  CHK(read_err(ctx));
+  CHK(agree(ctx, read_err(ctx)));              // weights off the simplex are detected per rank
   for (int c = 0; c < K; ++c)
     if (!(ctx->h_rho[c] > 0.0) || !std::isfinite(ctx->h_rho[c]))
       return ctx->fail(AD2_ERR_ZERO_RHO, "cluster %d: rho = %g", c, ctx->h_rho[c]);
   if (rho_out) memcpy(rho_out, ctx->h_rho.data(), sizeof(double) * K);
   ctx->state = 1;
   return AD2_OK;
+  };
+
+  ad2_status st = agree(ctx, validate());
+  if (st != AD2_OK) return st;
+  st = agree(ctx, commit());
+  if (st != AD2_OK) {
+    ctx->state = 0;
+    return st;
+  }
+  return global();
 }
 
 ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
@@ -1092,7 +1228,7 @@ ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
   CHK(cluster_dsum(ctx, s));
   std::vector<double> S(ctx->K);
   CU(cudaMemcpyAsync(S.data(), ctx->Sd.p, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, s));
-  CHK(read_err(ctx));
+  CHK(agree(ctx, read_err(ctx)));               // a non-finite value on one rank fails every rank
   for (int c = 0; c < ctx->K; ++c) obj_out[c] = S[c] / ctx->h_nmem[c];
   return AD2_OK;
 }
@@ -1429,8 +1565,8 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
     if (obj_out) CHK(ad2_objective(ctx, obj_out + (size_t)r * K));
     CHK(ad2_get_centroids(ctx, ctx->cl_x.p, ctx->cl_w.p, AD2_DEVICE));
     // assignment against the new centroids (identical on every rank)
-    CHK(assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE, nullptr,
-                    prm->cost_mode == AD2_COST_TABLE));
+    CHK(agree(ctx, assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE,
+                               nullptr, prm->cost_mode == AD2_COST_TABLE)));
     CU(cudaMemsetAsync(ctx->cl_cnt.p, 0, sizeof(unsigned long long) * ((size_t)K + 1), s));
     if (N > 0) {
       k_label_diff<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ctx->cl_lab.as<int32_t>(), ctx->cl_lab2.as<int32_t>(),
@@ -1438,10 +1574,7 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
                                                               ctx->cl_cnt.as<unsigned long long>());
       CHK(launch_check(ctx, "k_label_diff"));
     }
-    if (ctx->comm) {
-      ncclResult_t rr = g_nccl.AllReduce(ctx->cl_cnt.p, ctx->cl_cnt.p, (size_t)K + 1, ncclUint64, ncclSum, ctx->comm, s);
-      if (rr != ncclSuccess) return ctx->fail(AD2_ERR_NCCL, "ncclAllReduce (label counts)");
-    }
+    CHK(allreduce(ctx, ctx->cl_cnt.p, (size_t)K + 1, ncclUint64, s));
     CU(cudaMemcpyAsync(hc.data(), ctx->cl_cnt.p, sizeof(unsigned long long) * ((size_t)K + 1),
                        cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -1541,5 +1674,5 @@ ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch* b, const int64_t* pick, 
 ad2_status ad2_sync(ad2_ctx ctx) {
   if (!ctx) return AD2_ERR_ARG;
   CHK(set_dev(ctx));
-  return read_err(ctx);
+  return agree(ctx, read_err(ctx));
 }

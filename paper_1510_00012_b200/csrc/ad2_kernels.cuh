@@ -438,13 +438,16 @@ __host__ __device__ __forceinline__ int64_t blk_idx(int i, int j, int mk, int ld
 }
 
 // Pi^(2),0 = w_i w_j^(k) or, for warm members, the cached block;
-// Lambda = 0.  Writes the new Pi2 into `dst` (a buffer distinct from the warm source).
+// Lambda = 0.  Writes the new Pi2 into `dst` (a buffer distinct from the warm source).  The warm
+// source keeps the previous round's block layout (ld_src rows, pair layout or not), which differs
+// from this round's when the kernel variant changed (e.g. the largest m_k crossed 32).
 template <typename T>
 __global__ void __launch_bounds__(128)
 k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
              const int32_t* __restrict__ item_cl, const int64_t* __restrict__ warm_src,
              const T* __restrict__ om, const T* __restrict__ w, const T* __restrict__ Qold,
-             T* __restrict__ dst, T* __restrict__ L, int m, int ld, bool pair) {
+             T* __restrict__ dst, T* __restrict__ L, int m, int ld, bool pair, int ld_src, bool pair_src) {
+  const bool same = ld_src == ld && pair_src == pair;
   // warp per member, lane = row i (rows in chunks of 32), one column per step: coalesced rows
   const int item = blockIdx.x;
   const int c = item_cl[item];
@@ -464,8 +467,11 @@ k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
           const int64_t e = (int64_t)j * ld + 2 * i;
           typedef typename std::conditional<sizeof(T) == 4, float2, double2>::type T2;
           T2 v;
-          if (src >= 0) {
+          if (src >= 0 && same) {
             v = *reinterpret_cast<const T2*>(Qold + src + e);
+          } else if (src >= 0) {
+            v.x = i < m ? Qold[src + blk_idx(i, j, mk, ld_src, pair_src)] : T(0);
+            v.y = i < m ? Qold[src + blk_idx(i, j + 1, mk, ld_src, pair_src)] : T(0);
           } else {
             v.x = wi * om[o0 + j];
             v.y = wi * om[o0 + j + 1];
@@ -478,7 +484,9 @@ k_init_plans(const int64_t* __restrict__ off, const int64_t* __restrict__ item_m
         }
       for (; j < mk; ++j) {
         const int64_t e = blk_idx(i, j, mk, ld, pair);
-        dst[base + e] = (src >= 0) ? Qold[src + e] : wi * om[o0 + j];
+        T q = wi * om[o0 + j];
+        if (src >= 0) q = same ? Qold[src + e] : (i < m ? Qold[src + blk_idx(i, j, mk, ld_src, pair_src)] : T(0));
+        dst[base + e] = q;
         L[base + e] = T(0);
       }
     }

@@ -191,3 +191,24 @@ def test_next_row_api_errors():
     # the context still works after the errors
     lab, w2, _ = ctx.assign(b.offsets, b.supports, b.weights, b.x0, b.w0, mem="host")
     assert (lab >= 0).all() and (lab < b.K).all() and np.isfinite(w2).all()
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_assign_full_size_sampled_members(cfg):
+    """The assignment at BASELINE.json's full size (config 3: N = 200k, K = 64; config 5: N = 4M,
+    K = 256), where the pruning bounds meet many near-equal candidates; the oracle recomputes 300
+    random members against every centroid (same x, w on both sides)."""
+    from paper_1510_00012_b200 import ad2
+    torch = torch_cuda()
+    b = wl.make_config(cfg)
+    ctx = ad2.Context(0)
+    a = to_dev(b, torch)
+    lab, w2, n_exact = ctx.assign(a["offsets"], a["supports"], a["weights"], a["x0"], a["w0"], dtype=b.dtype)
+    ctx.close()
+    sample = np.sort(np.random.default_rng(cfg).choice(b.N, 300, replace=False))
+    sub = b.subset(sample)
+    olab, obest, osecond = oracle.assign(b.x0, b.w0, sub.offsets, sub.supports, sub.weights)
+    sure = (osecond - obest) > 1e-6
+    assert sure.mean() > 0.8
+    assert (lab[sample][sure] == olab[sure]).all()
+    np.testing.assert_allclose(w2[sample], obest, rtol=1e-9, atol=1e-12 * float(np.abs(obest).max()))
