@@ -89,12 +89,9 @@ static void dbuf_swap(DBuf& a, DBuf& b) {
 // between a device->host and a host->device copy of the buffer; lives as long as the context
 struct HostSum {
   ad2_group g = nullptr;
-  void* host = nullptr;          // pinned staging copy of the device buffer
+  void* host = nullptr;          // the context's pinned staging buffer (collectives are stream-ordered)
   size_t count = 0;
   int dtype = 0;
-  ~HostSum() {
-    if (host) cudaFreeHost(host);
-  }
 };
 static void CUDART_CB host_sum_fn(void* p) {
   HostSum* h = static_cast<HostSum*>(p);
@@ -120,6 +117,8 @@ struct ad2_ctx_s {
   ncclComm_t comm = nullptr;
   ad2_group grp = nullptr;           // host process group (borrowed; ad2_attach_group)
   std::map<std::pair<void*, size_t>, HostSum*> host_sums;
+  void* hg_stage = nullptr;          // pinned host staging of the group collectives
+  size_t hg_cap = 0;
   DBuf agree_d;
   int nranks = 1, rank = 0;
 
@@ -175,6 +174,7 @@ struct ad2_ctx_s {
   ~ad2_ctx_s() {
     clear_graphs();
     for (auto& kv : host_sums) delete kv.second;
+    if (hg_stage) cudaFreeHost(hg_stage);
     if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
     if (cap) cudaStreamDestroy(cap);
     if (pfs) {
@@ -224,18 +224,35 @@ static ad2_status launch_check(ad2_ctx ctx, const char* what) {
 // several ranks share the per-cluster sums (NCCL communicator or host process group)
 static bool multi(ad2_ctx ctx) { return ctx->comm != nullptr || ctx->grp != nullptr; }
 
+// the pinned staging of the group collectives, grown outside graph capture only (init)
+static ad2_status host_stage_reserve(ad2_ctx ctx, size_t bytes) {
+  if (!ctx->grp || bytes <= ctx->hg_cap) return AD2_OK;
+  CU(cudaStreamSynchronize(ctx->stream));          // no queued collective still uses the old buffer
+  if (ctx->hg_stage) cudaFreeHost(ctx->hg_stage);
+  ctx->hg_stage = nullptr;
+  ctx->hg_cap = 0;
+  CU(cudaMallocHost(&ctx->hg_stage, bytes));
+  ctx->hg_cap = bytes;
+  for (auto& kv : ctx->host_sums) kv.second->host = ctx->hg_stage;
+  return AD2_OK;
+}
+
 static ad2_status host_allreduce(ad2_ctx ctx, void* buf, size_t count, ncclDataType_t dt, cudaStream_t s) {
   const int gt = dt == ncclFloat32 ? AD2_GROUP_F32 : dt == ncclFloat64 ? AD2_GROUP_F64 : AD2_GROUP_U64;
   const size_t bytes = count * ad2_group_type_size(gt);
+  if (bytes > ctx->hg_cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return ctx->fail(AD2_ERR_STATE, "host group: %zu-byte collective above the staging reserved at init", bytes);
+    CHK(host_stage_reserve(ctx, bytes));
+  }
   HostSum*& h = ctx->host_sums[std::make_pair(buf, bytes)];
   if (!h) {
     h = new HostSum();
     h->g = ctx->grp;
-    if (cudaMallocHost(&h->host, bytes ? bytes : 8) != cudaSuccess) {
-      h->host = nullptr;
-      return ctx->fail(AD2_ERR_OOM, "host group: pinned staging of %zu bytes", bytes);
-    }
   }
+  h->host = ctx->hg_stage;
   h->count = count;
   h->dtype = gt;
   CU(cudaMemcpyAsync(h->host, buf, bytes, cudaMemcpyDeviceToHost, s));
@@ -949,6 +966,8 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   CU(ctx->Sd.reserve(8 * (size_t)K));
   CU(ctx->npts.reserve(8 * (size_t)K * 2));
   if (variant == 0) CU(ctx->scr.reserve(es * (size_t)n_items * 2 * m));
+  // the largest collective of the round: x partials K m (d + 1), counts 2K / K + 1, status words
+  CHK(host_stage_reserve(ctx, std::max<size_t>(es * (size_t)K * m * (d + 1), 16 * ((size_t)K + 8))));
 
   // ---- commit the new round shape
   ctx->dtype = b->dtype;
