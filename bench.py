@@ -155,6 +155,7 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     entries_total = b.entries()
     stream = torch.cuda.current_stream(dev)
     ctx = ad2.Context(local_rank, stream.cuda_stream)
+    ctx.set_state_mode(args.state_mode)
     if dist_on:
         bootstrap_nccl(ctx)
 
@@ -223,6 +224,11 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     # Lambda (16 B fp32, 32 B fp64), plus the read of a cached C (variants 3 / 0 keep C in HBM)
     es = 8 if b.dtype == "f64" else 4
     bytes_per_entry = 4 * es + (es if info["variant"] in (0, 3) else 0)
+    gz = args.state_mode == 1 and info["variant"] == 2 and tau >= 3
+    if gz:
+        # compressed state: the middle passes (GMID) read the anchor G and read + write U (3 x es per
+        # entry) and read + write the per-member log-factors (m per member, one per point)
+        bytes_per_entry = 3 * es + 2 * es * (mine.N * b.m + mine.n) / max(1, entries_local)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -233,8 +239,9 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        if prof.get("workload") == b.name and prof.get("kernel_variant") == "fused":
-            traffic = prof.get("dram_bytes_per_launch")
+        for rec in (prof if isinstance(prof, list) else [prof]):
+            if rec.get("workload") == b.name and rec.get("kernel_variant") == ("gmid" if gz else "fused"):
+                traffic = rec.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
     # the profiled graph is one step(tau); a round runs T/tau of them
@@ -291,11 +298,12 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
                    "parallelism": f"dp{world} (members sharded, NCCL all-reduce of per-cluster partials)",
                    "l2": "inputs larger than L2 (state %.1f GB)" % (info["state_bytes"] / 1e9),
                    "cost_build": ["fp32", "tcgen05-bf16"][args.cost_mode],
+                   "state": ["exact (Pi1, Lambda)", "epoch-anchored compressed (G, U, log-factors)"][args.state_mode],
                    "kernel_variant": {3: "wide", 2: "tma", 1: "warp", 0: "generic"}[info["variant"]]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": {3: "k_badmm_wide", 2: "k_badmm_tma", 1: "k_badmm_warp", 0: "k_badmm_generic"}[info["variant"]]
-                     + "<FUSED> (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
+                     + ("<GMID>" if gz else "<FUSED>") + " (one B-ADMM iteration: phase 2 of t-1 + phase 1 of t)",
                      "bytes_per_entry": bytes_per_entry, "entries_per_launch": entries_local,
                      "avg_launch_ms": avg_fused_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "iteration_kernels_share_of_step": iter_share},
@@ -409,6 +417,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cost-mode", type=int, default=0, help="0: fp32 cost build, 1: bf16 tcgen05 (cached-cost kernels)")
+    ap.add_argument("--state-mode", type=int, default=0,
+                    help="0: exact Pi1/Lambda state, 1: epoch-anchored compressed state (ad2_set_state_mode)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU path (torch.distributed + NCCL communicator in libad2) even with 1 rank")
     args = ap.parse_args()

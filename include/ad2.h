@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define AD2_ABI_VERSION 1
+#define AD2_ABI_VERSION 2
 
 typedef struct ad2_ctx_s *ad2_ctx;
 
@@ -124,6 +124,9 @@ typedef struct {
     int32_t nranks, rank;
     int64_t launches;           /* kernels launched by this context so far (graph nodes counted) */
     int64_t state_bytes;        /* device bytes owned by the context */
+    int32_t state_mode;         /* ad2_set_state_mode */
+    int32_t eps_floor_columns;  /* 1: a compressed-state pass met a column whose mass is the eps floor's
+                                   (the eps-free recursion does not hold there; use state mode 0) */
 } ad2_info;
 
 /* Create a context on CUDA device `cuda_device`; `cuda_stream` is a cudaStream_t (NULL = legacy
@@ -162,6 +165,21 @@ ad2_status ad2_group_open(ad2_group *out, const char *name, int nranks, int rank
 ad2_status ad2_group_allreduce(ad2_group g, void *host_buf, int64_t count, int32_t dtype);
 ad2_status ad2_attach_group(ad2_ctx ctx, ad2_group g);
 void ad2_group_close(ad2_group g);
+
+/* State representation of the iteration kernel (variant 2, steps of >= 3 iterations):
+ *   0 (default): Pi1 and Lambda stream through HBM every iteration (16 B per plan entry in fp32),
+ *     Alg. 4 exactly as written.
+ *   1: epoch-anchored compressed state.  With the eps of
+ *     Eq.badmmc0b / Eq.badmmc1b dropped from the Pi2 recursion, Lambda cancels between them and
+ *     Pi2^t = G exp(-s C / rho) a_i b_j from an anchor G = Pi2^{t0} (pin P4).  Inside a step the
+ *     passes stream G (read-only), U = Lambda + rho Pi1 and per-member log-factors: 12 B per
+ *     entry instead of 16.  The first pass of a step forms G exactly (with eps) and the last pass
+ *     stores Pi1 and Lambda again, so everything outside a step (read-back, objective, warm
+ *     start) is unchanged.  Entries whose value is decided by eps differ (they keep decaying
+ *     below the floor instead of sitting on it); a column whose whole mass is the floor's raises
+ *     ad2_info.eps_floor_columns.
+ * Takes effect at the next ad2_badmm_step. */
+ad2_status ad2_set_state_mode(ad2_ctx ctx, int32_t mode);
 
 /* Start a round (a1-a3 of SURVEY.md §8(a)): copy/sort the batch by cluster, build C, compute
  * rho per cluster (fixed for the round, X2), Lambda = 0, Pi^(2) = product measure or, for

@@ -130,6 +130,9 @@ struct ad2_ctx_s {
   int64_t N = 0, n = 0, n_items = 0;
   int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;   // wcfg: rows per member block of variant 3
   int cost_mode = 0;                 // ad2_cost_mode
+  int state_mode = 0;                // ad2_set_state_mode: 1 = epoch-anchored compressed state (variant 2)
+  int cur_gs = 0;                    // compressed state: iterations since the anchor (launch argument)
+  DBuf gra, gcb;                     // compressed state: row [N][ld] and column [n] log-factors
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
   size_t es = 4;                     // element size
@@ -301,6 +304,9 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.d = ctx->table ? 0 : ctx->d;     // symbolic supports: no coordinates (support update skipped)
   a.rule = ctx->rule;
   a.eps = (T)ctx->eps;
+  a.ra = ctx->gra.as<T>();
+  a.cb = ctx->gcb.as<T>();
+  a.gs = ctx->cur_gs;
   return a;
 }
 
@@ -1129,9 +1135,19 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   static const bool no_fx = getenv("AD2_NO_FUSEDX") != nullptr;   // A/B knob (bench experiments)
   const bool fx = p2x && n >= 2 && !no_fx;
   const int npass = fx ? n : n + 1;
+  // compressed state (ad2_set_state_mode 1): the step's middle passes run from the epoch anchor
+  // (GIN at the first pass that has a phase 2, GMID after it, GXOUT last), steps of >= 3
+  const bool gz = ctx->state_mode == 1 && fx && n >= 3;
+  const int g0 = (fresh || !pending) ? 1 : 0;           // the GIN pass
   for (int t = 0; t < npass && st == AD2_OK; ++t) {
     int mode;
-    if (t == 0) mode = fresh ? P1INIT : (pending ? FUSED : P1ONLY);
+    ctx->cur_gs = 0;
+    if (t == 0) mode = fresh ? P1INIT : (pending ? (gz ? GIN : FUSED) : P1ONLY);
+    else if (gz && t == g0) mode = GIN;
+    else if (gz) {
+      mode = t == npass - 1 ? GXOUT : GMID;
+      ctx->cur_gs = t - g0;
+    }
     else if (t == npass - 1) mode = fx ? FUSEDX : (p2x ? P2X : P2ONLY);
     else mode = FUSED;
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
@@ -1170,7 +1186,11 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   CHK(set_dev(ctx));
   const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
   const bool fresh = ctx->fresh, pending = ctx->pending, p2x = ctx->variant == 2;
-  const int key = 8 * n_iters + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
+  const int key = 16 * n_iters + (ctx->state_mode ? 8 : 0) + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
+  if (ctx->state_mode == 1 && ctx->variant == 2) {     // log-factor buffers of the compressed state
+    CU(ctx->gra.reserve(ctx->es * (size_t)(ctx->N > 0 ? ctx->N : 1) * ctx->ld));
+    CU(ctx->gcb.reserve(ctx->es * (size_t)(ctx->n > 0 ? ctx->n : 1)));
+  }
   auto it = ctx->graphs.find(key);
   StepGraph* g = nullptr;
   if (it == ctx->graphs.end()) {
@@ -1346,9 +1366,24 @@ ad2_status ad2_get_info(ad2_ctx ctx, ad2_info* info) {
   info->nranks = ctx->nranks;
   info->rank = ctx->rank;
   info->launches = ctx->launches;
+  info->state_mode = ctx->state_mode;
+  info->eps_floor_columns = 0;
+  if (ctx->d_err.p && cudaSetDevice(ctx->device) == cudaSuccess) {
+    int h = 0;
+    if (cudaMemcpyAsync(&h, ctx->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess &&
+        cudaStreamSynchronize(ctx->stream) == cudaSuccess)
+      info->eps_floor_columns = (h & ERR_EPSCOL) ? 1 : 0;
+  }
   const DBuf* all[] = {&ctx->Y, &ctx->om, &ctx->P, &ctx->Q, &ctx->L, &ctx->Cc, &ctx->x, &ctx->w, &ctx->pw,
                        &ctx->px, &ctx->Sw, &ctx->Sx, &ctx->pd, &ctx->scr, &ctx->stage_Y, &ctx->stage_W, &ctx->tmp_out};
   for (auto p : all) info->state_bytes += (int64_t)p->cap;
+  return AD2_OK;
+}
+
+ad2_status ad2_set_state_mode(ad2_ctx ctx, int32_t mode) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (mode != 0 && mode != 1) return ctx->fail(AD2_ERR_ARG, "set_state_mode: mode %d", mode);
+  ctx->state_mode = mode;             // graphs are cached per mode (the step key)
   return AD2_OK;
 }
 

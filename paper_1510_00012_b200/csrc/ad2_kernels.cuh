@@ -23,8 +23,16 @@ namespace ad2k {
 // FUSED pass that recomputes the same phase 2 (variant-2 kernel)
 // FUSEDX: FUSED that also forms the support-update partials of the Pi2 its phase 1 implies
 // (x_i = mean over members of sum_j (pe_ij + eps) y_j / r_i, w_i cancels): the last pass of a step
-enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5 };
-enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2 };
+// Epoch-anchored compressed state, variant 2, steps of >= 3:
+// with the eps of Eq.badmmc0b/c1b dropped from the Pi2 recursion, Lambda cancels between them
+// and Pi2^t = G (.) exp(-s C / rho) (.) a_i b_j from an anchor G = Pi2^{t0}
+// (pin P4).  Between launches the state is G (read-only), U = Lambda + rho Pi1 (one array) and
+// per-member log-factors ra [N][ld], cb [n]:
+// GIN: FUSED that stores G = Pi2^{t-1} (exact, with eps) into Q and U, ra, cb instead of Pi1, Lambda
+// GMID: Pi2^{t-1} from (G, ra, cb), then phase 1; stores U, ra, cb (12 B/entry instead of 16)
+// GXOUT: GMID's phase 2 and phase 1 storing Pi1 and Lambda (the exact state again) + x partials
+enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5, GIN = 6, GMID = 7, GXOUT = 8 };
+enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2, ERR_EPSCOL = 16 };   // ERR_EPSCOL: a flag, not an error
 
 constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels
 constexpr int ITEM_PASSES = 8;    // member passes per warp per work item
@@ -44,9 +52,12 @@ template <> struct Num<float> {
   static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
   // kx * rho for kx = log2(e)/rho: the scale of a pre-scaled Lambda's dual step
   static __device__ __forceinline__ float kappa() { return 1.4426950408889634f; }
+  // logarithm in the base of ex (log2), per row / column only: the accurate library function
+  static __device__ __forceinline__ float lg(float a) { return log2f(a); }
 };
 template <> struct Num<double> {
   static __device__ __forceinline__ double ex(double a) { return exp(a); }
+  static __device__ __forceinline__ double lg(double a) { return log(a); }
   static __device__ __forceinline__ double ld(const double* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(double* p, double v) { __stcs(p, v); }
   static __device__ __forceinline__ double div(double a, double b) { return a / b; }
@@ -76,6 +87,9 @@ struct IterArgs {
   int dy;                  // row stride of Y (>= d, zero-padded)
   int xext;                // 1: the x partials come from k_xpart (d > 64), P2ONLY skips them
   T eps;
+  T* ra;                   // compressed state: [N][ld] row log-factors (GIN / GMID / GXOUT)
+  T* cb;                   // compressed state: [n] column log-factors
+  int gs;                  // compressed state: iterations since the anchor of this launch's phase 2
 };
 
 // 16-byte vectors of the element type (shared-memory tiles, staged rows)

@@ -73,7 +73,7 @@ struct TmaLayout {
   // in-bounds over-reads past a pass region: G == 1 reads at most 3 masked columns past m_k
   static constexpr int SLACK = ((G == 1 ? 4 * DY : MK * DY + MP * MK) + 63) / 64 * 64;
   static constexpr int TILE = (G == 1) ? 0 : MP * 32;               // G == 1: tile = the pass's P slot
-  static constexpr int FB = G * MK;
+  static constexpr int FB = 2 * G * MK;                            // column factors + log-factors
   static constexpr size_t WARP_BYTES =
       ((sizeof(T) * (size_t)(RING + SLACK + TILE + FB) + 16 + 127) / 128) * 128;
   static constexpr size_t CTA_BYTES = NWARP * WARP_BYTES;
@@ -101,7 +101,7 @@ template <> struct Pr<double> {
 };
 
 template <typename T, int MP, int NCH, int MODE, int DP>
-__global__ void __launch_bounds__(NWARP * 32, MODE == FUSEDX ? 2 : 3)
+__global__ void __launch_bounds__(NWARP * 32, (MODE == FUSEDX || MODE == GXOUT) ? 2 : 3)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
@@ -117,6 +117,7 @@ k_badmm_tma(const IterArgs<T> a) {
   T* const ring = wb;                                  // per-warp ring of pass regions [P|L|Y]
   T* const tile_sep = wb + RING + Lay::SLACK;          // G > 1: column-sum transpose tile [MP][32]
   T* const fbuf = tile_sep + Lay::TILE;                // per-column factors [G][MK]
+  T* const cbuf = fbuf + G * MK;                       // compressed state: column log-factors [G][MK]
   uint64_t* const bar = reinterpret_cast<uint64_t*>(
       reinterpret_cast<unsigned char*>(fbuf + Lay::FB) + ((16 - ((uintptr_t)(fbuf + Lay::FB) & 15)) & 15));
 
@@ -156,8 +157,11 @@ k_badmm_tma(const IterArgs<T> a) {
   }
   T accw = T(0), accm = T(0);
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);     // phase 2 only (+ x partials)
-  constexpr bool XP = (MODE == FUSEDX);                      // FUSED + x partials
-  constexpr int FM = XP ? FUSED : MODE;                      // the mode the sweeps follow
+  constexpr bool XP = (MODE == FUSEDX || MODE == GXOUT);     // FUSED + x partials
+  constexpr bool GI = (MODE == GIN);                          // compressed state: anchor launch
+  constexpr bool GC = (MODE == GMID || MODE == GXOUT);       // phase 2 from (G, U, ra, cb)
+  constexpr bool GW = (MODE == GIN || MODE == GMID);         // phase 1 stores (U, ra, cb)
+  constexpr int FM = (XP || GI || GC) ? FUSED : MODE;        // the mode the sweeps follow
   constexpr bool NOSTORE = (MODE == P2X);
   T accx[(PH2 || XP) ? DP : 1];
   T accy[XP ? DP : 1];                                        // FUSEDX: the member's sum (pe + eps) y
@@ -167,8 +171,10 @@ k_badmm_tma(const IterArgs<T> a) {
   for (int t = 0; t < (XP ? DP : 1); ++t) accy[t] = T(0);
   bool bad = false;
 
-  const T* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
-  T* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
+  const T* src_plan = (MODE == P1ONLY || GC) ? a.Q : a.P;     // GC: the anchor G lives in Q
+  T* dst_plan = (MODE == P2ONLY || GI) ? a.Q : a.P;
+  const T gsn = -(T)a.gs;                                       // GC: -(iterations since the anchor)
+  bool epshit = false;
   const int64_t step = (int64_t)NWARP * G;
 
   // ring (and its over-read slack) zeroed once: every value it ever holds is then finite
@@ -217,6 +223,19 @@ k_badmm_tma(const IterArgs<T> a) {
   int nnp = pass_pts(1, np0, np1);
   int cbase = 0;                                       // ring offset of the current pass
   if (lane == 0 && cnp > 0) issue(0, 0, cp0, cnp);
+  // GC: the member's log-factors (global loads) are fetched one pass ahead for G == 1, so their
+  // latency hides behind a pass instead of stalling the start of the next one
+  const T lgw = (GC && rowok && wi > T(0)) ? N::lg(wi) : T(0);
+  T pf_cb[NCH], pf_ra = T(0), pf_om[NCH];
+  if constexpr (G == 1) {                              // w^(k)_j of the first pass (then one ahead)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) pf_om[ch] = (ch * MP + i < cnp) ? __ldg(a.om + cp0 + ch * MP + i) : T(0);
+  }
+  if constexpr (GC && G == 1) {
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) pf_cb[ch] = (ch * MP + i < cnp) ? a.cb[cp0 + ch * MP + i] : T(0);
+    if (cnp > 0 && rowok) pf_ra = a.ra[(mb + warp) * MP + i];
+  }
 
   for (int t = 0; cnp > 0; ++t) {
     // place pass t+1 behind pass t (or at the ring start) while t computes
@@ -248,8 +267,41 @@ k_badmm_tma(const IterArgs<T> a) {
     const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
     const T mkeps = (T)mk * eps_r;
     T omv[NCH];                                        // w^(k)_j for the column this lane sums
+    if constexpr (G == 1) {                            // prefetched one pass ahead
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) omv[ch] = (ch * MP + i < mk) ? __ldg(a.om + o0 + ch * MP + i) : T(0);
+      for (int ch = 0; ch < NCH; ++ch) {
+        omv[ch] = pf_om[ch];
+        pf_om[ch] = (ch * MP + i < nnp) ? __ldg(a.om + np0 + ch * MP + i) : T(0);
+      }
+    } else {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) omv[ch] = (ch * MP + i < mk) ? __ldg(a.om + o0 + ch * MP + i) : T(0);
+    }
+    T cbv[NCH];                                        // compressed state: this lane's column log-factor
+    T rowexp = T(0);                                   // GC: log-factor of row i, incl. w^{t-1}_i
+    if constexpr (GC) {
+      T rav = T(0);
+      if constexpr (G == 1) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) cbv[ch] = pf_cb[ch];
+        rav = pf_ra;
+        const int64_t kn = k + step;                   // the next pass's member
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) pf_cb[ch] = (ch * MP + i < nnp) ? a.cb[np0 + ch * MP + i] : T(0);
+        pf_ra = (nnp > 0 && rowok) ? a.ra[kn * MP + i] : T(0);
+      } else {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) cbv[ch] = (ch * MP + i < mk) ? a.cb[o0 + ch * MP + i] : T(0);
+        if (has && rowok) rav = a.ra[k * MP + i];
+      }
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) cbuf[seg * MK + ch * MP + i] = cbv[ch];
+      if (has && rowok) rowexp = rav + lgw;
+      __syncwarp();                                    // cbuf complete before the sweeps read it
+    } else {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) cbv[ch] = T(0);
+    }
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     T* const st = ring + cbase;
     const int rel = (int)(o0 - cp0);
@@ -307,8 +359,8 @@ k_badmm_tma(const IterArgs<T> a) {
           p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
           l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
         }
-        if constexpr (PH1) {
-          q2[jp] = p2[jp];                                             // Pi2^(0)
+        if constexpr (PH1 || GC) {
+          q2[jp] = p2[jp];                                             // Pi2^(0) / unused (GC)
         } else {
           const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
           q2[jp] = PR::mul(p2[jp], e);
@@ -317,7 +369,7 @@ k_badmm_tma(const IterArgs<T> a) {
       }
     }
     T f = T(0);
-    if constexpr (!PH1) {
+    if constexpr (!PH1 && !GC) {
       const T r = (racc[0].x + racc[1].x) + (racc[0].y + racc[1].y) + mkeps;
       f = (has && rowok) ? N::div(wi, r) : T(0);                    // Eq.badmmc1: w_i / rowsum
     }
@@ -381,11 +433,19 @@ k_badmm_tma(const IterArgs<T> a) {
         for (int h = 0; h < 2; ++h) {
           const int jp = 2 * jb + h, j = 2 * jp;
           T2 q = q2[jp];
-          if constexpr (FM == FUSED) {
+          const T2 cst = PR::make(c2[2 * h].x + c2[2 * h].y, c2[2 * h + 1].x + c2[2 * h + 1].y);
+          if constexpr (GC) {
+            // Pi2^{t-1} = G exp(rowexp_i + cb_j - s C kx) (P4), Lambda^{t-1} = U - rho Pi2^{t-1}
+            const T2 cbj = *reinterpret_cast<const T2*>(&cbuf[seg * MK + j]);
+            const T2 ck = PR::mul(cst, PR::make(kx, kx));
+            const T2 ex = PR::fma(ck, PR::make(gsn, gsn), PR::add(PR::make(rowexp, rowexp), cbj));
+            q = PR::mul(p2[jp], PR::make(N::ex(ex.x), N::ex(ex.y)));
+            l2[jp] = PR::fma(nrho2, q, l2[jp]);
+          } else if constexpr (FM == FUSED) {
             q = PR::fma(q2[jp], f2, ef2);                                 // Pi2 (Eq.badmmc1)
             l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
+            if constexpr (GI) q2[jp] = q;                                  // the anchor G, stored below
           }
-          const T2 cst = PR::make(c2[2 * h].x + c2[2 * h].y, c2[2 * h + 1].x + c2[2 * h + 1].y);
           const T2 ar = PR::fma(cst, nkx2, PR::make(-l2[jp].x, -l2[jp].y));   // -(C kx + L')
           const T2 e = PR::make(N::ex(ar.x), N::ex(ar.y));
           p2[jp] = PR::fma(q, e, eps2);                                    // pt2 (column j >= m_k: finite)
@@ -423,7 +483,17 @@ k_badmm_tma(const IterArgs<T> a) {
             for (int cc = 0; cc < w; ++cc) sp[cc] = PR::add(sp[cc], sp[cc + w]);
           s = sp[0].x + sp[0].y;
         }
-        fbuf[seg * MK + jc] = (jc < mk) ? N::div(omv[ch], s) : T(0);   // Eq.badmmc0: w_j^(k) / colsum
+        const T fcol = (jc < mk) ? N::div(omv[ch], s) : T(0);           // Eq.badmmc0: w_j^(k) / colsum
+        fbuf[seg * MK + jc] = fcol;
+        if constexpr (GW) {
+          if (jc < mk) a.cb[o0 + jc] = cbv[ch] + N::lg(fcol);             // b_j *= w_j / colsum_j
+        }
+        if constexpr (GC) {
+          // the column's mass is the eps floor's, so the eps-free recursion is off by up to the
+          // column's weight w_j^(k): flagged when that weight is not negligible (>= 1e-7 of the
+          // member's mass; Dirichlet weights far below it are common and move nothing)
+          if (jc < mk && s <= T(2) * (T)m * a.eps && omv[ch] >= T(1e-7)) epshit = true;
+        }
       }
       __syncwarp();
       // ---- Pi1 = pt2 * factor_j; pt1 = Pi1 exp(Lambda/rho) + eps (Eq.badmmc1b) row masses
@@ -460,16 +530,19 @@ k_badmm_tma(const IterArgs<T> a) {
           } else {
             racc2[h] = PR::fma(p2[jp], e, racc2[h]);
           }
+          // P slot: Pi1, or the anchor G (GIN), or nothing (GMID); L slot: Lambda, or U = Lambda + rho Pi1
+          const T2 pv = GI ? q2[jp] : p2[jp];
+          const T2 lv = GW ? PR::fma(rho2, p2[jp], l2[jp]) : l2[jp];
           if constexpr (PAD) {
-            *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = p2[jp];
-            if (FM == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = l2[jp];
+            if (MODE != GMID) *reinterpret_cast<T2*>(Ps + j * MP + 2 * i) = pv;
+            if (FM == FUSED || INIT) *reinterpret_cast<T2*>(Ls + j * MP + 2 * i) = lv;
           } else {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int jj = j + u;
               if (jj < mk) {                 // packed blocks (G > 1): no tail writes
-                Ps[jj * MP + i] = u ? p2[jp].y : p2[jp].x;
-                if (FM == FUSED || INIT) Ls[jj * MP + i] = u ? l2[jp].y : l2[jp].x;
+                if (MODE != GMID) Ps[jj * MP + i] = u ? pv.y : pv.x;
+                if (FM == FUSED || INIT) Ls[jj * MP + i] = u ? lv.y : lv.x;
               }
             }
           }
@@ -487,6 +560,9 @@ k_badmm_tma(const IterArgs<T> a) {
           accy[t] = T(0);
         }
         if (has && rowok) accm += T(1);
+      }
+      if constexpr (GW) {                  // a_i *= w_i / r_i: w^t_i is added by the next launch
+        if (has && rowok) a.ra[k * MP + i] = rowexp - N::lg(r2);
       }
       T R = r2;
 #pragma unroll
@@ -513,7 +589,7 @@ k_badmm_tma(const IterArgs<T> a) {
     if (lane == 0) {
       const uint32_t bp = (uint32_t)(MP * cnp * (int)sizeof(T));
       if constexpr (!NOSTORE) {
-        tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
+        if (MODE != GMID) tma_store(dst_plan + (int64_t)MP * cp0, st, bp);
         if (MODE != P1ONLY) tma_store(a.L + (int64_t)MP * cp0, st + MP * cns, bp);
         bulk_commit();
       }
@@ -533,6 +609,7 @@ k_badmm_tma(const IterArgs<T> a) {
   }
   if (lane == 0) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);
+  if (__any_sync(0xffffffffu, epshit) && lane == 0) atomicOr(a.err, ERR_EPSCOL);
 
   // this warp's partial sums of the item (segments added in a fixed butterfly order); the
   // consensus kernels add the NWARP warp partials of every item in order: no CTA barrier here

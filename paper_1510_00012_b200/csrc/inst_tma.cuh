@@ -23,6 +23,7 @@ struct TmaLaunch {
     static PerDevice once;                 // the smem attribute is per device
     if (once.first()) {
       attr<P1ONLY>(); attr<FUSED>(); attr<P2ONLY>(); attr<P1INIT>(); attr<P2X>(); attr<FUSEDX>();
+      attr<GIN>(); attr<GMID>(); attr<GXOUT>();
       once.done();
     }
     switch (mode) {
@@ -31,6 +32,9 @@ struct TmaLaunch {
       case P1INIT: go<P1INIT>(a, n_items, s); break;
       case P2X: go<P2X>(a, n_items, s); break;
       case FUSEDX: go<FUSEDX>(a, n_items, s); break;
+      case GIN: go<GIN>(a, n_items, s); break;
+      case GMID: go<GMID>(a, n_items, s); break;
+      case GXOUT: go<GXOUT>(a, n_items, s); break;
       default: go<P2ONLY>(a, n_items, s); break;
     }
   }

@@ -14,11 +14,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=3)
 ap.add_argument("--N", type=int, default=None)
 ap.add_argument("--rounds", type=int, default=1)
+ap.add_argument("--state-mode", type=int, default=0)
 args = ap.parse_args()
 b = wl.make_config(args.cfg, N=args.N)
 dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 D = [dev(a) for a in (b.offsets, b.supports, b.weights, b.labels, b.x0, b.w0)]
 ctx = ad2.Context(0, torch.cuda.current_stream().cuda_stream)
+ctx.set_state_mode(args.state_mode)
 s = b.sched
 for r in range(args.rounds):
     ctx.init(*D, b.K, b.m, s.rho0, s.eps, s.rule, dtype=b.dtype)

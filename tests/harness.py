@@ -21,7 +21,7 @@ def to_dev(b: wl.Bundle, torch):
 
 
 def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False, ctx=None, warm_mask=None,
-            x0=None, w0=None, profile=False, cost_mode=0):
+            x0=None, w0=None, profile=False, cost_mode=0, state_mode=0, eps=None):
     """Run one round of Alg. 4 on the GPU; returns (ctx, rho, objective)."""
     from paper_1510_00012_b200 import ad2
     torch = torch_cuda()
@@ -35,6 +35,7 @@ def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False,
             ctx.attach_nccl(1, 0, ad2.nccl_unique_id())
     if profile:
         ctx.set_profiling(True)
+    ctx.set_state_mode(state_mode)
     x0 = b.x0 if x0 is None else x0
     w0 = b.w0 if w0 is None else w0
     if mem == "device":
@@ -45,7 +46,7 @@ def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False,
         a = dict(offsets=b.offsets, supports=b.supports, weights=b.weights, labels=b.labels,
                  x0=np.ascontiguousarray(x0), w0=np.ascontiguousarray(w0))
     rho = ctx.init(a["offsets"], a["supports"], a["weights"], a["labels"], a["x0"], a["w0"], b.K, b.m,
-                   s.rho0, s.eps, rule, warm_mask=warm_mask, mem=mem, dtype=b.dtype, cost_mode=cost_mode)
+                   s.rho0, s.eps if eps is None else eps, rule, warm_mask=warm_mask, mem=mem, dtype=b.dtype, cost_mode=cost_mode)
     ad2.run_schedule(ctx, T, tau)
     obj = ctx.objective() if T > 0 else None
     torch.cuda.synchronize()
