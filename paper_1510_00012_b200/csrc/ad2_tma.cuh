@@ -101,7 +101,7 @@ template <> struct Pr<double> {
 };
 
 template <typename T, int MP, int NCH, int MODE, int DP>
-__global__ void __launch_bounds__(NWARP * 32, (MODE == FUSEDX || MODE == GXOUT) ? 2 : 3)
+__global__ void __launch_bounds__(NWARP * 32, 3)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
@@ -162,13 +162,16 @@ k_badmm_tma(const IterArgs<T> a) {
   constexpr bool GC = (MODE == GMID || MODE == GXOUT);       // phase 2 from (G, U, ra, cb)
   constexpr bool GW = (MODE == GIN || MODE == GMID);         // phase 1 stores (U, ra, cb)
   constexpr int FM = (XP || GI || GC) ? FUSED : MODE;        // the mode the sweeps follow
+  // FUSEDX recomputes pe = Pi1 exp(Lambda/rho) in the second sweep instead of keeping it from the
+  // first (one more exp per entry, 32 fewer registers: 3 CTAs per SM instead of 2, same values)
+  constexpr bool RECOMP = (MODE == FUSEDX);
   constexpr bool NOSTORE = (MODE == P2X);
   T accx[(PH2 || XP) ? DP : 1];
-  T accy[XP ? DP : 1];                                        // FUSEDX: the member's sum (pe + eps) y
+  T2 accy[XP ? DP / 2 : 1];                                  // FUSEDX: the member's sum (pe + eps) y
 #pragma unroll
   for (int t = 0; t < ((PH2 || XP) ? DP : 1); ++t) accx[t] = T(0);
 #pragma unroll
-  for (int t = 0; t < (XP ? DP : 1); ++t) accy[t] = T(0);
+  for (int t = 0; t < (XP ? DP / 2 : 1); ++t) accy[t] = PR::make(T(0), T(0));
   bool bad = false;
 
   const T* src_plan = (MODE == P1ONLY || GC) ? a.Q : a.P;     // GC: the anchor G lives in Q
@@ -361,6 +364,9 @@ k_badmm_tma(const IterArgs<T> a) {
         }
         if constexpr (PH1 || GC) {
           q2[jp] = p2[jp];                                             // Pi2^(0) / unused (GC)
+        } else if constexpr (RECOMP) {
+          const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
+          racc[h] = PR::add(racc[h], PR::mul(p2[jp], e));
         } else {
           const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
           q2[jp] = PR::mul(p2[jp], e);
@@ -442,7 +448,8 @@ k_badmm_tma(const IterArgs<T> a) {
             q = PR::mul(p2[jp], PR::make(N::ex(ex.x), N::ex(ex.y)));
             l2[jp] = PR::fma(nrho2, q, l2[jp]);
           } else if constexpr (FM == FUSED) {
-            q = PR::fma(q2[jp], f2, ef2);                                 // Pi2 (Eq.badmmc1)
+            if constexpr (RECOMP) q = PR::mul(p2[jp], PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y)));
+            q = PR::fma(RECOMP ? q : q2[jp], f2, ef2);                    // Pi2 (Eq.badmmc1)
             l2[jp] = PR::fma(nrho2, q, PR::fma(rho2, p2[jp], l2[jp]));     // Eq.badmm2
             if constexpr (GI) q2[jp] = q;                                  // the anchor G, stored below
           }
@@ -516,15 +523,14 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int jj = j + u;
-              if (jj < mk) {
-                const T qv = (u ? pe.y : pe.x) + eps_r;
+              const T qv = (jj < mk) ? (u ? pe.y : pe.x) + eps_r : T(0);   // masked column: adds exactly 0
+              const T2 qv2 = PR::make(qv, qv);
 #pragma unroll
-                for (int tt = 0; tt < DP / E; ++tt) {
-                  const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
-                  const T* ve = reinterpret_cast<const T*>(&v);
+              for (int tt = 0; tt < DP / E; ++tt) {
+                const V v = *reinterpret_cast<const V*>(Ys + jj * DY + tt * E);
+                const T2* ve = reinterpret_cast<const T2*>(&v);
 #pragma unroll
-                  for (int u2 = 0; u2 < E; ++u2) accy[tt * E + u2] += qv * ve[u2];
-                }
+                for (int u2 = 0; u2 < E / 2; ++u2) accy[tt * (E / 2) + u2] = PR::fma(qv2, ve[u2], accy[tt * (E / 2) + u2]);
               }
             }
           } else {
@@ -555,9 +561,10 @@ k_badmm_tma(const IterArgs<T> a) {
         // sweep above) and a count of 1 per row (w_i cancels in Eq.updatex, X5)
         const T ir = (has && rowok) ? N::div(T(1), r2) : T(0);
 #pragma unroll
-        for (int t = 0; t < DP; ++t) {
-          accx[t] += accy[t] * ir;
-          accy[t] = T(0);
+        for (int t = 0; t < DP / 2; ++t) {
+          accx[2 * t] += accy[t].x * ir;
+          accx[2 * t + 1] += accy[t].y * ir;
+          accy[t] = PR::make(T(0), T(0));
         }
         if (has && rowok) accm += T(1);
       }
