@@ -132,6 +132,7 @@ struct ad2_ctx_s {
   int cost_mode = 0;                 // ad2_cost_mode
   int state_mode = 0;                // ad2_set_state_mode: 1 = epoch-anchored compressed state (variant 2)
   int cur_gs = 0;                    // compressed state: iterations since the anchor (launch argument)
+  bool cur_pdl = false;              // the next iteration / consensus launch is a programmatic dependent
   DBuf gra, gcb;                     // compressed state: row [N][ld] and column [n] log-factors
   int ld = 0, dy = 0;                // member-block leading dimension (>= m), Y row stride (>= d)
   int parts = 1;                     // partial-sum rows per work item (variant 2: one per warp)
@@ -307,6 +308,7 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.ra = ctx->gra.as<T>();
   a.cb = ctx->gcb.as<T>();
   a.gs = ctx->cur_gs;
+  a.pdl = ctx->cur_pdl ? 1 : 0;
   return a;
 }
 
@@ -371,8 +373,21 @@ template <typename T>
 static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
   const bool fin = !multi(ctx);
   const size_t sh = sizeof(T) * (size_t)ctx->m;
-  k_wsum<T><<<ctx->K, 256, sh + 256 * sizeof(T), s>>>(ctx->pw.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->Sw.as<T>(),
-                                    ctx->w.as<T>(), ctx->rule, fin ? 1 : 0, ctx->d_err.as<int>());
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctx->K);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = sh + 256 * sizeof(T);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = ctx->cur_pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_wsum<T>, (const T*)ctx->pw.as<T>(), (const int64_t*)ctx->d_cl_item.as<int64_t>(),
+                       ctx->parts, ctx->m, ctx->Sw.as<T>(), ctx->w.as<T>(), ctx->rule, fin ? 1 : 0,
+                       ctx->d_err.as<int>());
+  }
   CHK(launch_check(ctx, "k_wsum"));
   if (!fin) {
     CHK(allreduce(ctx, ctx->Sw.p, (size_t)ctx->K * ctx->m, nccl_t(ctx), s));
@@ -1139,6 +1154,10 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   // (GIN at the first pass that has a phase 2, GMID after it, GXOUT last), steps of >= 3
   const bool gz = ctx->state_mode == 1 && fx && n >= 3;
   const int g0 = (fresh || !pending) ? 1 : 0;           // the GIN pass
+  // programmatic dependent launches inside the step (variant 2 iteration kernel <-> k_wsum): not
+  // across a collective (multi-rank) nor across the profiling event nodes
+  static const bool no_pdl = getenv("AD2_NO_PDL") != nullptr;   // A/B knob (bench experiments)
+  const bool pdl = ctx->variant == 2 && !multi(ctx) && !prof && !no_pdl;
   for (int t = 0; t < npass && st == AD2_OK; ++t) {
     int mode;
     ctx->cur_gs = 0;
@@ -1151,10 +1170,14 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
     else if (t == npass - 1) mode = fx ? FUSEDX : (p2x ? P2X : P2ONLY);
     else mode = FUSED;
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t], s, cudaEventRecordExternal);
+    ctx->cur_pdl = pdl && t > 0;
     st = launch_iter(ctx, mode, s);
     if (prof) cudaEventRecordWithFlags(g->ev[2 * t + 1], s, cudaEventRecordExternal);
+    ctx->cur_pdl = pdl;
     if (st == AD2_OK && (fx || t < n)) st = consensus(ctx, s);
+    ctx->cur_pdl = false;
   }
+  ctx->cur_pdl = false;
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &graph);
   if (st != AD2_OK) {

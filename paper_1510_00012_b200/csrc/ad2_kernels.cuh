@@ -35,6 +35,13 @@ enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5, GIN =
 enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2, ERR_EPSCOL = 16 };   // ERR_EPSCOL: a flag, not an error
 
 constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels
+
+// Programmatic dependent launch (the step graph of variant 2): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its predecessor drains;
+// pdl_wait() blocks until the predecessor has completed and its writes are visible (a no-op for a
+// normal launch), pdl_trigger() lets the successor's CTAs be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 constexpr int ITEM_PASSES = 8;    // member passes per warp per work item
 
 // exp(v) is evaluated as ex(v * kx): kx = log2(e)/rho with MUFU ex2.approx for fp32,
@@ -90,6 +97,7 @@ struct IterArgs {
   T* ra;                   // compressed state: [N][ld] row log-factors (GIN / GMID / GXOUT)
   T* cb;                   // compressed state: [n] column log-factors
   int gs;                  // compressed state: iterations since the anchor of this launch's phase 2
+  int pdl;                 // host: launch with programmatic stream serialization (the kernel pdl_wait()s)
 };
 
 // 16-byte vectors of the element type (shared-memory tiles, staged rows)
@@ -196,6 +204,8 @@ __global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_
   // then slice partials are added in slice order: deterministic for a fixed launch shape.
   const int c = blockIdx.x;
   const int64_t ib = cl_item[c] * parts, ie = cl_item[c + 1] * parts;   // `parts` partial rows per item
+  pdl_wait();                                          // the iteration kernel's partials
+  pdl_trigger();                                       // the next iteration kernel may start its set-up
   extern __shared__ unsigned char smraw[];
   T* red = reinterpret_cast<T*>(smraw);               // [blockDim]
   T* sh = red + blockDim.x;                            // [m]

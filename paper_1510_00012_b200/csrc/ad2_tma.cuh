@@ -136,6 +136,9 @@ k_badmm_tma(const IterArgs<T> a) {
   const T eps_r = rowok ? a.eps : T(0);
   constexpr bool PH1 = (MODE == P1ONLY || MODE == P1INIT);   // phase 1 only
   constexpr bool INIT = (MODE == P1INIT);
+  // launched as a programmatic dependent of the consensus kernel: everything above (geometry, x,
+  // rho) is fixed within a step; w and the plan state are the predecessors' results
+  pdl_wait();
   const T wi = (MODE != P1ONLY && rowok) ? a.w[(int64_t)c * m + i] : T(0);
   // Lambda is stored pre-scaled, L' = Lambda * kx (kx = log2(e)/rho for fp32, 1/rho for fp64), so
   // exp(Lambda/rho) = ex(L') and Eq.badmm2 becomes L' += kappa (Pi1 - Pi2) with kappa = kx * rho
@@ -614,6 +617,7 @@ k_badmm_tma(const IterArgs<T> a) {
     np0 = fp0;
     np1 = fp1;
   }
+  pdl_trigger();                                       // the consensus kernel may be scheduled
   if (lane == 0) bulk_wait_all();
   if (bad) atomicOr(a.err, ERR_NONFINITE);
   if (__any_sync(0xffffffffu, epshit) && lane == 0) atomicOr(a.err, ERR_EPSCOL);

@@ -17,7 +17,17 @@ struct TmaLaunch {
   }
   template <int MODE>
   static void go(const IterArgs<T>& a, int64_t n_items, cudaStream_t s) {
-    k_badmm_tma<T, MP, NCH, MODE, DP><<<(unsigned)n_items, NWARP * 32, Lay::CTA_BYTES, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)n_items);
+    cfg.blockDim = dim3(NWARP * 32);
+    cfg.dynamicSmemBytes = Lay::CTA_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_badmm_tma<T, MP, NCH, MODE, DP>, a);
   }
   static void run(int mode, const IterArgs<T>& a, int64_t n_items, cudaStream_t s) {
     static PerDevice once;                 // the smem attribute is per device
