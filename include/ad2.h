@@ -127,6 +127,8 @@ typedef struct {
     int32_t state_mode;         /* ad2_set_state_mode */
     int32_t eps_floor_columns;  /* 1: a compressed-state pass met a column whose mass is the eps floor's
                                    (the eps-free recursion does not hold there; use state mode 0) */
+    int64_t assign_certified;   /* last ad2_cluster: member-rounds whose label the bounds certified (no solve) */
+    int64_t assign_exact;       /* last ad2_cluster: exact transport solves (incl. the centroid drifts) */
 } ad2_info;
 
 /* Create a context on CUDA device `cuda_device`; `cuda_stream` is a cudaStream_t (NULL = legacy

@@ -54,7 +54,8 @@ class Info(C.Structure):
                 ("K", C.c_int32), ("n_members", C.c_int64), ("n_points", C.c_int64), ("entries", C.c_int64),
                 ("n_items", C.c_int64), ("variant", C.c_int32), ("mp", C.c_int32), ("nch", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("launches", C.c_int64),
-                ("state_bytes", C.c_int64), ("state_mode", C.c_int32), ("eps_floor_columns", C.c_int32)]
+                ("state_bytes", C.c_int64), ("state_mode", C.c_int32), ("eps_floor_columns", C.c_int32),
+                ("assign_certified", C.c_int64), ("assign_exact", C.c_int64)]
 
 
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",

@@ -164,6 +164,10 @@ struct ad2_ctx_s {
   size_t pf_ysz = 0, pf_wsz = 0;
   DBuf asg_cx, asg_x, asg_lab, asg_best, asg_scal, asg_tab;   // assignment step scratch
   DBuf cl_lab, cl_lab2, cl_x, cl_w, cl_warm, cl_cnt, cl_off, cl_Y, cl_W;   // outer loop (ad2_cluster)
+  // cross-round pruning of the loop's assignment: bounds u, l (W units) per member, certified mask,
+  // the centroids of the last assignment, their drift, and the centroid "batch" layout
+  DBuf el_u, el_lb, el_skip, el_xa, el_wa, el_drift, el_cnt, el_off, el_iota, el_lab;
+  int64_t asg_certified = 0, asg_exact = 0;
   // symbolic supports: cost table D [V][V] (dtype tab_dtype), sorted member ids, centroid ids
   DBuf tab, ysym, xsym;
   int tab_V = 0, tab_dtype = -1;
@@ -1390,6 +1394,8 @@ ad2_status ad2_get_info(ad2_ctx ctx, ad2_info* info) {
   info->rank = ctx->rank;
   info->launches = ctx->launches;
   info->state_mode = ctx->state_mode;
+  info->assign_certified = ctx->asg_certified;
+  info->assign_exact = ctx->asg_exact;
   info->eps_floor_columns = 0;
   if (ctx->d_err.p && cudaSetDevice(ctx->device) == cudaSuccess) {
     int h = 0;
@@ -1460,11 +1466,26 @@ size_t assign_warp_bytes(int m, int mkmax, int K, int d);
 int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
                   const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
                   const int32_t* xs, const void* D, int V, double* Dtab,
-                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s);
+                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s,
+                  const uint8_t* skip, const int32_t* lab_in, const int32_t* fixed, double* bu, float* blb,
+                  int prior);
 void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int* err, cudaStream_t s);
+void elkan_launch(const double* drift2, int K, const int32_t* lab, int64_t N, double* u, float* lb, uint8_t* skip,
+                  unsigned long long* n_skip, cudaStream_t s);
+
+// cross-round pruning of the outer loop's assignment (Elkan)
+struct AsgPrune {
+  const uint8_t* skip = nullptr;     // certified members (label kept)
+  const int32_t* lab_in = nullptr;   // their labels
+  const int32_t* fixed = nullptr;    // exact W^2 to this centroid only
+  double* u = nullptr;               // out: upper bound to the label of the searched members
+  float* lb = nullptr;               // in/out: [N][K] lower bounds (W units)
+  int prior = 0;                     // lb holds bounds carried from the last round
+};
 
 static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
-                              double* w2_out, ad2_mem where, int64_t* n_exact_out, bool symbolic) {
+                              double* w2_out, ad2_mem where, int64_t* n_exact_out, bool symbolic,
+                              const AsgPrune& pr = AsgPrune()) {
   if (!ctx) return AD2_ERR_ARG;
   if (symbolic && (b && (b->d != 1 || ctx->tab_V < 1 || ctx->tab_dtype != (int)b->dtype)))
     return ctx->fail(AD2_ERR_ARG, "symbolic assign needs d = 1 (int32 ids) and a cost table of the batch dtype");
@@ -1533,7 +1554,7 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
   if (assign_launch(b->dtype == AD2_F64, static_cast<const int64_t*>(off), N, Y, W, ctx->asg_cx.p, wdev, K, m, d,
                     (int)hs[0], xc, wc, xb, symbolic ? ctx->asg_cx.as<int32_t>() : nullptr, ctx->tab.p, ctx->tab_V,
                     ctx->asg_tab.as<double>(), ctx->asg_lab.as<int32_t>(), ctx->asg_best.as<double>(), scal + 1, err,
-                    optin, s) != 0)
+                    optin, s, pr.skip, pr.lab_in, pr.fixed, pr.u, pr.lb, pr.prior) != 0)
     return ctx->fail(AD2_ERR_ARG, "assign: workspace does not fit");
   CHK(launch_check(ctx, "k_assign"));
   const cudaMemcpyKind d2o = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -1628,6 +1649,31 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
   std::vector<unsigned long long> hc((size_t)K + 1);
   int rounds = 0;
   ad2_status ret = AD2_OK;
+  // cross-round pruning: not for symbolic supports (a cost table need not satisfy the
+  // triangle inequality that the bounds rely on)
+  const bool no_prune = getenv("AD2_NO_PRUNE") != nullptr;          // A/B knob (read per call)
+  const bool prune = prm->cost_mode != AD2_COST_TABLE && !no_prune;
+  ctx->asg_certified = ctx->asg_exact = 0;
+  if (prune) {
+    const size_t NN = (size_t)(N > 0 ? N : 1);
+    CU(ctx->el_u.reserve(8 * NN));
+    CU(ctx->el_lb.reserve(4 * NN * (size_t)K));       // Elkan: one lower bound per (member, centroid)
+    CU(ctx->el_skip.reserve(NN));
+    CU(ctx->el_xa.reserve(es * (size_t)K * m * d));
+    CU(ctx->el_wa.reserve(es * (size_t)K * m));
+    CU(ctx->el_drift.reserve(8 * (size_t)K));
+    CU(ctx->el_cnt.reserve(8));
+    CU(ctx->el_off.reserve(8 * ((size_t)K + 1)));
+    CU(ctx->el_iota.reserve(4 * (size_t)K));
+    CU(ctx->el_lab.reserve(4 * (size_t)K));
+    std::vector<int64_t> hoff((size_t)K + 1);
+    std::vector<int32_t> hio((size_t)K);
+    for (int c = 0; c <= K; ++c) hoff[c] = (int64_t)c * m;
+    for (int c = 0; c < K; ++c) hio[c] = c;
+    CU(cudaMemcpyAsync(ctx->el_off.p, hoff.data(), 8 * ((size_t)K + 1), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->el_iota.p, hio.data(), 4 * (size_t)K, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));             // host vectors go out of scope
+  }
   for (int r = 0; r < loop->max_rounds; ++r) {
     bd.labels = ctx->cl_lab.as<int32_t>();
     // round r: Alg. 4 from the current centroids (warm Pi^(2) for members whose label held)
@@ -1642,8 +1688,47 @@ ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, c
     if (obj_out) CHK(ad2_objective(ctx, obj_out + (size_t)r * K));
     CHK(ad2_get_centroids(ctx, ctx->cl_x.p, ctx->cl_w.p, AD2_DEVICE));
     // assignment against the new centroids (identical on every rank)
-    CHK(agree(ctx, assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE,
-                               nullptr, prm->cost_mode == AD2_COST_TABLE)));
+    if (!prune) {
+      int64_t nx = 0;
+      CHK(agree(ctx, assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE,
+                                 &nx, prm->cost_mode == AD2_COST_TABLE)));
+      ctx->asg_exact += nx;
+    } else {
+      AsgPrune pr;
+      pr.u = ctx->el_u.as<double>();
+      pr.lb = ctx->el_lb.as<float>();
+      pr.prior = r > 0 ? 1 : 0;
+      int64_t nx = 0;
+      if (r > 0) {
+        // drift of every centroid since the last assignment, W^2(Q_c^old, Q_c^new) exactly: the
+        // new centroids as a K-member batch, each solved against its own old centroid only
+        ad2_batch cb = bd;
+        cb.n_members = K;
+        cb.offsets = ctx->el_off.as<int64_t>();
+        cb.supports = ctx->cl_x.p;
+        cb.weights = ctx->cl_w.p;
+        AsgPrune fx;
+        fx.fixed = ctx->el_iota.as<int32_t>();
+        CHK(agree(ctx, assign_impl(ctx, &cb, ctx->el_xa.p, ctx->el_wa.p, ctx->el_lab.as<int32_t>(),
+                                   ctx->el_drift.as<double>(), AD2_DEVICE, &nx, false, fx)));
+        ctx->asg_exact += nx;
+        CU(cudaMemsetAsync(ctx->el_cnt.p, 0, 8, s));
+        elkan_launch(ctx->el_drift.as<double>(), K, ctx->cl_lab.as<int32_t>(), N, pr.u, pr.lb,
+                     ctx->el_skip.as<uint8_t>(), ctx->el_cnt.as<unsigned long long>(), s);
+        CHK(launch_check(ctx, "k_elkan"));
+        pr.skip = ctx->el_skip.as<uint8_t>();
+        pr.lab_in = ctx->cl_lab.as<int32_t>();
+        unsigned long long ns = 0;
+        CU(cudaMemcpyAsync(&ns, ctx->el_cnt.p, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        ctx->asg_certified += (int64_t)ns;
+      }
+      CHK(agree(ctx, assign_impl(ctx, &bd, ctx->cl_x.p, ctx->cl_w.p, ctx->cl_lab2.as<int32_t>(), nullptr, AD2_DEVICE,
+                                 &nx, false, pr)));
+      ctx->asg_exact += nx;
+      CU(cudaMemcpyAsync(ctx->el_xa.p, ctx->cl_x.p, es * (size_t)K * m * d, cudaMemcpyDeviceToDevice, s));
+      CU(cudaMemcpyAsync(ctx->el_wa.p, ctx->cl_w.p, es * (size_t)K * m, cudaMemcpyDeviceToDevice, s));
+    }
     CU(cudaMemsetAsync(ctx->cl_cnt.p, 0, sizeof(unsigned long long) * ((size_t)K + 1), s));
     if (N > 0) {
       k_label_diff<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(ctx->cl_lab.as<int32_t>(), ctx->cl_lab2.as<int32_t>(),

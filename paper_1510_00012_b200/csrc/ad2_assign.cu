@@ -791,12 +791,27 @@ __global__ void k_assign_mk(const int64_t* __restrict__ off, int64_t N, unsigned
 // Dtab != nullptr: symbolic supports — Y and xs hold int32 symbol ids, the cost is the
 // table entry D[xs_ci][y_j] (fp64 copy), and there is no vector-space mean bound (all bounds 0:
 // centroids are visited in index order, the relaxed-marginal bounds still prune).
+// Cross-round pruning (Elkan; AsgBounds) with W = sqrt(W^2), a metric: skip[k]
+// certifies member k's label (lab_in[k]) and the member is not visited; otherwise the search
+// starts from the carried lower bounds lb[k][c] <= W(P_k, Q_c) (prior != 0) and writes back
+// u[k] >= W(P_k, Q_label) and lb[k][c] for every centroid (W units, rounded down in fp32).
+// fixed != nullptr: only the exact W^2 to centroid fixed[k] (label = fixed[k]).
+struct AsgBounds {
+  const uint8_t* skip;
+  const int32_t* lab_in;
+  const int32_t* fixed;
+  double* u;
+  float* lb;
+  int prior;
+};
+
 template <typename T>
 __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __restrict__ Y,
                          const T* __restrict__ Wt, const double* __restrict__ xc, const double* __restrict__ wc,
                          const double* __restrict__ xb, const int32_t* __restrict__ xs, const double* __restrict__ Dtab,
                          int V, AsgLay L, int32_t* __restrict__ labels,
-                         double* __restrict__ best_out, unsigned long long* __restrict__ n_exact, int* err) {
+                         double* __restrict__ best_out, unsigned long long* __restrict__ n_exact, int* err,
+                         AsgBounds bnd) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ws = smem + (size_t)warp * L.bytes;
@@ -807,6 +822,10 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
     if (lane == 0) kq = atomicAdd(n_exact + 5, 1ull);
     const int64_t k = (int64_t)__shfl_sync(0xffffffffu, kq, 0);
     if (k >= N) break;
+    if (bnd.skip && bnd.skip[k]) {                    // certified: the label holds, nothing to solve
+      if (lane == 0) labels[k] = bnd.lab_in[k];
+      continue;
+    }
     const int m = L.m, K = L.K, d = L.d;
     double* C = reinterpret_cast<double*>(ws + L.oC);
     double* om = reinterpret_cast<double*>(ws + L.oom);
@@ -831,6 +850,26 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
         for (int j = 0; j < mk; ++j) a += om[j] * (double)Yk[(int64_t)j * d + t];
         yb[t] = a;
       }
+    if (bnd.fixed) {                                   // one exact W^2 (e.g. a centroid's drift)
+      const int cs = bnd.fixed[k];
+      const double* wn = wc + (int64_t)cs * m;
+      build_cost(L, ws, xc + (int64_t)cs * m * d, mk, lane, Dtab ? xs + (int64_t)cs * m : nullptr, Ysym, Dtab, V, err, Yk);
+      __syncwarp();
+      double dlb, dub;
+      dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
+      const int qn = ((m > mk ? m : mk) + 31) >> 5;
+      const double W = qn <= 1   ? ssp_reg<1>(L, ws, wn, mk, lane, err, n_exact + 3)
+                       : qn <= 2 ? ssp_reg<2>(L, ws, wn, mk, lane, err, n_exact + 3)
+                       : qn <= 4 ? ssp_reg<4>(L, ws, wn, mk, lane, err, n_exact + 3)
+                                 : ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
+      if (lane == 0) {
+        labels[k] = cs;
+        if (best_out) best_out[k] = W;
+        atomicAdd(n_exact, 1ull);
+      }
+      __syncwarp();
+      continue;
+    }
     for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
     __syncwarp();
     for (int c = lane; c < K; c += 32) {              // |mean_c - mean_k|^2 <= W^2
@@ -840,6 +879,10 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
           const double df = xb[(int64_t)c * d + t] - yb[t];
           a += df * df;
         }
+      if (bnd.lb && bnd.prior) {                      // the carried Elkan bound, W^2 units
+        const double e = fmax((double)bnd.lb[k * K + c], 0.0);
+        a = fmax(a, e * e * (1.0 - 1e-12));
+      }
       LB[c] = a;
     }
     __syncwarp();
@@ -891,12 +934,10 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
       }
       __syncwarp();
     }
-    // phase B: only phase-A centroids can win (the others have mean bound > ubest); exact solves
-    // in increasing sharpened-bound order until the bound exceeds the best exact W^2
-    for (int c = lane; c < K; c += 32) {
-      const bool vis = (solved[c >> 5] >> (c & 31)) & 1u;
-      if (!vis) LB[c] = CUDART_INF;
-    }
+    // phase B: only phase-A centroids can win (the others have mean bound > ubest >= the best
+    // exact W^2, so the loop below stops before reaching them; their mean bounds stay in LB as
+    // lower bounds for the pruning of the next round); exact solves in increasing sharpened-bound
+    // order until the bound exceeds the best exact W^2
     for (int q = lane; q < (K + 31) / 32; q += 32) solved[q] = 0u;
     __syncwarp();
     for (int visit = 0; visit < K; ++visit) {
@@ -940,6 +981,7 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
         l2 += wn[i] * mn;
       }
       const double lbr = fmax(wsum(l1), wsum(l2)) * shrink;
+      if (lane == 0) LB[cs] = fmax(LB[cs], lbr);
       if (lbr > best || (lbr == best && cs > bc)) continue;
       double dlb, dub;
       dual_bounds(L, ws, wn, mk, lane, CUDART_INF, dlb, dub, true);
@@ -949,11 +991,20 @@ __global__ void k_assign(const int64_t* __restrict__ off, int64_t N, const T* __
                        : qn <= 4 ? ssp_reg<4>(L, ws, wn, mk, lane, err, n_exact + 3)
                                  : ssp_w2(L, ws, wn, mk, lane, err, true, n_exact + 3);
       ++nsolve;
+      if (lane == 0) LB[cs] = W;                        // exact
       if (W < best || (W == best && cs < bc)) {
         best = W;
         bc = cs;
       }
       __syncwarp();
+    }
+    if (bnd.u) {
+      // Elkan bounds in W units with rounding margins: u >= W(P_k, Q_bc) (exact here); lb[k][c] <=
+      // W(P_k, Q_c): exact where solved, else the sharpened / mean / carried lower bound
+      __syncwarp();
+      for (int c = lane; c < K; c += 32)
+        bnd.lb[k * K + c] = __double2float_rd(sqrt(fmax(LB[c], 0.0)) * (1.0 - 1e-9));
+      if (lane == 0) bnd.u[k] = sqrt(fmax(best, 0.0)) * (1.0 + 1e-9) + 1e-300;
     }
     if (lane == 0) {
       labels[k] = bc;
@@ -986,7 +1037,10 @@ __global__ void k_to_f64(const T* __restrict__ a, double* __restrict__ b, int64_
 int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const void* Wt, const void* x,
                   const void* w, int K, int m, int d, int mkmax, double* xc, double* wc, double* xb,
                   const int32_t* xs, const void* D, int V, double* Dtab,
-                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s) {
+                  int32_t* labels, double* best, unsigned long long* n_exact, int* err, int optin, cudaStream_t s,
+                  const uint8_t* skip, const int32_t* lab_in, const int32_t* fixed, double* bu, float* blb,
+                  int prior) {
+  const AsgBounds bnd{skip, lab_in, fixed, bu, blb, prior};
   if (f64) k_assign_prep<double><<<K, 128, 0, s>>>(xs ? nullptr : (const double*)x, (const double*)w, K, m, d, xc, wc, xb);
   else k_assign_prep<float><<<K, 128, 0, s>>>(xs ? nullptr : (const float*)x, (const float*)w, K, m, d, xc, wc, xb);
   if (xs) {
@@ -1014,13 +1068,46 @@ int assign_launch(int f64, const int64_t* off, int64_t N, const void* Y, const v
   if (f64) {
     cudaFuncSetAttribute(k_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_assign<double><<<grid, 32 * wpc, sm, s>>>(off, N, (const double*)Y, (const double*)Wt, xc, wc, xb, xs,
-                                                xs ? Dtab : nullptr, V, L, labels, best, n_exact, err);
+                                                xs ? Dtab : nullptr, V, L, labels, best, n_exact, err, bnd);
   } else {
     cudaFuncSetAttribute(k_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_assign<float><<<grid, 32 * wpc, sm, s>>>(off, N, (const float*)Y, (const float*)Wt, xc, wc, xb, xs,
-                                               xs ? Dtab : nullptr, V, L, labels, best, n_exact, err);
+                                               xs ? Dtab : nullptr, V, L, labels, best, n_exact, err, bnd);
   }
   return 0;
+}
+
+// ---- cross-round pruning (Elkan) -------------------------------------------------
+// drift2[c] = W^2(Q_c^old, Q_c^new) (exact).  One warp per member: lb[k][c] -= delta_c (rounded
+// down), u[k] += delta_label; certified when every other centroid's lower bound exceeds u.
+__global__ void k_elkan_update(const int32_t* __restrict__ lab, int64_t N, int K, const double* __restrict__ drift2,
+                               double* __restrict__ u, float* __restrict__ lb, uint8_t* __restrict__ skip,
+                               unsigned long long* __restrict__ n_skip) {
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (k >= N) return;
+  const int lk = lab[k];
+  auto delta = [&](int c) { return sqrt(fmax(drift2[c], 0.0)) * (1.0 + 1e-9) + 1e-300; };
+  const double uu = (u[k] + delta(lk)) * (1.0 + 1e-15);
+  float mn = CUDART_INF_F;
+  for (int c = lane; c < K; c += 32) {
+    const float v = __double2float_rd((double)lb[k * K + c] - delta(c));
+    lb[k * K + c] = v;
+    if (c != lk) mn = fminf(mn, v);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) {
+    u[k] = uu;
+    const bool ok = (double)mn > uu;
+    skip[k] = ok ? 1 : 0;
+    if (ok) atomicAdd(n_skip, 1ull);
+  }
+}
+
+void elkan_launch(const double* drift2, int K, const int32_t* lab, int64_t N, double* u, float* lb, uint8_t* skip,
+                  unsigned long long* n_skip, cudaStream_t s) {
+  if (N > 0) k_elkan_update<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(lab, N, K, drift2, u, lb, skip, n_skip);
 }
 
 void assign_mkmax(const int64_t* off, int64_t N, unsigned long long* mkmax, int* err, cudaStream_t s) {

@@ -141,6 +141,70 @@ def test_cluster_loop_fp32_stops_on_stable_labels():
     np.testing.assert_array_equal(lab, res["labels"])
 
 
+def _separated_groups(N=2000, K=6, m=8, d=3, seed=5, dtype="f32"):
+    """K groups of distributions 60 units apart (members of a group scattered around its centre),
+    initial labels with a fifth of the members mislabelled, centroids from a correct member each:
+    the loop converges in a few rounds and later rounds move the centroids by << the gaps."""
+    rng = np.random.default_rng(seed)
+    truth = rng.integers(0, K, N).astype(np.int32)
+    sizes = rng.integers(3, 12, N)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    centres = rng.normal(0, 60, (K, d))
+    Y = np.repeat(centres[truth], sizes, axis=0) + rng.normal(0, 1.5, (off[-1], d))
+    W = np.concatenate([rng.dirichlet(np.ones(s)) for s in sizes])
+    lab0 = truth.copy()
+    flip = rng.choice(N, N // 5, replace=False)
+    lab0[flip] = rng.integers(0, K, len(flip))
+    x0 = np.stack([centres[c] + rng.normal(0, 1.5, (m, d)) for c in range(K)])
+    w0 = np.full((K, m), 1.0 / m)
+    nt = np.float64 if dtype == "f64" else np.float32
+    return wl.Bundle("separated", d, m, K, off, Y.astype(nt), W.astype(nt), lab0, x0.astype(nt), w0.astype(nt), dtype,
+                     wl.Schedule(T=20, tau=10))
+
+
+@pytest.mark.parametrize("case", ["cfg2", "cfg3", "cfg5", "separated"])
+def test_cluster_pruning_keeps_every_label(case, monkeypatch):
+    """Cross-round pruning of the loop's assignment (Elkan, with W = sqrt(W^2) a metric,
+    P:855-862): the labels, rounds, changed fractions and objectives of every round are those of
+    the unpruned loop, bit for bit, and the returned labels are the exact assignment against the
+    returned centroids.  On well-separated groups later rounds certify members without a solve;
+    on the BASELINE workloads the centroids' drift between rounds (W(Q_c^r, Q_c^r+1)) exceeds
+    the members' best / second-best gaps many times, so few or none are certified."""
+    from paper_1510_00012_b200 import ad2
+    torch = torch_cuda()
+    b = {"cfg2": lambda: wl.make_config(2, N=3000, K=10), "cfg3": lambda: wl.make_config(3, N=4000, K=16, dtype="f64"),
+         "cfg5": lambda: wl.make_config(5, N=6000, K=24), "separated": _separated_groups}[case]()
+    a = to_dev(b, torch)
+    out = {}
+    for prune in (False, True):
+        if prune:
+            monkeypatch.delenv("AD2_NO_PRUNE", raising=False)
+        else:
+            monkeypatch.setenv("AD2_NO_PRUNE", "1")
+        ctx = ad2.Context(0)
+        res = ctx.cluster(a["offsets"], a["supports"], a["weights"], a["labels"], a["x0"], a["w0"], b.K, b.m, 20, 10, 5,
+                          dtype=b.dtype)
+        out[prune] = (res, ctx.info(), ctx.centroids())
+        ctx.close()
+    r0, r1 = out[False][0], out[True][0]
+    assert r0["rounds"] == r1["rounds"]
+    np.testing.assert_array_equal(r0["labels"], r1["labels"])
+    np.testing.assert_array_equal(r0["changed"], r1["changed"])
+    np.testing.assert_array_equal(r0["objective"], r1["objective"])
+    info, info0 = out[True][1], out[False][1]
+    assert info0["assign_certified"] == 0
+    print(f"{case}: rounds {r1['rounds']}, certified {info['assign_certified']} of {b.N * (r1['rounds'] - 1)} "
+          f"member-rounds after round 1, exact solves {info['assign_exact']} vs {info0['assign_exact']} unpruned")
+    if case == "separated":
+        assert r1["rounds"] >= 2 and info["assign_certified"] > 0.25 * b.N * (r1["rounds"] - 1)
+        assert info["assign_exact"] < info0["assign_exact"]
+    x, w = out[True][2]
+    ctx = ad2.Context(0)
+    lab, _, _ = ctx.assign(a["offsets"], a["supports"], a["weights"], torch.from_numpy(x).cuda(),
+                           torch.from_numpy(w).cuda(), dtype=b.dtype)
+    np.testing.assert_array_equal(lab, r1["labels"])
+
+
 # ------------------------------------------------------------------ Eq.merge initialisation (P:820-840)
 
 @pytest.mark.parametrize("cfg,N,K,dtype", [(2, 600, 10, "f32"), (3, 400, 6, "f64"), (4, 120, 5, "f32")])
