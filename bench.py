@@ -247,6 +247,28 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     # the profiled graph is one step(tau); a round runs T/tau of them
     iter_share = float(np.sum(launch_ms)) * (T // tau) / ms if ms > 0 else None
 
+    # the other state representation on the same box (§13 of DESIGN.md), reported beside the headline:
+    # variant 2 only (the compressed passes exist there), same workload, same timing rules
+    alt = None
+    if info["variant"] == 2 and tau >= 3 and not args.no_alt:
+        other = 1 - args.state_mode
+        ctx.set_state_mode(other)
+        with ClockSampler(local_rank) as clk_alt:
+            ms_alt, _ = timed(lambda: step(D, "device"), args.steps, max(3, args.warmup),
+                              before_last=lambda: prof_box.update(arm=True))
+        lm_alt, _ = ctx.prof_read()
+        dom = lm_alt[1:-1] if len(lm_alt) > 2 else lm_alt
+        bpe_alt = (3 * es + 2 * es * (mine.N * b.m + mine.n) / max(1, entries_local)) if other == 1 else 4 * es
+        ach_alt = bpe_alt * entries_local / (float(np.mean(dom)) / 1e3) / 1e9
+        alt = {"state": ["exact (Pi1, Lambda)", "epoch-anchored compressed (G, U, log-factors)"][other],
+               "value": entries_total * T / (ms_alt / 1e3), "unit": UNIT, "ms_per_step": ms_alt,
+               "kernel": "k_badmm_tma<" + ("GMID" if other == 1 else "FUSED") + ">",
+               "avg_launch_ms": float(np.mean(dom)), "bytes_per_entry": bpe_alt, "achieved_gbs": ach_alt,
+               "frac": ach_alt / peak, "clocks": clk_alt.summary(),
+               "parity": "exact path" if other == 0 else
+               "north_star tolerances except x of centroid rows with w_i < 1e-8 (eps-decided; DESIGN.md 13)"}
+        ctx.set_state_mode(args.state_mode)
+
     # e2e: the same step through the C ABI from pinned host buffers (H2D inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -314,6 +336,7 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
                               "note": "SURVEY.md 8(d) definition: ad2_badmm_step + ad2_update_support only "
                                       "(value above is the whole round incl. init and objective)"},
         "e2e": e2e,
+        "alt_state_mode": alt,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
@@ -415,6 +438,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other state representation's measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cost-mode", type=int, default=0, help="0: fp32 cost build, 1: bf16 tcgen05 (cached-cost kernels)")
     ap.add_argument("--state-mode", type=int, default=0,

@@ -63,12 +63,23 @@ def full(rep, out, entries=None, workload=None):
         js.append(rec)
     open(out, "w").write("\n".join(lines) + "\n")
     if workload:
+        # one record per (workload, kernel mode) in profiles/ncu_traffic.json: the MODE template
+        # argument of k_badmm_tma<T, MP, NCH, MODE, DP> names it (1 FUSED, 7 GMID, ...)
         tr = os.path.join(os.path.dirname(out), "ncu_traffic.json")
-        fused = [x for x in js if "1, 16>" in x["kernel"] or ", 1, 1, 16>" in x["kernel"] or "FUSED" in x["kernel"]]
-        pick = fused[0] if fused else js[0]
-        json.dump({"workload": workload, "kernel_variant": "fused", "kernel": pick["kernel"],
-                   "dram_bytes_per_launch": pick["dram_bytes"], "duration_ms_cold": pick["duration_ms"],
-                   "source": os.path.basename(out)}, open(tr, "w"), indent=1)
+        names = {"1": "fused", "5": "fusedx", "6": "gin", "7": "gmid", "8": "gxout", "3": "p1init"}
+        try:
+            recs = json.load(open(tr))
+            recs = recs if isinstance(recs, list) else [recs]
+        except (OSError, ValueError):
+            recs = []
+        for x in js:
+            parts = x["kernel"].split("k_badmm_tma<")[-1].split(">")[0].split(",")
+            variant = names.get(parts[3].strip(), "other") if len(parts) >= 5 else "other"
+            recs = [r for r in recs if not (r.get("workload") == workload and r.get("kernel_variant") == variant)]
+            recs.append({"workload": workload, "kernel_variant": variant, "kernel": x["kernel"],
+                         "dram_bytes_per_launch": x["dram_bytes"], "duration_ms_cold": x["duration_ms"],
+                         "source": os.path.basename(out)})
+        json.dump(recs, open(tr, "w"), indent=1)
     print(open(out).read())
 
 
