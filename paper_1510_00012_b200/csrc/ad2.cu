@@ -1143,7 +1143,7 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
   if (prof) {
-    g->ev.resize(2 * (size_t)(p2x && n >= 2 && !getenv("AD2_NO_FUSEDX") ? n : n + 1));
+    g->ev.resize(2 * (size_t)(ctx->variant == 2 && p2x && n >= 2 && !getenv("AD2_NO_FUSEDX") ? n : n + 1));
     for (auto& e : g->ev) CU(cudaEventCreate(&e));
   }
   CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -1152,7 +1152,7 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   // (FUSEDX), so the step has n passes and no P2 pass; otherwise n + 1 passes ending with P2X /
   // P2ONLY.  Phase 2 of the last iteration is then deferred to the next step's first (FUSED) pass.
   static const bool no_fx = getenv("AD2_NO_FUSEDX") != nullptr;   // A/B knob (bench experiments)
-  const bool fx = p2x && n >= 2 && !no_fx;
+  const bool fx = ctx->variant == 2 && p2x && n >= 2 && !no_fx;
   const int npass = fx ? n : n + 1;
   // compressed state (ad2_set_state_mode 1): the step's middle passes run from the epoch anchor
   // (GIN at the first pass that has a phase 2, GMID after it, GXOUT last), steps of >= 3
@@ -1212,7 +1212,10 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   if (n_iters == 0) return AD2_OK;
   CHK(set_dev(ctx));
   const bool prof = ctx->prof == 1 || (ctx->prof == 2 && ctx->prof_pending);
-  const bool fresh = ctx->fresh, pending = ctx->pending, p2x = ctx->variant == 2;
+  // the step's last phase 2 is deferred to the next step's first (FUSED) pass: variant 2, and
+  // variant 3 unless its support-update partials come from the stored Pi2 (d > 64, k_xpart)
+  const bool p2x = ctx->variant == 2 || (ctx->variant == 3 && ctx->d <= 64 && !ctx->table);
+  const bool fresh = ctx->fresh, pending = ctx->pending;
   const int key = 16 * n_iters + (ctx->state_mode ? 8 : 0) + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
   if (ctx->state_mode == 1 && ctx->variant == 2) {     // log-factor buffers of the compressed state
     CU(ctx->gra.reserve(ctx->es * (size_t)(ctx->N > 0 ? ctx->N : 1) * ctx->ld));

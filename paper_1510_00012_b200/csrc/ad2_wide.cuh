@@ -18,6 +18,8 @@
 //                sweep C -> P = Pi1, L = Lambda, w-partials
 //   MODE P2ONLY: sweep A -> sweep B2 (Eq.badmmc1, Eq.badmm2, support-update partials of
 //                Eq.updatex) -> Q = Pi2, L = Lambda, x-partials
+//   MODE P2X   : P2ONLY without the stores (the x partials only): the step's phase 2 stays deferred
+//                and the next step's first FUSED pass recomputes it (it reads no cost)
 #pragma once
 #include "ad2_tma.cuh"
 
@@ -76,9 +78,10 @@ k_badmm_wide(const IterArgs<float> a) {
   const float2 rho2 = make_float2(kap, kap), nrho2 = make_float2(-kap, -kap);
   const float2 eps2 = make_float2(eps_r, eps_r);
   float accw = 0.f, accm = 0.f;
-  float2 accx[(MODE == P2ONLY) ? DP / 2 : 1];                     // coordinate pairs (FFMA2)
+  constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);
+  float2 accx[PH2 ? DP / 2 : 1];                                  // coordinate pairs (FFMA2)
 #pragma unroll
-  for (int t = 0; t < ((MODE == P2ONLY) ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
+  for (int t = 0; t < (PH2 ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
   bool bad = false;
   const float* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
   float* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
@@ -99,14 +102,14 @@ k_badmm_wide(const IterArgs<float> a) {
   // pass region [P | L | C] (P2ONLY: [P | L | Y], the supports for the x partials); dy % 4 == 0
   const int dy = a.dy;
   // P2ONLY with external x partials (d > 64, k_xpart) stages no supports
-  const int third = (MODE == P2ONLY) ? (a.xext ? 0 : dy) : WMP;    // floats per point of the 3rd array
+  const int third = PH2 ? (a.xext ? 0 : dy) : WMP;                 // floats per point of the 3rd array
   auto issue = [&](int t, int base, int64_t p0, int np) {          // leader only
     const uint32_t bp = (uint32_t)(WMP * np * 4), b3 = (uint32_t)(third * np * 4);
     float* st = ring + base;
     mbar_expect_tx(&bar[t & 1], 2 * bp + b3);
     tma_load(st, src_plan + (int64_t)WMP * p0, bp, &bar[t & 1]);
     tma_load(st + WMP * np, a.L + (int64_t)WMP * p0, bp, &bar[t & 1]);
-    if (MODE == P2ONLY) {
+    if (PH2) {
       if (b3) tma_load(st + 2 * WMP * np, a.Y + (int64_t)dy * p0, b3, &bar[t & 1]);
     }
     else tma_load(st + 2 * WMP * np, a.Cc + (int64_t)WMP * p0, b3, &bar[t & 1]);
@@ -138,11 +141,10 @@ k_badmm_wide(const IterArgs<float> a) {
     }
     const int mk = cnp;
     const int jc = ig;                 // the column this lane sums (jc < mk)
-    const float om_j = (MODE != P2ONLY && jc < mk) ? __ldg(a.om + cp0 + jc) : 0.f;
     float om_jc[(MKX + WM - 1) / WM];               // w^(k)_j of the columns this lane sums
 #pragma unroll
     for (int cj = 0; cj < (MKX + WM - 1) / WM; ++cj)
-      om_jc[cj] = (MODE != P2ONLY && jc + cj * WM < mk) ? __ldg(a.om + cp0 + jc + cj * WM) : 0.f;
+      om_jc[cj] = (!PH2 && jc + cj * WM < mk) ? __ldg(a.om + cp0 + jc + cj * WM) : 0.f;
     mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     float* const Ps = ring + cbase;
     float* const Ls = Ps + WMP * mk;
@@ -166,7 +168,7 @@ k_badmm_wide(const IterArgs<float> a) {
     }
     const float2 f2 = make_float2(f, f), ef2 = make_float2(eps_r * f, eps_r * f);
 
-    if constexpr (MODE == P2ONLY) {
+    if constexpr (PH2) {
       // ---- sweep B2: Pi2 = (pe + eps) w_i / r (Eq.badmmc1), L' += kappa (Pi1 - Pi2) (Eq.badmm2),
       //      support-update partials sum_j pi2_ij y_j, sum_j pi2_ij (Eq.updatex, X5)
 #pragma unroll 2
@@ -175,8 +177,10 @@ k_badmm_wide(const IterArgs<float> a) {
         const float p = Ps[e0], l = Ls[e0];
         const float q = fmaf(p * N::ex(l), f, eps_r * f);
         const float2 q2 = make_float2(q, q);
-        Ps[e0] = q;
-        Ls[e0] = fmaf(-kap, q, fmaf(kap, p, l));
+        if constexpr (MODE == P2ONLY) {
+          Ps[e0] = q;
+          Ls[e0] = fmaf(-kap, q, fmaf(kap, p, l));
+        }
         if (a.xext) continue;
         accm += q;
         const float* yj = Cs + j * dy;
@@ -272,9 +276,11 @@ k_badmm_wide(const IterArgs<float> a) {
     // ---- results leave by bulk stores from the same slots
     if (leader) {
       const uint32_t bp = (uint32_t)(WMP * mk * 4);
-      tma_store(dst_plan + (int64_t)WMP * cp0, Ps, bp);
-      if (MODE != P1ONLY) tma_store(a.L + (int64_t)WMP * cp0, Ls, bp);
-      bulk_commit();
+      if (MODE != P2X) {
+        tma_store(dst_plan + (int64_t)WMP * cp0, Ps, bp);
+        if (MODE != P1ONLY) tma_store(a.L + (int64_t)WMP * cp0, Ls, bp);
+        bulk_commit();
+      }
       if (nnp > 0 && nbase < 0) {      // pass t+1 did not fit beside pass t: issue it at the ring start
         bulk_wait_read_all();
         issue(t + 1, 0, np0, nnp);
@@ -293,7 +299,7 @@ k_badmm_wide(const IterArgs<float> a) {
   // this pair's partial sums of the item (rows are lane-owned); consensus adds the NPAIR pair
   // partials of every item in order
   const int64_t part = (int64_t)item * NPAIR + pair;
-  if constexpr (MODE != P2ONLY) {
+  if constexpr (!PH2) {
     if (rowok) a.pw[part * m + ig] = accw;
   } else {
     if (rowok && !a.xext) {

@@ -2,6 +2,7 @@
 // and of the tiled cost build (ad2_wide.cuh).
 #include <cstdlib>
 
+#include "ad2_launch.cuh"
 #include "ad2_tc.cuh"
 #include "ad2_wide.cuh"
 
@@ -12,16 +13,18 @@ namespace ad2k {
 template <int WM, int MKX, int NPAIR, int RKB, int DP>
 static void go_wide(int mode, const IterArgs<float>& a, int64_t n_items, cudaStream_t s) {
   using Lay = WideLayout<WM, MKX, NPAIR, RKB>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice once;                   // the smem attribute is per device
+  if (once.first()) {
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P1ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, FUSED, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
-    attr = true;
+    cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P2X, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    once.done();
   }
   dim3 g((unsigned)n_items), b(NPAIR * WM);
   if (mode == P1ONLY) k_badmm_wide<WM, MKX, NPAIR, RKB, P1ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else if (mode == FUSED) k_badmm_wide<WM, MKX, NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == P2X) k_badmm_wide<WM, MKX, NPAIR, RKB, P2X, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
 }
 
@@ -82,10 +85,10 @@ void launch_cost_tc32(const int64_t* off, const int64_t* imb, const int32_t* icl
                       float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
   constexpr int SMEM = 98304 + 1024;             // + alignment slack
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice once;
+  if (once.first()) {
     cudaFuncSetAttribute(k_cost_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
+    once.done();
   }
   k_cost_tc32<<<(unsigned)n_items, 128, SMEM, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
 }
