@@ -17,7 +17,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libad2.so")
+# AD2_LIB selects another build of the same library (e.g. libad2_checked.so, device assertions on)
+LIB_PATH = os.environ.get("AD2_LIB") or os.path.join(_HERE, "libad2.so")
 
 F32, F64 = 0, 1
 R1, R2 = 0, 1

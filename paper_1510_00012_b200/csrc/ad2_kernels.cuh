@@ -11,6 +11,7 @@
 // items of a cluster in item order, so every result is deterministic.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <type_traits>
 #include <math_constants.h>
 #include <stdint.h>
@@ -35,6 +36,24 @@ enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5, GIN =
 enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2, ERR_EPSCOL = 16 };   // ERR_EPSCOL: a flag, not an error
 
 constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels
+
+// Checked build (python -m paper_1510_00012_b200.build --checked -> libad2_checked.so): device
+// assertions on the shared-memory ring placement and pass geometry of the staged kernels, a
+// stand-in for compute-sanitizer (closed on the GPU pool).  Compiled out otherwise.
+#ifdef AD2_CHECKS
+#define AD2_CHECK(c)                                                                             \
+  do {                                                                                           \
+    if (!(c)) {                                                                                  \
+      printf("AD2_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x, #c);                                                                   \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define AD2_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
 
 // Programmatic dependent launch (the step graph of variant 2): a kernel launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization may start while its predecessor drains;

@@ -256,6 +256,10 @@ k_badmm_tma(const IterArgs<T> a) {
         nbase = 0;
       }
     }
+    // the current and the next pass regions lie inside the ring and do not overlap; a pass never
+    // holds more than G members of at most MK columns
+    AD2_CHECK(cnp <= G * MK && nnp <= G * MK && cbase >= 0 && cbase + csize <= RING);
+    AD2_CHECK(nbase < 0 || (nbase + nsize <= RING && (nbase >= cbase + csize || nbase + nsize <= cbase)));
     if (lane == 0 && nbase >= 0) {
       bulk_wait_read_all();          // pass t-1 has left its region
       issue(t + 1, nbase, np0, nnp);
@@ -271,6 +275,7 @@ k_badmm_tma(const IterArgs<T> a) {
       mk = has ? (int)(a.off[k + 1] - o0) : 0;
     }
     const int mkw = (G == 1) ? mk : (int)__reduce_max_sync(0xffffffffu, (unsigned)mk);
+    AD2_CHECK(mk >= 0 && mk <= MK && mkw <= MK);
     const T mkeps = (T)mk * eps_r;
     T omv[NCH];                                        // w^(k)_j for the column this lane sums
     if constexpr (G == 1) {                            // prefetched one pass ahead

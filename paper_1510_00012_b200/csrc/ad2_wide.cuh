@@ -135,6 +135,8 @@ k_badmm_wide(const IterArgs<float> a) {
         nbase = 0;
       }
     }
+    AD2_CHECK(cnp <= MKX && nnp <= MKX && cbase >= 0 && cbase + csize <= RING);
+    AD2_CHECK(nbase < 0 || (nbase + nsize <= RING && (nbase >= cbase + csize || nbase + nsize <= cbase)));
     if (leader && nbase >= 0) {
       bulk_wait_read_all();            // pass t-1 has left its region
       issue(t + 1, nbase, np0, nnp);
