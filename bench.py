@@ -156,6 +156,8 @@ def run_ours(args, rank, world, local_rank, dist_on=False):
     stream = torch.cuda.current_stream(dev)
     ctx = ad2.Context(local_rank, stream.cuda_stream)
     ctx.set_state_mode(args.state_mode)
+    if args.tc_cost >= 0:
+        ctx.set_tc_cost(args.tc_cost)
     if dist_on:
         bootstrap_nccl(ctx)
 
@@ -441,6 +443,8 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the other state representation's measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cost-mode", type=int, default=0, help="0: fp32 cost build, 1: bf16 tcgen05 (cached-cost kernels)")
+    ap.add_argument("--tc-cost", type=int, default=-1,
+                    help="1/0: tensor-core / FFMA2 dot products in the variant-2 cost (ad2_set_tc_cost); -1: library default")
     ap.add_argument("--state-mode", type=int, default=0,
                     help="0: exact Pi1/Lambda state, 1: epoch-anchored compressed state (ad2_set_state_mode)")
     ap.add_argument("--dist", action="store_true",

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define AD2_ABI_VERSION 2
+#define AD2_ABI_VERSION 3
 
 typedef struct ad2_ctx_s *ad2_ctx;
 
@@ -129,6 +129,8 @@ typedef struct {
                                    (the eps-free recursion does not hold there; use state mode 0) */
     int64_t assign_certified;   /* last ad2_cluster: member-rounds whose label the bounds certified (no solve) */
     int64_t assign_exact;       /* last ad2_cluster: exact transport solves (incl. the centroid drifts) */
+    int32_t tc_cost;            /* 1: the iteration kernel forms the cost's dot products on the tensor
+                                   cores (ad2_set_tc_cost and the round's shape allow it) */
 } ad2_info;
 
 /* Create a context on CUDA device `cuda_device`; `cuda_stream` is a cudaStream_t (NULL = legacy
@@ -182,6 +184,20 @@ void ad2_group_close(ad2_group g);
  *     ad2_info.eps_floor_columns.
  * Takes effect at the next ad2_badmm_step. */
 ad2_status ad2_set_state_mode(ad2_ctx ctx, int32_t mode);
+
+/* Cost of the variant-2 iteration kernel (C_ij = ||x_i - y_j||^2, recomputed every
+ * iteration from the staged supports):
+ *   1 (the environment variable AD2_TC=1 makes it the default): for fp32 rounds whose passes are single
+ *     32-row members (m <= 32, m_k <= 32, 32 row blocks) with 4 < d <= 16, the dot products
+ *     x'_i . y'_j of the centred coordinates (x' = x - o, y' = y - o, o the cluster's mean centroid
+ *     point; C is translation invariant) run on the tensor cores: tcgen05.mma kind::tf32 with tf32
+ *     hi / lo splits of both operands (hi.hi + hi.lo + lo.hi) accumulated in fp32 in TMEM, and
+ *     C = |x'|^2 + |y'|^2 - 2 x'.y' in fp32.  ad2_info.tc_cost reports whether it is in use.
+ *   0 (default): the dot products in fp32 FMAs (packed FFMA2) on the CUDA cores.  Measured on
+ *     config 5 the tensor-core form is slower (9.65 vs 8.75 ms per iteration: the per-pass operand
+ *     split and six single-thread MMA issues cost what the dot products saved).
+ * Takes effect at the next ad2_badmm_step; AD2_ERR_ARG for other values. */
+ad2_status ad2_set_tc_cost(ad2_ctx ctx, int32_t enable);
 
 /* Start a round (a1-a3 of SURVEY.md §8(a)): copy/sort the batch by cluster, build C, compute
  * rho per cluster (fixed for the round, X2), Lambda = 0, Pi^(2) = product measure or, for

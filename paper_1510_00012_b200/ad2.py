@@ -56,14 +56,14 @@ class Info(C.Structure):
                 ("n_items", C.c_int64), ("variant", C.c_int32), ("mp", C.c_int32), ("nch", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("launches", C.c_int64),
                 ("state_bytes", C.c_int64), ("state_mode", C.c_int32), ("eps_floor_columns", C.c_int32),
-                ("assign_certified", C.c_int64), ("assign_exact", C.c_int64)]
+                ("assign_certified", C.c_int64), ("assign_exact", C.c_int64), ("tc_cost", C.c_int32)]
 
 
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
            "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
            "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_prefetch", "ad2_sync",
-           "ad2_set_state_mode", "ad2_group_open", "ad2_group_allreduce", "ad2_attach_group", "ad2_group_close",
+           "ad2_set_state_mode", "ad2_set_tc_cost", "ad2_group_open", "ad2_group_allreduce", "ad2_attach_group", "ad2_group_close",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
 
@@ -107,6 +107,7 @@ def load_library(path: str = LIB_PATH):
     L.ad2_destroy.argtypes = [p]
     L.ad2_destroy.restype = None
     L.ad2_set_state_mode.argtypes = [p, i32]
+    L.ad2_set_tc_cost.argtypes = [p, i32]
     L.ad2_group_open.argtypes = [C.POINTER(p), C.c_char_p, C.c_int, C.c_int, i64]
     L.ad2_group_allreduce.argtypes = [p, p, i64, i32]
     L.ad2_attach_group.argtypes = [p, p]
@@ -304,6 +305,10 @@ class Context:
         i = Info()
         self._chk(self.L.ad2_get_info(self.h, C.byref(i)))
         return {f: getattr(i, f) for f, _ in Info._fields_}
+
+    def set_tc_cost(self, enable: int):
+        """ad2_set_tc_cost: 1 tensor-core dot products in the variant-2 cost (default), 0 FFMA2."""
+        self._chk(self.L.ad2_set_tc_cost(self.h, int(enable)))
 
     def set_state_mode(self, mode: int):
         """ad2_set_state_mode: 0 exact Pi1/Lambda streaming, 1 epoch-anchored compressed state."""

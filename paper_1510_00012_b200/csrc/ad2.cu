@@ -131,6 +131,7 @@ struct ad2_ctx_s {
   int variant = 0, mp = 0, nch = 0, dp = 0, wcfg = 0;   // wcfg: rows per member block of variant 3
   int cost_mode = 0;                 // ad2_cost_mode
   int state_mode = 0;                // ad2_set_state_mode: 1 = epoch-anchored compressed state (variant 2)
+  int tc_cost = getenv("AD2_TC") ? 1 : 0;      // ad2_set_tc_cost: tensor-core cost in the variant-2 kernel
   int cur_gs = 0;                    // compressed state: iterations since the anchor (launch argument)
   bool cur_pdl = false;              // the next iteration / consensus launch is a programmatic dependent
   DBuf gra, gcb;                     // compressed state: row [N][ld] and column [n] log-factors
@@ -313,6 +314,7 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.cb = ctx->gcb.as<T>();
   a.gs = ctx->cur_gs;
   a.pdl = ctx->cur_pdl ? 1 : 0;
+  a.tc = ctx->tc_cost;
   return a;
 }
 
@@ -1216,7 +1218,8 @@ ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
   // variant 3 unless its support-update partials come from the stored Pi2 (d > 64, k_xpart)
   const bool p2x = ctx->variant == 2 || (ctx->variant == 3 && ctx->d <= 64 && !ctx->table);
   const bool fresh = ctx->fresh, pending = ctx->pending;
-  const int key = 16 * n_iters + (ctx->state_mode ? 8 : 0) + (pending ? 4 : 0) + (fresh ? 2 : 0) + (prof ? 1 : 0);
+  const int key = 32 * n_iters + (ctx->tc_cost ? 16 : 0) + (ctx->state_mode ? 8 : 0) + (pending ? 4 : 0) +
+                  (fresh ? 2 : 0) + (prof ? 1 : 0);
   if (ctx->state_mode == 1 && ctx->variant == 2) {     // log-factor buffers of the compressed state
     CU(ctx->gra.reserve(ctx->es * (size_t)(ctx->N > 0 ? ctx->N : 1) * ctx->ld));
     CU(ctx->gcb.reserve(ctx->es * (size_t)(ctx->n > 0 ? ctx->n : 1)));
@@ -1399,6 +1402,8 @@ ad2_status ad2_get_info(ad2_ctx ctx, ad2_info* info) {
   info->state_mode = ctx->state_mode;
   info->assign_certified = ctx->asg_certified;
   info->assign_exact = ctx->asg_exact;
+  info->tc_cost = (ctx->tc_cost && ctx->variant == 2 && ctx->dtype == AD2_F32 && ctx->mp == 32 && ctx->nch == 1 &&
+                   ctx->dp > 4) ? 1 : 0;
   info->eps_floor_columns = 0;
   if (ctx->d_err.p && cudaSetDevice(ctx->device) == cudaSuccess) {
     int h = 0;
@@ -1416,6 +1421,13 @@ ad2_status ad2_set_state_mode(ad2_ctx ctx, int32_t mode) {
   if (!ctx) return AD2_ERR_ARG;
   if (mode != 0 && mode != 1) return ctx->fail(AD2_ERR_ARG, "set_state_mode: mode %d", mode);
   ctx->state_mode = mode;             // graphs are cached per mode (the step key)
+  return AD2_OK;
+}
+
+ad2_status ad2_set_tc_cost(ad2_ctx ctx, int32_t enable) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (enable != 0 && enable != 1) return ctx->fail(AD2_ERR_ARG, "set_tc_cost: %d", enable);
+  ctx->tc_cost = enable;              // graphs are cached per setting (the step key)
   return AD2_OK;
 }
 

@@ -74,8 +74,13 @@ template <> struct Num<float> {
   }
   static __device__ __forceinline__ float ld(const float* p) { return __ldcs(p); }
   static __device__ __forceinline__ void st(float* p, float v) { __stcs(p, v); }
-  // fp32 normalisations: MUFU reciprocal based quotient (<= 2 ulp), far inside the fp32 parity bar
-  static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+  // fp32 normalisations: MUFU reciprocal based quotient (<= 2 ulp), far inside the fp32 parity bar;
+  // the operands are row / column masses >= m_k eps or m eps, far from the denormal range
+  static __device__ __forceinline__ float div(float a, float b) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+    return a * r;
+  }
   // kx * rho for kx = log2(e)/rho: the scale of a pre-scaled Lambda's dual step
   static __device__ __forceinline__ float kappa() { return 1.4426950408889634f; }
   // logarithm in the base of ex (log2), per row / column only: the accurate library function
@@ -117,6 +122,8 @@ struct IterArgs {
   T* cb;                   // compressed state: [n] column log-factors
   int gs;                  // compressed state: iterations since the anchor of this launch's phase 2
   int pdl;                 // host: launch with programmatic stream serialization (the kernel pdl_wait()s)
+  int tc;                  // host: variant 2 with 32-row single-member passes and 4 < d <= 16 takes the
+                           // tensor-core cost instantiation (ad2_set_tc_cost)
 };
 
 // 16-byte vectors of the element type (shared-memory tiles, staged rows)

@@ -57,6 +57,34 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- tcgen05 pieces of the tensor-core cost (TC instantiation, see k_badmm_tma) ----
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// shared-memory matrix descriptor, K-major without swizzle: 8-row core matrices of 16-byte rows,
+// LBO = byte stride between the two K-adjacent core matrices of an MMA, SBO = between 8-row groups
+__device__ __forceinline__ uint64_t tc_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor kind::tf32: D fp32, A/B tf32, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t tc_idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T, issued by one thread
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+// tf32 split: hi keeps the 10 stored mantissa bits (the MMA reads tf32 by truncation), lo = v - hi
+__device__ __forceinline__ float tc_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
 template <typename T, int MP, int NCH, int DP>
 struct TmaLayout {
   static constexpr int G = 32 / MP;
@@ -74,8 +102,9 @@ struct TmaLayout {
   static constexpr int SLACK = ((G == 1 ? 4 * DY : MK * DY + MP * MK) + 63) / 64 * 64;
   static constexpr int TILE = (G == 1) ? 0 : MP * 32;               // G == 1: tile = the pass's P slot
   static constexpr int FB = 2 * G * MK;                            // column factors + log-factors
+  // + three mbarriers (the 2-stage load pipeline and, for the tensor-core cost, the MMA)
   static constexpr size_t WARP_BYTES =
-      ((sizeof(T) * (size_t)(RING + SLACK + TILE + FB) + 16 + 127) / 128) * 128;
+      ((sizeof(T) * (size_t)(RING + SLACK + TILE + FB) + 24 + 127) / 128) * 128;
   static constexpr size_t CTA_BYTES = NWARP * WARP_BYTES;
   // static shared memory of the kernel (item-partial combination), for the capacity check
   static constexpr size_t STATIC_BYTES = sizeof(T) * (size_t)NWARP * G * MP * (DP + 1);
@@ -100,7 +129,16 @@ template <> struct Pr<double> {
   }
 };
 
-template <typename T, int MP, int NCH, int MODE, int DP>
+// TCC = 1 (fp32, 32-row single-member passes, 4 < d <= 16): the cost's dot products run on the
+// tensor cores.  Per CTA, the centroid rows centred on their mean, x'_i = x_i - o, scaled by -2 and
+// split into tf32 hi / lo, sit in TMEM (every warp writes them into its own 32 lanes, so rows
+// 32 w + i of the M = 128 operand are x'_i for warp w); per member pass, the warp writes its
+// points y'_j = y_j - o (hi / lo, canonical K-major layout) into the pass's P and L slots, which
+// are free once the state is in registers, and one lane issues 6 tcgen05.mma kind::tf32 (hi.hi,
+// hi.lo, lo.hi over K = 16) into the warp's 32 TMEM columns; sweep 2 reads
+// D_ij = -2 x'_i . y'_j with tcgen05.ld and forms C_ij = |x'_i|^2 + |y'_j|^2 + D_ij (C is
+// translation invariant; centring keeps the products at the scale of C).
+template <typename T, int MP, int NCH, int MODE, int DP, int TCC = 0>
 __global__ void __launch_bounds__(NWARP * 32, 3)
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
@@ -160,6 +198,62 @@ k_badmm_tma(const IterArgs<T> a) {
   }
   T accw = T(0), accm = T(0);
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);     // phase 2 only (+ x partials)
+  constexpr bool TC = TCC != 0 && sizeof(T) == 4 && MP == 32 && NCH == 1 && DP == 16 && !PH2;
+  T* const yyb = fbuf;                                       // TC: |y'_j|^2 of the pass (fbuf is free in sweep 2)
+  __shared__ uint32_t tm_s[2];                               // TC: TMEM bases of D (128 columns) and A (32)
+  uint32_t tm_d = 0, tm_a = 0;
+  float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);               // TC: centre coordinates 4q .. 4q+3 (q = lane & 3)
+  if constexpr (TC) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_s[0])));
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(&tm_s[1])));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // centre o = mean of the m centroid rows; A row i = -2 (x_i - o), tf32 hi in columns 0..15 and
+    // lo in 16..31; |x_i - o|^2 in fp32 replaces |x_i|^2
+    float xv[16], o[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      xv[t] = (rowok && t < d) ? (float)a.x[((int64_t)c * m + i) * d + t] : 0.f;
+      float s = xv[t];
+#pragma unroll
+      for (int h = 16; h >= 1; h >>= 1) s += __shfl_xor_sync(0xffffffffu, s, h);
+      o[t] = s / (float)m;
+    }
+    uint32_t r[32];
+    float xc = 0.f;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const float v = (rowok && t < d) ? xv[t] - o[t] : 0.f;
+      xc = fmaf(v, v, xc);
+      const float av = -2.f * v, h = tc_hi(av);
+      r[t] = __float_as_uint(h);
+      r[16 + t] = __float_as_uint(av - h);
+    }
+    xx = (T)xc;
+    const int q = lane & 3;
+    oq.x = q == 0 ? o[0] : q == 1 ? o[4] : q == 2 ? o[8] : o[12];
+    oq.y = q == 0 ? o[1] : q == 1 ? o[5] : q == 2 ? o[9] : o[13];
+    oq.z = q == 0 ? o[2] : q == 1 ? o[6] : q == 2 ? o[10] : o[14];
+    oq.w = q == 0 ? o[3] : q == 1 ? o[7] : q == 2 ? o[11] : o[15];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    tm_d = tm_s[0];
+    tm_a = tm_s[1];
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tm_a + ((uint32_t)(32 * warp) << 16)),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();                                         // all 128 A lanes written before any MMA reads them
+    tc_fence_after();
+  }
+  uint32_t mph = 0;                                          // TC: phase of the MMA mbarrier
   constexpr bool XP = (MODE == FUSEDX || MODE == GXOUT);     // FUSED + x partials
   constexpr bool GI = (MODE == GIN);                          // compressed state: anchor launch
   constexpr bool GC = (MODE == GMID || MODE == GXOUT);       // phase 2 from (G, U, ra, cb)
@@ -190,6 +284,7 @@ k_badmm_tma(const IterArgs<T> a) {
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    if constexpr (TC) mbar_init(&bar[2], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -201,6 +296,16 @@ k_badmm_tma(const IterArgs<T> a) {
     p0 = a.off[k0];
     p1 = a.off[k1];
     return (int)(p1 - p0);
+  };
+  // the same, loads only: the size of pass t+2 is formed at the end of pass t, so the warp does
+  // not wait for the offsets' global-load latency at the start of a pass (in-order issue)
+  auto pass_raw = [&](int t, int64_t& p0, int64_t& p1) -> bool {
+    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;
+    if (k0 >= me) return false;
+    const int64_t k1 = (k0 + G < me) ? k0 + G : me;
+    p0 = a.off[k0];
+    p1 = a.off[k1];
+    return true;
   };
   // G == 1: the slots of a pass region hold ceil4(m_k) columns ([P | L | Y] at 0, MP*np4,
   // 2*MP*np4); the 0-3 padding columns of P and L are zeroed by the lanes, so the column blocks
@@ -246,7 +351,7 @@ k_badmm_tma(const IterArgs<T> a) {
   for (int t = 0; cnp > 0; ++t) {
     // place pass t+1 behind pass t (or at the ring start) while t computes
     int64_t fp0 = 0, fp1 = 0;
-    const int fnp = pass_pts(t + 2, fp0, fp1);          // consumed next pass
+    const bool fva = pass_raw(t + 2, fp0, fp1);         // consumed next pass
     const int csize = (2 * MP + DY) * slot(cnp), nsize = (2 * MP + DY) * slot(nnp);
     int nbase = -1;
     if (nnp > 0) {
@@ -324,31 +429,50 @@ k_badmm_tma(const IterArgs<T> a) {
       // G == 1 blocks use the pair layout (blk_idx, ad2_kernels.cuh): columns 2q, 2q+1 interleaved
       // by row, so a lane moves both with one 8-byte access; an odd m_k's last column arrives in the
       // single-column layout and is rewritten here as the pair (m_k - 1, pad) with a zero partner
+      // (a lane only ever touches its own row's pairs below and in sweep 1: one __syncwarp, between
+      // the single-layout reads of the odd column and the pair writes over them)
       const bool odd = mk & 1;
+      const int mk2 = (mk + 1) & ~1;                   // columns [mk2, cns): one padding pair, or none
+      T* const po = Ps + (mk - 1) * MP;
+      T* const lo = Ls + (mk - 1) * MP;
       T px = T(0), lx = T(0);
       if (odd) {
-        px = Ps[(mk - 1) * MP + i];
-        lx = Ls[(mk - 1) * MP + i];
+        px = po[i];
+        lx = lo[i];
       }
-#pragma unroll
-      for (int u = 0; u < 3; ++u)                      // padding columns (at most 3): p = Lambda = 0
-        if (mk + u < cns) {
-          Ps[(mk + u) * MP + i] = T(0);
-          Ls[(mk + u) * MP + i] = T(0);
-        }
+      if (mk2 < cns) {                                 // p = Lambda = 0
+        *reinterpret_cast<T2*>(Ps + mk2 * MP + 2 * i) = PR::make(T(0), T(0));
+        *reinterpret_cast<T2*>(Ls + mk2 * MP + 2 * i) = PR::make(T(0), T(0));
+      }
       __syncwarp();
       if (odd) {
-        *reinterpret_cast<T2*>(Ps + (mk - 1) * MP + 2 * i) = PR::make(px, T(0));
-        *reinterpret_cast<T2*>(Ls + (mk - 1) * MP + 2 * i) = PR::make(lx, T(0));
+        *reinterpret_cast<T2*>(po + 2 * i) = PR::make(px, T(0));
+        *reinterpret_cast<T2*>(lo + 2 * i) = PR::make(lx, T(0));
       }
-      __syncwarp();
     }
     T* const tile = (G == 1) ? st : tile_sep;          // G == 1: reuse this pass's P slot
+    // fp32 single-member passes: the tile has rows of 36 (column jt at jt*36: conflict-free 4-byte
+    // stores, lane i reads its column with 16-byte loads at i*36 + 4cc, banks 4i .. 4i+3 per
+    // quarter warp); 36 m_k <= 64 ns floats, so it stays inside the P and L slots, both free
+    // between sweep 2 and sweep 3 (the state is in registers)
+    constexpr bool TPAD = PAD && (E == 4) && MP == 32;
 
     T2 p2[MK / 2], l2[MK / 2], q2[MK / 2];
     // ---- load (columns >= m_k masked to 0) and, unless P1ONLY, the first half of phase 2:
     //      pe = Pi1 exp(Lambda/rho) (Eq.badmmc1b without eps), r = sum_j pe_j + m_k eps
     T2 racc[2] = {PR::make(T(0), T(0)), PR::make(T(0), T(0))};
+    auto ph2_first = [&](int jp, int h) {
+      if constexpr (PH1 || GC) {
+        q2[jp] = p2[jp];                                               // Pi2^(0) / unused (GC)
+      } else if constexpr (RECOMP) {
+        const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
+        racc[h] = PR::add(racc[h], PR::mul(p2[jp], e));
+      } else {
+        const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
+        q2[jp] = PR::mul(p2[jp], e);
+        racc[h] = PR::add(racc[h], q2[jp]);
+      }
+    };
 #pragma unroll
     for (int jb = 0; jb < NB; ++jb) {
       if (4 * jb >= mkw) break;
@@ -370,16 +494,66 @@ k_badmm_tma(const IterArgs<T> a) {
           p2[jp] = PR::make(v0 ? pa : T(0), v1 ? pb : T(0));
           l2[jp] = PR::make(v0 ? la : T(0), v1 ? lb : T(0));
         }
-        if constexpr (PH1 || GC) {
-          q2[jp] = p2[jp];                                             // Pi2^(0) / unused (GC)
-        } else if constexpr (RECOMP) {
-          const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
-          racc[h] = PR::add(racc[h], PR::mul(p2[jp], e));
-        } else {
-          const T2 e = PR::make(N::ex(l2[jp].x), N::ex(l2[jp].y));
-          q2[jp] = PR::mul(p2[jp], e);
-          racc[h] = PR::add(racc[h], q2[jp]);
+        if constexpr (!TC) ph2_first(jp, h);
+      }
+    }
+    if constexpr (TC) {
+      // the state is in registers: the P and L slots take the B operand, y'_j = y_j - o split into
+      // tf32 hi / lo, point j coordinates 4q..4q+3 at byte (j/8)*512 + q*128 + (j%8)*16 (8-row core
+      // matrices; rows j >= m_k are zero, so padding columns see C = |x'_i|^2)
+      T* const Bh = st;
+      const int g8 = (cnp + 7) >> 3;
+      T* const Bl = Bh + g8 * 128;
+      const int q = lane & 3, jr = lane >> 2;
+      __syncwarp();
+      for (int r = 0; r < g8; ++r) {
+        const int j = 8 * r + jr;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < cnp) {
+          v = *reinterpret_cast<const float4*>(Ys + j * DY + 4 * q);
+          v.x -= oq.x; v.y -= oq.y; v.z -= oq.z; v.w -= oq.w;
         }
+        const float4 hv = make_float4(tc_hi(v.x), tc_hi(v.y), tc_hi(v.z), tc_hi(v.w));
+        const float4 lv = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+        *reinterpret_cast<float4*>(Bh + r * 128 + q * 32 + jr * 4) = hv;
+        *reinterpret_cast<float4*>(Bl + r * 128 + q * 32 + jr * 4) = lv;
+        float s = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, v.w * v.w)));
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (q == 0) yyb[j] = s;
+      }
+      fence_proxy_async_smem();                        // generic writes -> tensor core (async proxy)
+      tc_fence_before();                               // the previous pass's tcgen05.ld are complete
+      __syncwarp();
+      if (lane == 0) {
+        tc_fence_after();
+        const uint32_t dcol = tm_d + 32 * warp;
+        const uint32_t idesc = cnp <= 16 ? tc_idesc_tf32(16) : tc_idesc_tf32(32);
+        const uint64_t dh = tc_desc_kmajor(smem_u32(Bh), 128, 512), dl = tc_desc_kmajor(smem_u32(Bl), 128, 512);
+        // K = 16 in two MMAs of 8 (+256 bytes = +16 in the descriptor's address field): hi.hi,
+        // hi.lo, lo.hi, issued from one asm block (one set of uniform operands)
+        asm volatile(
+            "{\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 h1, l1;\n\t.reg .pred p0, p1;\n\t"
+            "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+            "add.u64 h1, %2, 16;\n\tadd.u64 l1, %3, 16;\n\t"
+            "setp.ne.b32 p0, 0, 0;\n\tsetp.eq.b32 p1, 0, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], h1, %4, p1;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, p1;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], l1, %4, p1;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], %2, %4, p1;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], h1, %4, p1;\n\t"
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(dcol),
+            "r"(tm_a), "l"(dh), "l"(dl), "r"(idesc), "r"(smem_u32(&bar[2]))
+            : "memory");
+      }
+      __syncwarp();
+      // the first half of phase 2 runs while the tensor core works
+#pragma unroll
+      for (int jb = 0; jb < NB; ++jb) {
+        if (4 * jb >= mkw) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ph2_first(2 * jb + h, h);
       }
     }
     T f = T(0);
@@ -426,10 +600,28 @@ k_badmm_tma(const IterArgs<T> a) {
     } else {
       // ---- rest of phase 2 (FUSED) and phase 1, four columns at a time:
       //      C_ij; pt2 = Pi2 exp(-(C + Lambda)/rho) + eps (Eq.badmmc0b) -> tile
+      if constexpr (TC) {                                // the pass's MMAs have landed in TMEM
+        mbar_wait(&bar[2], mph);
+        mph ^= 1;
+        tc_fence_after();
+      }
 #pragma unroll
       for (int jb = 0; jb < NB; ++jb) {
         if (4 * jb >= mkw) break;
         T2 c2[4];
+        if constexpr (TC) {
+          // (|x'_i|^2 + |y'_j|^2, -2 x'_i . y'_j): row i of the warp's TMEM lanes, columns 4jb..4jb+3
+          uint32_t dv[4];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(dv[0]), "=r"(dv[1]), "=r"(dv[2]), "=r"(dv[3])
+                       : "r"(tm_d + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * warp + 4 * jb)));
+          const float4 yv = *reinterpret_cast<const float4*>(&yyb[4 * jb]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          c2[0] = PR::make(xx + (T)yv.x, (T)__uint_as_float(dv[0]));
+          c2[1] = PR::make(xx + (T)yv.y, (T)__uint_as_float(dv[1]));
+          c2[2] = PR::make(xx + (T)yv.z, (T)__uint_as_float(dv[2]));
+          c2[3] = PR::make(xx + (T)yv.w, (T)__uint_as_float(dv[3]));
+        } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) c2[u] = PR::make(xx, Ys[(4 * jb + u) * DY + YYI]);   // (|x|^2, |y|^2) + dot pairs
 #pragma unroll
@@ -442,6 +634,7 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               c2[u] = PR::fma(xn2[tt * (E / 2) + u2], reinterpret_cast<const T2*>(&v[u])[u2], c2[u]);
+        }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -477,8 +670,12 @@ k_badmm_tma(const IterArgs<T> a) {
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * jb + u, jt = j - ch * MP;
             const T v = (u & 1) ? p2[j / 2].y : p2[j / 2].x;
-            // swizzle ((lane / E) ^ (jt & 7)) * E + lane % E == lane ^ ((jt & 7) * E) (E a power of 2)
-            if (PAD || j < mkw) tile[jt * 32 + (lane ^ ((jt & 7) * E))] = v;   // P slot bound
+            if constexpr (TPAD) {
+              tile[jt * 36 + lane] = v;                // padded rows: immediate offsets, no conflicts
+            } else {
+              // swizzle ((lane / E) ^ (jt & 7)) * E + lane % E == lane ^ ((jt & 7) * E) (E a power of 2)
+              if (PAD || j < mkw) tile[jt * 32 + (lane ^ ((jt & 7) * E))] = v;   // P slot bound
+            }
           }
         }
         __syncwarp();
@@ -488,7 +685,8 @@ k_badmm_tma(const IterArgs<T> a) {
           T2 sp[MP / E];
 #pragma unroll
           for (int cc = 0; cc < MP / E; ++cc) {
-            const V v = *reinterpret_cast<const V*>(&tile[i * 32 + (((seg * (MP / E) + cc) * E) ^ ((i & 7) * E))]);
+            const V v = TPAD ? *reinterpret_cast<const V*>(&tile[i * 36 + cc * E])
+                             : *reinterpret_cast<const V*>(&tile[i * 32 + (((seg * (MP / E) + cc) * E) ^ ((i & 7) * E))]);
             const T2* v2 = reinterpret_cast<const T2*>(&v);
             sp[cc] = (E == 4) ? PR::add(v2[0], v2[(E == 4) ? 1 : 0]) : v2[0];
           }
@@ -590,12 +788,13 @@ k_badmm_tma(const IterArgs<T> a) {
     }
     if constexpr (PAD && !NOSTORE) {                   // an odd m_k's last column back to its
       if (mk & 1) {                                    // single-column layout for the store
+        T* const po = Ps + (mk - 1) * MP;              // (the lane wrote position 2i itself)
+        T* const lo = Ls + (mk - 1) * MP;
+        const T px = po[2 * i];
+        const T lx = (MODE != P1ONLY) ? lo[2 * i] : T(0);
         __syncwarp();
-        const T px = Ps[(mk - 1) * MP + 2 * i];
-        const T lx = (MODE != P1ONLY) ? Ls[(mk - 1) * MP + 2 * i] : T(0);
-        __syncwarp();
-        Ps[(mk - 1) * MP + i] = px;
-        if (MODE != P1ONLY) Ls[(mk - 1) * MP + i] = lx;
+        po[i] = px;
+        if (MODE != P1ONLY) lo[i] = lx;
       }
     }
     // results leave by bulk stores from the same slots
@@ -618,7 +817,7 @@ k_badmm_tma(const IterArgs<T> a) {
     cnp = nnp;
     cp0 = np0;
     cp1 = np1;
-    nnp = fnp;
+    nnp = fva ? (int)(fp1 - fp0) : 0;
     np0 = fp0;
     np1 = fp1;
   }
@@ -648,6 +847,15 @@ k_badmm_tma(const IterArgs<T> a) {
 #pragma unroll
       for (int h = MP; h < 32; h <<= 1) sx += __shfl_xor_sync(0xffffffffu, sx, h);
       if (seg == 0 && rowok && tt < d) px[tt] = sx;
+    }
+  }
+  if constexpr (TC) {                                  // every warp's last tcgen05.ld is complete
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_d));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tm_a));
     }
   }
 }

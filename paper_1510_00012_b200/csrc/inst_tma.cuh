@@ -7,12 +7,12 @@
 
 namespace ad2k {
 
-template <typename T, int MP, int NCH, int DP>
+template <typename T, int MP, int NCH, int DP, int TCC = 0>
 struct TmaLaunch {
   using Lay = TmaLayout<T, MP, NCH, DP>;
   template <int MODE>
   static void attr() {
-    cudaFuncSetAttribute(k_badmm_tma<T, MP, NCH, MODE, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_badmm_tma<T, MP, NCH, MODE, DP, TCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Lay::CTA_BYTES);
   }
   template <int MODE>
@@ -27,7 +27,7 @@ struct TmaLaunch {
     at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_badmm_tma<T, MP, NCH, MODE, DP>, a);
+    cudaLaunchKernelEx(&cfg, k_badmm_tma<T, MP, NCH, MODE, DP, TCC>, a);
   }
   static void run(int mode, const IterArgs<T>& a, int64_t n_items, cudaStream_t s) {
     static PerDevice once;                 // the smem attribute is per device
@@ -72,8 +72,17 @@ void launch_tma_impl(int variant, int mode, int nch, int dp, const IterArgs<T>& 
       return;
     }
   }
-  if (dp <= 4) TmaLaunch<T, MP, 1, 4>::run(mode, a, n_items, s);
-  else TmaLaunch<T, MP, 1, 16>::run(mode, a, n_items, s);
+  if (dp <= 4) {
+    TmaLaunch<T, MP, 1, 4>::run(mode, a, n_items, s);
+    return;
+  }
+  if constexpr (sizeof(T) == 4 && MP == 32) {
+    if (a.tc) {                                // tensor-core cost (single-member 32-row passes)
+      TmaLaunch<T, MP, 1, 16, 1>::run(mode, a, n_items, s);
+      return;
+    }
+  }
+  TmaLaunch<T, MP, 1, 16>::run(mode, a, n_items, s);
 }
 
 template <typename T>

@@ -15,12 +15,15 @@ ap.add_argument("--cfg", type=int, default=3)
 ap.add_argument("--N", type=int, default=None)
 ap.add_argument("--rounds", type=int, default=1)
 ap.add_argument("--state-mode", type=int, default=0)
+ap.add_argument("--tc", type=int, default=-1, help="ad2_set_tc_cost (1/0); -1: library default")
 args = ap.parse_args()
 b = wl.make_config(args.cfg, N=args.N)
 dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 D = [dev(a) for a in (b.offsets, b.supports, b.weights, b.labels, b.x0, b.w0)]
 ctx = ad2.Context(0, torch.cuda.current_stream().cuda_stream)
 ctx.set_state_mode(args.state_mode)
+if args.tc >= 0:
+    ctx.set_tc_cost(args.tc)
 s = b.sched
 for r in range(args.rounds):
     ctx.init(*D, b.K, b.m, s.rho0, s.eps, s.rule, dtype=b.dtype)

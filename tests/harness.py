@@ -21,7 +21,7 @@ def to_dev(b: wl.Bundle, torch):
 
 
 def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False, ctx=None, warm_mask=None,
-            x0=None, w0=None, profile=False, cost_mode=0, state_mode=0, eps=None):
+            x0=None, w0=None, profile=False, cost_mode=0, state_mode=0, eps=None, tc_cost=None):
     """Run one round of Alg. 4 on the GPU; returns (ctx, rho, objective)."""
     from paper_1510_00012_b200 import ad2
     torch = torch_cuda()
@@ -36,6 +36,8 @@ def run_gpu(b: wl.Bundle, T=None, tau=None, rule=None, mem="device", nccl=False,
     if profile:
         ctx.set_profiling(True)
     ctx.set_state_mode(state_mode)
+    if tc_cost is not None:
+        ctx.set_tc_cost(tc_cost)
     x0 = b.x0 if x0 is None else x0
     w0 = b.w0 if w0 is None else w0
     if mem == "device":
