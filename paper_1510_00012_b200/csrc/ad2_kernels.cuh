@@ -62,6 +62,7 @@ constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernel
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 constexpr int ITEM_PASSES = 8;    // member passes per warp per work item
+constexpr int CT_WORDS = 32 + 32 + 64 + 8;   // doubles per cluster of the 3 x TF32 cost build's centres
 
 // exp(v) is evaluated as ex(v * kx): kx = log2(e)/rho with MUFU ex2.approx for fp32,
 // kx = 1/rho with the IEEE double exp for fp64 (fp64 has no MUFU path).

@@ -188,14 +188,19 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
 namespace ad2k {
 
 // ---------------------------------------------------------------------------------------------
-// fp32-accurate tensor-core cost build: 3 x TF32 (tcgen05.mma kind::tf32).  Each operand is split
-// into hi = tf32(v) and lo = tf32(v - hi) (11 + 11 significant bits), and
-//   x . y = x_hi.y_hi + x_hi.y_lo + x_lo.y_hi   (+ x_lo.y_lo, ~2^-22 relative, dropped)
-// is accumulated in fp32 in TMEM: 24 MMAs (3 terms x K = 64 in steps of 8) per 128-point tile.
+// fp32-accurate tensor-core cost build: 3 x TF32 (tcgen05.mma kind::tf32).  The points are
+// centred on the cluster's mean centroid point o (k_cost_centre; C is translation invariant), each
+// operand is split into hi = tf32(v) and lo = tf32(v - hi) (11 + 11 significant bits), and
+//   x'.y' = x'_hi.y'_hi + x'_hi.y'_lo + x'_lo.y'_hi   (+ x'_lo.y'_lo, ~2^-22 relative, dropped)
+// is accumulated in fp32 in TMEM: 24 MMAs (3 terms x K = 64 in steps of 8) per 128-point tile;
+// C = |x'|^2 + |y'|^2 - 2 x'.y'.  The rho numerator (psum) is the closed form
+// sum_p (m |y'_p|^2 - 2 S.y'_p) + X2 in fp64 with exact operands, not a sum of the built C.
 // Operands are K-major with the 128-byte swizzle: a 64-element fp32 row spans two 128-byte
-// K-blocks, stored as two [rows][128 B] tiles.  Experimental (AD2_COST_TC32=1): measured on
-// config 4 the accumulation leaves ~2e-6 absolute error (C of coincident points ~1.7e-6), outside
-// the fp32 parity bar, so the FFMA2 tile kernel stays the cost_mode-0 default.
+// K-blocks, stored as two [rows][128 B] tiles.  Opt-in (AD2_COST_TC32=1): uncentred, the
+// accumulation's ~2^-20 relative error on |x||y| broke the 1e-5 plan parity on config 4's unit
+// vectors (round 1); centred with the closed-form rho, the whole GPU suite passes on it, but the
+// single-stage pipeline (2 CTAs per SM, loads -> MMA -> epilogue in sequence) takes 8.7 ms on
+// config 4 against 5.7 ms for the FFMA2 tile build.
 // ---------------------------------------------------------------------------------------------
 // instruction descriptor, kind::tf32: D fp32, A/B tf32 (format 2), K-major, N = 64, M = 128
 constexpr uint32_t TC32_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
@@ -214,10 +219,54 @@ __device__ __forceinline__ float tf32_rna(float v) {
   return __uint_as_float(u);
 }
 
+// Per-cluster centre for the 3 x TF32 build (one CTA of 64 threads per cluster c, d <= 64):
+//   o_c = mean of the m centroid points (fp32), S_k = sum_i (x_ik - o_k) and
+//   X2 = sum_i |x_i - o|^2 in fp64 (exact operands: fp32 differences are exact in fp64), and
+//   xx_i = |x_i - o|^2 in fp32 for the epilogue.  Layout of ct per cluster (CT_WORDS doubles):
+//   [o: 64 floats = 32 doubles | xx: 64 floats = 32 doubles | S: 64 doubles | X2: 1 double | pad]
+//   (CT_WORDS, ad2_kernels.cuh)
+__global__ void __launch_bounds__(64) k_cost_centre(const float* __restrict__ x, double* __restrict__ ct, int m, int d) {
+  const int c = blockIdx.x, k = threadIdx.x;
+  double* cc = ct + (size_t)c * CT_WORDS;
+  float* o = reinterpret_cast<float*>(cc);
+  float* xx = reinterpret_cast<float*>(cc + 32);
+  __shared__ float os[64];
+  __shared__ double x2s[64];
+  float ok = 0.f;
+  double s1 = 0.0, s2 = 0.0;
+  if (k < d) {
+    double sm = 0.0;
+    for (int i = 0; i < m; ++i) sm += (double)x[((int64_t)c * m + i) * d + k];
+    ok = (float)(sm / m);
+    for (int i = 0; i < m; ++i) {
+      const double v = (double)x[((int64_t)c * m + i) * d + k] - (double)ok;
+      s1 += v;
+      s2 = fma(v, v, s2);
+    }
+  }
+  os[k] = ok;
+  x2s[k] = s2;
+  o[k] = ok;
+  cc[64 + k] = s1;
+  __syncthreads();
+  if (k == 0) {
+    double t = 0.0;
+    for (int j = 0; j < 64; ++j) t += x2s[j];
+    cc[128] = t;
+  }
+  float sx = 0.f;                                     // row k: |x_k - o|^2 in fp32
+  if (k < m)
+    for (int j = 0; j < d; ++j) {
+      const float v = x[((int64_t)c * m + k) * d + j] - os[j];
+      sx = fmaf(v, v, sx);
+    }
+  xx[k] = sx;
+}
+
 __global__ void __launch_bounds__(128)
 k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
             const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
-            float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
+            const double* __restrict__ ct, float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // the 128-byte swizzle needs 1024-byte aligned atoms: align the dynamic region by hand
   unsigned char* tsm = reinterpret_cast<unsigned char*>(
@@ -226,7 +275,8 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
   unsigned char* sAl = tsm + 32768;
   unsigned char* sBh = tsm + 65536;                  // 64 x 64 fp32 = 16 KB each
   unsigned char* sBl = tsm + 81920;
-  __shared__ float xx[64], yy[128];
+  __shared__ float xx[64], yy[128], oc[64];
+  __shared__ double sxd[64], x2d[64];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ double red[4];
@@ -242,7 +292,18 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // B = x_c split into tf32 hi / lo (rows >= m and coordinates >= d are zero); |x_i|^2 in fp32
+  // the cluster's centre and fp64 sums (k_cost_centre)
+  {
+    const double* cc = ct + (size_t)c * CT_WORDS;
+    if (tid < 64) {
+      oc[tid] = reinterpret_cast<const float*>(cc)[tid];
+      xx[tid] = reinterpret_cast<const float*>(cc + 32)[tid];
+      sxd[tid] = cc[64 + tid];
+    }
+    if (tid == 0) x2d[0] = cc[128];
+  }
+  __syncthreads();
+  // B = x'_c split into tf32 hi / lo (rows >= m and coordinates >= d are zero); |x'_i|^2 in fp32
   for (int v = tid; v < 64 * 16; v += 128) {
     const int r = v >> 4, k0 = (v & 15) * 4;
     float4 h, l;
@@ -250,21 +311,14 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
     float* le = reinterpret_cast<float*>(&l);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const float val = (r < m && k0 + u < d) ? x[((int64_t)c * m + r) * d + k0 + u] : 0.f;
+      const float val = (r < m && k0 + u < d) ? x[((int64_t)c * m + r) * d + k0 + u] - oc[k0 + u] : 0.f;
       he[u] = tf32_rna(val);
       le[u] = tf32_rna(val - he[u]);
     }
     *reinterpret_cast<float4*>(sBh + tc32_off(64, r, k0)) = h;
     *reinterpret_cast<float4*>(sBl + tc32_off(64, r, k0)) = l;
   }
-  if (tid < 64) {
-    float s = 0.f;
-    for (int k = 0; k < d; ++k) {
-      const float v = tid < m ? x[((int64_t)c * m + tid) * d + k] : 0.f;
-      s = fmaf(v, v, s);
-    }
-    xx[tid] = s;
-  }
+  const double x2tot = x2d[0];                        // sum_i |x_i - o|^2 (fp64)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -279,11 +333,31 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
     for (int v = tid; v < 128 * 16; v += 128) {
       const int r = v >> 4, k0 = (v & 15) * 4;
       float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < np && k0 < d) f = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0
+      double q = 0.0;                                  // this chunk's part of sum_i |x_i - y_p|^2
+      if (r < np && k0 < d) {
+        const float4 y4 = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0
+        const float* ye = reinterpret_cast<const float*>(&y4);
+        float* fe = reinterpret_cast<float*>(&f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k0 + u < d) {
+            fe[u] = ye[u] - oc[k0 + u];
+            if (psum) {                                // fp64: m (y - o)^2 - 2 S_k (y - o), exact operands
+              const double yd = (double)ye[u] - (double)oc[k0 + u];
+              q = fma(yd, (double)m * yd - 2.0 * sxd[k0 + u], q);
+            }
+          }
+        }
+      }
       float s = fmaf(f.x, f.x, fmaf(f.y, f.y, fmaf(f.z, f.z, f.w * f.w)));
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if ((v & 15) == 0) yy[r] = s;
+      if (psum) {
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if ((v & 15) == 0 && r < np) acc += q + x2tot;   // rho numerator in closed form (fp64)
+      }
       const float4 h = make_float4(tf32_rna(f.x), tf32_rna(f.y), tf32_rna(f.z), tf32_rna(f.w));
       const float4 l = make_float4(tf32_rna(f.x - h.x), tf32_rna(f.y - h.y), tf32_rna(f.z - h.z), tf32_rna(f.w - h.w));
       *reinterpret_cast<float4*>(sAh + tc32_off(128, r, k0)) = h;
@@ -325,7 +399,6 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int p = 32 * warp + lane;
     const float yp = yy[p];
-    float s = 0.f;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       uint32_t r[32];
@@ -350,13 +423,11 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
             const int i = 32 * h + 4 * u + e;
             const float dot = __uint_as_float(r[4 * u + e]);
             o[e] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yp), 0.f) : 0.f;
-            s += o[e];
           }
           dst[u] = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
     }
-    acc += (double)s;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
   }

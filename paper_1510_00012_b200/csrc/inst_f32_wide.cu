@@ -82,15 +82,16 @@ void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, 
 
 // fp32-accurate 3 x TF32 tensor-core cost build (ld 64)
 void launch_cost_tc32(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
-                      float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
+                      double* ct, int K, float* Cc, double* psum, int m, int d, int dy, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
+  k_cost_centre<<<K, 64, 0, s>>>(x, ct, m, d);
   constexpr int SMEM = 98304 + 1024;             // + alignment slack
   static PerDevice once;
   if (once.first()) {
     cudaFuncSetAttribute(k_cost_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     once.done();
   }
-  k_cost_tc32<<<(unsigned)n_items, 128, SMEM, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy);
+  k_cost_tc32<<<(unsigned)n_items, 128, SMEM, s>>>(off, imb, icl, Y, x, ct, Cc, psum, m, d, dy);
 }
 
 void launch_cost_tile_big(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
