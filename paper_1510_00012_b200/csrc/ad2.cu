@@ -435,8 +435,8 @@ static ad2_status build_cost_T(ad2_ctx ctx, bool with_sum, cudaStream_t s) {
     }
     // cost_mode 0 = the fp32 FFMA2 tile build.  AD2_COST_TC32=1: the 3 x TF32 tensor-core build on
     // centred points (k_cost_tc32, rho's numerator in closed form in fp64) for 64-row blocks and
-    // 16 < d <= 64; it meets the fp32 parity bar (the whole GPU suite passes on it) but its
-    // single-stage pipeline is slower than the FFMA2 build on config 4 (8.7 vs 5.7 ms)
+    // 16 < d <= 64; it meets the fp32 parity bar (the whole GPU suite passes on it) and runs a
+    // config-4 round in the same time as the FFMA2 build (317.7 vs 318.6 ms)
     static const bool use_tc32 = getenv("AD2_COST_TC32") != nullptr;
     if (ctx->variant == 3 && ctx->ld == 64 && ctx->d > 16 && ctx->d <= 64 && use_tc32) {
       launch_cost_tc32(ctx->d_off.as<int64_t>(), ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>(),

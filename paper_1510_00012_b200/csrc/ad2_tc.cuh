@@ -199,8 +199,9 @@ namespace ad2k {
 // K-blocks, stored as two [rows][128 B] tiles.  Opt-in (AD2_COST_TC32=1): uncentred, the
 // accumulation's ~2^-20 relative error on |x||y| broke the 1e-5 plan parity on config 4's unit
 // vectors (round 1); centred with the closed-form rho, the whole GPU suite passes on it, but the
-// single-stage pipeline (2 CTAs per SM, loads -> MMA -> epilogue in sequence) takes 8.7 ms on
-// config 4 against 5.7 ms for the FFMA2 tile build.
+// single-stage pipeline (2 CTAs per SM, loads -> MMA -> epilogue in sequence) took 8.7 ms on
+// config 4; with the next tile's rows loaded into registers during the MMAs and the epilogue the
+// config-4 round is the same as with the FFMA2 tile build (317.7 vs 318.6 ms).
 // ---------------------------------------------------------------------------------------------
 // instruction descriptor, kind::tf32: D fp32, A/B tf32 (format 2), K-major, N = 64, M = 128
 constexpr uint32_t TC32_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
@@ -327,15 +328,30 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
   const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
   double acc = 0.0;
   uint32_t phase = 0;
+  // thread tid converts coordinates k0 .. k0+3 of tile rows tid/16 + 8 it (it < 16); the next
+  // tile's rows are loaded into registers while this tile's MMAs and epilogue run
+  const int kq = (tid & 15) * 4, rq = tid >> 4;
+  float4 yr[16];
+  auto load_tile = [&](int64_t qs) {
+    const int npn = (int)((p_end - qs) < 128 ? (p_end - qs) : 128);
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int r = rq + 8 * it;
+      yr[it] = (r < npn && kq < d) ? __ldg(reinterpret_cast<const float4*>(Y + (qs + r) * dy + kq))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);   // dy % 4 == 0
+    }
+  };
+  if (p_beg < p_end) load_tile(p_beg);
   for (int64_t q0 = p_beg; q0 < p_end; q0 += 128) {
     const int np = (int)((p_end - q0) < 128 ? (p_end - q0) : 128);
-    // A = Y tile split into tf32 hi / lo: 16 threads per point row, 4 coordinates each
-    for (int v = tid; v < 128 * 16; v += 128) {
-      const int r = v >> 4, k0 = (v & 15) * 4;
+    // A = Y' tile split into tf32 hi / lo: 16 threads per point row, 4 coordinates each
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int r = rq + 8 * it, k0 = kq;
       float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
       double q = 0.0;                                  // this chunk's part of sum_i |x_i - y_p|^2
       if (r < np && k0 < d) {
-        const float4 y4 = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0
+        const float4 y4 = yr[it];
         const float* ye = reinterpret_cast<const float*>(&y4);
         float* fe = reinterpret_cast<float*>(&f);
 #pragma unroll
@@ -352,11 +368,11 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
       float s = fmaf(f.x, f.x, fmaf(f.y, f.y, fmaf(f.z, f.z, f.w * f.w)));
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((v & 15) == 0) yy[r] = s;
+      if ((tid & 15) == 0) yy[r] = s;
       if (psum) {
 #pragma unroll
         for (int o = 8; o >= 1; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if ((v & 15) == 0 && r < np) acc += q + x2tot;   // rho numerator in closed form (fp64)
+        if ((tid & 15) == 0 && r < np) acc += q + x2tot;   // rho numerator in closed form (fp64)
       }
       const float4 h = make_float4(tf32_rna(f.x), tf32_rna(f.y), tf32_rna(f.z), tf32_rna(f.w));
       const float4 l = make_float4(tf32_rna(f.x - h.x), tf32_rna(f.y - h.y), tf32_rna(f.z - h.z), tf32_rna(f.w - h.w));
@@ -389,6 +405,7 @@ k_cost_tc32(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb
                        tc_smem(&mbar))
                    : "memory");
     }
+    if (q0 + 128 < p_end) load_tile(q0 + 128);       // in flight during the MMAs and the epilogue
     asm volatile(
         "{\n\t.reg .pred p;\nTW%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
