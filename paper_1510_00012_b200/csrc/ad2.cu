@@ -880,6 +880,17 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     const int64_t per_pass = variant == 3 ? (int64_t)wide_npair(wcfg) : (int64_t)NWARP * (32 / mp);
     const int64_t want = N / (per_pass * 6 * (int64_t)sms);          // >= ~6 CTAs per SM slot
     passes = (int)std::max<int64_t>(8, std::min<int64_t>(32, want));
+    if (variant == 2) {
+      // a small batch (config 2): the fewest passes per warp whose items still fit one wave of
+      // resident CTAs (3 per SM, register-bound), ~N / (per_pass p) + K items (each cluster's last
+      // item is partial).  A second, partial wave costs a whole pass time: measured on config 2,
+      // FUSED 22.5 us at 8 passes (313 items), 19.0 us at 6 (427), 24.9 / 23.2 / 20.5 us at 5 / 4 / 3
+      const int64_t slots = 3 * (int64_t)sms - K;
+      if (slots > 0) {
+        const int64_t p1 = (N + per_pass * slots - 1) / (per_pass * slots);
+        if (p1 < passes) passes = (int)std::max<int64_t>(1, p1);
+      }
+    }
     if (const char* e = getenv("AD2_PASSES")) passes = std::max(1, atoi(e));   // tuning knob (bench experiments)
   }
   per_item = variant == 3 ? (int64_t)wide_npair(wcfg) * passes

@@ -297,16 +297,6 @@ k_badmm_tma(const IterArgs<T> a) {
     p1 = a.off[k1];
     return (int)(p1 - p0);
   };
-  // the same, loads only: the size of pass t+2 is formed at the end of pass t, so the warp does
-  // not wait for the offsets' global-load latency at the start of a pass (in-order issue)
-  auto pass_raw = [&](int t, int64_t& p0, int64_t& p1) -> bool {
-    const int64_t k0 = mb + (int64_t)warp * G + (int64_t)t * step;
-    if (k0 >= me) return false;
-    const int64_t k1 = (k0 + G < me) ? k0 + G : me;
-    p0 = a.off[k0];
-    p1 = a.off[k1];
-    return true;
-  };
   // G == 1: the slots of a pass region hold ceil4(m_k) columns ([P | L | Y] at 0, MP*np4,
   // 2*MP*np4); the 0-3 padding columns of P and L are zeroed by the lanes, so the column blocks
   // of 4 need no masks and the stores no predicates.  G > 1: packed slots, masked blocks.
@@ -351,7 +341,7 @@ k_badmm_tma(const IterArgs<T> a) {
   for (int t = 0; cnp > 0; ++t) {
     // place pass t+1 behind pass t (or at the ring start) while t computes
     int64_t fp0 = 0, fp1 = 0;
-    const bool fva = pass_raw(t + 2, fp0, fp1);         // consumed next pass
+    const int fnp = pass_pts(t + 2, fp0, fp1);          // consumed next pass
     const int csize = (2 * MP + DY) * slot(cnp), nsize = (2 * MP + DY) * slot(nnp);
     int nbase = -1;
     if (nnp > 0) {
@@ -817,7 +807,7 @@ k_badmm_tma(const IterArgs<T> a) {
     cnp = nnp;
     cp0 = np0;
     cp1 = np1;
-    nnp = fva ? (int)(fp1 - fp0) : 0;
+    nnp = fnp;
     np0 = fp0;
     np1 = fp1;
   }
