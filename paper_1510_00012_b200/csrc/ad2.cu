@@ -383,8 +383,8 @@ static ad2_status consensus_T(ad2_ctx ctx, cudaStream_t s) {
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ctx->K);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = sh + 256 * sizeof(T);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = sh + 1024 * sizeof(T);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1267,7 +1267,8 @@ static ad2_status update_support_T(ad2_ctx ctx) {
       CHK(launch_check(ctx, "k_xpart"));
     }
   }
-  k_xsum<T><<<ctx->K, 256, 0, s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m, ctx->d, ctx->Sx.as<T>());
+  k_xsum<T><<<ctx->K, 1024, 1024 * sizeof(T), s>>>(ctx->px.as<T>(), ctx->d_cl_item.as<int64_t>(), ctx->parts, ctx->m,
+                                                  ctx->d, ctx->Sx.as<T>());
   CHK(launch_check(ctx, "k_xsum"));
   CHK(allreduce(ctx, ctx->Sx.p, (size_t)ctx->K * ctx->m * (ctx->d + 1), nccl_t(ctx), s));
   k_xfinal<T><<<ctx->K, 128, 0, s>>>(ctx->Sx.as<T>(), ctx->w.as<T>(), ctx->x.as<T>(), ctx->m, ctx->d);

@@ -224,6 +224,22 @@ k_badmm_generic(const IterArgs<T> a, T* __restrict__ scr, int64_t n_items) {
 // ---------------------------------------------------------------------------------------------
 // w consensus: S_i = sum over the cluster's items of pw; with `finalize` (single rank) also
 //   R1 (Eq.badmmw):  w_i = S_i / sum_i S_i          R2 (Eq.badmmw2): w_i = S_i^2 / sum_i S_i^2
+// sum over rows it0, it0 + st, it0 + 2 st, ... < ie of column i of a row-major [rows][w] array,
+// four independent accumulators (loads in flight together), combined in a fixed order
+template <typename T>
+__device__ __forceinline__ T slice_sum(const T* __restrict__ a, int64_t it0, int64_t ie, int st, int w, int i) {
+  T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+  int64_t it = it0;
+  for (; it + 3 * (int64_t)st < ie; it += 4 * (int64_t)st) {
+    s0 += a[it * w + i];
+    s1 += a[(it + st) * w + i];
+    s2 += a[(it + 2 * st) * w + i];
+    s3 += a[(it + 3 * st) * w + i];
+  }
+  for (; it < ie; it += st) s0 += a[it * w + i];
+  return (s0 + s1) + (s2 + s3);
+}
+
 template <typename T>
 __global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_item, int parts, int m,
                        T* __restrict__ S, T* __restrict__ w, int rule, int finalize, int* err) {
@@ -242,13 +258,18 @@ __global__ void k_wsum(const T* __restrict__ pw, const int64_t* __restrict__ cl_
   for (int i0 = 0; i0 < m; i0 += R) {
     const int i = i0 + r;
     T s = T(0);
-    if (sl < NS && i < m)
-      for (int64_t it = ib + sl; it < ie; it += NS) s += pw[it * m + i];
+    if (sl < NS && i < m) s = slice_sum(pw, ib + sl, ie, NS, m, i);
     red[threadIdx.x] = s;
     __syncthreads();
     if (sl == 0 && i < m) {
-      T t = T(0);
-      for (int u = 0; u < NS; ++u) t += red[u * R + r];
+      T t0 = T(0), t1 = T(0);
+      int u = 0;
+      for (; u + 1 < NS; u += 2) {
+        t0 += red[u * R + r];
+        t1 += red[(u + 1) * R + r];
+      }
+      if (u < NS) t0 += red[u * R + r];
+      const T t = t0 + t1;
       S[(int64_t)c * m + i] = t;
       sh[i] = (rule == 1) ? t * t : t;
     }
@@ -294,16 +315,36 @@ __global__ void k_wfinal(const T* __restrict__ S, T* __restrict__ w, int m, int 
 }
 
 // x partial sums -> Sx[K][m][d+1]
+// (as k_wsum: elements in passes of R = min(W, blockDim), S = blockDim / R slices of the partial
+// rows, slice sums added in slice order: deterministic for a fixed launch shape)
 template <typename T>
 __global__ void k_xsum(const T* __restrict__ px, const int64_t* __restrict__ cl_item, int parts, int m, int d,
                        T* __restrict__ Sx) {
+  extern __shared__ unsigned char smraw[];
+  T* red = reinterpret_cast<T*>(smraw);               // [blockDim]
   const int c = blockIdx.x;
   const int64_t ib = cl_item[c] * parts, ie = cl_item[c + 1] * parts;
   const int W = m * (d + 1);
-  for (int v = threadIdx.x; v < W; v += blockDim.x) {
+  const int R = W < (int)blockDim.x ? W : (int)blockDim.x;
+  const int NS = (int)blockDim.x / R;
+  const int r = threadIdx.x % R, sl = threadIdx.x / R;
+  for (int v0 = 0; v0 < W; v0 += R) {
+    const int v = v0 + r;
     T s = T(0);
-    for (int64_t it = ib; it < ie; ++it) s += px[it * W + v];
-    Sx[(int64_t)c * W + v] = s;
+    if (sl < NS && v < W) s = slice_sum(px, ib + sl, ie, NS, W, v);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (sl == 0 && v < W) {
+      T t0 = T(0), t1 = T(0);
+      int u = 0;
+      for (; u + 1 < NS; u += 2) {
+        t0 += red[u * R + r];
+        t1 += red[(u + 1) * R + r];
+      }
+      if (u < NS) t0 += red[u * R + r];
+      Sx[(int64_t)c * W + v] = t0 + t1;
+    }
+    __syncthreads();
   }
 }
 
