@@ -176,6 +176,27 @@ struct ad2_ctx_s {
   bool table = false;                // the current round uses AD2_COST_TABLE
 
   std::map<int, StepGraph*> graphs;  // key 2 n + (profiled)
+  uint64_t graph_sig = 0;            // signature() of the round the cached graphs were captured for
+  // Everything a captured step graph bakes in by value (shapes, scalars, device pointers, the
+  // communicator): an init that reproduces it keeps the graphs (no re-capture per round)
+  uint64_t signature() const {
+    uint64_t h = 1469598103934665603ull;
+    auto add = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    uint64_t eb;
+    memcpy(&eb, &eps, sizeof eb);
+    for (uint64_t v : {(uint64_t)dtype, (uint64_t)d, (uint64_t)m, (uint64_t)K, (uint64_t)rule, eb, (uint64_t)N,
+                       (uint64_t)n, (uint64_t)n_items, (uint64_t)variant, (uint64_t)mp, (uint64_t)nch, (uint64_t)dp,
+                       (uint64_t)wcfg, (uint64_t)cost_mode, (uint64_t)ld, (uint64_t)dy, (uint64_t)parts,
+                       (uint64_t)table, (uint64_t)tab_V, (uint64_t)nranks, (uint64_t)rank, (uint64_t)rho_in_gather,
+                       (uint64_t)(uintptr_t)comm, (uint64_t)(uintptr_t)grp, (uint64_t)(uintptr_t)hg_stage})
+      add(v);
+    for (const DBuf* b : {&agree_d, &gra, &gcb, &d_order, &d_off, &d_orig_off, &d_item_mb, &d_item_cl, &d_cl_item,
+                          &d_warm, &d_pos_of, &lay_cstart, &mem_cl, &pm, &xsum, &Y, &om, &P, &Q, &L, &Cc, &x, &w,
+                          &rho, &kx, &rho_d, &pw, &px, &Sw, &Sx, &pd, &Sd, &npts, &scr, &d_err, &tab, &ysym, &xsym,
+                          &cto})
+      add((uint64_t)(uintptr_t)b->p);
+    return h;
+  }
   int prof = 0;                      // 0 off, 1 every step, 2 the next step only (ad2_set_profiling)
   bool prof_pending = false;
   StepGraph* last_graph = nullptr;   // the most recent profiled step graph (ad2_prof_read)
@@ -905,7 +926,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   ctx->state = 0;
   ctx->fresh = false;
   ctx->pending = false;
-  ctx->clear_graphs();
+  // (the step graphs are dropped at the end unless the new round reproduces their signature)
   const int64_t old_N = ctx->N;
   const int old_ld = ctx->ld;
   const bool old_pair = pair_layout(ctx);     // layout of the previous round's Q (warm source)
@@ -1132,6 +1153,11 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     if (!(ctx->h_rho[c] > 0.0) || !std::isfinite(ctx->h_rho[c]))
       return ctx->fail(AD2_ERR_ZERO_RHO, "cluster %d: rho = %g", c, ctx->h_rho[c]);
   if (rho_out) memcpy(rho_out, ctx->h_rho.data(), sizeof(double) * K);
+  const uint64_t sig = ctx->signature();
+  if (sig != ctx->graph_sig) {
+    ctx->clear_graphs();
+    ctx->graph_sig = sig;
+  }
   ctx->state = 1;
   return AD2_OK;
   };

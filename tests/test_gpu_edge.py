@@ -10,6 +10,8 @@ closed form the paper fixes, through the C ABI:
   - the library state contract: an init that fails on its arguments leaves the previous
     round steppable; a warm start across a kernel-variant change reads the old Pi2 layout.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -177,3 +179,27 @@ def test_warm_start_across_a_kernel_variant_change(first_step, dtype):
                                    warm=wpi, warm_mask=warm[mem2])
         assert np.abs(w2[c] - r2.w).max() <= tw, np.abs(w2[c] - r2.w).max()
         assert_hybrid(x2[c], r2.x, tx, floor=1.0, what=f"x c{c}")
+
+
+@pytest.mark.parametrize("cfg,N", [(3, 1500), (4, 600)])
+def test_step_graphs_kept_across_identical_rounds(cfg, N):
+    """A context keeps its captured step graphs across an init that reproduces every shape, scalar
+    and device pointer they bake in (round after round of the same layout): a second round with the
+    same layout but other supports, weights and centroids matches a fresh context bit for bit and
+    the oracle; a round with another layout (recaptured) as well."""
+    b = wl.make_config(cfg, N=N)
+    rs = np.random.default_rng(5)
+    b2 = dataclasses.replace(
+        b, supports=(b.supports + 0.05 * rs.standard_normal(b.supports.shape)).astype(b.supports.dtype),
+        x0=(b.x0 + 0.05 * rs.standard_normal(b.x0.shape)).astype(b.x0.dtype))
+    ctx = run_gpu(b, 20, 10)[0]
+    ctx2 = run_gpu(b2, 20, 10, ctx=ctx)[0]
+    fresh = run_gpu(b2, 20, 10)[0]
+    for which in (ad2.PI1, ad2.LAMBDA):
+        np.testing.assert_array_equal(ctx2.plans(which), fresh.plans(which))
+    np.testing.assert_array_equal(ctx2.centroids()[0], fresh.centroids()[0])
+    compare_round(b2, T=20, tau=10, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False,
+                  ctx=ctx2)
+    b3 = wl.make_config(cfg, N=N + 37, seed=3)
+    compare_round(b3, T=20, tau=10, rtol_plan=None, rtol_x=1e-3, atol_w=1e-4, rtol_obj=1e-3, check_plans=False,
+                  ctx=ctx2)
