@@ -1183,21 +1183,23 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
   StepGraph* g = new StepGraph();
   cudaStream_t s = ctx->cap;
   const int64_t l0 = ctx->launches;
+  // n >= 2 with the deferred phase 2 (variant 2, and variant 3 with d <= 64): the last FUSED pass
+  // also forms the support-update partials (FUSEDX), so the step has n passes and no P2 pass;
+  // otherwise n + 1 passes ending with P2X / P2ONLY.  Phase 2 of the last iteration is then
+  // deferred to the next step's first (FUSED) pass.
+  static const bool no_fx = getenv("AD2_NO_FUSEDX") != nullptr;   // A/B knob (bench experiments)
+  // (variant 3: the support rows replace the consumed C in its slot, so they must fit: dy <= ld)
+  const bool fx = (ctx->variant == 2 || (ctx->variant == 3 && ctx->dy <= ctx->ld)) && p2x && n >= 2 && !no_fx;
   if (prof) {
-    g->ev.resize(2 * (size_t)(ctx->variant == 2 && p2x && n >= 2 && !getenv("AD2_NO_FUSEDX") ? n : n + 1));
+    g->ev.resize(2 * (size_t)(fx ? n : n + 1));
     for (auto& e : g->ev) CU(cudaEventCreate(&e));
   }
   CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ad2_status st = AD2_OK;
-  // 32-row blocks with n >= 2: the last FUSED pass also forms the support-update partials
-  // (FUSEDX), so the step has n passes and no P2 pass; otherwise n + 1 passes ending with P2X /
-  // P2ONLY.  Phase 2 of the last iteration is then deferred to the next step's first (FUSED) pass.
-  static const bool no_fx = getenv("AD2_NO_FUSEDX") != nullptr;   // A/B knob (bench experiments)
-  const bool fx = ctx->variant == 2 && p2x && n >= 2 && !no_fx;
   const int npass = fx ? n : n + 1;
   // compressed state (ad2_set_state_mode 1): the step's middle passes run from the epoch anchor
   // (GIN at the first pass that has a phase 2, GMID after it, GXOUT last), steps of >= 3
-  const bool gz = ctx->state_mode == 1 && fx && n >= 3;
+  const bool gz = ctx->state_mode == 1 && ctx->variant == 2 && fx && n >= 3;
   const int g0 = (fresh || !pending) ? 1 : 0;           // the GIN pass
   // programmatic dependent launches inside the step (variant 2 iteration kernel <-> k_wsum): not
   // across a collective (multi-rank) nor across the profiling event nodes

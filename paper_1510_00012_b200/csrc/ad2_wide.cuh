@@ -20,6 +20,9 @@
 //                Eq.updatex) -> Q = Pi2, L = Lambda, x-partials
 //   MODE P2X   : P2ONLY without the stores (the x partials only): the step's phase 2 stays deferred
 //                and the next step's first FUSED pass recomputes it (it reads no cost)
+//   MODE FUSEDX: FUSED + a sweep D forming the support-update partials of the Pi2 that the deferred
+//                phase 2 will produce, (pe + eps) / r2 with pe = Pi1 exp(Lambda/rho) (w_i cancels in
+//                Eq.updatex): the last pass of a step of n >= 2 iterations, so no P2 pass
 #pragma once
 #include "ad2_tma.cuh"
 
@@ -30,8 +33,8 @@ namespace ad2k {
 template <int WM, int MKX, int NPAIR, int RING_KB>
 struct WideLayout {
   static constexpr int RING = RING_KB * 1024 / 4;               // floats per group
-  // [ring | fbuf[MKX] | Rw[4] | 2 mbarriers]
-  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + MKX + 4) + 16) + 127) / 128 * 128;
+  // [ring | fbuf[MKX] | Rw[4] | 3 mbarriers (load pipeline; FUSEDX: the supports into the C slot)]
+  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + MKX + 4) + 24) + 127) / 128 * 128;   // + 3 mbarriers
   static constexpr size_t CTA_BYTES = NPAIR * PAIR_BYTES;
   static_assert(RING >= 3 * WM * MKX, "ring must hold the largest pass");
   static_assert(CTA_BYTES <= 227 * 1024, "shared memory");
@@ -79,9 +82,11 @@ k_badmm_wide(const IterArgs<float> a) {
   const float2 eps2 = make_float2(eps_r, eps_r);
   float accw = 0.f, accm = 0.f;
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);
-  float2 accx[PH2 ? DP / 2 : 1];                                  // coordinate pairs (FFMA2)
+  constexpr bool XP = (MODE == FUSEDX);                            // FUSED + the support-update partials
+  constexpr int FM = XP ? FUSED : MODE;                            // the mode the sweeps follow
+  float2 accx[(PH2 || XP) ? DP / 2 : 1];                           // coordinate pairs (FFMA2)
 #pragma unroll
-  for (int t = 0; t < (PH2 ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
+  for (int t = 0; t < ((PH2 || XP) ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
   bool bad = false;
   const float* src_plan = (MODE == P1ONLY) ? a.Q : a.P;
   float* dst_plan = (MODE == P2ONLY) ? a.Q : a.P;
@@ -89,6 +94,7 @@ k_badmm_wide(const IterArgs<float> a) {
   if (leader) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    if constexpr (MODE == FUSEDX) mbar_init(&bar[2], 1);
     fence_mbar_init();
   }
   group_sync<WM>(bar_id);
@@ -209,20 +215,30 @@ k_badmm_wide(const IterArgs<float> a) {
         float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
         const float2 cst = make_float2(Cs[e0], v1 ? Cs[e1] : 0.f);
         float2 q = p;                                                  // P1ONLY: Pi2^(0)
-        if constexpr (MODE == FUSED) {
+        if constexpr (FM == FUSED) {
           q = __ffma2_rn(__fmul2_rn(p, make_float2(N::ex(l.x), N::ex(l.y))), f2, ef2);
           l = __ffma2_rn(nrho2, q, __ffma2_rn(rho2, p, l));
         }
         const float2 ar = __ffma2_rn(cst, nkx2, make_float2(-l.x, -l.y));
         const float2 pt = __ffma2_rn(q, make_float2(N::ex(ar.x), N::ex(ar.y)), eps2);
         Ps[e0] = pt.x;
-        if (MODE == FUSED) Ls[e0] = l.x;
+        if (FM == FUSED) Ls[e0] = l.x;
         if (v1) {
           Ps[e1] = pt.y;
-          if (MODE == FUSED) Ls[e1] = l.y;
+          if (FM == FUSED) Ls[e1] = l.y;
         }
       }
+      if constexpr (XP) fence_proxy_async_smem();                       // the C slot's reads -> the async write below
       group_sync<WM>(bar_id);
+      if constexpr (XP) {
+        // C is consumed: the member's support rows (dy <= WM floats each) come into the C slot while
+        // the column sums and sweep C run, for sweep D below
+        if (leader) {
+          const uint32_t by = (uint32_t)(dy * mk * 4);
+          mbar_expect_tx(&bar[2], by);
+          tma_load(const_cast<float*>(Cs), a.Y + (int64_t)dy * cp0, by, &bar[2]);
+        }
+      }
       // ---- column sums over the 64 rows (Eq.badmmc0 denominators): lane jc reads its column in
       //      16 chunks of 4 rows, starting at chunk jc mod 16 (4 lanes per bank quad: no conflicts)
 #pragma unroll
@@ -274,6 +290,33 @@ k_badmm_wide(const IterArgs<float> a) {
         accw += (a.rule == 1) ? sqrtf(wt) : wt;
         bad |= !isfinite(wt);
       }
+      if constexpr (XP) {
+        // support-update partials of the Pi2 = (pe + eps) w_i / r2 that phase 2 of this iteration
+        // will form (Eq.badmmc1; w_i cancels in Eq.updatex, X5): per row sum_j (pe_ij + eps) y_j / r2
+        // and a count of 1, pe = Pi1 exp(Lambda/rho) re-read from the slots (the lane's own row);
+        // the support rows are broadcast 16-byte loads from the C slot
+        const float ir = rowok ? __fdividef(1.f, r2) : 0.f;
+        mbar_wait(&bar[2], (uint32_t)(t & 1));
+#pragma unroll 2
+        for (int j = 0; j < mk; ++j) {
+          const int e0 = j * WMP + ig;
+          const float q = fmaf(Ps[e0], N::ex(Ls[e0]), eps_r) * ir;
+          const float2 q2 = make_float2(q, q);
+          const float4* yj = reinterpret_cast<const float4*>(Cs + j * dy);
+#pragma unroll
+          for (int tt = 0; tt < DP / 4; ++tt) {
+            if (4 * tt < d) {
+              const float4 v = yj[tt];
+              accx[2 * tt + 0] = __ffma2_rn(q2, make_float2(v.x, v.y), accx[2 * tt + 0]);
+              accx[2 * tt + 1] = __ffma2_rn(q2, make_float2(v.z, v.w), accx[2 * tt + 1]);
+            }
+          }
+        }
+        if (rowok) accm += 1.f;
+        // the group's reads of the slot are done before the leader may load the next pass over it
+        fence_proxy_async_smem();
+        group_sync<WM>(bar_id);
+      }
     }
     // ---- results leave by bulk stores from the same slots
     if (leader) {
@@ -303,7 +346,8 @@ k_badmm_wide(const IterArgs<float> a) {
   const int64_t part = (int64_t)item * NPAIR + pair;
   if constexpr (!PH2) {
     if (rowok) a.pw[part * m + ig] = accw;
-  } else {
+  }
+  if constexpr (PH2 || XP) {
     if (rowok && !a.xext) {
       float* px = a.px + (part * m + ig) * (d + 1);
       px[d] = accm;
