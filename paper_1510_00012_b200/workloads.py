@@ -1,10 +1,14 @@
 """Seeded synthetic workloads for the B-ADMM barycenter path (shared by the oracle tests and the GPU path).
 
-This module holds NO arithmetic of the method (no cost matrix, no B-ADMM step, no rho):
-it only draws the ragged discrete distributions of BASELINE.json ``configs`` (recipes in
-SURVEY.md §8(d) and DESIGN.md "Input recipe") and the harness initialisation that
-precedes the centroid update (k-means++ on member means, random-member centroid with the
-paper's merge rule, §V).  The paper's own datasets are not available;
+This module holds none of the centroid update's arithmetic (no cost matrix, no B-ADMM step,
+no rho, no support update): it draws the ragged discrete distributions of BASELINE.json
+``configs`` (recipes in SURVEY.md §8(d) and DESIGN.md "Input recipe") and the harness
+initialisation that precedes the centroid update (k-means++ on member means, and a random
+member merged down to m points by the paper's merge rule, §V P:820-840 Eq.merge).
+That merge (``merge_to_size``) is the one piece of the paper's arithmetic here; it only produces
+the initial centroids x0 / w0 that the oracle and the GPU path both read, never a compared
+value (the oracle's own Eq.merge, ``oracle.merge``, and the device's ``ad2_merge_init`` are
+tested against each other separately).  The paper's own datasets are not available;
 these generators stand in for them (Table II is the shape model for
 config 5).
 
