@@ -1110,7 +1110,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     std::swap(ctx->P.p, ctx->Q.p);
     std::swap(ctx->P.cap, ctx->Q.cap);
     CU(ctx->P.reserve(es * EL));
-  } else if (ctx->variant == 2) {
+  } else if (ctx->variant == 2 || ctx->variant == 3) {
     ctx->fresh = true;              // cold round: the first step's P1INIT pass forms Pi2^0, Lambda = 0
   } else {
     if (b->dtype == AD2_F64) launch_init_plans<double>(ctx, false, ctx->Q.as<double>());

@@ -20,6 +20,8 @@
 //                Eq.updatex) -> Q = Pi2, L = Lambda, x-partials
 //   MODE P2X   : P2ONLY without the stores (the x partials only): the step's phase 2 stays deferred
 //                and the next step's first FUSED pass recomputes it (it reads no cost)
+//   MODE P1INIT: P1ONLY of a cold round with Pi2^0 = w_i w_j^(k) and Lambda = 0 formed in the sweep
+//                (only C is loaded; L = 0 is stored with Pi1): no k_init_plans pass
 //   MODE FUSEDX: FUSED + a sweep D forming the support-update partials of the Pi2 that the deferred
 //                phase 2 will produce, (pe + eps) / r2 with pe = Pi1 exp(Lambda/rho) (w_i cancels in
 //                Eq.updatex): the last pass of a step of n >= 2 iterations, so no P2 pass
@@ -83,6 +85,8 @@ k_badmm_wide(const IterArgs<float> a) {
   float accw = 0.f, accm = 0.f;
   constexpr bool PH2 = (MODE == P2ONLY || MODE == P2X);
   constexpr bool XP = (MODE == FUSEDX);                            // FUSED + the support-update partials
+  constexpr bool INIT = (MODE == P1INIT);                          // cold round's first pass: Pi2^0 = w_i w_j^(k), Lambda = 0
+  constexpr bool PH1 = (MODE == P1ONLY || INIT);
   constexpr int FM = XP ? FUSED : MODE;                            // the mode the sweeps follow
   float2 accx[(PH2 || XP) ? DP / 2 : 1];                           // coordinate pairs (FFMA2)
 #pragma unroll
@@ -112,9 +116,11 @@ k_badmm_wide(const IterArgs<float> a) {
   auto issue = [&](int t, int base, int64_t p0, int np) {          // leader only
     const uint32_t bp = (uint32_t)(WMP * np * 4), b3 = (uint32_t)(third * np * 4);
     float* st = ring + base;
-    mbar_expect_tx(&bar[t & 1], 2 * bp + b3);
-    tma_load(st, src_plan + (int64_t)WMP * p0, bp, &bar[t & 1]);
-    tma_load(st + WMP * np, a.L + (int64_t)WMP * p0, bp, &bar[t & 1]);
+    mbar_expect_tx(&bar[t & 1], INIT ? b3 : 2 * bp + b3);
+    if (!INIT) {                                                   // P1INIT forms P and L itself
+      tma_load(st, src_plan + (int64_t)WMP * p0, bp, &bar[t & 1]);
+      tma_load(st + WMP * np, a.L + (int64_t)WMP * p0, bp, &bar[t & 1]);
+    }
     if (PH2) {
       if (b3) tma_load(st + 2 * WMP * np, a.Y + (int64_t)dy * p0, b3, &bar[t & 1]);
     }
@@ -161,7 +167,7 @@ k_badmm_wide(const IterArgs<float> a) {
     // ---- sweep A (phase 2 of iteration t-1): row mass r = sum_j Pi1 exp(Lambda/rho) + m_k eps
     //      (Eq.badmmc1b; Lambda is stored pre-scaled, L' = Lambda kx, so exp(Lambda/rho) = ex(L'))
     float f = 0.f;
-    if constexpr (MODE != P1ONLY) {
+    if constexpr (!PH1) {
       float2 racc = make_float2(0.f, 0.f);
 #pragma unroll 4
       for (int j = 0; j < mk; j += 2) {
@@ -207,12 +213,20 @@ k_badmm_wide(const IterArgs<float> a) {
       // ---- sweep B: (FUSED) Pi2 = (Pi1 exp(Lambda/rho) + eps) f (Eq.badmmc1, pe recomputed),
       //      L' += kappa (Pi1 - Pi2) (Eq.badmm2); pt2 = Pi2 exp(-(C + Lambda)/rho) + eps
       //      (Eq.badmmc0b) = Pi2 ex(-(C kx + L')) + eps -> Ps
+      if constexpr (INIT) {                                            // w^(k)_j for sweep B (fbuf is free)
+#pragma unroll
+        for (int cj = 0; cj < (MKX + WM - 1) / WM; ++cj)
+          if (jc + cj * WM < mk) fbuf[jc + cj * WM] = om_jc[cj];
+        group_sync<WM>(bar_id);
+      }
 #pragma unroll 4
       for (int j = 0; j < mk; j += 2) {
         const bool v1 = j + 1 < mk;
         const int e0 = j * WMP + ig, e1 = e0 + WMP;
-        const float2 p = make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
-        float2 l = make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
+        // P1INIT: Pi2^0 = w_i w_j^(k), Lambda = 0; else Pi1 / Pi2 and Lambda from the slots
+        const float2 p = INIT ? make_float2(wi * fbuf[j], v1 ? wi * fbuf[j + 1] : 0.f)
+                              : make_float2(Ps[e0], v1 ? Ps[e1] : 0.f);
+        float2 l = INIT ? make_float2(0.f, 0.f) : make_float2(Ls[e0], v1 ? Ls[e1] : 0.f);
         const float2 cst = make_float2(Cs[e0], v1 ? Cs[e1] : 0.f);
         float2 q = p;                                                  // P1ONLY: Pi2^(0)
         if constexpr (FM == FUSED) {
@@ -222,10 +236,10 @@ k_badmm_wide(const IterArgs<float> a) {
         const float2 ar = __ffma2_rn(cst, nkx2, make_float2(-l.x, -l.y));
         const float2 pt = __ffma2_rn(q, make_float2(N::ex(ar.x), N::ex(ar.y)), eps2);
         Ps[e0] = pt.x;
-        if (FM == FUSED) Ls[e0] = l.x;
+        if (FM == FUSED || INIT) Ls[e0] = l.x;
         if (v1) {
           Ps[e1] = pt.y;
-          if (FM == FUSED) Ls[e1] = l.y;
+          if (FM == FUSED || INIT) Ls[e1] = l.y;
         }
       }
       if constexpr (XP) fence_proxy_async_smem();                       // the C slot's reads -> the async write below

@@ -20,6 +20,7 @@ static void go_wide(int mode, const IterArgs<float>& a, int64_t n_items, cudaStr
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P2X, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, FUSEDX, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
+    cudaFuncSetAttribute(k_badmm_wide<WM, MKX, NPAIR, RKB, P1INIT, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::CTA_BYTES);
     once.done();
   }
   dim3 g((unsigned)n_items), b(NPAIR * WM);
@@ -27,6 +28,7 @@ static void go_wide(int mode, const IterArgs<float>& a, int64_t n_items, cudaStr
   else if (mode == FUSED) k_badmm_wide<WM, MKX, NPAIR, RKB, FUSED, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else if (mode == P2X) k_badmm_wide<WM, MKX, NPAIR, RKB, P2X, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else if (mode == FUSEDX) k_badmm_wide<WM, MKX, NPAIR, RKB, FUSEDX, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
+  else if (mode == P1INIT) k_badmm_wide<WM, MKX, NPAIR, RKB, P1INIT, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
   else k_badmm_wide<WM, MKX, NPAIR, RKB, P2ONLY, DP><<<g, b, Lay::CTA_BYTES, s>>>(a);
 }
 
