@@ -82,6 +82,20 @@ def test_fp64_32_row_blocks_step_shapes(m, mk, d):
 
 # ------------------------------------------------------------------ fp32
 
+@pytest.mark.parametrize("m,mk,d", [(64, (20, 64), 64), (48, (1, 64), 24), (40, (5, 33), 64)])
+def test_fp32_warp_pair_step_shapes(m, mk, d):
+    """The cached-cost warp-pair kernel (variant 3): a cold round's P1INIT pass (Pi2^0, Lambda = 0
+    formed in the pass), steps of 2 and 3 ending with FUSEDX (support-update partials from the
+    supports staged into the consumed C slot, phase 2 deferred), a step of 1 (P2X), and the
+    deferred phase 2 stored on read-back, against the oracle (fp32 after a few iterations: plans
+    within 1e-4 relative, x within 1e-4, w within 1e-5)."""
+    b = wl.make_random(300, m, d, K=3, mk_range=mk, seed=300 + m + d, dtype="f32", T=1, tau=1, spread=2.0)
+    ctx, _ = compare_round(b, T=2, tau=2, rtol_plan=1e-4, rtol_x=1e-4, atol_w=1e-5)
+    assert ctx.info()["variant"] == 3, ctx.info()
+    compare_round(b, T=6, tau=3, rtol_plan=1e-4, rtol_x=1e-4, atol_w=1e-5, rtol_obj=1e-4)
+    compare_round(b, T=5, tau=2, rtol_plan=1e-4, rtol_x=1e-4, atol_w=1e-5, rtol_obj=1e-4)
+
+
 @pytest.mark.parametrize("cfg,N", [(2, 2000), (3, 2000), (5, 3000), (4, 1500)])
 def test_fp32_one_iteration(cfg, N):
     b = wl.make_config(cfg, N=N)
