@@ -902,6 +902,13 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     const int64_t want = N / (per_pass * 6 * (int64_t)sms);          // >= ~6 CTAs per SM slot
     passes = (int)std::max<int64_t>(8, std::min<int64_t>(32, want));
     if (variant == 2) {
+      // ~6 waves of the 3 resident CTAs per SM: fewer items mean less per-CTA set-up (ring
+      // zeroing, centroid loads), but a short last wave idles SMs (measured passes per warp on
+      // config 3: 8 / 12 / 16 / 24 / 32 / 48 -> 260 / 271 / 271 / 273 / 266 / 255 G entry-iter/s;
+      // config 5: 8 / 16 / 32 / 48 / 64 -> 261 / 273 / 280 / 282 / 282)
+      passes = (int)std::max<int64_t>(8, std::min<int64_t>(64, N / (per_pass * 6 * 3 * (int64_t)sms)));
+    }
+    if (variant == 2) {
       // a small batch (config 2): the fewest passes per warp whose items still fit one wave of
       // resident CTAs (3 per SM, register-bound), ~N / (per_pass p) + K items (each cluster's last
       // item is partial).  A second, partial wave costs a whole pass time: measured on config 2,
