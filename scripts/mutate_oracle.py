@@ -19,6 +19,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORC = "oracle/ad2_oracle.c"
 OT = "oracle/ad2_oracle_ot.c"
+SEED = "oracle/seed.py"
 
 # id: (file, old, new, occurrence (1-based), what it models)
 MUTATIONS = {
@@ -71,6 +72,23 @@ MUTATIONS = {
     "M25": (OT, "s += df * df;", "s += fabs(df);", 1, "W^2 cost not squared"),
     "M26": (OT, "x[bi * d + t] = (w[bi] * x[bi * d + t] + w[bj] * x[bj * d + t]) / wb;",
             "x[bi * d + t] = (x[bi * d + t] + x[bj * d + t]) / 2;", 1, "Eq.merge unweighted mean"),
+    # initial partition (oracle/seed.py, X20-X23)
+    "S1": (SEED, 'side="right"', 'side="left"', 1, "X20: D^2 draw on the prefix boundary (left)"),
+    "S2": (SEED, "d2 = np.minimum(d2, sq_dist(P, centres[c]))", "d2 = sq_dist(P, centres[c])", 1,
+           "D^2 to the newest centre only"),
+    "S3": (SEED, "acc = acc + diff * diff", "acc = acc + np.abs(diff)", 1, "distance not squared"),
+    "S4": (SEED, "return np.argmin(D, axis=1).astype(np.int32)",
+           "return (D.shape[1] - 1 - np.argmin(D[:, ::-1], axis=1)).astype(np.int32)", 1, "ties to the highest index"),
+    "S5": (SEED, "centres[cnt > 0, t] = s[cnt > 0] / cnt[cnt > 0]", "centres[cnt > 0, t] = s[cnt > 0] / cnt.sum()", 1,
+           "Lloyd centre divided by the wrong count"),
+    "S6": (SEED, "dist[counts[lab] <= 1] = -1.0", "", 1, "repair may empty a singleton cluster"),
+    "S7": (SEED, "k = int(np.argmax(dist))", "k = int(np.argmin(np.where(dist < 0, np.inf, dist)))", 1,
+           "repair takes the nearest member"),
+    "S8": (SEED, "mu[has] = mu[has] + om[idx, None] * Y[idx]", "mu[has] = mu[has] + Y[idx] / mk[has, None]", 1,
+           "unweighted member means"),
+    "S9": (SEED, "pick[c] = big[min(int(u[c] * len(big)), len(big) - 1)]", "pick[c] = big[0]", 1,
+           "X23: the draw ignored"),
+    "S10": (SEED, "centres[0] = P[min(int(u[0] * ns), ns - 1)]", "centres[0] = P[0]", 1, "X20: first draw ignored"),
 }
 
 
@@ -102,7 +120,7 @@ def run(ids):
             src = open(p).read()
             open(p, "w").write(mutate(src, old, new, occ))
             r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                                "tests/test_oracle_pins.py"] + [f"--deselect=tests/test_oracle_pins.py::{t}" for t in SELF_REFERENTIAL],
+                                "tests/test_oracle_pins.py", "tests/test_oracle_seed_pins.py"] + [f"--deselect=tests/test_oracle_pins.py::{t}" for t in SELF_REFERENTIAL],
                                cwd=tmp, capture_output=True, text=True)
             killed = r.returncode != 0
             first = ""
