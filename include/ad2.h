@@ -294,6 +294,36 @@ ad2_status ad2_prof_read(ad2_ctx ctx, double *launch_ms, int64_t capacity, int64
 ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch *batch, const int64_t *pick, void *x0_out, void *w0_out,
                           ad2_mem where);
 
+/* Initial partition.  Alg. 1 starts from "K random centroid[s]"
+ * and a labelling; the recipe is k-means++ on member means (the paper's own
+ * comparison method), every member labelled to its nearest mean, then per cluster a
+ * random member with >= m support points reduced by Eq.merge (ad2_merge_init).
+ * Every random draw is an argument; X20-X23 fix how a draw becomes an index.  All
+ * arithmetic is fp64 with fixed summation orders (ad2_seed.cu); synchronous; single-rank calls
+ * (a sharded job runs the seeding once and broadcasts the K*d centres).  Host batches are staged
+ * in the context's staging buffers, as for ad2_merge_init.
+ *
+ * ad2_kmeanspp: member means mean(P^(k)) = sum_j w_j y_j of the members sample[0..ns) (host int64,
+ * each in [0, N)), k-means++ D^2 seeding with the uniforms u[0..K) (host, each in [0, 1)): centre 0
+ * = sampled mean floor(u_0 ns), centre c = the first sampled mean whose prefix sum of D^2 exceeds
+ * u_c * sum D^2 (X20), then lloyd_iters Lloyd iterations (X21).  batch->K, d give the shapes
+ * (1 <= d <= 256, ns >= K); labels and m are ignored.  centres_out [K][d] fp64 in `where` memory.
+ * AD2_ERR_ARG on a bad shape, sample index or uniform. */
+ad2_status ad2_kmeanspp(ad2_ctx ctx, const ad2_batch *batch, const int64_t *sample, int64_t ns, const double *u,
+                        int32_t lloyd_iters, double *centres_out, ad2_mem where);
+/* ad2_label_nearest: every member's mean to its nearest centre (ties: lowest index, X21), then while
+ * a cluster is empty the lowest empty cluster takes the member farthest from its own centre among
+ * clusters with >= 2 members (lowest index on ties) and that member's mean becomes its centre
+ * (X22).  centres [K][d] fp64 in `where` memory (read), labels_out [N] int32 and centres_out
+ * [K][d] fp64 (the centres after the repair) in `where` memory.  Needs N >= K. */
+ad2_status ad2_label_nearest(ad2_ctx ctx, const ad2_batch *batch, const double *centres, int32_t *labels_out,
+                             double *centres_out, ad2_mem where);
+/* ad2_pick_members: per cluster c the member whose support initialises the centroid (X23): among
+ * c's members with m_k >= batch->m in index order the one at position floor(u_c * n_big) (u host
+ * double [K] in [0, 1)), else the first member of c with the largest m_k.  Needs batch->labels.
+ * pick_out host int64 [K] (feed it to ad2_merge_init).  AD2_ERR_EMPTY if a cluster has no member. */
+ad2_status ad2_pick_members(ad2_ctx ctx, const ad2_batch *batch, const double *u, int64_t *pick_out);
+
 /* The AD2 outer loop (Alg. 1, P:259-266 with Alg. 4 as the centroid update; SURVEY.md §8(f)
  * NEXT #2), on the device: the shard is staged once and stays on this GPU; each
  * round r = ad2_barycenter_init (round 0 cold; later rounds warm-start Pi^(2) for members whose

@@ -62,7 +62,8 @@ class Info(C.Structure):
 EXPORTS = ["ad2_create", "ad2_nccl_unique_id", "ad2_attach_nccl", "ad2_barycenter_init", "ad2_badmm_step",
            "ad2_update_support", "ad2_objective", "ad2_get_centroids", "ad2_get_plans", "ad2_get_rho",
            "ad2_get_info", "ad2_set_profiling", "ad2_prof_read", "ad2_assign", "ad2_assign_symbolic",
-           "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_prefetch", "ad2_sync",
+           "ad2_set_cost_table", "ad2_cluster", "ad2_merge_init", "ad2_kmeanspp", "ad2_label_nearest",
+           "ad2_pick_members", "ad2_prefetch", "ad2_sync",
            "ad2_set_state_mode", "ad2_set_tc_cost", "ad2_group_open", "ad2_group_allreduce", "ad2_attach_group", "ad2_group_close",
            "ad2_last_error",
            "ad2_status_string", "ad2_destroy"]
@@ -98,6 +99,9 @@ def load_library(path: str = LIB_PATH):
     L.ad2_cluster.argtypes = [p, C.POINTER(Batch), C.POINTER(Params), C.POINTER(Loop), p, p, p, C.POINTER(i32),
                               p, p]
     L.ad2_merge_init.argtypes = [p, C.POINTER(Batch), p, p, p, C.c_int]
+    L.ad2_kmeanspp.argtypes = [p, C.POINTER(Batch), p, i64, p, i32, p, C.c_int]
+    L.ad2_label_nearest.argtypes = [p, C.POINTER(Batch), p, p, p, C.c_int]
+    L.ad2_pick_members.argtypes = [p, C.POINTER(Batch), p, p]
     L.ad2_prefetch.argtypes = [p, C.POINTER(Batch), C.c_int]
     L.ad2_sync.argtypes = [p]
     L.ad2_last_error.argtypes = [p]
@@ -414,6 +418,45 @@ class Context:
         w0 = np.zeros((int(K), int(m)), ft)
         self._chk(self.L.ad2_merge_init(self.h, C.byref(b), pk.ctypes.data, x0.ctypes.data, w0.ctypes.data, HOST))
         return x0, w0
+
+    @staticmethod
+    def _seed_batch(offsets, supports, weights, labels, K, m, mem, dtype):
+        if dtype is None:
+            dtype = "f64" if str(getattr(weights, "dtype", "")) in ("float64", "torch.float64") else "f32"
+        return Batch(F64 if dtype == "f64" else F32, HOST if mem == "host" else DEVICE, int(supports.shape[1]),
+                     int(m), int(K), int(offsets.shape[0]) - 1, _ptr(offsets), _ptr(supports), _ptr(weights),
+                     _ptr(labels))
+
+    def kmeanspp(self, offsets, supports, weights, sample, u, lloyd_iters: int, mem: str = "device",
+                 dtype: Optional[str] = None):
+        """ad2_kmeanspp: k-means++ (X20) + Lloyd (X21) on the sampled member means; host centres [K][d]."""
+        u = np.ascontiguousarray(u, np.float64)
+        smp = np.ascontiguousarray(sample, np.int64)
+        b = self._seed_batch(offsets, supports, weights, None, len(u), 1, mem, dtype)
+        cen = np.zeros((len(u), b.d))
+        self._chk(self.L.ad2_kmeanspp(self.h, C.byref(b), smp.ctypes.data, len(smp), u.ctypes.data,
+                                      int(lloyd_iters), cen.ctypes.data, HOST))
+        return cen
+
+    def label_nearest(self, offsets, supports, weights, centres, mem: str = "device", dtype: Optional[str] = None):
+        """ad2_label_nearest: nearest-mean labels with the empty-cluster repair (X21, X22);
+        returns host (labels int32 [N], centres [K][d] after the repair)."""
+        cen = np.ascontiguousarray(centres, np.float64)
+        b = self._seed_batch(offsets, supports, weights, None, len(cen), 1, mem, dtype)
+        lab = np.zeros(b.n_members, np.int32)
+        out = np.zeros_like(cen)
+        self._chk(self.L.ad2_label_nearest(self.h, C.byref(b), cen.ctypes.data, lab.ctypes.data, out.ctypes.data,
+                                           HOST))
+        return lab, out
+
+    def pick_members(self, offsets, supports, weights, labels, m: int, u, mem: str = "device",
+                     dtype: Optional[str] = None):
+        """ad2_pick_members: the member per cluster whose support Eq.merge reduces (X23); host int64 [K]."""
+        u = np.ascontiguousarray(u, np.float64)
+        b = self._seed_batch(offsets, supports, weights, labels, len(u), m, mem, dtype)
+        pick = np.zeros(len(u), np.int64)
+        self._chk(self.L.ad2_pick_members(self.h, C.byref(b), u.ctypes.data, pick.ctypes.data))
+        return pick
 
     def sync(self):
         self._chk(self.L.ad2_sync(self.h))

@@ -168,6 +168,7 @@ struct ad2_ctx_s {
   // cross-round pruning of the loop's assignment: bounds u, l (W units) per member, certified mask,
   // the centroids of the last assignment, their drift, and the centroid "batch" layout
   DBuf el_u, el_lb, el_skip, el_xa, el_wa, el_drift, el_cnt, el_off, el_iota, el_lab;
+  DBuf sd_buf, sd_mu;                // initial partition (ad2_kmeanspp / ad2_label_nearest / ad2_pick_members)
   int64_t asg_certified = 0, asg_exact = 0;
   // symbolic supports: cost table D [V][V] (dtype tab_dtype), sorted member ids, centroid ids
   DBuf tab, ysym, xsym;
@@ -1894,6 +1895,198 @@ ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch* b, const int64_t* pick, 
   CU(cudaMemcpyAsync(x0_out, x0, es * (size_t)K * m * d, kind, s));
   CU(cudaMemcpyAsync(w0_out, w0, es * (size_t)K * m, kind, s));
   CU(cudaStreamSynchronize(s));
+  return AD2_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// initial partition (readings X20-X23): ad2_seed.cu
+// ------------------------------------------------------------------------------------------
+int seed_blk();
+void seed_means_launch(int f64, const int64_t* off, const void* Y, const void* W, const int64_t* idx, int64_t rows,
+                       int d, double* mu, cudaStream_t s);
+void seed_d2_launch(const double* P, int64_t ns, int d, const double* centre, int first, double* d2, double* bsum,
+                    cudaStream_t s);
+void seed_select_launch(const double* P, int64_t ns, int d, const double* d2, const double* bsum, double u,
+                        double* centre, int64_t* chosen, cudaStream_t s);
+void seed_nearest_launch(const double* P, int64_t n, int d, const double* cen, int K, int32_t* lab, int* counts,
+                         cudaStream_t s);
+void seed_lloyd_launch(const double* P, int64_t n, int d, const int32_t* lab, int K, double* cen, cudaStream_t s);
+size_t seed_far_scratch();
+void seed_repair_launch(const double* mu, int64_t N, int d, int32_t* lab, double* cen, int* counts, int c,
+                        void* scratch, cudaStream_t s);
+void seed_pick_launch(const int64_t* off, const int32_t* lab, int64_t N, int m, const double* u, int K, int64_t* pick,
+                      cudaStream_t s);
+
+// validate a batch for the partition calls and stage it (host batches) into the context;
+// *off/*Y/*W/*lab receive device pointers
+static ad2_status seed_stage(ad2_ctx ctx, const ad2_batch* b, const char* who, bool need_labels, const int64_t** off,
+                             const void** Y, const void** W, const int32_t** lab) {
+  if (!b) return ctx->fail(AD2_ERR_ARG, "%s: null batch", who);
+  if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "%s: dtype", who);
+  if (b->mem != AD2_DEVICE && b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "%s: mem", who);
+  if (b->d < 1 || b->d > 256 || b->K < 1 || b->n_members < 1 || !b->offsets || !b->supports || !b->weights ||
+      (need_labels && !b->labels))
+    return ctx->fail(AD2_ERR_ARG, "%s: shape (1 <= d <= 256, K >= 1, N >= 1) / batch arrays", who);
+  cudaStream_t s = ctx->stream;
+  const int64_t N = b->n_members;
+  const size_t es = b->dtype == AD2_F64 ? 8 : 4;
+  *off = static_cast<const int64_t*>(b->offsets);
+  *Y = b->supports;
+  *W = b->weights;
+  if (lab) *lab = static_cast<const int32_t*>(b->labels);
+  if (b->mem == AD2_HOST) {
+    const int64_t n = (*off)[N];
+    if ((*off)[0] != 0 || n < N) return ctx->fail(AD2_ERR_ARG, "%s: offsets", who);
+    CU(ctx->stage_off.reserve(sizeof(int64_t) * (N + 1)));
+    CU(ctx->stage_Y.reserve(es * (size_t)n * b->d));
+    CU(ctx->stage_W.reserve(es * (size_t)n));
+    CU(cudaMemcpyAsync(ctx->stage_off.p, b->offsets, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_Y.p, b->supports, es * (size_t)n * b->d, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->stage_W.p, b->weights, es * (size_t)n, cudaMemcpyHostToDevice, s));
+    *off = ctx->stage_off.as<int64_t>();
+    *Y = ctx->stage_Y.p;
+    *W = ctx->stage_W.p;
+    if (need_labels && lab) {
+      CU(ctx->stage_lab.reserve(sizeof(int32_t) * N));
+      CU(cudaMemcpyAsync(ctx->stage_lab.p, b->labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+      *lab = ctx->stage_lab.as<int32_t>();
+    }
+  }
+  return AD2_OK;
+}
+
+ad2_status ad2_kmeanspp(ad2_ctx ctx, const ad2_batch* b, const int64_t* sample, int64_t ns, const double* u,
+                        int32_t lloyd_iters, double* centres_out, ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!sample || !u || !centres_out || ns < 1 || lloyd_iters < 0)
+    return ctx->fail(AD2_ERR_ARG, "kmeanspp: null sample/u/centres_out, ns < 1 or lloyd_iters < 0");
+  if (where != AD2_DEVICE && where != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "where");
+  CHK(set_dev(ctx));
+  const int64_t* off;
+  const void *Y, *W;
+  CHK(seed_stage(ctx, b, "kmeanspp", false, &off, &Y, &W, nullptr));
+  const int64_t N = b->n_members;
+  const int d = b->d, K = b->K;
+  if (ns < K) return ctx->fail(AD2_ERR_ARG, "kmeanspp: ns = %lld < K = %d", (long long)ns, K);
+  for (int64_t r = 0; r < ns; ++r)
+    if (sample[r] < 0 || sample[r] >= N) return ctx->fail(AD2_ERR_ARG, "kmeanspp: sample[%lld] outside [0, N)", (long long)r);
+  for (int c = 0; c < K; ++c)
+    if (!(u[c] >= 0.0 && u[c] < 1.0)) return ctx->fail(AD2_ERR_ARG, "kmeanspp: u[%d] outside [0, 1)", c);
+  cudaStream_t s = ctx->stream;
+  const int64_t nb = (ns + seed_blk() - 1) / seed_blk();
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t o_idx = 0, o_P = o_idx + al(8 * ns), o_d2 = o_P + al(8 * (size_t)ns * d), o_bs = o_d2 + al(8 * ns),
+               o_cen = o_bs + al(8 * nb), o_lab = o_cen + al(8 * (size_t)K * d), o_ch = o_lab + al(4 * ns),
+               total = o_ch + 256;
+  CU(ctx->sd_buf.reserve(total));
+  char* base = static_cast<char*>(ctx->sd_buf.p);
+  int64_t* didx = reinterpret_cast<int64_t*>(base + o_idx);
+  double* P = reinterpret_cast<double*>(base + o_P);
+  double* d2 = reinterpret_cast<double*>(base + o_d2);
+  double* bsum = reinterpret_cast<double*>(base + o_bs);
+  double* cen = reinterpret_cast<double*>(base + o_cen);
+  int32_t* lab = reinterpret_cast<int32_t*>(base + o_lab);
+  int64_t* chosen = reinterpret_cast<int64_t*>(base + o_ch);
+  CU(cudaMemcpyAsync(didx, sample, 8 * ns, cudaMemcpyHostToDevice, s));
+  seed_means_launch(b->dtype == AD2_F64, off, Y, W, didx, ns, d, P, s);
+  CHK(launch_check(ctx, "k_member_means"));
+  // X20: the first centre is sample point floor(u_0 ns); then one D^2 draw per centre
+  int64_t i0 = (int64_t)(u[0] * (double)ns);
+  if (i0 > ns - 1) i0 = ns - 1;
+  CU(cudaMemcpyAsync(cen, P + i0 * d, 8 * (size_t)d, cudaMemcpyDeviceToDevice, s));
+  for (int c = 1; c < K; ++c) {
+    seed_d2_launch(P, ns, d, cen + (size_t)(c - 1) * d, c == 1, d2, bsum, s);
+    seed_select_launch(P, ns, d, d2, bsum, u[c], cen + (size_t)c * d, chosen, s);
+  }
+  CHK(launch_check(ctx, "k_d2_update / k_d2_select"));
+  for (int it = 0; it < lloyd_iters; ++it) {
+    seed_nearest_launch(P, ns, d, cen, K, lab, nullptr, s);
+    seed_lloyd_launch(P, ns, d, lab, K, cen, s);
+  }
+  CHK(launch_check(ctx, "k_nearest / k_lloyd_centres"));
+  CU(cudaMemcpyAsync(centres_out, cen, 8 * (size_t)K * d,
+                     where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return AD2_OK;
+}
+
+ad2_status ad2_label_nearest(ad2_ctx ctx, const ad2_batch* b, const double* centres, int32_t* labels_out,
+                             double* centres_out, ad2_mem where) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!centres || !labels_out || !centres_out) return ctx->fail(AD2_ERR_ARG, "label_nearest: null argument");
+  if (where != AD2_DEVICE && where != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "where");
+  CHK(set_dev(ctx));
+  const int64_t* off;
+  const void *Y, *W;
+  CHK(seed_stage(ctx, b, "label_nearest", false, &off, &Y, &W, nullptr));
+  const int64_t N = b->n_members;
+  const int d = b->d, K = b->K;
+  if (N < K) return ctx->fail(AD2_ERR_ARG, "label_nearest: N = %lld < K = %d (the repair needs a donor)", (long long)N, K);
+  cudaStream_t s = ctx->stream;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t o_cen = 0, o_lab = o_cen + al(8 * (size_t)K * d), o_cnt = o_lab + al(4 * (size_t)N),
+               o_far = o_cnt + al(4 * (size_t)K), total = o_far + al(seed_far_scratch());
+  CU(ctx->sd_buf.reserve(total));
+  CU(ctx->sd_mu.reserve(8 * (size_t)N * d));
+  char* base = static_cast<char*>(ctx->sd_buf.p);
+  double* cen = reinterpret_cast<double*>(base + o_cen);
+  int32_t* lab = reinterpret_cast<int32_t*>(base + o_lab);
+  int* cnt = reinterpret_cast<int*>(base + o_cnt);
+  double* mu = ctx->sd_mu.as<double>();
+  CU(cudaMemcpyAsync(cen, centres, 8 * (size_t)K * d,
+                     where == AD2_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemsetAsync(cnt, 0, 4 * (size_t)K, s));
+  seed_means_launch(b->dtype == AD2_F64, off, Y, W, nullptr, N, d, mu, s);
+  seed_nearest_launch(mu, N, d, cen, K, lab, cnt, s);
+  CHK(launch_check(ctx, "k_member_means / k_nearest"));
+  std::vector<int> hc(K);
+  CU(cudaMemcpyAsync(hc.data(), cnt, 4 * (size_t)K, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  // X22: the lowest empty cluster takes the farthest member of a cluster with >= 2 members
+  for (;;) {
+    int c = -1;
+    for (int e = 0; e < K; ++e)
+      if (hc[e] == 0) {
+        c = e;
+        break;
+      }
+    if (c < 0) break;
+    seed_repair_launch(mu, N, d, lab, cen, cnt, c, base + o_far, s);
+    CHK(launch_check(ctx, "k_far_blocks / k_repair_move"));
+    CU(cudaMemcpyAsync(hc.data(), cnt, 4 * (size_t)K, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  const cudaMemcpyKind kind = where == AD2_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(labels_out, lab, 4 * (size_t)N, kind, s));
+  CU(cudaMemcpyAsync(centres_out, cen, 8 * (size_t)K * d, kind, s));
+  CU(cudaStreamSynchronize(s));
+  return AD2_OK;
+}
+
+ad2_status ad2_pick_members(ad2_ctx ctx, const ad2_batch* b, const double* u, int64_t* pick_out) {
+  if (!ctx) return AD2_ERR_ARG;
+  if (!u || !pick_out) return ctx->fail(AD2_ERR_ARG, "pick_members: null argument");
+  CHK(set_dev(ctx));
+  const int64_t* off;
+  const void *Y, *W;
+  const int32_t* lab;
+  CHK(seed_stage(ctx, b, "pick_members", true, &off, &Y, &W, &lab));
+  const int64_t N = b->n_members;
+  const int K = b->K;
+  if (b->m < 1) return ctx->fail(AD2_ERR_ARG, "pick_members: m < 1");
+  for (int c = 0; c < K; ++c)
+    if (!(u[c] >= 0.0 && u[c] < 1.0)) return ctx->fail(AD2_ERR_ARG, "pick_members: u[%d] outside [0, 1)", c);
+  cudaStream_t s = ctx->stream;
+  CU(ctx->sd_buf.reserve(16 * (size_t)K + 256));
+  double* du = ctx->sd_buf.as<double>();
+  int64_t* dp = reinterpret_cast<int64_t*>(du + K);
+  CU(cudaMemcpyAsync(du, u, 8 * (size_t)K, cudaMemcpyHostToDevice, s));
+  seed_pick_launch(off, lab, N, b->m, du, K, dp, s);
+  CHK(launch_check(ctx, "k_pick_members"));
+  CU(cudaMemcpyAsync(pick_out, dp, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  for (int c = 0; c < K; ++c)
+    if (pick_out[c] < 0) return ctx->fail(AD2_ERR_EMPTY, "pick_members: cluster %d has no members", c);
   return AD2_OK;
 }
 
