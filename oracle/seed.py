@@ -97,6 +97,8 @@ def label_nearest(mu, centres):
     mu = np.asarray(mu, np.float64)
     centres = np.array(centres, np.float64)
     K = len(centres)
+    if len(mu) < K:
+        raise ValueError("label_nearest needs N >= K (X22: a donor cluster with >= 2 members)")
     lab = nearest(mu, centres)
     counts = np.bincount(lab, minlength=K)
     while (counts == 0).any():
