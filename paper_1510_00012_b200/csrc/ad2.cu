@@ -911,10 +911,11 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     }
     if (variant == 2) {
       // a small batch (config 2): the fewest passes per warp whose items still fit one wave of
-      // resident CTAs (3 per SM, register-bound), ~N / (per_pass p) + K items (each cluster's last
+      // resident CTAs (3 per SM, register-bound; 4 for the fp32 16-row small-d build), ~N / (per_pass p) + K items (each cluster's last
       // item is partial).  A second, partial wave costs a whole pass time: measured on config 2,
       // FUSED 22.5 us at 8 passes (313 items), 19.0 us at 6 (427), 24.9 / 23.2 / 20.5 us at 5 / 4 / 3
-      const int64_t slots = 3 * (int64_t)sms - K;
+      const int resident = (b->dtype == AD2_F32 && mp == 16 && nch == 1 && dp == 4) ? AD2_TMA_MINB16 : 3;
+      const int64_t slots = resident * (int64_t)sms - K;
       if (slots > 0) {
         const int64_t p1 = (N + per_pass * slots - 1) / (per_pass * slots);
         if (p1 < passes) passes = (int)std::max<int64_t>(1, p1);

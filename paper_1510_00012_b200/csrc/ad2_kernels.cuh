@@ -36,6 +36,10 @@ enum { P1ONLY = 0, FUSED = 1, P2ONLY = 2, P1INIT = 3, P2X = 4, FUSEDX = 5, GIN =
 enum { ERR_NONFINITE = 1, ERR_WEIGHTS = 2, ERR_EPSCOL = 16 };   // ERR_EPSCOL: a flag, not an error
 
 constexpr int NWARP = 4;          // warps per CTA in the warp-per-member kernels
+// resident CTAs per SM of the fp32 16-row single-chunk small-d variant-2 build (k_badmm_tma)
+#ifndef AD2_TMA_MINB16
+#define AD2_TMA_MINB16 4
+#endif
 
 // Checked build (python -m paper_1510_00012_b200.build --checked -> libad2_checked.so): device
 // assertions on the shared-memory ring placement and pass geometry of the staged kernels, a

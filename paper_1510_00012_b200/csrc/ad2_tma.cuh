@@ -138,8 +138,16 @@ template <> struct Pr<double> {
 // hi.lo, lo.hi over K = 16) into the warp's 32 TMEM columns; sweep 2 reads
 // D_ij = -2 x'_i . y'_j with tcgen05.ld and forms C_ij = |x'_i|^2 + |y'_j|^2 + D_ij (C is
 // translation invariant; centring keeps the products at the scale of C).
+// resident CTAs per SM the kernel is compiled for (register cap 65536 / (128 x this)): 4 for the
+// fp32 16-row single-chunk small-d passes (118-124 registers, no spill; a small batch such as
+// config 2 is latency-bound at 3 warps per scheduler), else 3 (the others would spill at 128)
+template <typename T, int MP, int NCH, int DP>
+constexpr int tma_min_blocks() {
+  return (sizeof(T) == 4 && MP == 16 && NCH == 1 && DP == 4) ? AD2_TMA_MINB16 : 3;
+}
+
 template <typename T, int MP, int NCH, int MODE, int DP, int TCC = 0>
-__global__ void __launch_bounds__(NWARP * 32, 3)
+__global__ void __launch_bounds__(NWARP * 32, (tma_min_blocks<T, MP, NCH, DP>()))
 k_badmm_tma(const IterArgs<T> a) {
   using N = Num<T>;
   using V = typename Vec16<T>::type;
