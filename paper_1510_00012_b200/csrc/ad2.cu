@@ -1138,9 +1138,11 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     cnts[K + c] = (double)hpts[c];
   }
   CU(cudaMemcpyAsync(ctx->npts.p, cnts.data(), sizeof(double) * 2 * K, cudaMemcpyHostToDevice, s));
-  CHK(allreduce(ctx, ctx->npts.p, 2 * (size_t)K, ncclFloat64, s));
-  CU(cudaMemcpyAsync(cnts.data(), ctx->npts.p, sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
+  if (multi(ctx)) {                 // one rank: the host counts are already the global ones (no sync)
+    CHK(allreduce(ctx, ctx->npts.p, 2 * (size_t)K, ncclFloat64, s));
+    CU(cudaMemcpyAsync(cnts.data(), ctx->npts.p, sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
   ctx->h_nmem.assign(cnts.begin(), cnts.begin() + K);
   for (int c = 0; c < K; ++c)
     if (cnts[c] == 0.0) return ctx->fail(AD2_ERR_EMPTY, "cluster %d has no members", c);
