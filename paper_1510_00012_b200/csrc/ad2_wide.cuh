@@ -373,90 +373,132 @@ k_badmm_wide(const IterArgs<float> a) {
 }
 
 // Cost build for the cached-C variants: C_ij = |x_i|^2 + |y_j|^2 - 2 x_i.y_j in fp32,
-// clamped at 0, for a 64 x 64 (rows x points) tile per step: X_c^T and a chunk of 64 points are
-// staged in shared memory, each thread accumulates a 4 x 4 register tile of dot products.
+// clamped at 0, for a 64 x 64 (rows x points) tile per step: X_c^T (coordinate-major) stays in
+// shared memory per row block; the points come in chunks of 64 rows (row-major, 16-byte cp.async,
+// coalesced) into two buffers, the next chunk landing while the current one computes; each thread
+// accumulates a 4 x 4 register tile of dot products over t = 0..d-1 in order (per 4 coordinates:
+// four 16-byte x loads of 4 rows, four broadcast 16-byte y loads of 4 points, 32 FFMA2).
 // Entries of rows >= m are written as 0.  With psum != nullptr the per-item double sum of C
 // (Eq.rho numerator) is formed in a fixed order.  One CTA (256 threads) per work item.
+template <int DMAX>
+struct CostTile {
+  static constexpr int YP = DMAX + 4;                  // row pitch of a staged point (floats)
+  static constexpr size_t XS = sizeof(float) * DMAX * 68;
+  static constexpr size_t YS = sizeof(float) * 64 * YP;
+  static constexpr size_t BYTES = XS + 2 * YS + sizeof(float) * (64 + 2 * 64);
+};
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int DMAX>
 __global__ void __launch_bounds__(256)
 k_cost_tile(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
             const int32_t* __restrict__ item_cl, const float* __restrict__ Y, const float* __restrict__ x,
             float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy, int ld) {
-  __shared__ __align__(16) float xs[DMAX][68];       // x_c^T (coordinate-major, padded rows)
-  __shared__ __align__(16) float ys[DMAX][68];       // chunk of 64 points, coordinate-major
-  __shared__ float xx[64], yy[64];
+  using L = CostTile<DMAX>;
+  constexpr int YP = L::YP;
+  extern __shared__ __align__(16) unsigned char ct_smem[];
+  float (*xs)[68] = reinterpret_cast<float (*)[68]>(ct_smem);                  // [DMAX][68]
+  float (*ysb)[64][YP] = reinterpret_cast<float (*)[64][YP]>(ct_smem + L::XS);  // [2][64][YP]
+  float* xx = reinterpret_cast<float*>(ct_smem + L::XS + 2 * L::YS);           // [64]
+  float* yyb = xx + 64;                                                        // [2][64]
   __shared__ double red[8];
   const int item = blockIdx.x;
   const int c = item_cl[item];
   const int tid = threadIdx.x;
   const int ti = tid & 15, tj = tid >> 4;              // rows 4ti..4ti+3, points 4tj..4tj+3
   const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
+  const int dpad = (d + 3) & ~3;                       // Y rows are zero-padded to dpad (= dy)
+  const int pieces = dpad >> 2;
+  auto load_chunk = [&](int buf, int64_t q0) {
+    const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
+    for (int v = tid; v < np * pieces; v += 256) {
+      const int j = v / pieces, k = v - j * pieces;
+      cp_async16(&ysb[buf][j][4 * k], Y + (q0 + j) * dy + 4 * k);
+    }
+    cp_async_commit();
+  };
   double acc = 0.0;
   for (int rb = 0; rb < ld; rb += 64) {                // row blocks of 64 (ld = 128 for m > 64)
-  __syncthreads();
-  for (int v = tid; v < DMAX * 64; v += 256) {
-    const int t = v >> 6, i = v & 63;
-    xs[t][i] = (rb + i < m && t < d) ? x[((int64_t)c * m + rb + i) * d + t] : 0.f;
-  }
-  __syncthreads();
-  if (tid < 64) {
-    float s = 0.f;
-    for (int t = 0; t < d; ++t) s = fmaf(xs[t][tid], xs[t][tid], s);
-    xx[tid] = s;
-  }
-  for (int64_t q0 = p_beg; q0 < p_end; q0 += 64) {
-    const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
-    __syncthreads();                                   // previous chunk consumed
+    __syncthreads();                                   // the previous row block's buffers are free
+    if (p_beg < p_end) load_chunk(0, p_beg);
     for (int v = tid; v < DMAX * 64; v += 256) {
-      const int j = v / DMAX, t = v - j * DMAX;
-      ys[t][j] = (j < np && t < d) ? Y[(q0 + j) * dy + t] : 0.f;
+      const int t = v >> 6, i = v & 63;
+      xs[t][i] = (rb + i < m && t < d) ? x[((int64_t)c * m + rb + i) * d + t] : 0.f;
     }
     __syncthreads();
     if (tid < 64) {
       float s = 0.f;
-      for (int t = 0; t < d; ++t) s = fmaf(ys[t][tid], ys[t][tid], s);
-      yy[tid] = s;
+      for (int t = 0; t < d; ++t) s = fmaf(xs[t][tid], xs[t][tid], s);
+      xx[tid] = s;
     }
-    float2 a2[2][4];                                   // rows (4ti, 4ti+1) and (4ti+2, 4ti+3) x 4 points
+    int buf = 0;
+    for (int64_t q0 = p_beg; q0 < p_end; q0 += 64, buf ^= 1) {
+      const int np = (int)((p_end - q0) < 64 ? (p_end - q0) : 64);
+      if (q0 + 64 < p_end) {                           // the next chunk lands while this one computes
+        load_chunk(buf ^ 1, q0 + 64);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();                                 // chunk `buf` visible to every thread
+      float (*ys)[YP] = ysb[buf];
+      float* yy = yyb + 64 * buf;
+      if (tid < 64) {
+        float s = 0.f;
+        for (int t = 0; t < d; ++t) s = fmaf(ys[tid][t], ys[tid][t], s);
+        yy[tid] = s;
+      }
+      float2 a2[2][4];                                 // rows (4ti, 4ti+1) and (4ti+2, 4ti+3) x 4 points
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) a2[u][v] = make_float2(0.f, 0.f);
-    const int dpad = (d + 3) & ~3;                     // coordinates >= d are zero in xs / ys
-#pragma unroll 4
-    for (int t = 0; t < dpad; ++t) {
-      const float4 xv = *reinterpret_cast<const float4*>(&xs[t][4 * ti]);
-      const float4 yv = *reinterpret_cast<const float4*>(&ys[t][4 * tj]);
-      const float2 x01 = make_float2(xv.x, xv.y), x23 = make_float2(xv.z, xv.w);
-      const float ya[4] = {yv.x, yv.y, yv.z, yv.w};
+        for (int v = 0; v < 4; ++v) a2[u][v] = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int t = 0; t < dpad; t += 4) {
+        float4 y4[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) y4[v] = *reinterpret_cast<const float4*>(&ys[4 * tj + v][t]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 xv = *reinterpret_cast<const float4*>(&xs[t + k][4 * ti]);
+          const float2 x01 = make_float2(xv.x, xv.y), x23 = make_float2(xv.z, xv.w);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float yk = k == 0 ? y4[v].x : (k == 1 ? y4[v].y : (k == 2 ? y4[v].z : y4[v].w));
+            const float2 yy2 = make_float2(yk, yk);
+            a2[0][v] = __ffma2_rn(x01, yy2, a2[0][v]);
+            a2[1][v] = __ffma2_rn(x23, yy2, a2[1][v]);
+          }
+        }
+      }
+      __syncthreads();                                 // yy ready; every read of ys[buf] done
+      float s = 0.f;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const float2 yy2 = make_float2(ya[v], ya[v]);
-        a2[0][v] = __ffma2_rn(x01, yy2, a2[0][v]);
-        a2[1][v] = __ffma2_rn(x23, yy2, a2[1][v]);
-      }
-    }
-    __syncthreads();                                   // yy ready
-    float s = 0.f;
+        const int j = 4 * tj + v;
+        if (j < np && rb + 4 * ti < ld) {
+          float4 o;
+          float* oe = reinterpret_cast<float*>(&o);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int j = 4 * tj + v;
-      if (j < np && rb + 4 * ti < ld) {
-        float4 o;
-        float* oe = reinterpret_cast<float*>(&o);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = rb + 4 * ti + u;
-          const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
-          const float cv = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i - rb] + yy[j]), 0.f) : 0.f;
-          oe[u] = cv;
-          s += cv;
+          for (int u = 0; u < 4; ++u) {
+            const int i = rb + 4 * ti + u;
+            const float dot = (u & 1) ? a2[u >> 1][v].y : a2[u >> 1][v].x;
+            const float cv = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i - rb] + yy[j]), 0.f) : 0.f;
+            oe[u] = cv;
+            s += cv;
+          }
+          *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + rb + 4 * ti) = o;
         }
-        *reinterpret_cast<float4*>(Cc + (q0 + j) * ld + rb + 4 * ti) = o;
       }
+      acc += (double)s;
     }
-    acc += (double)s;
-  }
   }
   if (psum) {
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -74,8 +74,16 @@ void launch_wide(int cfg, int mode, int d, const IterArgs<float>& a, int64_t n_i
 void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
                       float* Cc, double* psum, int m, int d, int dy, int ld, int64_t n_items, cudaStream_t s) {
   if (n_items == 0) return;
-  if (d <= 16) k_cost_tile<16><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
-  else k_cost_tile<64><<<(unsigned)n_items, 256, 0, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
+  static PerDevice once;                   // the smem attribute is per device
+  if (once.first()) {
+    cudaFuncSetAttribute(k_cost_tile<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CostTile<16>::BYTES);
+    cudaFuncSetAttribute(k_cost_tile<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CostTile<64>::BYTES);
+    once.done();
+  }
+  if (d <= 16)
+    k_cost_tile<16><<<(unsigned)n_items, 256, CostTile<16>::BYTES, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
+  else
+    k_cost_tile<64><<<(unsigned)n_items, 256, CostTile<64>::BYTES, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
 }
 
 void launch_cost_tc(const int64_t* off, const int64_t* imb, const int32_t* icl, const float* Y, const float* x,
