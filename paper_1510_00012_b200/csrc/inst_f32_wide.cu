@@ -80,6 +80,16 @@ void launch_cost_tile(const int64_t* off, const int64_t* imb, const int32_t* icl
     cudaFuncSetAttribute(k_cost_tile<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CostTile<64>::BYTES);
     once.done();
   }
+  static const bool tile4 = getenv("AD2_COST_TILE4") != nullptr;   // A/B knob: the 4 x 4 thread tiles
+  if (d > 16 && !tile4) {
+    static PerDevice once8;
+    if (once8.first()) {
+      cudaFuncSetAttribute(k_cost_tile8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CostTile8::BYTES);
+      once8.done();
+    }
+    k_cost_tile8<<<(unsigned)n_items, 128, CostTile8::BYTES, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
+    return;
+  }
   if (d <= 16)
     k_cost_tile<16><<<(unsigned)n_items, 256, CostTile<16>::BYTES, s>>>(off, imb, icl, Y, x, Cc, psum, m, d, dy, ld);
   else

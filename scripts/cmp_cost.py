@@ -1,5 +1,6 @@
 """Bit-compare the cached cost C (and one round's w, x) of two builds of libad2 on the same inputs:
-    python scripts/cmp_cost.py libad2.so libad2_old.so [cfg N K]"""
+    python scripts/cmp_cost.py libad2.so libad2_old.so [cfg N K]
+A library argument may carry environment settings: libad2.so:AD2_COST_TILE4=1"""
 import os
 import subprocess
 import sys
@@ -33,7 +34,9 @@ def main():
     out = []
     for k, lib in enumerate(libs):
         f = f"/tmp/cmp_cost_{k}.npz"
-        env = dict(os.environ, AD2_LIB=os.path.join(ROOT, "paper_1510_00012_b200", lib))
+        name, *kv = lib.split(":")
+        env = dict(os.environ, AD2_LIB=os.path.join(ROOT, "paper_1510_00012_b200", name))
+        env.update(dict(e.split("=", 1) for e in kv))
         r = subprocess.run([sys.executable, "-c", CHILD, ROOT, f] + cfg, env=env, capture_output=True, text=True)
         print(lib, r.stdout.strip(), r.stderr.strip()[-500:])
         out.append(np.load(f))
