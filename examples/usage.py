@@ -1,5 +1,5 @@
 """The README's usage example, runnable: one centroid update, the assignment step, the AD2 loop
-and the Eq.merge initialisation on a small seeded config-3 workload (needs a B200)."""
+and the initial partition (k-means++, nearest labels, member picks, Eq.merge) on a small seeded config-3 workload (needs a B200)."""
 import os
 import sys
 
@@ -27,7 +27,12 @@ res = ctx.cluster(dev(b.offsets), dev(b.supports), dev(b.weights), dev(b.labels)
                   b.K, b.m, T=50, tau=10, max_rounds=4, stop_frac=0.001)
 print("loop:", res["rounds"], "rounds, changed", np.round(res["changed"], 4))
 
-sizes = np.diff(b.offsets)
-pick = [int(np.nonzero((b.labels == c) & (sizes >= b.m))[0][0]) for c in range(b.K)]
+rng = np.random.default_rng(0)
+cen = ctx.kmeanspp(dev(b.offsets), dev(b.supports), dev(b.weights), rng.choice(b.N, 2000, replace=False),
+                   rng.uniform(size=b.K), 10)
+labels0, cen = ctx.label_nearest(dev(b.offsets), dev(b.supports), dev(b.weights), cen)
+print("initial partition: cluster sizes", np.bincount(labels0, minlength=b.K).min(), "..",
+      np.bincount(labels0, minlength=b.K).max())
+pick = ctx.pick_members(dev(b.offsets), dev(b.supports), dev(b.weights), dev(labels0), b.m, rng.uniform(size=b.K))
 x0, w0 = ctx.merge_init(dev(b.offsets), dev(b.supports), dev(b.weights), pick, b.K, b.m)
 print("merge init:", x0.shape, float(w0.sum(1).min()), float(w0.sum(1).max()))
