@@ -50,6 +50,7 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
           float* __restrict__ Cc, double* __restrict__ psum, int m, int d, int dy) {
   __shared__ __align__(1024) unsigned char sA[128 * 128];     // 16 KB, 16 atoms
   __shared__ __align__(1024) unsigned char sB[64 * 128];      // 8 KB
+  __shared__ __align__(16) float4 sO[4][32][8];                // per warp: 32 points x 32 costs (16 KB)
   __shared__ float xx[64], yy[128];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t mbar;
@@ -93,13 +94,29 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
   const int64_t p_beg = off[item_mb[item]], p_end = off[item_mb[item + 1]];
   double acc = 0.0;
   uint32_t phase = 0;
+  // the Y tile in fp32 registers: 16 threads per point row, 4 coordinates each (coalesced reads),
+  // all 16 loads of a thread issued before the first is consumed (memory-level parallelism; loading
+  // the next tile during the MMA and epilogue instead needs 156 registers, 3 CTAs per SM: slower)
+  float4 fv[16];
+  auto load_tile = [&](int64_t t0) {
+    const int n = (int)((p_end - t0) < 128 ? (p_end - t0) : 128);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int v = tid + 128 * u;
+      const int r = v >> 4, k0 = (v & 15) * 4;
+      fv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < n && k0 < d) fv[u] = *reinterpret_cast<const float4*>(Y + (t0 + r) * dy + k0);   // dy % 4 == 0, pad = 0
+    }
+  };
   for (int64_t q0 = p_beg; q0 < p_end; q0 += 128) {
     const int np = (int)((p_end - q0) < 128 ? (p_end - q0) : 128);
-    // A = Y tile in bf16: 16 threads per point row, 4 coordinates each (coalesced fp32 reads)
-    for (int v = tid; v < 128 * 16; v += 128) {
+    load_tile(q0);
+    // A = Y tile in bf16
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int v = tid + 128 * u;
       const int r = v >> 4, k0 = (v & 15) * 4;
-      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < np && k0 < d) f = *reinterpret_cast<const float4*>(Y + (q0 + r) * dy + k0);   // dy % 4 == 0, pad = 0
+      const float4 f = fv[u];
       float s = f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -152,8 +169,9 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
             "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // the point's 32 costs of this half into the warp's tile (16-byte chunk u at u ^ (p & 7):
+      // conflict-free), then the warp stores 4 points' 128-byte half rows per instruction
       if (p < np) {
-        float4* dst = reinterpret_cast<float4*>(Cc + (q0 + p) * 64 + 32 * h);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           float o[4];
@@ -164,9 +182,17 @@ k_cost_tc(const int64_t* __restrict__ off, const int64_t* __restrict__ item_mb,
             o[e] = (i < m) ? fmaxf(fmaf(-2.f, dot, xx[i] + yp), 0.f) : 0.f;
             s += o[e];
           }
-          dst[u] = make_float4(o[0], o[1], o[2], o[3]);
+          sO[warp][lane][u ^ (lane & 7)] = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int pl = 4 * k + (lane >> 3), u = lane & 7;     // point within the warp, chunk
+        if (32 * warp + pl < np)
+          reinterpret_cast<float4*>(Cc + (q0 + 32 * warp + pl) * 64 + 32 * h)[u] = sO[warp][pl][u ^ (pl & 7)];
+      }
+      __syncwarp();
     }
     acc += (double)s;
     // TMEM and the A tile are reused by the next tile

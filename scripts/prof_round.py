@@ -16,6 +16,7 @@ ap.add_argument("--N", type=int, default=None)
 ap.add_argument("--rounds", type=int, default=1)
 ap.add_argument("--state-mode", type=int, default=0)
 ap.add_argument("--tc", type=int, default=-1, help="ad2_set_tc_cost (1/0); -1: library default")
+ap.add_argument("--cost-mode", type=int, default=0, help="params cost_mode (1: bf16 tensor-core cost build)")
 args = ap.parse_args()
 b = wl.make_config(args.cfg, N=args.N)
 dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
@@ -26,7 +27,7 @@ if args.tc >= 0:
     ctx.set_tc_cost(args.tc)
 s = b.sched
 for r in range(args.rounds):
-    ctx.init(*D, b.K, b.m, s.rho0, s.eps, s.rule, dtype=b.dtype)
+    ctx.init(*D, b.K, b.m, s.rho0, s.eps, s.rule, dtype=b.dtype, cost_mode=args.cost_mode)
     ad2.run_schedule(ctx, s.T, s.tau)
     obj = ctx.objective()
 torch.cuda.synchronize()
