@@ -24,6 +24,7 @@
 #include "../../include/ad2.h"
 #include "ad2_group.h"
 #include "ad2_kernels.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace ad2k;
 
@@ -245,6 +246,14 @@ struct ad2_ctx_s {
     ad2_status s_ = (call);               \
     if (s_ != AD2_OK) return s_;          \
   } while (0)
+
+// NVTX range per ABI call (header-only NVTX v3: a no-op unless a profiler injects a handler), so
+// nsys / ncu --nvtx timelines show init / step / update_support / objective / assign / cluster
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define AD2_NVTX(name) NvtxRange ad2_nvtx_range_(name)
 
 static ad2_status launch_check(ad2_ctx ctx, const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -620,6 +629,7 @@ void ad2_destroy(ad2_ctx ctx) {
 }
 
 ad2_status ad2_prefetch(ad2_ctx ctx, const ad2_batch* b, ad2_cost_mode cost_mode) {
+  AD2_NVTX("ad2_prefetch");
   if (!ctx) return AD2_ERR_ARG;
   if (!b || b->mem != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "prefetch: needs a host batch");
   if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "prefetch: dtype");
@@ -1185,6 +1195,7 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
 
 ad2_status ad2_barycenter_init(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const void* x0,
                                const void* w0, const uint8_t* warm_mask, double* rho_out) {
+  AD2_NVTX("ad2_barycenter_init");
   return init_impl(ctx, b, prm, x0, w0, warm_mask, false, rho_out);
 }
 
@@ -1260,6 +1271,7 @@ static ad2_status capture_step(ad2_ctx ctx, int n, bool prof, bool fresh, bool p
 }
 
 ad2_status ad2_badmm_step(ad2_ctx ctx, int32_t n_iters) {
+  AD2_NVTX("ad2_badmm_step");
   if (!ctx) return AD2_ERR_ARG;
   if (n_iters < 0) return ctx->fail(AD2_ERR_ARG, "n_iters < 0");
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "step before init");
@@ -1316,6 +1328,7 @@ static ad2_status update_support_T(ad2_ctx ctx) {
 }
 
 ad2_status ad2_update_support(ad2_ctx ctx) {
+  AD2_NVTX("ad2_update_support");
   if (!ctx) return AD2_ERR_ARG;
   if (ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "update_support needs a step since init (X6)");
   if (ctx->table) return AD2_OK;      // symbolic supports are fixed: the update is skipped
@@ -1324,6 +1337,7 @@ ad2_status ad2_update_support(ad2_ctx ctx) {
 }
 
 ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
+  AD2_NVTX("ad2_objective");
   if (!ctx || !obj_out) return ctx ? ctx->fail(AD2_ERR_ARG, "null obj_out") : AD2_ERR_ARG;
   if (ctx->state < 2) return ctx->fail(AD2_ERR_STATE, "objective needs a step since init");
   CHK(set_dev(ctx));
@@ -1380,6 +1394,7 @@ static ad2_status materialise_phase2(ad2_ctx ctx) {
 }
 
 ad2_status ad2_get_plans(ad2_ctx ctx, int which, void* out, ad2_mem where) {
+  AD2_NVTX("ad2_get_plans");
   if (!ctx) return AD2_ERR_ARG;
   if (!out || which < 0 || which > 3) return ctx->fail(AD2_ERR_ARG, "get_plans args");
   if (ctx->state < 1) return ctx->fail(AD2_ERR_STATE, "no round");
@@ -1643,11 +1658,13 @@ static ad2_status assign_impl(ad2_ctx ctx, const ad2_batch* b, const void* x, co
 
 ad2_status ad2_assign(ad2_ctx ctx, const ad2_batch* b, const void* x, const void* w, int32_t* labels_out,
                       double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+  AD2_NVTX("ad2_assign");
   return assign_impl(ctx, b, x, w, labels_out, w2_out, where, n_exact_out, false);
 }
 
 ad2_status ad2_assign_symbolic(ad2_ctx ctx, const ad2_batch* b, const int32_t* xs, const void* w, int32_t* labels_out,
                                double* w2_out, ad2_mem where, int64_t* n_exact_out) {
+  AD2_NVTX("ad2_assign_symbolic");
   return assign_impl(ctx, b, xs, w, labels_out, w2_out, where, n_exact_out, true);
 }
 
@@ -1668,6 +1685,7 @@ static __global__ void k_label_diff(const int32_t* __restrict__ old_lab, const i
 ad2_status ad2_cluster(ad2_ctx ctx, const ad2_batch* b, const ad2_params* prm, const ad2_loop* loop,
                        const void* x0, const void* w0, int32_t* labels_out, int32_t* rounds_out, double* changed_out,
                        double* obj_out) {
+  AD2_NVTX("ad2_cluster");
   if (!ctx) return AD2_ERR_ARG;
   if (!b || !prm || !loop || !x0 || !w0) return ctx->fail(AD2_ERR_ARG, "cluster: null argument");
   if (loop->T < 1 || loop->tau < 1 || loop->max_rounds < 1 || !(loop->stop_frac >= 0.0))
@@ -1841,6 +1859,7 @@ void pick_sizes_launch(const int64_t* off, const int64_t* pick, int K, int64_t N
 
 ad2_status ad2_merge_init(ad2_ctx ctx, const ad2_batch* b, const int64_t* pick, void* x0_out, void* w0_out,
                           ad2_mem where) {
+  AD2_NVTX("ad2_merge_init");
   if (!ctx) return AD2_ERR_ARG;
   if (!b || !pick || !x0_out || !w0_out) return ctx->fail(AD2_ERR_ARG, "merge_init: null argument");
   if (b->dtype != AD2_F32 && b->dtype != AD2_F64) return ctx->fail(AD2_ERR_ARG, "dtype");
@@ -1960,6 +1979,7 @@ static ad2_status seed_stage(ad2_ctx ctx, const ad2_batch* b, const char* who, b
 
 ad2_status ad2_kmeanspp(ad2_ctx ctx, const ad2_batch* b, const int64_t* sample, int64_t ns, const double* u,
                         int32_t lloyd_iters, double* centres_out, ad2_mem where) {
+  AD2_NVTX("ad2_kmeanspp");
   if (!ctx) return AD2_ERR_ARG;
   if (!sample || !u || !centres_out || ns < 1 || lloyd_iters < 0)
     return ctx->fail(AD2_ERR_ARG, "kmeanspp: null sample/u/centres_out, ns < 1 or lloyd_iters < 0");
@@ -2015,6 +2035,7 @@ ad2_status ad2_kmeanspp(ad2_ctx ctx, const ad2_batch* b, const int64_t* sample, 
 
 ad2_status ad2_label_nearest(ad2_ctx ctx, const ad2_batch* b, const double* centres, int32_t* labels_out,
                              double* centres_out, ad2_mem where) {
+  AD2_NVTX("ad2_label_nearest");
   if (!ctx) return AD2_ERR_ARG;
   if (!centres || !labels_out || !centres_out) return ctx->fail(AD2_ERR_ARG, "label_nearest: null argument");
   if (where != AD2_DEVICE && where != AD2_HOST) return ctx->fail(AD2_ERR_ARG, "where");
@@ -2067,6 +2088,7 @@ ad2_status ad2_label_nearest(ad2_ctx ctx, const ad2_batch* b, const double* cent
 }
 
 ad2_status ad2_pick_members(ad2_ctx ctx, const ad2_batch* b, const double* u, int64_t* pick_out) {
+  AD2_NVTX("ad2_pick_members");
   if (!ctx) return AD2_ERR_ARG;
   if (!u || !pick_out) return ctx->fail(AD2_ERR_ARG, "pick_members: null argument");
   CHK(set_dev(ctx));
