@@ -131,3 +131,18 @@ def test_partition_argument_errors():
     with pytest.raises(ad2.AD2Error, match="EMPTY"):
         ctx.pick_members(*args, np.zeros(500, np.int32), b.m, np.full(5, 0.5), mem="host")
     ctx.close()
+
+
+def test_partition_edge_shapes():
+    """ns = K (every sampled mean becomes a centre), d = 256 (the largest d), one-point members."""
+    for d, N, K, ns in ((5, 400, 8, 8), (256, 300, 4, 40), (1, 500, 3, 3)):
+        rng = np.random.default_rng(100 + d)
+        sizes = rng.integers(1, 4, size=N) if d != 1 else np.ones(N, np.int64)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        Y = rng.normal(size=(off[-1], d)) * 3.0
+        Wf = np.concatenate([rng.dirichlet(np.ones(s)) for s in sizes])
+        b = wl.Bundle("edge", d, 2, K, off, Y, Wf, np.zeros(N, np.int32), np.zeros((K, 2, d)), np.zeros((K, 2)),
+                      "f64", None)
+        lab, pick = run_both(b, K, ns, iters=3, mem="host")
+        if ns == K:                                   # distinct means: every sampled mean is a centre
+            assert len(np.unique(lab)) == K
