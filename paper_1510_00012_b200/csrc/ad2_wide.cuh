@@ -35,8 +35,8 @@ namespace ad2k {
 template <int WM, int MKX, int NPAIR, int RING_KB>
 struct WideLayout {
   static constexpr int RING = RING_KB * 1024 / 4;               // floats per group
-  // [ring | fbuf[MKX] | Rw[4] | 3 mbarriers (load pipeline; FUSEDX: the supports into the C slot)]
-  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + MKX + 4) + 24) + 127) / 128 * 128;   // + 3 mbarriers
+  // [ring | fbuf[MKX] | Rw[4] | Rr[WM] | 3 mbarriers (load pipeline; FUSEDX: the supports into the C slot)]
+  static constexpr size_t PAIR_BYTES = ((4 * (size_t)(RING + MKX + 4 + WM) + 24) + 127) / 128 * 128;   // + 3 mbarriers
   static constexpr size_t CTA_BYTES = NPAIR * PAIR_BYTES;
   static_assert(RING >= 3 * WM * MKX, "ring must hold the largest pass");
   static_assert(CTA_BYTES <= 227 * 1024, "shared memory");
@@ -64,7 +64,8 @@ k_badmm_wide(const IterArgs<float> a) {
   float* const ring = reinterpret_cast<float*>(smem_raw + (size_t)pair * Lay::PAIR_BYTES);
   float* const fbuf = ring + RING;                                 // Eq.badmmc0 column factors
   float* const Rw = fbuf + WMK;                                    // per-warp row-mass totals
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(Rw + 4);
+  float* const Rr = Rw + 4;                                        // FUSEDX: 1 / row mass of every row
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(Rr + WM);
   const bool leader = (h == 0 && lane == 0);
   const int bar_id = 1 + pair;
   const int ig = 32 * h + lane;                                    // this lane's centroid row
@@ -288,6 +289,7 @@ k_badmm_wide(const IterArgs<float> a) {
         if (v1) Ps[e1] = p1.y;
       }
       const float r2 = (racc.x + racc.y) + (float)mk * eps_r;
+      if constexpr (XP) Rr[ig] = rowok ? __fdividef(1.f, r2) : 0.f;   // for sweep D (group-synced below)
       float R = r2;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
@@ -307,26 +309,44 @@ k_badmm_wide(const IterArgs<float> a) {
       if constexpr (XP) {
         // support-update partials of the Pi2 = (pe + eps) w_i / r2 that phase 2 of this iteration
         // will form (Eq.badmmc1; w_i cancels in Eq.updatex, X5): per row sum_j (pe_ij + eps) y_j / r2
-        // and a count of 1, pe = Pi1 exp(Lambda/rho) re-read from the slots (the lane's own row);
-        // the support rows are broadcast 16-byte loads from the C slot
-        const float ir = rowok ? __fdividef(1.f, r2) : 0.f;
+        // and a count of 1, pe = Pi1 exp(Lambda/rho) re-read from the slots.  Warp h of the group
+        // forms coordinates [h TS, (h + 1) TS) for every row 32 g + lane (g < GW), so each broadcast
+        // 16-byte load of a support row (four quarter-warp wavefronts) feeds GW rows; per (row,
+        // coordinate) the sum over j has the same order as with one row per lane (bit-identical)
+        constexpr int TS = DP / GW;
+        const int t0 = h * TS;
+        float irg[GW], epsg[GW];
+#pragma unroll
+        for (int g = 0; g < GW; ++g) {
+          irg[g] = Rr[32 * g + lane];
+          epsg[g] = (32 * g + lane < m) ? a.eps : 0.f;
+        }
         mbar_wait(&bar[2], (uint32_t)(t & 1));
 #pragma unroll 2
         for (int j = 0; j < mk; ++j) {
-          const int e0 = j * WMP + ig;
-          const float q = fmaf(Ps[e0], N::ex(Ls[e0]), eps_r) * ir;
-          const float2 q2 = make_float2(q, q);
-          const float4* yj = reinterpret_cast<const float4*>(Cs + j * dy);
+          float q[GW];
 #pragma unroll
-          for (int tt = 0; tt < DP / 4; ++tt) {
-            if (4 * tt < d) {
+          for (int g = 0; g < GW; ++g) {
+            const int e0 = j * WMP + 32 * g + lane;
+            q[g] = fmaf(Ps[e0], N::ex(Ls[e0]), epsg[g]) * irg[g];
+          }
+          const float4* yj = reinterpret_cast<const float4*>(Cs + j * dy + t0);
+#pragma unroll
+          for (int tt = 0; tt < TS / 4; ++tt) {
+            if (t0 + 4 * tt < d) {
               const float4 v = yj[tt];
-              accx[2 * tt + 0] = __ffma2_rn(q2, make_float2(v.x, v.y), accx[2 * tt + 0]);
-              accx[2 * tt + 1] = __ffma2_rn(q2, make_float2(v.z, v.w), accx[2 * tt + 1]);
+#pragma unroll
+              for (int g = 0; g < GW; ++g) {
+                const float2 q2 = make_float2(q[g], q[g]);
+                float2& a0 = accx[g * (TS / 2) + 2 * tt + 0];
+                float2& a1 = accx[g * (TS / 2) + 2 * tt + 1];
+                a0 = __ffma2_rn(q2, make_float2(v.x, v.y), a0);
+                a1 = __ffma2_rn(q2, make_float2(v.z, v.w), a1);
+              }
             }
           }
         }
-        if (rowok) accm += 1.f;
+        accm += 1.f;                                   // member passes (rows >= m are never written)
         // the group's reads of the slot are done before the leader may load the next pass over it
         fence_proxy_async_smem();
         group_sync<WM>(bar_id);
@@ -361,13 +381,29 @@ k_badmm_wide(const IterArgs<float> a) {
   if constexpr (!PH2) {
     if (rowok) a.pw[part * m + ig] = accw;
   }
-  if constexpr (PH2 || XP) {
+  if constexpr (PH2) {
     if (rowok && !a.xext) {
       float* px = a.px + (part * m + ig) * (d + 1);
       px[d] = accm;
 #pragma unroll
       for (int t = 0; t < DP; ++t)
         if (t < d) px[t] = (t & 1) ? accx[t / 2].y : accx[t / 2].x;
+    }
+  }
+  if constexpr (XP) {                                  // warp h: coordinates [h TS, (h + 1) TS) of every row
+    constexpr int TS = DP / GW;
+#pragma unroll
+    for (int g = 0; g < GW; ++g) {
+      const int row = 32 * g + lane;
+      if (row < m) {
+        float* px = a.px + (part * m + row) * (d + 1);
+        if (h == 0) px[d] = accm;
+#pragma unroll
+        for (int u = 0; u < TS; ++u) {
+          const int tc = h * TS + u;
+          if (tc < d) px[tc] = (u & 1) ? accx[g * (TS / 2) + u / 2].y : accx[g * (TS / 2) + u / 2].x;
+        }
+      }
     }
   }
 }
