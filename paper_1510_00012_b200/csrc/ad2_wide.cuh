@@ -28,6 +28,10 @@
 #pragma once
 #include "ad2_tma.cuh"
 
+#ifndef AD2_WIDE_XMMA
+#define AD2_WIDE_XMMA 1
+#endif
+
 namespace ad2k {
 
 // WM = rows of a member block (ld) = 32 x warps per member group; MKX = largest m_k; NPAIR groups
@@ -47,6 +51,21 @@ __device__ __forceinline__ void group_sync(int id) {
   if constexpr (WM == 128) asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
   else if constexpr (WM == 64) asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
   else __syncwarp();
+}
+
+// 3 x TF32 on the warp-level tensor-core MMA (mma.sync m16n8k8, fp32 accumulate): v = hi + lo with
+// hi = tf32(v), lo = tf32(v - hi); a.b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi (a_lo b_lo ~ 2^-22 dropped)
+__device__ __forceinline__ void tf32_split(float v, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
+  const float r = v - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 template <int WM, int MKX, int NPAIR, int RING_KB, int MODE, int DP>
@@ -90,6 +109,9 @@ k_badmm_wide(const IterArgs<float> a) {
   constexpr bool PH1 = (MODE == P1ONLY || INIT);
   constexpr int FM = XP ? FUSED : MODE;                            // the mode the sweeps follow
   float2 accx[(PH2 || XP) ? DP / 2 : 1];                           // coordinate pairs (FFMA2)
+  // FUSEDX of the 64-row pair with d <= 64: the partials on the tensor cores (3 x TF32 mma.sync)
+  constexpr bool XMMA = XP && WM == 64 && DP == 64 && AD2_WIDE_XMMA;
+  float* const xacc = reinterpret_cast<float*>(accx);            // XMMA: [2 row tiles][8 col tiles][4]
 #pragma unroll
   for (int t = 0; t < ((PH2 || XP) ? DP / 2 : 1); ++t) accx[t] = make_float2(0.f, 0.f);
   bool bad = false;
@@ -313,6 +335,59 @@ k_badmm_wide(const IterArgs<float> a) {
         // forms coordinates [h TS, (h + 1) TS) for every row 32 g + lane (g < GW), so each broadcast
         // 16-byte load of a support row (four quarter-warp wavefronts) feeds GW rows; per (row,
         // coordinate) the sum over j has the same order as with one row per lane (bit-identical)
+        if constexpr (XMMA) {
+          // X_part[r][t] += sum_j q_rj y_jt on the tensor cores: warp h owns rows [32h, 32h + 32)
+          // (two 16-row tiles) x 64 coordinates (eight 8-column tiles), K = the member's points in
+          // steps of 8; the A fragments q_rj are formed in place from the P / L slots, the B
+          // fragments are the support rows in the C slot (points >= m_k: q = 0 and y = 0)
+          const int gid = lane >> 2, tig = lane & 3;
+          float irr[2][2], epr[2][2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+              const int r = 32 * h + 16 * mt + gid + 8 * hr;
+              irr[mt][hr] = Rr[r];
+              epr[mt][hr] = r < m ? a.eps : 0.f;
+            }
+          mbar_wait(&bar[2], (uint32_t)(t & 1));
+          for (int k0 = 0; k0 < mk; k0 += 8) {
+            uint32_t ah[2][4], al[2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {            // a0 (gid, tig) a1 (gid+8, tig) a2 (gid, tig+4) a3 (gid+8, tig+4)
+                const int hr = e & 1, j = k0 + tig + 4 * (e >> 1);
+                const int r = 32 * h + 16 * mt + gid + 8 * hr;
+                float q = 0.f;
+                if (j < mk) {
+                  const int e0 = j * WMP + r;
+                  q = fmaf(Ps[e0], N::ex(Ls[e0]), epr[mt][hr]) * irr[mt][hr];
+                }
+                tf32_split(q, ah[mt][e], al[mt][e]);
+              }
+            const int j0 = k0 + tig, j1 = j0 + 4;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+              const int tc = 8 * nt + gid;
+              const float y0 = (j0 < mk && tc < dy) ? Cs[j0 * dy + tc] : 0.f;
+              const float y1 = (j1 < mk && tc < dy) ? Cs[j1 * dy + tc] : 0.f;
+              uint32_t bh0, bl0, bh1, bl1;
+              tf32_split(y0, bh0, bl0);
+              tf32_split(y1, bh1, bl1);
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) {
+                float* acc = xacc + (mt * 8 + nt) * 4;
+                mma_tf32(acc, ah[mt], bh0, bh1);
+                mma_tf32(acc, ah[mt], bl0, bl1);
+                mma_tf32(acc, al[mt], bh0, bh1);
+              }
+            }
+          }
+          accm += 1.f;
+          fence_proxy_async_smem();
+          group_sync<WM>(bar_id);
+        } else {
         constexpr int TS = DP / GW;
         const int t0 = h * TS;
         float irg[GW], epsg[GW];
@@ -350,6 +425,7 @@ k_badmm_wide(const IterArgs<float> a) {
         // the group's reads of the slot are done before the leader may load the next pass over it
         fence_proxy_async_smem();
         group_sync<WM>(bar_id);
+        }
       }
     }
     // ---- results leave by bulk stores from the same slots
@@ -390,7 +466,26 @@ k_badmm_wide(const IterArgs<float> a) {
         if (t < d) px[t] = (t & 1) ? accx[t / 2].y : accx[t / 2].x;
     }
   }
-  if constexpr (XP) {                                  // warp h: coordinates [h TS, (h + 1) TS) of every row
+  if constexpr (XMMA) {                                // C fragments: (gid, 2tig), (gid, 2tig+1), (gid+8, ..)
+    const int gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int row = 32 * h + 16 * mt + gid + 8 * hr;
+        if (row < m) {
+          float* px = a.px + (part * m + row) * (d + 1);
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int tc = 8 * nt + 2 * tig + e;
+              if (tc < d) px[tc] = xacc[(mt * 8 + nt) * 4 + 2 * hr + e];
+            }
+        }
+      }
+    if (32 * h + lane < m) a.px[(part * m + 32 * h + lane) * (d + 1) + d] = accm;
+  } else if constexpr (XP) {                           // warp h: coordinates [h TS, (h + 1) TS) of every row
     constexpr int TS = DP / GW;
 #pragma unroll
     for (int g = 0; g < GW; ++g) {
