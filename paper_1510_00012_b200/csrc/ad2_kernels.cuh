@@ -474,11 +474,21 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
   //  sums from k_xsums; fp32 inputs are exact in fp64)
   const double* xs = pm ? xsum + (int64_t)mem_cl[s] * (d + 1) : nullptr;
   double racc = 0.0;
-  for (int e = lane; e < mk * d; e += 32) {
-    const int j = e / d, t = e - j * d;
-    const T v = srcb[e];
-    dstb[(int64_t)j * dy + t] = v;
-    if (pm) racc += (double)v * fma((double)m, (double)v, -2.0 * xs[t]);
+  {
+    // element e = lane + 32 q of the block: (j, t) advanced incrementally (no integer division)
+    const int dj = 32 / d, dt = 32 % d;
+    int j = lane / d, t = lane - (lane / d) * d;
+    for (int e = lane; e < mk * d; e += 32) {
+      const T v = srcb[e];
+      dstb[(int64_t)j * dy + t] = v;
+      if (pm) racc += (double)v * fma((double)m, (double)v, -2.0 * xs[t]);
+      j += dj;
+      t += dt;
+      if (t >= d) {
+        t -= d;
+        ++j;
+      }
+    }
   }
   // zero padding and the |y|^2 column (sequential in t, like the oracle's sum): lane per point
   if (dy > d)
@@ -494,14 +504,18 @@ k_gather(const int32_t* __restrict__ order, const int64_t* __restrict__ src_off,
     for (int h = 16; h >= 1; h >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, h);
     if (lane == 0) pm[s] = (double)mk * xs[d] + racc;
   }
+  // weights: the simplex check (fp64, lane-strided then a butterfly) and the working-precision total
+  // in sequential order like the oracle (every lane adds the shuffled values j = 0, 1, ... in turn)
   double sum = 0.0;
-  for (int j = lane; j < mk; j += 32) sum += (double)Wsrc[so + j];
+  T tot = T(0);
+  for (int c0 = 0; c0 < mk; c0 += 32) {
+    const T wv = (c0 + lane < mk) ? Wsrc[so + c0 + lane] : T(0);
+    if (c0 + lane < mk) sum += (double)wv;
+    const int n = mk - c0 < 32 ? mk - c0 : 32;
+    for (int jj = 0; jj < n; ++jj) tot += __shfl_sync(0xffffffffu, wv, jj);
+  }
   for (int h = 16; h >= 1; h >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, h);
   if (lane == 0 && !(fabs(sum - 1.0) <= wtol)) atomicOr(err, ERR_WEIGHTS);
-  T tot = T(0);   // renormalise in the working precision, sequential order like the oracle
-  if (lane == 0)
-    for (int j = 0; j < mk; ++j) tot += Wsrc[so + j];
-  tot = __shfl_sync(0xffffffffu, tot, 0);
   for (int j = lane; j < mk; j += 32) om[dsto + j] = Wsrc[so + j] / tot;
 }
 
