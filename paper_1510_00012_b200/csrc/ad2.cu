@@ -146,6 +146,8 @@ struct ad2_ctx_s {
 
   // device buffers
   DBuf d_order, d_off, d_orig_off, d_item_mb, d_item_cl, d_cl_item, d_warm, d_pos_of;
+  DBuf d_perm;                       // CTA -> work item order of the iteration kernels (IterArgs::perm)
+  bool item_order = false;           // d_perm is used (launches of more than one wave of work items)
   DBuf d_off_old, d_pos_of_old;      // previous round's layout (warm starts)
   DBuf lay_keys, lay_keys2, lay_iota, lay_sz, lay_cnt, lay_pts, lay_cstart, lay_scal, lay_cub, lay_warm;
   DBuf stage_lab, mem_cl, pm, xsum;  // xsum: per-cluster sum x_i, sum |x_i|^2 (fp64, Eq.rho in k_gather)
@@ -190,9 +192,10 @@ struct ad2_ctx_s {
                        (uint64_t)n, (uint64_t)n_items, (uint64_t)variant, (uint64_t)mp, (uint64_t)nch, (uint64_t)dp,
                        (uint64_t)wcfg, (uint64_t)cost_mode, (uint64_t)ld, (uint64_t)dy, (uint64_t)parts,
                        (uint64_t)table, (uint64_t)tab_V, (uint64_t)nranks, (uint64_t)rank, (uint64_t)rho_in_gather,
-                       (uint64_t)(uintptr_t)comm, (uint64_t)(uintptr_t)grp, (uint64_t)(uintptr_t)hg_stage})
+                       (uint64_t)(uintptr_t)comm, (uint64_t)(uintptr_t)grp, (uint64_t)(uintptr_t)hg_stage,
+                       (uint64_t)item_order})
       add(v);
-    for (const DBuf* b : {&agree_d, &gra, &gcb, &d_order, &d_off, &d_orig_off, &d_item_mb, &d_item_cl, &d_cl_item,
+    for (const DBuf* b : {&agree_d, &gra, &gcb, &d_order, &d_off, &d_orig_off, &d_item_mb, &d_item_cl, &d_cl_item, &d_perm,
                           &d_warm, &d_pos_of, &lay_cstart, &mem_cl, &pm, &xsum, &Y, &om, &P, &Q, &L, &Cc, &x, &w,
                           &rho, &kx, &rho_d, &pw, &px, &Sw, &Sx, &pd, &Sd, &npts, &scr, &d_err, &tab, &ysym, &xsym,
                           &cto})
@@ -347,6 +350,9 @@ static IterArgs<T> iter_args(ad2_ctx ctx) {
   a.gs = ctx->cur_gs;
   a.pdl = ctx->cur_pdl ? 1 : 0;
   a.tc = ctx->tc_cost;
+  static const bool no_perm = getenv("AD2_NO_ITEM_ORDER") != nullptr;   // A/B knob (bench experiments)
+  a.perm = (no_perm || !ctx->item_order || (ctx->variant != 2 && ctx->variant != 3)) ? nullptr
+                                                                                      : ctx->d_perm.as<int32_t>();
   return a;
 }
 
@@ -997,6 +1003,34 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   n_items = (int64_t)hsc[2];
   CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
   CU(ctx->d_item_cl.reserve(sizeof(int32_t) * (n_items > 0 ? n_items : 1)));
+  {
+    // CTA order of the iteration kernels: every cluster's full items in index order, then the
+    // partial last items largest first, so the short items fill the launch's last wave
+    std::vector<int32_t> perm;
+    perm.reserve((size_t)n_items);
+    std::vector<std::pair<int64_t, int32_t>> part;
+    int64_t it0 = 0;
+    for (int c = 0; c < K; ++c) {
+      const int64_t nc = (int64_t)hcnt[c], ni = (nc + per_item - 1) / per_item;
+      for (int64_t q = 0; q < ni; ++q) {
+        const int64_t sz = std::min<int64_t>(per_item, nc - q * per_item);
+        if (sz == per_item) perm.push_back((int32_t)(it0 + q));
+        else part.push_back({sz, (int32_t)(it0 + q)});
+      }
+      it0 += ni;
+    }
+    std::stable_sort(part.begin(), part.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (const auto& pq : part) perm.push_back(pq.second);
+    if ((int64_t)perm.size() != n_items) return ctx->fail(AD2_ERR_STATE, "work-item order: %zu of %lld items",
+                                                          perm.size(), (long long)n_items);
+    CU(ctx->d_perm.reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(n_items, 1)));
+    if (n_items > 0)
+      CU(cudaMemcpyAsync(ctx->d_perm.p, perm.data(), sizeof(int32_t) * (size_t)n_items, cudaMemcpyHostToDevice, s));
+    // a launch of one wave gains nothing from the order (measured: config 2, 1 % slower with it)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    ctx->item_order = n_items > 4 * (int64_t)sms;
+  }
   k_layout_items_fill<<<K, 128, 0, s>>>(ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), K, per_item, N,
                                         ctx->d_item_mb.as<int64_t>(), ctx->d_item_cl.as<int32_t>());
   CHK(launch_check(ctx, "k_layout_items_fill"));

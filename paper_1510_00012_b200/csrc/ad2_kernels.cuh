@@ -129,6 +129,8 @@ struct IterArgs {
   int pdl;                 // host: launch with programmatic stream serialization (the kernel pdl_wait()s)
   int tc;                  // host: variant 2 with 32-row single-member passes and 4 < d <= 16 takes the
                            // tensor-core cost instantiation (ad2_set_tc_cost)
+  const int32_t* perm;     // [n_items] work item of each CTA (full items first, then each cluster's
+                           // partial last item, largest first: small items fill the launch's tail)
 };
 
 // 16-byte vectors of the element type (shared-memory tiles, staged rows)

@@ -172,7 +172,7 @@ k_badmm_tma(const IterArgs<T> a) {
   // load (p = Lambda = 0) and contribute exactly 0 to every sum: row masses are formed as
   // sum_j p_j e_j + m_k eps (= sum over the m_k real columns of (p_j e_j + eps)).
   const int seg = lane / MP, i = lane - seg * MP;
-  const int item = blockIdx.x;
+  const int item = a.perm ? a.perm[blockIdx.x] : (int)blockIdx.x;
   const int c = a.item_cl[item];
   const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
   const int m = a.m, d = a.d;

@@ -88,7 +88,7 @@ k_badmm_wide(const IterArgs<float> a) {
   const bool leader = (h == 0 && lane == 0);
   const int bar_id = 1 + pair;
   const int ig = 32 * h + lane;                                    // this lane's centroid row
-  const int item = blockIdx.x;
+  const int item = a.perm ? a.perm[blockIdx.x] : (int)blockIdx.x;
   const int c = a.item_cl[item];
   const int64_t mb = a.item_mb[item], me = a.item_mb[item + 1];
   const int m = a.m, d = a.d;
