@@ -119,6 +119,8 @@ struct ad2_ctx_s {
   ad2_group grp = nullptr;           // host process group (borrowed; ad2_attach_group)
   std::map<std::pair<void*, size_t>, HostSum*> host_sums;
   void* hg_stage = nullptr;          // pinned host staging of the group collectives
+  void* hpin = nullptr;              // pinned host buffer of init's read-backs (one synchronisation each)
+  size_t hpin_cap = 0;
   size_t hg_cap = 0;
   DBuf agree_d;
   int nranks = 1, rank = 0;
@@ -211,6 +213,7 @@ struct ad2_ctx_s {
     clear_graphs();
     for (auto& kv : host_sums) delete kv.second;
     if (hg_stage) cudaFreeHost(hg_stage);
+    if (hpin) cudaFreeHost(hpin);
     if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
     if (cap) cudaStreamDestroy(cap);
     if (pfs) {
@@ -269,6 +272,22 @@ static ad2_status launch_check(ad2_ctx ctx, const char* what) {
 static bool multi(ad2_ctx ctx) { return ctx->comm != nullptr || ctx->grp != nullptr; }
 
 // the pinned staging of the group collectives, grown outside graph capture only (init)
+// pinned host memory for small read-backs: copies into it are truly asynchronous, so several of
+// them share one stream synchronisation (a copy into pageable memory waits on its own)
+static ad2_status hpin_reserve(ad2_ctx ctx, size_t bytes) {
+  if (bytes <= ctx->hpin_cap) return AD2_OK;
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  ctx->hpin = nullptr;
+  ctx->hpin_cap = 0;
+  const size_t b = std::max<size_t>(bytes, 4096);
+  if (cudaMallocHost(&ctx->hpin, b) != cudaSuccess) {
+    ctx->hpin = nullptr;
+    return ctx->fail(AD2_ERR_OOM, "cudaMallocHost(%zu)", b);
+  }
+  ctx->hpin_cap = b;
+  return AD2_OK;
+}
+
 static ad2_status host_stage_reserve(ad2_ctx ctx, size_t bytes) {
   if (!ctx->grp || bytes <= ctx->hg_cap) return AD2_OK;
   CU(cudaStreamSynchronize(ctx->stream));          // no queued collective still uses the old buffer
@@ -846,13 +865,28 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
         off_in, lab_in, N, K, ctx->lay_keys.as<int32_t>(), ctx->lay_iota.as<int32_t>(),
         ctx->lay_cnt.as<unsigned long long>(), ctx->lay_pts.as<unsigned long long>(), scal);
     CHK(launch_check(ctx, "k_layout_hist"));
+    // flags, n and the per-cluster member / point counts (the work-item layout needs them):
+    // one synchronisation through pinned memory
     unsigned long long hs[2] = {0, 0};
-    CU(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(&n, off_in + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CHK(hpin_reserve(ctx, 32 + 16 * (size_t)K));
+    char* hp = static_cast<char*>(ctx->hpin);
+    CU(cudaMemcpyAsync(hp, scal, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hp + 16, off_in + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hp + 32, ctx->lay_cnt.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hp + 32 + 8 * (size_t)K, ctx->lay_pts.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    memcpy(hs, hp, sizeof hs);
+    memcpy(&n, hp + 16, sizeof(int64_t));
+    hcnt.assign(reinterpret_cast<unsigned long long*>(hp + 32), reinterpret_cast<unsigned long long*>(hp + 32) + K);
+    hpts.assign(reinterpret_cast<unsigned long long*>(hp + 32 + 8 * (size_t)K),
+                reinterpret_cast<unsigned long long*>(hp + 32 + 8 * (size_t)K) + K);
     if (hs[0] & 1) return ctx->fail(AD2_ERR_ARG, "offsets[0] != 0");
     if (hs[0] & 2) return ctx->fail(AD2_ERR_ARG, "a member has m_k < 1 or a label outside [0,%d)", K);
     mkmax = (int64_t)hs[1];
+  }
+  if (N == 0) {
+    hcnt.assign(K, 0);
+    hpts.assign(K, 0);
   }
   warm = warm_mask != nullptr && N > 0;
   if (warm) {
@@ -993,14 +1027,9 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
   k_layout_items_count<<<1, 1, 0, s>>>(ctx->lay_cnt.as<unsigned long long>(), K, per_item,
                                        ctx->lay_cstart.as<int64_t>(), ctx->d_cl_item.as<int64_t>(), scal);
   CHK(launch_check(ctx, "k_layout_items_count"));
-  hcnt.assign(K, 0);
-  hpts.assign(K, 0);
-  unsigned long long hsc[3] = {0, 0, 0};
-  CU(cudaMemcpyAsync(hcnt.data(), ctx->lay_cnt.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(hpts.data(), ctx->lay_pts.p, 8 * (size_t)K, cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(hsc, scal, sizeof hsc, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  n_items = (int64_t)hsc[2];
+  // the counts came back with the validation read-back: the item count is the device's formula
+  n_items = 0;
+  for (int c = 0; c < K; ++c) n_items += ((int64_t)hcnt[c] + per_item - 1) / per_item;
   CU(ctx->d_item_mb.reserve(sizeof(int64_t) * (n_items + 1)));
   CU(ctx->d_item_cl.reserve(sizeof(int32_t) * (n_items > 0 ? n_items : 1)));
   {
@@ -1201,9 +1230,10 @@ static ad2_status init_impl(ad2_ctx ctx, const ad2_batch* b, const ad2_params* p
     k_rho<float><<<(K + 127) / 128, 128, 0, s>>>(ctx->Sd.as<double>(), ctx->npts.as<double>() + K, K, m, prm->rho0,
                                                 ctx->rho.as<float>(), ctx->kx.as<float>(), ctx->rho_d.as<double>());
   CHK(launch_check(ctx, "k_rho"));
-  ctx->h_rho.assign(K, 0.0);
-  CU(cudaMemcpyAsync(ctx->h_rho.data(), ctx->rho_d.p, sizeof(double) * K, cudaMemcpyDeviceToHost, s));
+  CHK(hpin_reserve(ctx, sizeof(double) * (size_t)K));
+  CU(cudaMemcpyAsync(ctx->hpin, ctx->rho_d.p, sizeof(double) * K, cudaMemcpyDeviceToHost, s));
   CHK(agree(ctx, read_err(ctx)));              // weights off the simplex are detected per rank
+  ctx->h_rho.assign(static_cast<double*>(ctx->hpin), static_cast<double*>(ctx->hpin) + K);   // read_err synchronised
   for (int c = 0; c < K; ++c)
     if (!(ctx->h_rho[c] > 0.0) || !std::isfinite(ctx->h_rho[c]))
       return ctx->fail(AD2_ERR_ZERO_RHO, "cluster %d: rho = %g", c, ctx->h_rho[c]);
