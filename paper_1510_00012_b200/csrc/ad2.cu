@@ -1429,9 +1429,10 @@ ad2_status ad2_objective(ad2_ctx ctx, double* obj_out) {
     CHK(launch_check(ctx, "k_objective"));
   }
   CHK(cluster_dsum(ctx, s));
-  std::vector<double> S(ctx->K);
-  CU(cudaMemcpyAsync(S.data(), ctx->Sd.p, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, s));
+  CHK(hpin_reserve(ctx, sizeof(double) * (size_t)ctx->K));   // pinned: shares read_err's synchronisation
+  CU(cudaMemcpyAsync(ctx->hpin, ctx->Sd.p, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, s));
   CHK(agree(ctx, read_err(ctx)));               // a non-finite value on one rank fails every rank
+  const double* S = static_cast<const double*>(ctx->hpin);
   for (int c = 0; c < ctx->K; ++c) obj_out[c] = S[c] / ctx->h_nmem[c];
   return AD2_OK;
 }
